@@ -1,0 +1,209 @@
+"""Thin Python binding of the B200 H^2 library (C ABI: include/h2.h).
+
+Argument marshalling only: every step of the build and the matvec runs in the CUDA kernels of
+paper_2206_01885_b200/lib/libh2b200.so.  There is no CPU fallback: if the library is missing or
+no CUDA device is present the calls raise.  PyTorch is used by callers only for device memory
+and streams (pass tensor.data_ptr() / torch.cuda.current_stream().cuda_stream).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libh2b200.so")
+
+H2_KERNEL_COULOMB, H2_KERNEL_GAUSSIAN, H2_KERNEL_MATERN32 = 1, 2, 3
+H2_STORE_AUTO, H2_STORE_ALL, H2_STORE_ON_THE_FLY = 0, 1, 2
+
+EXPORT = dict(PERM=1, NODES=2, IL_OFF=4, IL_IDX=5, NF_OFF=6, NF_IDX=7, XS_OFF=8, XS_IDX=9, YS_OFF=10,
+              YS_IDX=11, K=12, SK_OFF=13, SK_IDX=14, U_OFF=15, U=16, XBAR_N=17, TREE_X=18)
+_EXPORT_DTYPE = dict(PERM=np.int32, NODES=np.int32, IL_OFF=np.int64, IL_IDX=np.int32, NF_OFF=np.int64,
+                     NF_IDX=np.int32, XS_OFF=np.int64, XS_IDX=np.int32, YS_OFF=np.int64, YS_IDX=np.int32,
+                     K=np.int32, SK_OFF=np.int64, SK_IDX=np.int32, U_OFF=np.int64, U=np.float64,
+                     XBAR_N=np.int32, TREE_X=np.float64)
+
+EXPORTED_SYMBOLS = ["h2_build", "h2_build_ex", "h2_options_default", "h2_matvec", "h2_free", "h2_last_error",
+                    "h2_last_error_message", "h2_info", "h2_export", "h2_sample_blocks"]
+
+
+class h2_options(C.Structure):
+    _fields_ = [("r_override", C.c_int32), ("storage", C.c_int32), ("mem_budget_bytes", C.c_int64),
+                ("stream", C.c_void_p), ("points_on_host", C.c_int32), ("timing", C.c_int32)]
+
+
+class h2_info_t(C.Structure):
+    _fields_ = [("n", C.c_int64), ("d", C.c_int32), ("depth", C.c_int32), ("r", C.c_int32),
+                ("nnodes", C.c_int32), ("nleaves", C.c_int32), ("csp", C.c_int32), ("n_il", C.c_int64),
+                ("n_nf", C.c_int64), ("coupling_entries", C.c_int64), ("nearfield_entries", C.c_int64),
+                ("stored_bytes", C.c_int64), ("coupling_stored", C.c_int32), ("nearfield_stored", C.c_int32),
+                ("hidr_dist_evals", C.c_int64), ("id_kernel_evals", C.c_int64), ("kmax", C.c_int32),
+                ("gpu_launches", C.c_int32), ("stage_ms", C.c_float * 9)]
+
+
+STAGES = ["tree", "lists", "calibrate", "hidr_up", "hidr_down", "id_sweep", "coupling_fill", "nearfield_fill",
+          "build"]
+
+
+class H2Error(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    """Loads libh2b200.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise H2Error(f"{LIB_PATH} not built; run python -m paper_2206_01885_b200.build or "
+                          f"__graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+        L.h2_build.restype = vp
+        L.h2_build.argtypes = [vp, i64, i32, i32, vp, f64, i32, f64]
+        L.h2_build_ex.restype = vp
+        L.h2_build_ex.argtypes = [vp, i64, i32, i32, vp, f64, i32, f64, C.POINTER(h2_options)]
+        L.h2_options_default.argtypes = [C.POINTER(h2_options)]
+        L.h2_matvec.restype = C.c_int
+        L.h2_matvec.argtypes = [vp, vp, vp]
+        L.h2_free.argtypes = [vp]
+        L.h2_last_error.restype = C.c_int
+        L.h2_last_error_message.restype = C.c_char_p
+        L.h2_info.restype = C.c_int
+        L.h2_info.argtypes = [vp, C.POINTER(h2_info_t)]
+        L.h2_export.restype = C.c_int
+        L.h2_export.argtypes = [vp, C.c_int, vp, C.c_size_t, C.POINTER(C.c_size_t)]
+        L.h2_sample_blocks.restype = C.c_int
+        L.h2_sample_blocks.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp]
+        _lib = L
+    return _lib
+
+
+def last_error() -> tuple[int, str]:
+    L = lib()
+    return int(L.h2_last_error()), L.h2_last_error_message().decode()
+
+
+def _raise():
+    code, msg = last_error()
+    raise H2Error(f"h2 error {code}: {msg}")
+
+
+def h2_options_default() -> h2_options:
+    o = h2_options()
+    lib().h2_options_default(C.byref(o))
+    return o
+
+
+def h2_build(points_ptr: int, n: int, d: int, kernel_id: int, kernel_params, id_tol: float, leaf_size: int,
+             admissibility: float = 0.5, options: h2_options | None = None) -> int:
+    """Calls h2_build_ex. points_ptr: DEVICE pointer (or HOST when options.points_on_host)."""
+    kp = (C.c_double * max(1, len(kernel_params or ())))(*(kernel_params or (0.0,)))
+    o = options if options is not None else h2_options_default()
+    h = lib().h2_build_ex(C.c_void_p(points_ptr), n, d, kernel_id, kp, id_tol, leaf_size, admissibility,
+                          C.byref(o))
+    if not h:
+        _raise()
+    return h
+
+
+def h2_matvec(h: int, x_ptr: int, y_ptr: int) -> None:
+    if lib().h2_matvec(C.c_void_p(h), C.c_void_p(x_ptr), C.c_void_p(y_ptr)) != 0:
+        _raise()
+
+
+def h2_free(h: int) -> None:
+    lib().h2_free(C.c_void_p(h))
+
+
+def h2_info(h: int) -> dict:
+    i = h2_info_t()
+    if lib().h2_info(C.c_void_p(h), C.byref(i)) != 0:
+        _raise()
+    out = {f: getattr(i, f) for f, _ in h2_info_t._fields_ if f != "stage_ms"}
+    out["stage_ms"] = dict(zip(STAGES, [float(v) for v in i.stage_ms]))
+    return out
+
+
+def h2_export(h: int, what: str) -> np.ndarray:
+    code = EXPORT[what]
+    need = C.c_size_t(0)
+    L = lib()
+    L.h2_export(C.c_void_p(h), code, None, 0, C.byref(need))
+    if need.value == 0 and L.h2_last_error() not in (0, -1):
+        _raise()
+    dt = _EXPORT_DTYPE[what]
+    a = np.empty(max(1, need.value // np.dtype(dt).itemsize), dt)
+    if L.h2_export(C.c_void_p(h), code, a.ctypes.data_as(C.c_void_p), a.nbytes, C.byref(need)) != 0:
+        _raise()
+    return a[: need.value // np.dtype(dt).itemsize]
+
+
+def h2_sample_blocks(h: int, kind, pair, entry):
+    kind = np.ascontiguousarray(kind, np.int32)
+    pair = np.ascontiguousarray(pair, np.int64)
+    entry = np.ascontiguousarray(entry, np.int64)
+    m = len(kind)
+    val = np.empty(m, np.float64)
+    rp = np.empty(m, np.int32)
+    cp = np.empty(m, np.int32)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    if lib().h2_sample_blocks(C.c_void_p(h), m, p(kind), p(pair), p(entry), p(val), p(rp), p(cp)) != 0:
+        _raise()
+    return val, rp, cp
+
+
+class H2Matrix:
+    """Owning wrapper: builds on the GPU from a torch CUDA tensor (n x d fp64) or a numpy array."""
+
+    def __init__(self, points, kernel_id: int, kernel_params=(), id_tol: float = 1e-6, leaf_size: int = 64,
+                 admissibility: float = 0.5, r: int = 0, storage: int = H2_STORE_AUTO, stream=None,
+                 timing: bool = False, mem_budget_bytes: int = 0):
+        import torch
+        o = h2_options_default()
+        o.r_override = int(r)
+        o.storage = int(storage)
+        o.timing = int(bool(timing))
+        o.mem_budget_bytes = int(mem_budget_bytes)
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        o.stream = C.c_void_p(stream.cuda_stream)
+        if isinstance(points, np.ndarray):
+            pts = np.ascontiguousarray(points, np.float64)
+            o.points_on_host = 1
+            self._keep = pts
+            ptr = pts.ctypes.data
+        else:
+            assert points.is_cuda and points.dtype == torch.float64 and points.is_contiguous()
+            self._keep = points
+            ptr = points.data_ptr()
+        self.n, self.d = int(points.shape[0]), int(points.shape[1])
+        self.stream = stream
+        self.h = h2_build(ptr, self.n, self.d, kernel_id, list(kernel_params), id_tol, leaf_size, admissibility, o)
+
+    def matvec(self, x):
+        import torch
+        y = torch.empty_like(x)
+        h2_matvec(self.h, x.data_ptr(), y.data_ptr())
+        return y
+
+    def info(self) -> dict:
+        return h2_info(self.h)
+
+    def export(self, what: str) -> np.ndarray:
+        return h2_export(self.h, what)
+
+    def close(self):
+        if getattr(self, "h", None):
+            h2_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

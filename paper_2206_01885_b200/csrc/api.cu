@@ -1,0 +1,322 @@
+// api.cu -- the C ABI of include/h2.h: argument validation, the Algorithm 2 stage sequence
+// (PAPER.md P:459-506), per-stage timing, export hooks and error reporting.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "h2_internal.cuh"
+
+namespace h2 {
+
+static thread_local int g_err = H2_OK;
+static thread_local std::string g_msg;
+
+void set_error(int code, const std::string& msg) {
+  g_err = code;
+  g_msg = msg;
+}
+void clear_error() {
+  g_err = H2_OK;
+  g_msg.clear();
+}
+
+static void free_handle(h2_handle* h) {
+  if (!h) return;
+  for (void* p : h->allocs)
+    if (p) dev_free(p, h->stream);
+  cudaStreamSynchronize(h->stream);
+  delete h;
+}
+
+template <class T>
+static std::vector<T> d2h(const T* d, size_t count, cudaStream_t s) {
+  std::vector<T> v(count);
+  if (count) H2_CUDA_TRY(cudaMemcpyAsync(v.data(), d, sizeof(T) * count, cudaMemcpyDeviceToHost, s));
+  H2_CUDA_TRY(cudaStreamSynchronize(s));
+  return v;
+}
+
+}  // namespace h2
+
+using namespace h2;
+
+extern "C" {
+
+int h2_last_error(void) { return g_err; }
+const char* h2_last_error_message(void) { return g_msg.c_str(); }
+
+void h2_options_default(h2_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->storage = H2_STORE_AUTO;
+}
+
+h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kernel_id, const double* kernel_params,
+                       double id_tol, int32_t leaf_size, double admissibility, const h2_options* opt) {
+  clear_error();
+  h2_options o;
+  h2_options_default(&o);
+  if (opt) o = *opt;
+  if (!points || n < 1 || n >= (1LL << 31) - 1 || d < 1 || d > kMaxD || leaf_size < 1 || !(admissibility > 0.0) ||
+      !(admissibility <= 0.7) || !(id_tol > 0.0) || !(id_tol < 1.0) || o.r_override < 0 || o.r_override > 4096 ||
+      o.storage < 0 || o.storage > 2) {
+    set_error(H2_ERR_INVALID_ARG, "invalid argument (n, d, leaf_size, admissibility, id_tol or options)");
+    return nullptr;
+  }
+  if (kernel_id != H2_KERNEL_COULOMB && kernel_id != H2_KERNEL_GAUSSIAN && kernel_id != H2_KERNEL_MATERN32) {
+    set_error(H2_ERR_UNKNOWN_KERNEL, "unknown kernel_id");
+    return nullptr;
+  }
+  double kp = 0.0;
+  if (kernel_id != H2_KERNEL_COULOMB) {
+    if (!kernel_params || !(kernel_params[0] > 0.0) || !std::isfinite(kernel_params[0])) {
+      set_error(H2_ERR_INVALID_ARG, "kernel parameter (h or l) must be finite and > 0");
+      return nullptr;
+    }
+    kp = kernel_params[0];
+  }
+  h2_handle* h = new h2_handle();
+  h->n = (int)n;
+  h->d = d;
+  h->kid = kernel_id;
+  h->kp = kp;
+  h->id_tol = id_tol;
+  h->q = leaf_size;
+  h->tau = admissibility;
+  h->stream = static_cast<cudaStream_t>(o.stream);
+  h->timing = o.timing;
+  cudaEvent_t ev[8];
+  int nev = 0;
+  try {
+    if (h->timing) {
+      for (auto& e : ev) H2_CUDA_TRY(cudaEventCreate(&e));
+      nev = 8;
+    }
+    auto mark = [&](int i) {
+      if (h->timing) H2_CUDA_TRY(cudaEventRecord(ev[i], h->stream));
+    };
+    const double* pts = points;
+    Scratch staged;
+    if (o.points_on_host) {
+      staged = Scratch(sizeof(double) * (size_t)n * d, h->stream);
+      H2_CUDA_TRY(cudaMemcpyAsync(staged.p, points, sizeof(double) * (size_t)n * d, cudaMemcpyHostToDevice,
+                                  h->stream));
+      pts = staged.as<double>();
+    }
+    mark(0);
+    build_tree(h, pts);  // a1-a3
+    mark(1);
+    build_lists(h);  // a4
+    mark(2);
+    h->r = o.r_override > 0 ? o.r_override : calibrate(h);  // a5
+    mark(3);
+    hidr_up(h);  // a6
+    mark(4);
+    hidr_down(h);  // a7
+    mark(5);
+    id_sweep(h);  // a8
+    mark(6);
+    fill_blocks(h, o.storage, o.mem_budget_bytes);  // a9, a10
+    mark(7);
+    H2_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (h->timing) {
+      for (int i = 0; i < 6; i++) cudaEventElapsedTime(&h->stage_ms[i], ev[i], ev[i + 1]);
+      cudaEventElapsedTime(&h->stage_ms[8], ev[0], ev[7]);
+    }
+  } catch (const Error& e) {
+    set_error(e.code, e.msg);
+    cudaGetLastError();
+    for (int i = 0; i < nev; i++) cudaEventDestroy(ev[i]);
+    free_handle(h);
+    return nullptr;
+  } catch (const std::exception& e) {
+    set_error(H2_ERR_INTERNAL, e.what());
+    for (int i = 0; i < nev; i++) cudaEventDestroy(ev[i]);
+    free_handle(h);
+    return nullptr;
+  }
+  for (int i = 0; i < nev; i++) cudaEventDestroy(ev[i]);
+  return h;
+}
+
+h2_handle* h2_build(const double* points, int64_t n, int32_t d, int32_t kernel_id, const double* kernel_params,
+                    double id_tol, int32_t leaf_size, double admissibility) {
+  return h2_build_ex(points, n, d, kernel_id, kernel_params, id_tol, leaf_size, admissibility, nullptr);
+}
+
+int h2_matvec(const h2_handle* h, const double* x, double* y) {
+  clear_error();
+  if (!h || !x || !y || x == y) {
+    set_error(H2_ERR_INVALID_ARG, "h2_matvec: null handle/pointer or aliasing x, y");
+    return H2_ERR_INVALID_ARG;
+  }
+  try {
+    matvec(h, x, y);
+  } catch (const Error& e) {
+    set_error(e.code, e.msg);
+    cudaGetLastError();
+    return e.code;
+  }
+  return H2_OK;
+}
+
+void h2_free(h2_handle* h) { free_handle(h); }
+
+int h2_info(const h2_handle* h, h2_info_t* out) {
+  clear_error();
+  if (!h || !out) {
+    set_error(H2_ERR_INVALID_ARG, "h2_info: null argument");
+    return H2_ERR_INVALID_ARG;
+  }
+  std::memset(out, 0, sizeof(*out));
+  out->n = h->n;
+  out->d = h->d;
+  out->depth = h->depth;
+  out->r = h->r;
+  out->nnodes = h->nnodes;
+  out->nleaves = h->nleaves;
+  out->csp = h->csp;
+  out->n_il = h->n_il;
+  out->n_nf = h->n_nf;
+  out->coupling_entries = h->cp_entries;
+  out->nearfield_entries = h->np_entries;
+  out->stored_bytes = 8 * ((h->cp_stored ? h->cp_entries : 0) + (h->np_stored ? h->np_entries : 0));
+  out->coupling_stored = h->cp_stored;
+  out->nearfield_stored = h->np_stored;
+  out->hidr_dist_evals = h->hidr_dist_evals;
+  out->id_kernel_evals = h->id_kernel_evals;
+  out->kmax = h->kmax;
+  out->gpu_launches = h->gpu_launches;
+  std::memcpy(out->stage_ms, h->stage_ms, sizeof(out->stage_ms));
+  return H2_OK;
+}
+
+static std::vector<char> export_bytes(const h2_handle* h, int what) {
+  cudaStream_t s = h->stream;
+  const int nn = h->nnodes, n = h->n, d = h->d, r = h->r;
+  auto bytes = [](const void* p, size_t b) {
+    std::vector<char> v(b);
+    std::memcpy(v.data(), p, b);
+    return v;
+  };
+  auto pack_slots = [&](const int* cnt_d, const int* slots_d, bool offsets) {
+    auto cnt = d2h(cnt_d, nn, s);
+    std::vector<int64_t> off(nn + 1, 0);
+    for (int i = 0; i < nn; i++) off[i + 1] = off[i] + cnt[i];
+    if (offsets) return bytes(off.data(), sizeof(int64_t) * (nn + 1));
+    auto sl = d2h(slots_d, (size_t)nn * r, s);
+    std::vector<int> out(off[nn]);
+    for (int i = 0; i < nn; i++)
+      for (int a = 0; a < cnt[i]; a++) out[off[i] + a] = sl[(size_t)i * r + a];
+    return bytes(out.data(), sizeof(int) * out.size());
+  };
+  switch (what) {
+    case H2_EXPORT_PERM: {
+      auto v = d2h(h->perm, n, s);
+      return bytes(v.data(), 4ull * n);
+    }
+    case H2_EXPORT_NODES: {
+      const int* arrs[7] = {h->level, h->nbegin, h->nend, h->parent, h->first_child, h->nchild, h->is_leaf};
+      std::vector<int> out((size_t)nn * 7);
+      for (int a = 0; a < 7; a++) {
+        auto v = d2h(arrs[a], nn, s);
+        for (int i = 0; i < nn; i++) out[(size_t)i * 7 + a] = v[i];
+      }
+      return bytes(out.data(), 4 * out.size());
+    }
+    case H2_EXPORT_IL_OFF:
+    case H2_EXPORT_NF_OFF: {
+      auto v = d2h(what == H2_EXPORT_IL_OFF ? h->il_off : h->nf_off, nn + 1, s);
+      return bytes(v.data(), 8 * v.size());
+    }
+    case H2_EXPORT_IL_IDX:
+    case H2_EXPORT_NF_IDX: {
+      int64_t m = what == H2_EXPORT_IL_IDX ? h->n_il : h->n_nf;
+      auto v = d2h(what == H2_EXPORT_IL_IDX ? h->il_idx : h->nf_idx, m, s);
+      return bytes(v.data(), 4 * v.size());
+    }
+    case H2_EXPORT_XS_OFF:
+    case H2_EXPORT_XS_IDX:
+      if (!h->xs) break;
+      return pack_slots(h->xs_cnt, h->xs, what == H2_EXPORT_XS_OFF);
+    case H2_EXPORT_YS_OFF:
+    case H2_EXPORT_YS_IDX:
+      if (!h->ys) break;
+      return pack_slots(h->ys_cnt, h->ys, what == H2_EXPORT_YS_OFF);
+    case H2_EXPORT_SK_OFF:
+    case H2_EXPORT_SK_IDX:
+      if (!h->k) break;
+      return pack_slots(h->k, h->sk, what == H2_EXPORT_SK_OFF);
+    case H2_EXPORT_K:
+    case H2_EXPORT_XBAR_N: {
+      if (!h->k) break;
+      auto v = d2h(what == H2_EXPORT_K ? h->k : h->xbar_n, nn, s);
+      return bytes(v.data(), 4 * v.size());
+    }
+    case H2_EXPORT_U_OFF:
+    case H2_EXPORT_U: {
+      if (!h->k) break;
+      auto k = d2h(h->k, nn, s);
+      auto xb = d2h(h->xbar_n, nn, s);
+      std::vector<int64_t> off(nn + 1, 0);
+      for (int i = 0; i < nn; i++) off[i + 1] = off[i] + (int64_t)k[i] * xb[i];
+      if (what == H2_EXPORT_U_OFF) return bytes(off.data(), 8 * off.size());
+      auto uo = d2h(h->u_off, nn + 1, s);
+      auto U = d2h(h->U, h->u_total, s);
+      std::vector<double> out(off[nn]);
+      for (int i = 0; i < nn; i++)
+        if (off[i + 1] > off[i]) std::memcpy(&out[off[i]], &U[uo[i]], 8 * (off[i + 1] - off[i]));
+      return bytes(out.data(), 8 * out.size());
+    }
+    case H2_EXPORT_TREE_X: {
+      auto v = d2h(h->X, (size_t)n * d, s);
+      std::vector<double> out((size_t)n * d);
+      for (int t = 0; t < n; t++)
+        for (int c = 0; c < d; c++) out[(size_t)t * d + c] = v[(size_t)c * n + t];
+      return bytes(out.data(), 8 * out.size());
+    }
+    default:
+      break;
+  }
+  throw Error{H2_ERR_INVALID_ARG, "unknown export id or stage not built"};
+}
+
+int h2_export(const h2_handle* h, int what, void* host_buf, size_t cap_bytes, size_t* needed_bytes) {
+  clear_error();
+  if (!h) {
+    set_error(H2_ERR_INVALID_ARG, "h2_export: null handle");
+    return H2_ERR_INVALID_ARG;
+  }
+  try {
+    auto v = export_bytes(h, what);
+    if (needed_bytes) *needed_bytes = v.size();
+    if (!host_buf || cap_bytes < v.size()) {
+      set_error(H2_ERR_INVALID_ARG, "h2_export: buffer too small");
+      return H2_ERR_INVALID_ARG;
+    }
+    if (!v.empty()) std::memcpy(host_buf, v.data(), v.size());
+  } catch (const Error& e) {
+    set_error(e.code, e.msg);
+    return e.code;
+  }
+  return H2_OK;
+}
+
+int h2_sample_blocks(const h2_handle* h, int64_t count, const int32_t* kind, const int64_t* pair,
+                     const int64_t* entry, double* value, int32_t* row_pt, int32_t* col_pt) {
+  clear_error();
+  if (!h || count < 0 || (count > 0 && (!kind || !pair || !entry || !value || !row_pt || !col_pt))) {
+    set_error(H2_ERR_INVALID_ARG, "h2_sample_blocks: invalid argument");
+    return H2_ERR_INVALID_ARG;
+  }
+  if (count == 0) return H2_OK;
+  try {
+    sample_blocks(h, count, kind, pair, entry, value, row_pt, col_pt);
+  } catch (const Error& e) {
+    set_error(e.code, e.msg);
+    return e.code;
+  }
+  return H2_OK;
+}
+
+}  // extern "C"

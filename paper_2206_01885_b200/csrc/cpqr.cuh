@@ -1,0 +1,169 @@
+// cpqr.cuh -- CTA-wide column-pivoted Householder QR interpolative decomposition (getBasis,
+// PAPER.md Eqs.(4.1)-(4.4); readings F1-F3).
+//
+// M (rows x cols, column-major, ld = rows) is held in global memory (L2-resident for the block
+// sizes of this method).  Per step t: residual column norms (recomputed, fused into the previous
+// step's update) -> pivot = largest norm, ties to the lowest position -> stop if
+// norm < tol * |R11| -> column swap -> Householder reflector -> one warp per trailing column
+// applies it and recomputes that column's residual norm.  On return M[0:k,0:k] = R11,
+// M[0:k,k:cols] = T = R11^{-1} R12 (so column piv[c] ~= sum_t T[t,c] column piv[t]).
+#pragma once
+#include <climits>
+
+#include "h2_internal.cuh"
+
+namespace h2 {
+
+template <int NT>
+struct CpqrSmem {
+  double rd[NT / 32];
+  int ri[NT / 32];
+  double bc_d[2];
+  int bc_i[2];
+};
+
+template <int NT>
+__device__ __forceinline__ double cta_sum(double v, CpqrSmem<NT>& sm) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sm.rd[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < NT / 32; w++) s += sm.rd[w];
+  return s;
+}
+
+// v: scratch of `rows` doubles (shared or global); nrm2, piv: `cols` entries (global ok)
+template <int NT>
+__device__ int cta_cpqr(double* __restrict__ M, int rows, int cols, double tol, int* __restrict__ piv,
+                        double* __restrict__ nrm2, double* __restrict__ v, CpqrSmem<NT>& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  for (int j = tid; j < cols; j += NT) piv[j] = j;
+  for (int j = warp; j < cols; j += NW) {
+    const double* col = M + (int64_t)rows * j;
+    double s = 0.0;
+    for (int i = lane; i < rows; i += 32) s += col[i] * col[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) nrm2[j] = s;
+  }
+  __syncthreads();
+  const int kmax = rows < cols ? rows : cols;
+  double r11 = 0.0;
+  int k = 0;
+  for (int t = 0; t < kmax; t++) {
+    // argmax of the residual norms over positions >= t (ties -> lowest position)
+    double best = -1.0;
+    int bj = INT_MAX;
+    for (int j = t + tid; j < cols; j += NT) {
+      double x = sqrt(nrm2[j]);
+      if (x > best) {
+        best = x;
+        bj = j;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      double b2 = __shfl_xor_sync(0xffffffffu, best, o);
+      int j2 = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (b2 > best || (b2 == best && j2 < bj)) {
+        best = b2;
+        bj = j2;
+      }
+    }
+    if (lane == 0) {
+      sm.rd[warp] = best;
+      sm.ri[warp] = bj;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double b = sm.rd[0];
+      int j = sm.ri[0];
+      for (int w = 1; w < NW; w++)
+        if (sm.rd[w] > b || (sm.rd[w] == b && sm.ri[w] < j)) {
+          b = sm.rd[w];
+          j = sm.ri[w];
+        }
+      sm.bc_d[0] = b;
+      sm.bc_i[0] = j;
+    }
+    __syncthreads();
+    const double nrm = sm.bc_d[0];
+    const int p = sm.bc_i[0];
+    if (t == 0) {
+      r11 = nrm;
+      if (r11 == 0.0) break;
+    }
+    if (nrm < tol * r11) break;
+    if (p != t) {
+      double* ct = M + (int64_t)rows * t;
+      double* cp = M + (int64_t)rows * p;
+      for (int i = tid; i < rows; i += NT) {
+        double a = ct[i];
+        ct[i] = cp[i];
+        cp[i] = a;
+      }
+      if (tid == 0) {
+        int tp = piv[t];
+        piv[t] = piv[p];
+        piv[p] = tp;
+        nrm2[p] = nrm2[t];
+      }
+    }
+    __syncthreads();
+    double* ct = M + (int64_t)rows * t;
+    const double x0 = ct[t];
+    const double alpha = x0 >= 0.0 ? -nrm : nrm;
+    double part = 0.0;
+    for (int i = t + tid; i < rows; i += NT) {
+      double vi = i == t ? x0 - alpha : ct[i];
+      v[i] = vi;
+      part += vi * vi;
+    }
+    const double vtv = cta_sum<NT>(part, sm);  // includes the syncs that publish v
+    __syncthreads();
+    if (vtv > 0.0) {
+      for (int j = t + 1 + warp; j < cols; j += NW) {
+        double* col = M + (int64_t)rows * j;
+        double s = 0.0;
+        for (int i = t + lane; i < rows; i += 32) s += v[i] * col[i];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const double f = 2.0 * s / vtv;
+        double nn = 0.0;
+        for (int i = t + lane; i < rows; i += 32) {
+          double a = col[i] - f * v[i];
+          col[i] = a;
+          if (i > t) nn += a * a;
+        }
+        for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+        if (lane == 0) nrm2[j] = nn;
+      }
+    } else {
+      for (int j = t + 1 + warp; j < cols; j += NW) {
+        double* col = M + (int64_t)rows * j;
+        double nn = 0.0;
+        for (int i = t + 1 + lane; i < rows; i += 32) nn += col[i] * col[i];
+        for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+        if (lane == 0) nrm2[j] = nn;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) ct[t] = alpha;
+    for (int i = t + 1 + tid; i < rows; i += NT) ct[i] = 0.0;
+    k = t + 1;
+    __syncthreads();
+  }
+  __syncthreads();
+  // T = R11^{-1} R12 by back substitution (one thread per column of R12)
+  for (int c = k + tid; c < cols; c += NT) {
+    double* col = M + (int64_t)rows * c;
+    for (int i = k - 1; i >= 0; i--) {
+      double s = col[i];
+      for (int l = i + 1; l < k; l++) s -= M[i + (int64_t)rows * l] * col[l];
+      col[i] = s / M[i + (int64_t)rows * i];
+    }
+  }
+  __syncthreads();
+  return k;
+}
+
+}  // namespace h2

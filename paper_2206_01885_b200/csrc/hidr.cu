@@ -1,0 +1,165 @@
+// hidr.cu -- a6/a7: HiDR, Algorithm 1.
+//
+// Bottom-up (lines 7-13): S_i = X_i at a leaf, S_p = U_{c in ch(p)} X_c^*; X_i^* = Vol(S_i, r1).
+// Top-down (lines 14-21): T_i = Y_p^* U (U_{j in IL(i)} X_j^*), Y_root^* = {} (reading D1); a node
+// with empty IL still gets T_i = Y_p^* (D2); Y_i^* = Vol(T_i, r2) (empty if T_i is empty).
+// Level-synchronous: per level, (1) a size kernel, (2) an exclusive scan, (3) a gather kernel
+// writing every node's S_i / T_i index list contiguously (the union is disjoint by the tiling of
+// the block partition, so it is a concatenation), (4) one CTA per node runs Vol.
+#include "vol.cuh"
+
+namespace h2 {
+
+constexpr int kHidrThreads = 256;
+
+// sizes of S_i (mode 0, bottom-up) or T_i (mode 1, top-down) for the nodes of one level
+__global__ void hidr_sizes_kernel(int mode, int base, int count, const int* __restrict__ is_leaf,
+                                  const int* __restrict__ nbegin, const int* __restrict__ nend,
+                                  const int* __restrict__ first_child, const int* __restrict__ nchild,
+                                  const int* __restrict__ parent, const int64_t* __restrict__ il_off,
+                                  const int* __restrict__ il_idx, const int* __restrict__ xs_cnt,
+                                  const int* __restrict__ ys_cnt, int64_t* sizes) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > count) return;
+  if (t == count) {
+    sizes[t] = 0;
+    return;
+  }
+  int i = base + t;
+  int64_t s = 0;
+  if (mode == 0) {
+    if (is_leaf[i]) s = nend[i] - nbegin[i];
+    else
+      for (int c = 0; c < nchild[i]; c++) s += xs_cnt[first_child[i] + c];
+  } else {
+    s = ys_cnt[parent[i]];
+    for (int64_t e = il_off[i]; e < il_off[i + 1]; e++) s += xs_cnt[il_idx[e]];
+  }
+  sizes[t] = s;
+}
+
+// one CTA per node: concatenate the segments of S_i / T_i into list[off[t] ...]
+__global__ void __launch_bounds__(kHidrThreads) hidr_gather_kernel(
+    int mode, int base, const int64_t* __restrict__ off, const int* __restrict__ is_leaf,
+    const int* __restrict__ nbegin, const int* __restrict__ first_child, const int* __restrict__ nchild,
+    const int* __restrict__ parent, const int64_t* __restrict__ il_off, const int* __restrict__ il_idx,
+    const int* __restrict__ xs_cnt, const int* __restrict__ xs, const int* __restrict__ ys_cnt,
+    const int* __restrict__ ys, int r, int* list) {
+  using Scan = cub::BlockScan<int, kHidrThreads>;
+  __shared__ typename Scan::TempStorage scan;
+  const int t = blockIdx.x;
+  const int i = base + t;
+  int* out = list + off[t];
+  const int64_t tot = off[t + 1] - off[t];
+  if (mode == 0 && is_leaf[i]) {
+    for (int64_t a = threadIdx.x; a < tot; a += blockDim.x) out[a] = nbegin[i] + (int)a;
+    return;
+  }
+  // segments: mode 0 -> children's X^* slots; mode 1 -> Y_p^* slot then X_j^* for j in IL(i)
+  int nseg = mode == 0 ? nchild[i] : 1 + (int)(il_off[i + 1] - il_off[i]);
+  int pos0 = 0;
+  for (int s0 = 0; s0 < nseg; s0 += kHidrThreads) {
+    int sidx = s0 + threadIdx.x;
+    const int* src = nullptr;
+    int cnt = 0;
+    if (sidx < nseg) {
+      int node;
+      if (mode == 0) {
+        node = first_child[i] + sidx;
+        src = xs + (int64_t)node * r;
+        cnt = xs_cnt[node];
+      } else if (sidx == 0) {
+        node = parent[i];
+        src = ys + (int64_t)node * r;
+        cnt = ys_cnt[node];
+      } else {
+        node = il_idx[il_off[i] + sidx - 1];
+        src = xs + (int64_t)node * r;
+        cnt = xs_cnt[node];
+      }
+    }
+    int pos, agg;
+    Scan(scan).ExclusiveSum(cnt, pos, agg);
+    for (int a = 0; a < cnt; a++) out[pos0 + pos + a] = src[a];
+    pos0 += agg;
+    __syncthreads();
+  }
+}
+
+struct ListAcc {
+  const double* X;
+  int64_t n;
+  const int* list;
+  __device__ __forceinline__ double coord(int pos, int c) const { return X[c * n + list[pos]]; }
+  __device__ __forceinline__ int index(int pos) const { return list[pos]; }
+};
+
+template <int D>
+__global__ void __launch_bounds__(kHidrThreads) hidr_vol_kernel(const double* __restrict__ X, int64_t n, int base,
+                                                                 const int64_t* __restrict__ off,
+                                                                 const int* __restrict__ list, int r, int* out_cnt,
+                                                                 int* out_slots, unsigned long long* evals) {
+  __shared__ VolSmem<D, kHidrThreads> sm;
+  const int t = blockIdx.x;
+  const int i = base + t;
+  ListAcc acc{X, n, list + off[t]};
+  int ns = (int)(off[t + 1] - off[t]);
+  int c = cta_vol<D, kHidrThreads>(acc, ns, r, out_slots + (int64_t)i * r, sm, evals);
+  if (threadIdx.x == 0) out_cnt[i] = c;
+}
+
+static void launch_vol(int d, unsigned grid, cudaStream_t s, const double* X, int64_t n, int base,
+                       const int64_t* off, const int* list, int r, int* cnt, int* slots, unsigned long long* ev) {
+  switch (d) {
+#define H2_VOL_CASE(DD) \
+  case DD:              \
+    hidr_vol_kernel<DD><<<grid, kHidrThreads, 0, s>>>(X, n, base, off, list, r, cnt, slots, ev); break;
+    H2_VOL_CASE(1) H2_VOL_CASE(2) H2_VOL_CASE(3) H2_VOL_CASE(4)
+    H2_VOL_CASE(5) H2_VOL_CASE(6) H2_VOL_CASE(7) H2_VOL_CASE(8)
+#undef H2_VOL_CASE
+  }
+}
+
+static void hidr_level(h2_handle* h, int mode, int l, unsigned long long* ev) {
+  cudaStream_t s = h->stream;
+  int base = h->lvl_start[l], count = h->lvl_start[l + 1] - base;
+  if (count == 0) return;
+  Scratch sizes(sizeof(int64_t) * (count + 1), s), off(sizeof(int64_t) * (count + 1), s);
+  hidr_sizes_kernel<<<(count + 1 + 255) / 256, 256, 0, s>>>(mode, base, count, h->is_leaf, h->nbegin, h->nend,
+                                                             h->first_child, h->nchild, h->parent, h->il_off,
+                                                             h->il_idx, h->xs_cnt, h->ys_cnt, sizes.as<int64_t>());
+  scan_excl_i64(sizes.as<int64_t>(), off.as<int64_t>(), count + 1, s);
+  H2_CHECK_LAUNCH();
+  int64_t total = read1(off.as<int64_t>() + count, s);
+  Scratch list(sizeof(int) * (total > 0 ? total : 1), s);
+  hidr_gather_kernel<<<count, kHidrThreads, 0, s>>>(mode, base, off.as<int64_t>(), h->is_leaf, h->nbegin,
+                                                    h->first_child, h->nchild, h->parent, h->il_off, h->il_idx,
+                                                    h->xs_cnt, h->xs, h->ys_cnt, h->ys, h->r, list.as<int>());
+  H2_CHECK_LAUNCH();
+  launch_vol(h->d, count, s, h->X, h->n, base, off.as<int64_t>(), list.as<int>(), h->r,
+             mode == 0 ? h->xs_cnt : h->ys_cnt, mode == 0 ? h->xs : h->ys, ev);
+  H2_CHECK_LAUNCH();
+  h->gpu_launches += 4;
+}
+
+void hidr_up(h2_handle* h) {
+  if (h->r > kVolSelCap) throw Error{H2_ERR_INVALID_ARG, "r exceeds the supported budget 4096"};
+  h->xs_cnt = halloc<int>(h, h->nnodes);
+  h->xs = halloc<int>(h, (size_t)h->nnodes * h->r);
+  h->ys_cnt = halloc<int>(h, h->nnodes);
+  h->ys = halloc<int>(h, (size_t)h->nnodes * h->r);
+  H2_CUDA_TRY(cudaMemsetAsync(h->ys_cnt, 0, sizeof(int) * h->nnodes, h->stream));
+  Scratch ev(sizeof(unsigned long long), h->stream);
+  H2_CUDA_TRY(cudaMemsetAsync(ev.p, 0, sizeof(unsigned long long), h->stream));
+  for (int l = h->depth; l >= 0; l--) hidr_level(h, 0, l, ev.as<unsigned long long>());
+  h->hidr_dist_evals = (int64_t)read1(ev.as<unsigned long long>(), h->stream);
+}
+
+void hidr_down(h2_handle* h) {
+  Scratch ev(sizeof(unsigned long long), h->stream);
+  H2_CUDA_TRY(cudaMemsetAsync(ev.p, 0, sizeof(unsigned long long), h->stream));
+  for (int l = 1; l <= h->depth; l++) hidr_level(h, 1, l, ev.as<unsigned long long>());
+  h->hidr_dist_evals += (int64_t)read1(ev.as<unsigned long long>(), h->stream);
+}
+
+}  // namespace h2

@@ -1,0 +1,180 @@
+// idsweep.cu -- a8: bottom-up skeleton sweep, Algorithm 2 lines 10-14.
+//
+// For every non-root node with Y_i^* != {} (level by level, deepest first):
+//   Xbar_i = X_i at a leaf, the concatenation of the children's X^_c (child order) otherwise;
+//   A = K(Xbar_i, Y_i^*) generated directly into the CTA's workspace as A^T (|Y^*| x |Xbar|);
+//   CPQR ID of A^T (cpqr.cuh) -> k_i, X^_i = Xbar_i[piv[0:k]], U_i = P [I; T^T] (|Xbar| x k);
+//   for a parent, the rows of U_i belonging to child c are the transfer matrix R_c.
+// Symmetric kernels: V = U, W = R (reading F6).
+#include "cpqr.cuh"
+
+namespace h2 {
+
+constexpr int kIdThreads = 256;
+
+// per node of one level: |Xbar| (and child offsets), workspace and U sizes
+__global__ void id_sizes_kernel(int base, int count, const int* __restrict__ is_leaf, const int* __restrict__ nbegin,
+                                const int* __restrict__ nend, const int* __restrict__ first_child,
+                                const int* __restrict__ nchild, const int* __restrict__ ys_cnt,
+                                const int* __restrict__ k, int* xbar_n, int* child_off, int64_t* wsz, int64_t* usz) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > count) return;
+  if (t == count) {
+    wsz[t] = 0;
+    usz[t] = 0;
+    return;
+  }
+  int i = base + t;
+  int ny = ys_cnt[i];
+  int nx = 0;
+  if (is_leaf[i]) {
+    nx = nend[i] - nbegin[i];
+  } else {
+    for (int c = 0; c < nchild[i]; c++) {
+      int ch = first_child[i] + c;
+      child_off[ch] = nx;
+      nx += k[ch];
+    }
+  }
+  if (ny == 0) nx = 0;
+  xbar_n[i] = nx;
+  int mn = nx < ny ? nx : ny;
+  // workspace: M (ny*nx doubles) + nrm2 (nx) + v (ny) + piv/xbar (2*nx ints, as doubles)
+  wsz[t] = nx > 0 ? (int64_t)ny * nx + nx + ny + nx + 2 : 0;
+  usz[t] = (int64_t)nx * mn;
+}
+
+__global__ void __launch_bounds__(kIdThreads) id_kernel(
+    int base, int kid, double p2, double tol, const double* __restrict__ X, int64_t n, int d, int r,
+    const int* __restrict__ is_leaf, const int* __restrict__ nbegin, const int* __restrict__ first_child,
+    const int* __restrict__ nchild, const int* __restrict__ ys_cnt, const int* __restrict__ ys,
+    const int* __restrict__ xbar_n, const int64_t* __restrict__ woff, double* work, const int64_t* __restrict__ uoff,
+    double* U, int* kout, int* sk, unsigned long long* evals) {
+  __shared__ CpqrSmem<kIdThreads> csm;
+  const int t = blockIdx.x;
+  const int i = base + t;
+  const int nx = xbar_n[i];
+  const int ny = ys_cnt[i];
+  const int tid = threadIdx.x;
+  if (nx == 0) {
+    if (tid == 0) kout[i] = 0;
+    return;
+  }
+  double* M = work + woff[t];
+  double* nrm2 = M + (int64_t)ny * nx;
+  double* v = nrm2 + nx;
+  int* piv = reinterpret_cast<int*>(v + ny);
+  int* xb = piv + nx;
+  // Xbar_i (tree-order point indices)
+  if (is_leaf[i]) {
+    for (int b = tid; b < nx; b += kIdThreads) xb[b] = nbegin[i] + b;
+  } else {
+    // children's skeletons in child order; child c's rows start at sum_{c'<c} k_c'
+    int o = 0;
+    for (int c = 0; c < nchild[i]; c++) {
+      int ch = first_child[i] + c;
+      int kc = kout[ch];
+      for (int a = tid; a < kc; a += kIdThreads) xb[o + a] = sk[(int64_t)ch * r + a];
+      o += kc;
+    }
+  }
+  __syncthreads();
+  // A^T: M[a + ny*b] = K(Xbar[b], Y^*[a]), Y^* ascending
+  const int* yv = ys + (int64_t)i * r;
+  for (int64_t e = tid; e < (int64_t)ny * nx; e += kIdThreads) {
+    int a = (int)(e % ny), b = (int)(e / ny);
+    M[e] = kernel_pts_d(kid, p2, X, n, d, xb[b], yv[a]);
+  }
+  __syncthreads();
+  const int k = cta_cpqr<kIdThreads>(M, ny, nx, tol, piv, nrm2, v, csm);
+  // outputs: k, skeleton (pivot order), U (nx x k column-major)
+  double* Ui = U + uoff[t];
+  for (int a = tid; a < k; a += kIdThreads) sk[(int64_t)i * r + a] = xb[piv[a]];
+  for (int64_t e = tid; e < (int64_t)nx * k; e += kIdThreads) {
+    int c = (int)(e % nx), tt = (int)(e / nx);
+    double val = c < k ? (c == tt ? 1.0 : 0.0) : M[tt + (int64_t)ny * c];
+    Ui[piv[c] + (int64_t)nx * tt] = val;
+  }
+  if (tid == 0) {
+    kout[i] = k;
+    atomicAdd(evals, (unsigned long long)nx * ny);
+  }
+}
+
+__global__ void uoff_scatter_kernel(int base, int count, const int64_t* __restrict__ off, int64_t shift,
+                                    int64_t* u_off) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < count) u_off[base + t] = shift + off[t];
+}
+
+__global__ void kmax_kernel(int nnodes, const int* __restrict__ k, int* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nnodes) atomicMax(out, k[i]);
+}
+
+void id_sweep(h2_handle* h) {
+  cudaStream_t s = h->stream;
+  const int nn = h->nnodes;
+  h->k = halloc<int>(h, nn);
+  h->sk = halloc<int>(h, (size_t)nn * h->r);
+  h->xbar_n = halloc<int>(h, nn);
+  h->child_off = halloc<int>(h, nn);
+  h->u_off = halloc<int64_t>(h, nn + 1);
+  H2_CUDA_TRY(cudaMemsetAsync(h->k, 0, sizeof(int) * nn, s));
+  H2_CUDA_TRY(cudaMemsetAsync(h->xbar_n, 0, sizeof(int) * nn, s));
+  H2_CUDA_TRY(cudaMemsetAsync(h->child_off, 0, sizeof(int) * nn, s));
+  H2_CUDA_TRY(cudaMemsetAsync(h->u_off, 0, sizeof(int64_t) * (nn + 1), s));
+  const double p2 = kernel_p2(h->kid, h->kp);
+  Scratch ev(sizeof(unsigned long long), s);
+  H2_CUDA_TRY(cudaMemsetAsync(ev.p, 0, sizeof(unsigned long long), s));
+  // U arena grows level by level (sizes depend on the children's ranks)
+  double* U = nullptr;
+  int64_t ucap = 0, uused = 0;
+  for (int l = h->depth; l >= 1; l--) {
+    int base = h->lvl_start[l], count = h->lvl_start[l + 1] - base;
+    if (count == 0) continue;
+    Scratch sz(sizeof(int64_t) * 2 * (count + 1), s), off(sizeof(int64_t) * 2 * (count + 1), s);
+    int64_t *wsz = sz.as<int64_t>(), *usz = wsz + count + 1;
+    int64_t *woff = off.as<int64_t>(), *uo = woff + count + 1;
+    id_sizes_kernel<<<(count + 1 + 255) / 256, 256, 0, s>>>(base, count, h->is_leaf, h->nbegin, h->nend,
+                                                            h->first_child, h->nchild, h->ys_cnt, h->k, h->xbar_n,
+                                                            h->child_off, wsz, usz);
+    scan_excl_i64(wsz, woff, count + 1, s);
+    scan_excl_i64(usz, uo, count + 1, s);
+    H2_CHECK_LAUNCH();
+    int64_t tot[2];
+    H2_CUDA_TRY(cudaMemcpyAsync(&tot[0], woff + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    H2_CUDA_TRY(cudaMemcpyAsync(&tot[1], uo + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    H2_CUDA_TRY(cudaStreamSynchronize(s));
+    if (uused + tot[1] > ucap) {
+      int64_t nc = uused + tot[1];
+      if (nc < 2 * ucap) nc = 2 * ucap;
+      double* nu = static_cast<double*>(dev_alloc(sizeof(double) * (nc > 0 ? nc : 1), s));
+      if (U && uused > 0) H2_CUDA_TRY(cudaMemcpyAsync(nu, U, sizeof(double) * uused, cudaMemcpyDeviceToDevice, s));
+      if (U) dev_free(U, s);
+      U = nu;
+      ucap = nc;
+    }
+    uoff_scatter_kernel<<<(count + 255) / 256, 256, 0, s>>>(base, count, uo, uused, h->u_off);
+    Scratch work(sizeof(double) * (tot[0] > 0 ? tot[0] : 1), s);
+    id_kernel<<<count, kIdThreads, 0, s>>>(base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf,
+                                           h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
+                                           work.as<double>(), h->u_off + base, U, h->k, h->sk,
+                                           ev.as<unsigned long long>());
+    H2_CHECK_LAUNCH();
+    h->gpu_launches += 5;
+    uused += tot[1];  // u_off[] holds global offsets into the arena
+  }
+  h->U = U ? U : static_cast<double*>(dev_alloc(8, s));
+  h->allocs.push_back(h->U);
+  h->u_total = uused;
+  H2_CUDA_TRY(cudaMemcpyAsync(h->u_off + nn, &h->u_total, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  Scratch km(sizeof(int), s);
+  H2_CUDA_TRY(cudaMemsetAsync(km.p, 0, sizeof(int), s));
+  kmax_kernel<<<(nn + 255) / 256, 256, 0, s>>>(nn, h->k, km.as<int>());
+  H2_CHECK_LAUNCH();
+  h->kmax = read1(km.as<int>(), s);
+  h->id_kernel_evals = (int64_t)read1(ev.as<unsigned long long>(), s);
+}
+
+}  // namespace h2

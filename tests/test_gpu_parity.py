@@ -1,0 +1,226 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded inputs.
+
+Acceptance (BASELINE.json north_star):
+  * bit-exact: tree permutation, node arrays, interaction / nearfield lists, calibrated r, HiDR
+    representor sets X_i^*, Y_i^*;
+  * matvec: GPU relative error vs exact K x (all rows for n <= 16384, else the 1024 seeded rows)
+    <= 2x the oracle's at the same id_tol, and GPU vs oracle matvec within 10 id_tol relative;
+  * skeletons: may differ at pivot near-ties; the agreement rate is reported and bounded below;
+  * stored block entries (sampled) equal the kernel at the recorded points to ~1 ulp-level.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2206_01885_b200 as P  # noqa: E402
+
+STRUCT = [("IL_OFF", oracle.IL_OFF), ("IL_IDX", oracle.IL_IDX), ("NF_OFF", oracle.NF_OFF), ("NF_IDX", oracle.NF_IDX),
+          ("XS_OFF", oracle.XS_OFF), ("XS_IDX", oracle.XS_IDX), ("YS_OFF", oracle.YS_OFF), ("YS_IDX", oracle.YS_IDX)]
+
+
+def gpu_build(pts, kid, kp, id_tol, q, tau=0.5, r=0, storage=P.H2_STORE_ALL):
+    X = torch.from_numpy(np.ascontiguousarray(pts)).cuda()
+    return P.H2Matrix(X, kid, kp, id_tol, q, tau, r=r, storage=storage, timing=True)
+
+
+def oracle_build(pts, kid, kp, id_tol, q, tau=0.5, r=None):
+    o = oracle.OracleH2(pts, q, tau)
+    r = o.build(kid, kp[0] if kp else 0.0, id_tol, r)
+    return o, r
+
+
+def assert_structure_equal(g, o):
+    assert np.array_equal(g.export("PERM"), o.perm)
+    assert np.array_equal(g.export("NODES").reshape(-1, 7), o.export(oracle.NODES).reshape(-1, 7))
+    for gname, oname in STRUCT:
+        a, b = g.export(gname), o.export(oname)
+        assert a.shape == b.shape and np.array_equal(a, b), gname
+
+
+def skeleton_agreement(g, o):
+    gk, ok = g.export("K"), o.export(oracle.K)
+    go, gi = g.export("SK_OFF"), g.export("SK_IDX")
+    oo, oi = o.skeletons()
+    nodes = np.flatnonzero((gk > 0) | (ok > 0))
+    same = sum(1 for i in nodes if gk[i] == ok[i] and set(gi[go[i]:go[i + 1]]) == set(oi[oo[i]:oo[i + 1]]))
+    return same / max(1, len(nodes))
+
+
+def matvec_check(g, o, pts, kid, kp, id_tol, cfg):
+    n = len(pts)
+    x = synth.matvec_vector(cfg, n)
+    rows = synth.sample_rows(cfg, n)
+    yg = g.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    yo = o.matvec(x, None if n <= 16384 else rows)
+    yo = yo if n > 16384 else yo[rows]
+    yd = oracle.dense_rows(pts, kid, kp[0] if kp else 0.0, x, rows)
+    eg = np.linalg.norm(yg[rows] - yd) / np.linalg.norm(yd)
+    eo = np.linalg.norm(yo - yd) / np.linalg.norm(yd)
+    agree = np.linalg.norm(yg[rows] - yo) / np.linalg.norm(yo)
+    return eg, eo, agree
+
+
+CASES = [  # name, config, n, q override
+    ("cfg1_full", 1, 8192, None),
+    ("cfg2_shape", 2, 40000, 64),
+    ("cfg3_shape", 3, 30000, None),
+    ("cfg4_shape", 4, 60000, None),
+    ("cfg5_shape", 5, 5000, 64),
+]
+
+
+@pytest.mark.parametrize("name,cfg,n,q", CASES)
+def test_parity_config_shapes(name, cfg, n, q):
+    c = synth.CONFIGS[cfg]
+    q = q or c["q"]
+    pts = synth.points(cfg, n)
+    kp = list(c["params"])
+    o, r = oracle_build(pts, c["kernel"], kp, c["id_tol"], q, c["tau"])
+    g = gpu_build(pts, c["kernel"], kp, c["id_tol"], q, c["tau"])
+    info = g.info()
+    assert info["r"] == r, (info["r"], r)
+    assert info["nnodes"] == o.info()["nnodes"] and info["depth"] == o.info()["depth"]
+    assert_structure_equal(g, o)
+    agree_sk = skeleton_agreement(g, o)
+    eg, eo, agree = matvec_check(g, o, pts, c["kernel"], kp, c["id_tol"], cfg)
+    print(f"{name}: r={r} skel-agree={agree_sk:.4f} err_gpu={eg:.3e} err_oracle={eo:.3e} gpu-vs-oracle={agree:.3e}")
+    assert agree_sk >= 0.9
+    assert eg <= 2.0 * eo + 1e-15
+    assert agree <= 10 * c["id_tol"]
+    g.close()
+
+
+def test_stored_blocks_sampled_against_kernel():
+    c = synth.CONFIGS[4]
+    pts = synth.points(4, 30000)
+    g = gpu_build(pts, c["kernel"], list(c["params"]), c["id_tol"], c["q"])
+    info = g.info()
+    assert info["coupling_stored"] and info["nearfield_stored"]
+    Xt = g.export("TREE_X").reshape(-1, 2)
+    assert np.array_equal(Xt, pts[g.export("PERM")])
+    rng = np.random.default_rng(0)
+    # pair counts from the symmetric-once lists (i < j coupling with ranks, i <= j nearfield)
+    il_off, il_idx = g.export("IL_OFF"), g.export("IL_IDX")
+    nf_off, nf_idx = g.export("NF_OFF"), g.export("NF_IDX")
+    k = g.export("K")
+    cp, nfp = [], []
+    for i in range(len(k)):
+        cp += [(i, j) for j in il_idx[il_off[i]:il_off[i + 1]] if j > i and k[i] > 0 and k[j] > 0]
+        nfp += [(i, j) for j in nf_idx[nf_off[i]:nf_off[i + 1]] if j >= i]
+    nodes = g.export("NODES").reshape(-1, 7)
+    kinds, pairs, entries = [], [], []
+    for _ in range(2000):
+        if rng.random() < 0.5:
+            p = rng.integers(len(cp))
+            i, j = cp[p]
+            kinds.append(0); pairs.append(p); entries.append(rng.integers(k[i] * k[j]))
+        else:
+            p = rng.integers(len(nfp))
+            i, j = nfp[p]
+            sz = (nodes[i, 2] - nodes[i, 1]) * (nodes[j, 2] - nodes[j, 1])
+            kinds.append(1); pairs.append(p); entries.append(rng.integers(sz))
+    val, rp, colp = P.h2_sample_blocks(g.h, kinds, pairs, entries)
+    ref = np.array([oracle.kernel(c["kernel"], c["params"][0], Xt[a], Xt[b]) for a, b in zip(rp, colp)])
+    np.testing.assert_allclose(val, ref, rtol=1e-13, atol=1e-300)
+    # the sampled rows / columns are the declared points of the pair
+    so, si = g.export("SK_OFF"), g.export("SK_IDX")
+    for kd, p, rr, cc in zip(kinds, pairs, rp, colp):
+        i, j = (cp if kd == 0 else nfp)[p]
+        if kd == 0:
+            assert rr in si[so[i]:so[i + 1]] and cc in si[so[j]:so[j + 1]]
+        else:
+            assert nodes[i, 1] <= rr < nodes[i, 2] and nodes[j, 1] <= cc < nodes[j, 2]
+    g.close()
+
+
+def test_on_the_fly_equals_stored():
+    c = synth.CONFIGS[1]
+    pts = synth.points(1, 8192)
+    a = gpu_build(pts, c["kernel"], [], c["id_tol"], c["q"], storage=P.H2_STORE_ALL)
+    b = gpu_build(pts, c["kernel"], [], c["id_tol"], c["q"], storage=P.H2_STORE_ON_THE_FLY)
+    assert b.info()["stored_bytes"] == 0 and a.info()["stored_bytes"] > 0
+    x = torch.from_numpy(synth.matvec_vector(1, 8192)).cuda()
+    ya, yb = a.matvec(x), b.matvec(x)
+    assert torch.allclose(ya, yb, rtol=1e-12, atol=1e-12 * ya.abs().max().item())
+
+
+@pytest.mark.parametrize("kid,kp", [(1, []), (2, [0.5]), (3, [0.1])])
+def test_single_leaf_dense_exact(kid, kp):
+    pts = synth.uniform_cube(50, 3, seed=3)
+    g = gpu_build(pts, kid, kp, 1e-6, 64)
+    assert g.info()["nnodes"] == 1
+    x = synth.matvec_vector(1, 50)
+    y = g.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    yd = oracle.dense_rows(pts, kid, kp[0] if kp else 0.0, x, np.arange(50))
+    np.testing.assert_allclose(y, yd, rtol=1e-12, atol=1e-12 * np.abs(yd).max())
+
+
+def test_edge_single_point_and_identical_points():
+    g = gpu_build(np.array([[0.5, 0.5]]), 1, [], 1e-6, 4)
+    assert g.info()["nnodes"] == 1
+    y = g.matvec(torch.ones(1, dtype=torch.float64, device="cuda"))
+    assert y.item() == 0.0                                           # kappa(x,x) = 0
+    pts = np.full((300, 3), 0.125)
+    g2 = gpu_build(pts, 2, [1.0], 1e-6, 8)
+    assert g2.info()["nnodes"] == 1
+    y2 = g2.matvec(torch.ones(300, dtype=torch.float64, device="cuda")).cpu().numpy()
+    np.testing.assert_allclose(y2, 300.0, rtol=1e-13)
+
+
+def test_paper_1d_lists_on_gpu():
+    pts = synth.equispaced_1d(16)
+    g = gpu_build(pts, 1, [], 1e-6, 2)
+    off, idx = g.export("IL_OFF"), g.export("IL_IDX")
+    assert sorted(idx[off[3]:off[4]]) == [5, 6]          # paper node 4 -> {6, 7}
+    assert sorted(idx[off[9]:off[10]]) == [7, 11, 12]    # paper node 10 -> {8,12,13}
+
+
+@pytest.mark.parametrize("d,n,q,seed", [(1, 3000, 5, 1), (2, 20000, 17, 2), (3, 25000, 33, 3), (2, 9000, 1, 4)])
+def test_parity_adaptive_clustered(d, n, q, seed):
+    pts = synth.clustered(n, d, seed=seed, k=5, sigma=0.03)
+    pts[:50] = pts[0]                                      # duplicates: deep leaves may exceed q
+    o, r = oracle_build(pts, 2, [0.3], 1e-5, q)
+    g = gpu_build(pts, 2, [0.3], 1e-5, q)
+    assert g.info()["r"] == r
+    assert_structure_equal(g, o)
+
+
+def test_r_override_and_storage_policy():
+    pts = synth.points(3, 20000)
+    g = gpu_build(pts, 2, [0.5], 1e-6, 128, r=27, storage=P.H2_STORE_ON_THE_FLY)
+    o, _ = oracle_build(pts, 2, [0.5], 1e-6, 128, r=27)
+    assert g.info()["r"] == 27
+    assert_structure_equal(g, o)
+
+
+@pytest.mark.slow
+def test_parity_bench_config_full_size():
+    """BASELINE configs[3] at full size (the bench workload): bit-exact structure, sampled fill,
+    sampled-row matvec error within 2x of the oracle's."""
+    c = synth.CONFIGS[4]
+    pts = synth.points(4)
+    kp = list(c["params"])
+    o, r = oracle_build(pts, c["kernel"], kp, c["id_tol"], c["q"])
+    g = gpu_build(pts, c["kernel"], kp, c["id_tol"], c["q"])
+    assert g.info()["r"] == r
+    assert_structure_equal(g, o)
+    assert skeleton_agreement(g, o) >= 0.9
+    n = len(pts)
+    x = synth.matvec_vector(4, n)
+    rows = synth.sample_rows(4, n)[:256]
+    yg = g.matvec(torch.from_numpy(x).cuda()).cpu().numpy()[rows]
+    yo = o.matvec(x, rows)
+    yd = oracle.dense_rows(pts, c["kernel"], kp[0], x, rows)
+    eg = np.linalg.norm(yg - yd) / np.linalg.norm(yd)
+    eo = np.linalg.norm(yo - yd) / np.linalg.norm(yd)
+    print(f"full cfg4: err_gpu={eg:.3e} err_oracle={eo:.3e}")
+    assert eg <= 2.0 * eo + 1e-15
+    assert np.linalg.norm(yg - yo) / np.linalg.norm(yo) <= 10 * c["id_tol"]
