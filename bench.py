@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 data-driven H^2 construction (arxiv 2206.01885).
+
+One step = one complete h2_build (a1-a10: tree, lists, r calibration, HiDR up/down, ID sweep,
+coupling + nearfield fill, every block stored) of BASELINE.json configs[3] (the largest
+configuration whose stored H^2 fits one B200: n = 4,194,304 points, 2-D 16-Gaussian mixture,
+Matern-3/2 l = 0.1, q = 256, id_tol 1e-6, tau 0.5).  configs[1] (1M cube, 1e-8) needs ~178 GB of
+blocks and configs[4] ~198 GB, so neither fits; they are parity cases, not bench lines.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+
+Timing: W untimed warm-up builds, then K timed builds, each bracketed by CUDA events on the
+library's stream with a barrier + synchronize on both sides of the timed region; L2 is flushed
+(512 MiB write) before every timed build; max over ranks.  value = total points built by all
+ranks / time (Mpoints/s).  Multi-GPU (torchrun): every rank builds its own independent problem
+instance of the same config (weak scaling, no data-path collective).
+--impl reference times the fp64 CPU oracle (the reference for this tier) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "H² construction Mpoints/s at fixed matvec rel. error; % of FP64/HBM roofline"
+UNIT = "Mpoints/s"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
+FALLBACK_HBM_GBS = 6650.0
+# FP64 vector peak of B200: 148 SMs x 64 FP64 lanes (DFMA = 2 flops) x clock; see DESIGN.md
+FP64_LANES_PER_SM = 64
+
+
+def workload_desc(cfg: int) -> str:
+    c = synth.CONFIGS[cfg]
+    kname = {1: "Coulomb", 2: "Gaussian", 3: "Matern-3/2"}[c["kernel"]]
+    par = f" param {c['params'][0]}" if c["params"] else ""
+    return (f"BASELINE configs[{cfg - 1}]: {c['name']} n={c['n']} d={c['d']} {kname}{par} q={c['q']} "
+            f"id_tol={c['id_tol']} tau={c['tau']}; full build a1-a10, all blocks stored symmetric-once")
+
+
+# ------------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                smax.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------ dist
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v: float, ws: int) -> float:
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------------------------------ oracle
+def oracle_sample_run(cfg: int, n_sample: int):
+    """The fp64 oracle, as it stands, on a bounded sample of the workload (same distribution,
+    n_sample points): a1-a8 plus an evaluate-only pass over every a9/a10 block."""
+    import oracle
+    c = synth.CONFIGS[cfg]
+    pts = synth.points(cfg, n_sample)
+    kp = c["params"][0] if c["params"] else 0.0
+    t0 = time.perf_counter()
+    h = oracle.OracleH2(pts, c["q"], c["tau"])
+    h.build(c["kernel"], kp, c["id_tol"])
+    entries, _ = h.fill(store=False)
+    dt = time.perf_counter() - t0
+    h.close()
+    return dt, entries
+
+
+def cpu_baseline(cfg: int, n_sample: int) -> dict:
+    import oracle
+    dt, entries = oracle_sample_run(cfg, n_sample)
+    return {"value": round(n_sample / dt / 1e6, 6), "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"oracle a1-a8 + evaluate-only a9/a10 ({entries} block entries) on n={n_sample} points "
+                      f"of the same distribution as the workload; wall {dt:.2f} s"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    cfg = args.config
+    n_s = args.cpu_sample
+    for _ in range(args.warmup):
+        oracle_sample_run(cfg, n_s // 4)
+    times = []
+    for _ in range(args.steps):
+        dt, entries = oracle_sample_run(cfg, n_s)
+        times.append(dt)
+    t = float(np.mean(times))
+    v = n_s / t / 1e6
+    line = {"metric": METRIC, "value": round(v, 6), "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": workload_desc(cfg), "sample_n": n_s,
+                       "note": "reference = the fp64 CPU oracle (oracle/h2_oracle.c) on the host cores"},
+            "cpu_baseline": {"value": round(v, 6), "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": f"n={n_s} points of the workload distribution per step, a1-a8 + "
+                                       f"evaluate-only a9/a10"},
+            "e2e": {"value": round(v, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------ ours
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    import paper_2206_01885_b200 as P
+
+    cfg = args.config
+    c = synth.CONFIGS[cfg]
+    n = c["n"] if args.n is None else args.n
+    # every rank builds its own independent instance (weak scaling); rank 0 uses the config's seed
+    pts_np = synth.points(cfg, n) if rank == 0 else _rank_points(cfg, n, rank)
+    pts = torch.from_numpy(pts_np).cuda()
+    stream = torch.cuda.Stream()
+    kp = list(c["params"])
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def opts(host=False):
+        o = P.h2_options_default()
+        o.storage = P.H2_STORE_ALL
+        o.timing = 1
+        o.stream = stream.cuda_stream
+        o.points_on_host = 1 if host else 0
+        return o
+
+    def one(host=False, src=None):
+        ptr = src if src is not None else pts.data_ptr()
+        return P.h2_build(ptr, n, c["d"], c["kernel"], kp, c["id_tol"], c["q"], c["tau"], opts(host))
+
+    for _ in range(args.warmup):
+        h = one()
+        P.h2_free(h)
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    times, fill_ms, cfill_ms, stages, launches = [], [], [], [], 0
+    info = None
+    barrier(ws)
+    torch.cuda.synchronize()
+    sampler.start()
+    t_wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        h = one()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        info = P.h2_info(h)
+        fill_ms.append(info["stage_ms"]["nearfield_fill"])
+        cfill_ms.append(info["stage_ms"]["coupling_fill"])
+        stages.append(info["stage_ms"])
+        launches = info["gpu_launches"]
+        P.h2_free(h)
+    torch.cuda.synchronize()
+    barrier(ws)
+    t_wall = time.perf_counter() - t_wall0
+    clocks = sampler.stop()
+
+    t_step = max_over_ranks(float(np.mean(times)), ws)
+    value = ws * n / (t_step * 1e-3) / 1e6
+
+    # e2e: same build through the C ABI from pinned HOST memory (H2D inside the call) plus the
+    # device->host read of the step's result (the skeleton ranks k_i of every node)
+    pinned = torch.from_numpy(pts_np).pin_memory()
+    e2e_times = []
+    h2d = n * c["d"] * 8
+    d2h = 0
+    for _ in range(max(1, min(args.steps, 3))):
+        with torch.cuda.stream(stream):
+            flush.fill_(2)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h = one(host=True, src=pinned.data_ptr())
+        kvec = P.h2_export(h, "K")
+        t1 = time.perf_counter()
+        d2h = kvec.nbytes
+        e2e_times.append(t1 - t0)
+        P.h2_free(h)
+    e2e_t = max_over_ranks(float(np.mean(e2e_times)), ws)
+    e2e = {"value": round(ws * n / e2e_t / 1e6, 4), "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": int(d2h)}
+
+    # roofline of the dominant kernel (nearfield fill, a10): algorithmic bytes = 8 B per stored entry
+    peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
+    hbm = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
+    nf_bytes = 8 * info["nearfield_entries"]
+    nf_ms = float(np.mean(fill_ms))
+    achieved = nf_bytes / (nf_ms * 1e-3) / 1e9
+    traffic = None
+    if os.path.exists(TRAFFIC_FILE):
+        try:
+            tr = json.load(open(TRAFFIC_FILE))
+            if tr.get("workload") == c["name"]:
+                traffic = tr.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    sm_mhz = clocks.get("sm_mhz") or 1965.0
+    fp64_peak = 148 * FP64_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": traffic,
+                "kernel": "fill_kernel<D=2,MATERN32,NEARFIELD> (a10)", "kernel_ms": round(nf_ms, 3),
+                "step_share": round(nf_ms / t_step, 4),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650 GB/s",
+                "fp64_peak_tflops_at_sm_clock": round(fp64_peak, 2)}
+
+    if rank == 0:
+        mean_stages = {k: round(float(np.mean([s[k] for s in stages])), 3) for k in stages[0]}
+        line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(t_step, 3), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload_desc(cfg), "n_per_gpu": n, "r": info["r"], "nnodes": info["nnodes"],
+                           "stored_bytes": info["stored_bytes"], "coupling_entries": info["coupling_entries"],
+                           "nearfield_entries": info["nearfield_entries"],
+                           "parallelism": "single GPU" if ws == 1 else f"{ws} independent instances (weak)",
+                           "l2": "flushed (512 MiB write) before every timed step",
+                           "wall_s_timed_region": round(t_wall, 3)},
+                "stages_ms": mean_stages, "clocks": clocks, "e2e": e2e, "gpu_launches": launches,
+                "roofline": roofline}
+        if ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def _rank_points(cfg, n, rank):
+    """Independent instance per rank: same distribution, seed offset by the rank."""
+    return synth.points(cfg, n, seed_offset=10_000 * rank)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--n", type=int, default=None, help="override n (not a bench line)")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 19)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

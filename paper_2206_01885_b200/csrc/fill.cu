@@ -1,189 +1,316 @@
 // fill.cu -- a9/a10: coupling blocks B_ij = K(X^_i, X^_j) over the admissible pairs and dense
 // nearfield blocks K(X_i, X_j) over the leaf nearfield pairs (Algorithm 2, PAPER.md P:496-503;
 // reading G1).  Symmetric kernels: only i < j (coupling) and i <= j (nearfield) are stored, each
-// block row-major.
+// block row-major, blocks concatenated in CSR pair order.
 //
-// The fill is HBM-write / FP64 bound.  Work is partitioned by a flat ENTRY index space cut into
-// tiles of kFillTile entries (a pair owns ceil(size/kFillTile) tiles), so a 60M-entry block and a
-// 16-entry block are balanced alike.  A persistent grid (blocks_per_SM x 148) walks the tiles;
-// one binary search per tile maps it to its pair; each thread then writes entries e, e+256, ...
-// (consecutive threads -> consecutive addresses, streaming stores).
+// The fill is FP64 / HBM-write bound (8 B stored per kernel evaluation).
+//  * nearfield (a10): the block space is cut into warp UNITS of one block (a row chunk x up to
+//    32*CW columns, ~kWarpUnitEntries entries); a persistent grid of warps walks the units.  A lane
+//    keeps CW column points in registers, rows are broadcast, stores of a row are coalesced and
+//    streaming; no CTA barrier is involved, so the loop is the kernel evaluation itself.  Big and
+//    small blocks are balanced alike (unit -> pair map precomputed).
+//  * coupling (a9): k_i x k_j blocks are small (ranks <= r): one warp per pair, lanes over columns
+//    (column skeleton coordinates in registers), rows broadcast.
+#include <cstdlib>
+#include <cub/block/block_scan.cuh>
+
 #include "h2_internal.cuh"
 
 namespace h2 {
 
 constexpr int kFillThreads = 256;
-constexpr int kFillTile = 4096;
 
-// number of symmetric-once pairs of each row (mode 0 coupling: j > i, both ranks > 0;
-// mode 1 nearfield: j >= i)
-__global__ void pair_count_kernel(int mode, int nnodes, const int64_t* __restrict__ off, const int* __restrict__ idx,
-                                  const int* __restrict__ k, int64_t* cnt) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i > nnodes) return;
-  if (i == nnodes) {
-    cnt[i] = 0;
-    return;
+// ---- symmetric-once pair lists, entry-parallel over the CSR ---------------------------------
+__device__ __forceinline__ int row_of(const int64_t* __restrict__ off, int nnodes, int64_t e) {
+  int lo = 0, hi = nnodes - 1;  // last i with off[i] <= e
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= e) lo = mid;
+    else hi = mid - 1;
   }
-  int64_t c = 0;
-  if (mode == 1 || k[i] > 0)
-    for (int64_t e = off[i]; e < off[i + 1]; e++) {
-      int j = idx[e];
-      if (mode == 0 ? (j > i && k[j] > 0) : (j >= i)) c++;
-    }
-  cnt[i] = c;
+  return lo;
 }
 
-__global__ void pair_emit_kernel(int mode, int nnodes, const int64_t* __restrict__ off, const int* __restrict__ idx,
-                                 const int* __restrict__ k, const int* __restrict__ nbegin,
+__global__ void pair_flag_kernel(int mode, int nnodes, int64_t m, const int64_t* __restrict__ off,
+                                 const int* __restrict__ idx, const int* __restrict__ k, int64_t* flag) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= m; e += (int64_t)gridDim.x * blockDim.x) {
+    if (e == m) {
+      flag[e] = 0;
+      continue;
+    }
+    int i = row_of(off, nnodes, e), j = idx[e];
+    flag[e] = mode == 0 ? (j > i && k[i] > 0 && k[j] > 0) : (j >= i);
+  }
+}
+
+__global__ void pair_emit_kernel(int mode, int nnodes, int64_t m, const int64_t* __restrict__ off,
+                                 const int* __restrict__ idx, const int* __restrict__ k, const int* __restrict__ nbegin,
                                  const int* __restrict__ nend, const int64_t* __restrict__ pos, int2* pairs,
                                  int64_t* size) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nnodes) return;
-  if (mode == 0 && k[i] == 0) return;
-  int64_t o = pos[i];
-  for (int64_t e = off[i]; e < off[i + 1]; e++) {
-    int j = idx[e];
-    if (mode == 0 ? (j > i && k[j] > 0) : (j >= i)) {
-      pairs[o] = make_int2(i, j);
-      size[o] = mode == 0 ? (int64_t)k[i] * k[j] : (int64_t)(nend[i] - nbegin[i]) * (nend[j] - nbegin[j]);
-      o++;
-    }
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    if (pos[e + 1] == pos[e]) continue;
+    int i = row_of(off, nnodes, e), j = idx[e];
+    int64_t o = pos[e];
+    pairs[o] = make_int2(i, j);
+    size[o] = mode == 0 ? (int64_t)k[i] * k[j] : (int64_t)(nend[i] - nbegin[i]) * (nend[j] - nbegin[j]);
   }
 }
 
-__global__ void tiles_kernel(int64_t np, const int64_t* __restrict__ size, int64_t* ntiles) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p <= np; p += (int64_t)gridDim.x * blockDim.x)
-    ntiles[p] = p < np ? (size[p] + kFillTile - 1) / kFillTile : 0;
+// ---- nearfield units (warp-level) ------------------------------------------------------------
+// A unit is (pair, row chunk, column chunk) of one block and is processed by ONE warp, without
+// CTA barriers: lane l owns the columns c0 + l + 32 s (s < CW), whose coordinates stay in
+// registers; rows are streamed with warp-uniform (broadcast) loads; slot s stores at a fixed
+// offset of 256 s bytes from the lane's row pointer.  The inner loop is the kernel evaluation.
+__host__ __device__ constexpr int warp_slots(int D) { return D <= 2 ? 8 : (D <= 3 ? 5 : (D <= 5 ? 3 : 2)); }
+constexpr int kWarpUnitEntries = 4096;
+
+// H2_FILL_VARIANT (tuning knob, read once): selects the (slots, rows per iteration, min blocks)
+// instantiation of the D = 2 nearfield kernel; 0 = default (8 slots, 2 CTAs/SM: fastest measured).
+static int nf_variant() {
+  static const int v = [] {
+    const char* e = getenv("H2_FILL_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+static int nf_slots(int d) {
+  if (d != 2) return warp_slots(d);
+  const int v = nf_variant();
+  return v == 1 || v == 2 ? 4 : (v == 3 ? 6 : (v == 5 ? 2 : 8));
 }
 
-template <int D, int KID, int MODE>
-__global__ void __launch_bounds__(kFillThreads) fill_kernel(int64_t ntiles, int64_t np, const int64_t* __restrict__ toff,
-                                                            const int2* __restrict__ pairs,
-                                                            const int64_t* __restrict__ voff,
-                                                            const int* __restrict__ nbegin,
-                                                            const int* __restrict__ nend, const int* __restrict__ k,
-                                                            const int* __restrict__ sk, int r,
-                                                            const double* __restrict__ X, int64_t n, double p2,
-                                                            double* __restrict__ out) {
-  __shared__ int64_t s_pair;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    if (threadIdx.x == 0) {
-      int64_t lo = 0, hi = np - 1;  // last p with toff[p] <= tile
-      while (lo < hi) {
-        int64_t mid = (lo + hi + 1) >> 1;
-        if (toff[mid] <= tile) lo = mid;
-        else hi = mid - 1;
-      }
-      s_pair = lo;
+__host__ __device__ __forceinline__ void unit_shape(int ni, int nj, int wc, int& R, int& nrb, int& ncb) {
+  int nc = nj < wc ? nj : wc;
+  R = kWarpUnitEntries / (nc > 0 ? nc : 1);
+  if (R < 1) R = 1;
+  nrb = (ni + R - 1) / R;
+  ncb = (nj + wc - 1) / wc;
+}
+
+__global__ void nf_units_kernel(int wc, int64_t np, const int2* __restrict__ pairs, const int* __restrict__ nbegin,
+                                const int* __restrict__ nend, int64_t* units) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p <= np; p += (int64_t)gridDim.x * blockDim.x) {
+    if (p == np) {
+      units[p] = 0;
+      continue;
     }
-    __syncthreads();
-    const int64_t p = s_pair;
-    __syncthreads();
-    const int2 pr = pairs[p];
-    const int i = pr.x, j = pr.y;
-    const int ni = MODE == 0 ? k[i] : nend[i] - nbegin[i];
-    const int nj = MODE == 0 ? k[j] : nend[j] - nbegin[j];
-    const int64_t size = (int64_t)ni * nj;
-    const int64_t e0 = (tile - toff[p]) * kFillTile;
-    const int64_t e1 = e0 + kFillTile < size ? e0 + kFillTile : size;
-    double* o = out + voff[p];
-    const int bi = nbegin[i], bj = nbegin[j];
-    const int* si = sk + (int64_t)i * r;
-    const int* sj = sk + (int64_t)j * r;
-    int64_t e = e0 + threadIdx.x;
-    if (e >= e1) continue;
-    int row = (int)(e / nj), col = (int)(e - (int64_t)row * nj);
-    const int dq = kFillThreads / nj, dr = kFillThreads - dq * nj;
-    for (; e < e1; e += kFillThreads) {
-      const int a = MODE == 0 ? si[row] : bi + row;
-      const int b = MODE == 0 ? sj[col] : bj + col;
-      double s = 0.0;
+    int2 pr = pairs[p];
+    int R, nrb, ncb;
+    unit_shape(nend[pr.x] - nbegin[pr.x], nend[pr.y] - nbegin[pr.y], wc, R, nrb, ncb);
+    units[p] = (int64_t)nrb * ncb;
+  }
+}
+
+__global__ void unit_map_kernel(int64_t np, const int64_t* __restrict__ uoff, int* umap) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np; p += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t u = uoff[p]; u < uoff[p + 1]; u++) umap[u] = (int)p;
+}
+
+// one unit's rows [r0, r1) over NS column slots: NS independent evaluation chains per row, no
+// control flow between them (so the compiler interleaves them), next row's point prefetched
+template <int D, int KID, int NS>
+__device__ __forceinline__ void nf_unit_rows(const double* __restrict__ xr, int64_t n, const double (&xb)[8][D],
+                                             const bool (&ok)[8], int r0, int r1, int nj, double* o, double p2,
+                                             const double* __restrict__ tab) {
+  double xa[D];
+#pragma unroll
+  for (int c = 0; c < D; c++) xa[c] = xr[c * n + r0];  // warp-uniform address: one broadcast
+  for (int row = r0; row < r1; row++, o += nj) {
+    double xn[D];
+    const int rn = row + 1 < r1 ? row + 1 : row;
+#pragma unroll
+    for (int c = 0; c < D; c++) xn[c] = xr[c * n + rn];
+    double v[NS];
+#pragma unroll
+    for (int s = 0; s < NS; s++) {
+      double sq = 0.0;
 #pragma unroll
       for (int c = 0; c < D; c++) {
-        double df = X[c * n + a] - X[c * n + b];
-        s = fma(df, df, s);
+        const double df = xa[c] - xb[s][c];
+        sq = fma(df, df, sq);
       }
-      __stcs(o + e, kernel_s(KID, p2, s));
-      col += dr;
-      row += dq;
-      if (col >= nj) {
-        col -= nj;
-        row++;
+      v[s] = kernel_s(KID, p2, sq, tab);
+    }
+#pragma unroll
+    for (int s = 0; s < NS; s++)
+      if (ok[s]) __stcs(o + 32 * s, v[s]);
+#pragma unroll
+    for (int c = 0; c < D; c++) xa[c] = xn[c];
+  }
+}
+
+template <int D, int KID, int CW, int RU, int MINB>
+__global__ void __launch_bounds__(kFillThreads, MINB) nf_fill_kernel(int64_t nunits, const int* __restrict__ umap,
+                                                                     const int64_t* __restrict__ uoff,
+                                                                     const int2* __restrict__ pairs,
+                                                                     const int64_t* __restrict__ voff,
+                                                                     const int* __restrict__ nbegin,
+                                                                     const int* __restrict__ nend,
+                                                                     const double* __restrict__ X, int64_t n,
+                                                                     double p2, double* __restrict__ out) {
+  static_assert(CW >= 1 && CW <= 8, "1..8 column slots");
+  constexpr int WC = 32 * CW;
+  __shared__ double tab[64];
+  if (threadIdx.x < 64) tab[threadIdx.x] = kExp2Tab64[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < nunits; u += nw) {
+    const int p = umap[u];
+    const int2 pr = pairs[p];
+    const int bi = nbegin[pr.x], bj = nbegin[pr.y];
+    const int ni = nend[pr.x] - bi, nj = nend[pr.y] - bj;
+    int R, nrb, ncb;
+    unit_shape(ni, nj, WC, R, nrb, ncb);
+    const int loc = (int)(u - uoff[p]);
+    const int rb = loc / ncb, cb = loc - rb * ncb;
+    const int r0 = rb * R, c0 = cb * WC;
+    const int r1 = ni < r0 + R ? ni : r0 + R;
+    double xb[8][D];
+    bool ok[8];
+#pragma unroll
+    for (int s = 0; s < 8; s++) {
+      const int col = c0 + lane + 32 * s;
+      ok[s] = s < CW && col < nj;
+#pragma unroll
+      for (int c = 0; c < D; c++) xb[s][c] = ok[s] ? X[c * n + bj + col] : 0.0;
+    }
+    double* o = out + voff[p] + (int64_t)r0 * nj + c0 + lane;
+    const double* xr = X + bi;
+    int nslot = (nj - c0 + 31) >> 5;  // warp-uniform: slots with at least one column
+    if (nslot > CW) nslot = CW;
+    switch (nslot) {
+      case 1: nf_unit_rows<D, KID, 1>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
+      case 2: nf_unit_rows<D, KID, (CW < 2 ? CW : 2)>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
+      case 3: nf_unit_rows<D, KID, (CW < 3 ? CW : 3)>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
+      case 4: nf_unit_rows<D, KID, (CW < 4 ? CW : 4)>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
+      case 5: nf_unit_rows<D, KID, (CW < 5 ? CW : 5)>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
+      case 6: nf_unit_rows<D, KID, (CW < 6 ? CW : 6)>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
+      case 7: nf_unit_rows<D, KID, (CW < 7 ? CW : 7)>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
+      default: nf_unit_rows<D, KID, CW>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
+    }
+  }
+}
+
+// ---- coupling: one warp per pair ------------------------------------------------------------
+template <int D, int KID>
+__global__ void __launch_bounds__(kFillThreads) cp_fill_kernel(int64_t np, const int2* __restrict__ pairs,
+                                                               const int64_t* __restrict__ voff,
+                                                               const int* __restrict__ k, const int* __restrict__ sk,
+                                                               int r, const double* __restrict__ X, int64_t n,
+                                                               double p2, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t p = gw; p < np; p += nw) {
+    const int2 pr = pairs[p];
+    const int ki = k[pr.x], kj = k[pr.y];
+    const int* si = sk + (int64_t)pr.x * r;
+    const int* sj = sk + (int64_t)pr.y * r;
+    double* o = out + voff[p];
+    for (int c0 = 0; c0 < kj; c0 += 32) {
+      const int col = c0 + lane;
+      double xb[D];
+      if (col < kj) {
+        const int b = sj[col];
+#pragma unroll
+        for (int c = 0; c < D; c++) xb[c] = X[c * n + b];
+      }
+      for (int row = 0; row < ki; row++) {
+        const int a = si[row];
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; c++) {
+          double df = X[c * n + a] - (col < kj ? xb[c] : 0.0);
+          s = fma(df, df, s);
+        }
+        if (col < kj) __stcs(o + (int64_t)row * kj + col, kernel_s(KID, p2, s));
       }
     }
   }
 }
 
-template <int KID, int MODE>
-static void launch_fill_k(int d, unsigned grid, cudaStream_t s, int64_t ntiles, int64_t np, const int64_t* toff,
-                          const int2* pairs, const int64_t* voff, const h2_handle* h, double p2, double* out) {
-  switch (d) {
-#define H2_FILL_CASE(DD)                                                                                     \
-  case DD:                                                                                                   \
-    fill_kernel<DD, KID, MODE><<<grid, kFillThreads, 0, s>>>(ntiles, np, toff, pairs, voff, h->nbegin,       \
-                                                             h->nend, h->k, h->sk, h->r, h->X, h->n, p2, out); \
+template <int KID>
+static void launch_fill_kid(const h2_handle* h, int mode, int64_t nwork, int64_t np, const int* umap, const int64_t* uoff,
+                            const int2* pairs, const int64_t* voff, double p2, double* out) {
+  cudaStream_t s = h->stream;
+  if (mode == 1) {
+    const int64_t blocks = (nwork + 7) / 8;  // one warp per unit, 8 warps per CTA
+    unsigned g = (unsigned)(blocks < 148 * 8 ? blocks : 148 * 8);
+#define H2_NF_ARGS nwork, umap, uoff, pairs, voff, h->nbegin, h->nend, h->X, h->n, p2, out
+    switch (h->d) {
+      case 2:
+        switch (nf_variant()) {  // tuning variants of the D = 2 kernel (CW, RU, MINB)
+          case 1: nf_fill_kernel<2, KID, 4, 1, 4><<<g, kFillThreads, 0, s>>>(H2_NF_ARGS); break;
+          case 2: nf_fill_kernel<2, KID, 4, 1, 2><<<g, kFillThreads, 0, s>>>(H2_NF_ARGS); break;
+          case 3: nf_fill_kernel<2, KID, 6, 1, 2><<<g, kFillThreads, 0, s>>>(H2_NF_ARGS); break;
+          case 4: nf_fill_kernel<2, KID, 8, 1, 1><<<g, kFillThreads, 0, s>>>(H2_NF_ARGS); break;
+          case 5: nf_fill_kernel<2, KID, 2, 1, 4><<<g, kFillThreads, 0, s>>>(H2_NF_ARGS); break;
+          default: nf_fill_kernel<2, KID, 8, 1, 2><<<g, kFillThreads, 0, s>>>(H2_NF_ARGS); break;
+        }
+        break;
+#define H2_NF_CASE(DD) \
+  case DD:             \
+    nf_fill_kernel<DD, KID, warp_slots(DD), 1, 2><<<g, kFillThreads, 0, s>>>(H2_NF_ARGS); break;
+      H2_NF_CASE(1) H2_NF_CASE(3) H2_NF_CASE(4)
+      H2_NF_CASE(5) H2_NF_CASE(6) H2_NF_CASE(7) H2_NF_CASE(8)
+#undef H2_NF_CASE
+#undef H2_NF_ARGS
+    }
+  } else {
+    int64_t blocks = (np + 7) / 8;
+    unsigned g = (unsigned)(blocks < 148 * 8 ? blocks : 148 * 8);
+    switch (h->d) {
+#define H2_CP_CASE(DD)                                                                                        \
+  case DD:                                                                                                    \
+    cp_fill_kernel<DD, KID><<<g, kFillThreads, 0, s>>>(np, pairs, voff, h->k, h->sk, h->r, h->X, h->n, p2, out); \
     break;
-    H2_FILL_CASE(1) H2_FILL_CASE(2) H2_FILL_CASE(3) H2_FILL_CASE(4)
-    H2_FILL_CASE(5) H2_FILL_CASE(6) H2_FILL_CASE(7) H2_FILL_CASE(8)
-#undef H2_FILL_CASE
+      H2_CP_CASE(1) H2_CP_CASE(2) H2_CP_CASE(3) H2_CP_CASE(4)
+      H2_CP_CASE(5) H2_CP_CASE(6) H2_CP_CASE(7) H2_CP_CASE(8)
+#undef H2_CP_CASE
+    }
   }
 }
 
-template <int MODE>
-static void launch_fill(const h2_handle* h, int64_t ntiles, int64_t np, const int64_t* toff, const int2* pairs,
-                        const int64_t* voff, double* out) {
+static void launch_fill(const h2_handle* h, int mode, int64_t nwork, int64_t np, const int* umap, const int64_t* uoff,
+                        const int2* pairs, const int64_t* voff, double* out) {
+  if (nwork < 1) return;
   const double p2 = kernel_p2(h->kid, h->kp);
-  int64_t g = ntiles < 148 * 8 ? ntiles : 148 * 8;
-  if (g < 1) return;
-  if (h->kid == H2_KERNEL_COULOMB)
-    launch_fill_k<H2_KERNEL_COULOMB, MODE>(h->d, (unsigned)g, h->stream, ntiles, np, toff, pairs, voff, h, p2, out);
+  if (h->kid == H2_KERNEL_COULOMB) launch_fill_kid<H2_KERNEL_COULOMB>(h, mode, nwork, np, umap, uoff, pairs, voff, p2, out);
   else if (h->kid == H2_KERNEL_GAUSSIAN)
-    launch_fill_k<H2_KERNEL_GAUSSIAN, MODE>(h->d, (unsigned)g, h->stream, ntiles, np, toff, pairs, voff, h, p2, out);
-  else
-    launch_fill_k<H2_KERNEL_MATERN32, MODE>(h->d, (unsigned)g, h->stream, ntiles, np, toff, pairs, voff, h, p2, out);
+    launch_fill_kid<H2_KERNEL_GAUSSIAN>(h, mode, nwork, np, umap, uoff, pairs, voff, p2, out);
+  else launch_fill_kid<H2_KERNEL_MATERN32>(h, mode, nwork, np, umap, uoff, pairs, voff, p2, out);
 }
 
-// builds the symmetric-once pair list of one class with entry offsets; returns (pairs, entries)
+// builds the symmetric-once pair list of one class (CSR order) with entry offsets
 static void make_pairs(h2_handle* h, int mode, int64_t& np, int2*& pairs, int64_t*& voff, int64_t& entries) {
   cudaStream_t s = h->stream;
   const int nn = h->nnodes;
   const int64_t* off = mode == 0 ? h->il_off : h->nf_off;
   const int* idx = mode == 0 ? h->il_idx : h->nf_idx;
-  Scratch cnt(sizeof(int64_t) * (nn + 1), s), pos(sizeof(int64_t) * (nn + 1), s);
-  pair_count_kernel<<<(nn + 1 + 255) / 256, 256, 0, s>>>(mode, nn, off, idx, h->k, cnt.as<int64_t>());
-  scan_excl_i64(cnt.as<int64_t>(), pos.as<int64_t>(), nn + 1, s);
+  const int64_t m = mode == 0 ? h->n_il : h->n_nf;
+  Scratch flag(sizeof(int64_t) * (m + 1), s), pos(sizeof(int64_t) * (m + 1), s);
+  pair_flag_kernel<<<grid_for(m + 1, 256), 256, 0, s>>>(mode, nn, m, off, idx, h->k, flag.as<int64_t>());
+  scan_excl_i64(flag.as<int64_t>(), pos.as<int64_t>(), m + 1, s);
   H2_CHECK_LAUNCH();
-  np = read1(pos.as<int64_t>() + nn, s);
+  np = read1(pos.as<int64_t>() + m, s);
   pairs = halloc<int2>(h, np);
   voff = halloc<int64_t>(h, np + 1);
   Scratch size(sizeof(int64_t) * (np + 1), s);
   H2_CUDA_TRY(cudaMemsetAsync(size.as<int64_t>() + np, 0, sizeof(int64_t), s));
-  pair_emit_kernel<<<(nn + 255) / 256, 256, 0, s>>>(mode, nn, off, idx, h->k, h->nbegin, h->nend,
-                                                    pos.as<int64_t>(), pairs, size.as<int64_t>());
+  if (m > 0)
+    pair_emit_kernel<<<grid_for(m, 256), 256, 0, s>>>(mode, nn, m, off, idx, h->k, h->nbegin, h->nend,
+                                                      pos.as<int64_t>(), pairs, size.as<int64_t>());
   scan_excl_i64(size.as<int64_t>(), voff, np + 1, s);
   H2_CHECK_LAUNCH();
   h->gpu_launches += 5;
   entries = read1(voff + np, s);
 }
 
-__global__ void adjdiff_kernel(int64_t np, const int64_t* __restrict__ voff, int64_t* size) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np; p += (int64_t)gridDim.x * blockDim.x)
-    size[p] = voff[p + 1] - voff[p];
-}
-
-static int64_t pool_available(cudaStream_t s) {
+static int64_t pool_available() {
   size_t fr = 0, tot = 0;
   H2_CUDA_TRY(cudaMemGetInfo(&fr, &tot));
-  int dev = 0;
-  H2_CUDA_TRY(cudaGetDevice(&dev));
-  cudaMemPool_t pool;
-  H2_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
-  uint64_t reserved = 0, used = 0;
-  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
-  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
-  (void)s;
-  return (int64_t)fr + (int64_t)(reserved > used ? reserved - used : 0);
+  return (int64_t)fr + (int64_t)cached_free_bytes();
 }
 
 void fill_blocks(h2_handle* h, int storage, int64_t budget) {
@@ -195,7 +322,7 @@ void fill_blocks(h2_handle* h, int storage, int64_t budget) {
   if (storage == H2_STORE_ALL) {
     store_cp = store_np = true;
   } else if (storage == H2_STORE_AUTO) {
-    int64_t avail = budget > 0 ? budget : pool_available(s) - ((int64_t)4 << 30);
+    int64_t avail = budget > 0 ? budget : pool_available() - ((int64_t)4 << 30);
     // greedy: the smaller class first
     if (cb <= nb) {
       if (cb <= avail) store_cp = true, avail -= cb;
@@ -216,27 +343,39 @@ void fill_blocks(h2_handle* h, int storage, int64_t budget) {
     h->np_val = halloc<double>(h, h->np_entries);
     h->np_stored = 1;
   }
-  for (int mode = 0; mode < 2; mode++) {
-    int64_t np = mode == 0 ? h->n_cp : h->n_np;
-    if (h->timing) H2_CUDA_TRY(cudaEventRecord(ev[2 * mode], s));
-    if ((mode == 0 ? store_cp : store_np) && np > 0) {
-      const int64_t* voff = mode == 0 ? h->cp_off : h->np_off;
-      Scratch sizes(sizeof(int64_t) * (np + 1), s), nt(sizeof(int64_t) * (np + 1), s),
-          toff(sizeof(int64_t) * (np + 1), s);
-      adjdiff_kernel<<<grid_for(np, 256), 256, 0, s>>>(np, voff, sizes.as<int64_t>());
-      tiles_kernel<<<grid_for(np + 1, 256), 256, 0, s>>>(np, sizes.as<int64_t>(), nt.as<int64_t>());
-      scan_excl_i64(nt.as<int64_t>(), toff.as<int64_t>(), np + 1, s);
-      H2_CHECK_LAUNCH();
-      int64_t ntiles = read1(toff.as<int64_t>() + np, s);
-      if (h->timing) H2_CUDA_TRY(cudaEventRecord(ev[2 * mode], s));
-      if (mode == 0) launch_fill<0>(h, ntiles, np, toff.as<int64_t>(), h->cp_pairs, voff, h->cp_val);
-      else launch_fill<1>(h, ntiles, np, toff.as<int64_t>(), h->np_pairs, voff, h->np_val);
-      H2_CHECK_LAUNCH();
-      h->gpu_launches += 4;
-    }
-    if (h->timing) H2_CUDA_TRY(cudaEventRecord(ev[2 * mode + 1], s));
+  // a9 coupling
+  if (h->timing) H2_CUDA_TRY(cudaEventRecord(ev[0], s));
+  if (store_cp && h->n_cp > 0) {
+    launch_fill(h, 0, h->n_cp, h->n_cp, nullptr, nullptr, h->cp_pairs, h->cp_off, h->cp_val);
+    H2_CHECK_LAUNCH();
+    h->gpu_launches += 1;
+  }
+  if (h->timing) H2_CUDA_TRY(cudaEventRecord(ev[1], s));
+  // a10 nearfield
+  Scratch units, uoff, umap;
+  int64_t nunits = 0;
+  if (store_np && h->n_np > 0) {
+    const int64_t np = h->n_np;
+    units = Scratch(sizeof(int64_t) * (np + 1), s);
+    uoff = Scratch(sizeof(int64_t) * (np + 1), s);
+    nf_units_kernel<<<grid_for(np + 1, 256), 256, 0, s>>>(32 * nf_slots(h->d), np, h->np_pairs, h->nbegin, h->nend,
+                                                          units.as<int64_t>());
+    scan_excl_i64(units.as<int64_t>(), uoff.as<int64_t>(), np + 1, s);
+    H2_CHECK_LAUNCH();
+    nunits = read1(uoff.as<int64_t>() + np, s);
+    umap = Scratch(sizeof(int) * (nunits > 0 ? nunits : 1), s);
+    unit_map_kernel<<<grid_for(np, 256), 256, 0, s>>>(np, uoff.as<int64_t>(), umap.as<int>());
+    H2_CHECK_LAUNCH();
+    h->gpu_launches += 3;
+  }
+  if (h->timing) H2_CUDA_TRY(cudaEventRecord(ev[2], s));
+  if (nunits > 0) {
+    launch_fill(h, 1, nunits, h->n_np, umap.as<int>(), uoff.as<int64_t>(), h->np_pairs, h->np_off, h->np_val);
+    H2_CHECK_LAUNCH();
+    h->gpu_launches += 1;
   }
   if (h->timing) {
+    H2_CUDA_TRY(cudaEventRecord(ev[3], s));
     H2_CUDA_TRY(cudaEventSynchronize(ev[3]));
     float a = 0, b = 0;
     cudaEventElapsedTime(&a, ev[0], ev[1]);

@@ -1,45 +1,98 @@
 // prims.cu -- device memory pool and the CUB primitives (scan, radix sort) used by the stages.
 #include <cub/cub.cuh>
+#include <map>
+#include <mutex>
+#include <unordered_map>
 
 #include "h2_internal.cuh"
 
 namespace h2 {
 
-static cudaMemPool_t pool_for_current_device() {
-  int dev = 0;
-  H2_CUDA_TRY(cudaGetDevice(&dev));
-  static cudaMemPool_t pools[64] = {nullptr};
-  if (!pools[dev]) {
-    cudaMemPool_t p;
-    H2_CUDA_TRY(cudaDeviceGetDefaultMemPool(&p, dev));
-    uint64_t thr = UINT64_MAX;  // keep freed blocks cached: repeated builds reuse HBM
-    H2_CUDA_TRY(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr));
-    pools[dev] = p;
+// Size-matched caching allocator.  Every allocation of the build is served from blocks freed by
+// earlier builds when one of a close size exists (the sizes repeat exactly from build to build),
+// otherwise from cudaMalloc.  Freed blocks are kept (never cudaFree'd except to recover from an
+// out-of-memory), so steady-state builds make no driver allocation calls at all.  A block is
+// tagged with the stream that freed it; handing it to another stream first synchronises that one.
+struct CachedBlock {
+  void* p;
+  size_t size;
+  cudaStream_t stream;
+  int dev;
+};
+static std::mutex g_mu;
+static std::multimap<size_t, CachedBlock> g_free;
+static std::unordered_map<void*, CachedBlock> g_live;
+
+static size_t round_size(size_t b) {
+  if (b < 512) return 512;
+  if (b < (1u << 20)) return (b + 511) & ~size_t(511);
+  return (b + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+}
+
+static void release_cached(int dev) {  // caller holds g_mu
+  H2_CUDA_TRY(cudaDeviceSynchronize());
+  for (auto it = g_free.begin(); it != g_free.end();) {
+    if (it->second.dev == dev) {
+      cudaFree(it->second.p);
+      it = g_free.erase(it);
+    } else {
+      ++it;
+    }
   }
-  return pools[dev];
 }
 
 void* dev_alloc(size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  H2_CUDA_TRY(cudaGetDevice(&dev));
+  const size_t size = round_size(bytes);
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto it = g_free.lower_bound(size); it != g_free.end() && it->first <= size + size / 4 + (size_t(2) << 20);
+       ++it) {
+    if (it->second.dev != dev) continue;
+    CachedBlock b = it->second;
+    g_free.erase(it);
+    if (b.stream != s) H2_CUDA_TRY(cudaStreamSynchronize(b.stream));
+    b.stream = s;
+    g_live[b.p] = b;
+    return b.p;
+  }
   void* p = nullptr;
-  cudaMemPool_t pool = pool_for_current_device();
-  cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, s);
+  cudaError_t e = cudaMalloc(&p, size);
   if (e == cudaErrorMemoryAllocation) {
-    // give cached blocks back and retry once
     cudaGetLastError();
-    H2_CUDA_TRY(cudaStreamSynchronize(s));
-    H2_CUDA_TRY(cudaMemPoolTrimTo(pool, 0));
-    e = cudaMallocFromPoolAsync(&p, bytes, pool, s);
+    release_cached(dev);
+    e = cudaMalloc(&p, size);
   }
   if (e != cudaSuccess) {
     cudaGetLastError();
     throw Error{H2_ERR_OOM, "device allocation of " + std::to_string(bytes) + " bytes failed: " +
                                 cudaGetErrorString(e)};
   }
+  g_live[p] = CachedBlock{p, size, s, dev};
   return p;
 }
 
 void dev_free(void* p, cudaStream_t s) {
-  if (p) cudaFreeAsync(p, s);
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_live.find(p);
+  if (it == g_live.end()) return;
+  CachedBlock b = it->second;
+  g_live.erase(it);
+  b.stream = s;
+  g_free.emplace(b.size, b);
+}
+
+// bytes held by the cache and free for reuse on the current device (the AUTO storage budget
+// counts them as available)
+size_t cached_free_bytes() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_mu);
+  size_t t = 0;
+  for (auto& kv : g_free)
+    if (kv.second.dev == dev) t += kv.second.size;
+  return t;
 }
 
 void hfree(h2_handle* h, void* p) {

@@ -43,11 +43,12 @@ def _rng(seed: int) -> np.random.Generator:
     return np.random.Generator(np.random.PCG64(seed))
 
 
-def points(config: int, n: int | None = None) -> np.ndarray:
-    """Point cloud of `config` (n x d, fp64, C-contiguous, point-major). `n` overrides the size."""
+def points(config: int, n: int | None = None, seed_offset: int = 0) -> np.ndarray:
+    """Point cloud of `config` (n x d, fp64, C-contiguous, point-major). `n` overrides the size;
+    `seed_offset` draws an independent instance (multi-GPU weak scaling)."""
     c = CONFIGS[config]
     n = c["n"] if n is None else int(n)
-    rng = _rng(SEED_BASE + config)
+    rng = _rng(SEED_BASE + config + seed_offset)
     if config in (1, 2):
         x = rng.random((n, 3))
     elif config == 3:
