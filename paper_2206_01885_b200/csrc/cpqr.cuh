@@ -166,4 +166,131 @@ __device__ int cta_cpqr(double* __restrict__ M, int rows, int cols, double tol, 
   return k;
 }
 
+// ---- shared-memory variant: M row-major (M[i*ld + j]), thread-per-column ownership ----------
+// Same algorithm and tie rules as cta_cpqr.  Per step: (1) every thread scans the residual norms
+// of its own columns, a warp argmax, the warps' winners are combined redundantly by every thread
+// (one barrier); (2) warp 0 swaps the pivot column in, builds the Householder vector and v^T v
+// (one barrier); (3) each thread applies the reflector to its columns and recomputes their
+// residual norms (one barrier).  Used when the block fits in shared memory.
+template <int NT>
+struct CpqrRmSmem {
+  double wb[NT / 32];
+  int wj[NT / 32];
+  double vtv;
+};
+
+template <int NT>
+__device__ int cta_cpqr_rm(double* __restrict__ M, int ny, int nx, int ld, double tol, int* __restrict__ piv,
+                           double* __restrict__ nrm2, double* __restrict__ v, CpqrRmSmem<NT>& sm) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int j = tid; j < nx; j += NT) {
+    piv[j] = j;
+    double s = 0.0;
+    for (int i = 0; i < ny; i++) s += M[i * ld + j] * M[i * ld + j];
+    nrm2[j] = s;
+  }
+  __syncthreads();
+  const int kmax = ny < nx ? ny : nx;
+  double r11 = 0.0;
+  int k = 0;
+  for (int t = 0; t < kmax; t++) {
+    double best = -1.0;
+    int bj = INT_MAX;
+    for (int j = t + tid; j < nx; j += NT) {
+      const double x = sqrt(nrm2[j]);
+      if (x > best) {
+        best = x;
+        bj = j;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double b2 = __shfl_xor_sync(0xffffffffu, best, o);
+      const int j2 = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (b2 > best || (b2 == best && j2 < bj)) {
+        best = b2;
+        bj = j2;
+      }
+    }
+    if (lane == 0) {
+      sm.wb[warp] = best;
+      sm.wj[warp] = bj;
+    }
+    __syncthreads();
+    double nrm = sm.wb[0];
+    int p = sm.wj[0];
+#pragma unroll
+    for (int w = 1; w < NW; w++)
+      if (sm.wb[w] > nrm || (sm.wb[w] == nrm && sm.wj[w] < p)) {
+        nrm = sm.wb[w];
+        p = sm.wj[w];
+      }
+    if (t == 0) {
+      r11 = nrm;
+      if (r11 == 0.0) break;
+    }
+    if (nrm < tol * r11) break;
+    if (warp == 0) {
+      // swap columns t <-> p, Householder vector of the new column t (rows t..ny-1)
+      const double x0 = M[t * ld + p];
+      const double alpha = x0 >= 0.0 ? -nrm : nrm;
+      __syncwarp();  // every lane has read x0 before row t is rewritten
+      double part = 0.0;
+      for (int i = lane; i < ny; i += 32) {
+        const double a = M[i * ld + p];
+        if (p != t) M[i * ld + p] = M[i * ld + t];
+        double vi = 0.0;
+        if (i > t) vi = a;
+        else if (i == t) vi = x0 - alpha;
+        if (i >= t) {
+          v[i] = vi;
+          part += vi * vi;
+          M[i * ld + t] = i == t ? alpha : 0.0;
+        } else {
+          M[i * ld + t] = a;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane == 0) {
+        sm.vtv = part;
+        const int tp = piv[t];
+        piv[t] = piv[p];
+        piv[p] = tp;
+        nrm2[p] = nrm2[t];
+      }
+    }
+    __syncthreads();
+    const double vtv = sm.vtv;
+    for (int j = t + 1 + tid; j < nx; j += NT) {
+      double nn = 0.0;
+      if (vtv > 0.0) {
+        double s = 0.0;
+        for (int i = t; i < ny; i++) s += v[i] * M[i * ld + j];
+        const double f = 2.0 * s / vtv;
+        for (int i = t; i < ny; i++) {
+          const double a = M[i * ld + j] - f * v[i];
+          M[i * ld + j] = a;
+          if (i > t) nn += a * a;
+        }
+      } else {
+        for (int i = t + 1; i < ny; i++) nn += M[i * ld + j] * M[i * ld + j];
+      }
+      nrm2[j] = nn;
+    }
+    k = t + 1;
+    __syncthreads();
+  }
+  __syncthreads();
+  // T = R11^{-1} R12 by back substitution (one thread per column of R12)
+  for (int c = k + tid; c < nx; c += NT) {
+    for (int i = k - 1; i >= 0; i--) {
+      double s = M[i * ld + c];
+      for (int l = i + 1; l < k; l++) s -= M[i * ld + l] * M[l * ld + c];
+      M[i * ld + c] = s / M[i * ld + i];
+    }
+  }
+  __syncthreads();
+  return k;
+}
+
 }  // namespace h2

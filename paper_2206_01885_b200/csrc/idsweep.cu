@@ -11,12 +11,20 @@
 namespace h2 {
 
 constexpr int kIdThreads = 256;
+constexpr int kIdSmemThreads = 128;
+constexpr int kIdSmemMax = 100 * 1024;  // dynamic shared memory budget of the shared-memory path
+
+// shared-memory footprint of one node's ID: M (ny x nx) + nrm2 (nx) + v (ny) + piv, Xbar (2 nx ints)
+__host__ __device__ __forceinline__ int64_t id_smem_bytes(int ny, int nx) {
+  return 8LL * ((int64_t)ny * nx + nx + ny) + 8LL * nx;
+}
 
 // per node of one level: |Xbar| (and child offsets), workspace and U sizes
 __global__ void id_sizes_kernel(int base, int count, const int* __restrict__ is_leaf, const int* __restrict__ nbegin,
                                 const int* __restrict__ nend, const int* __restrict__ first_child,
                                 const int* __restrict__ nchild, const int* __restrict__ ys_cnt,
-                                const int* __restrict__ k, int* xbar_n, int* child_off, int64_t* wsz, int64_t* usz) {
+                                const int* __restrict__ k, int* xbar_n, int* child_off, int64_t* wsz, int64_t* usz,
+                                int* smax) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t > count) return;
   if (t == count) {
@@ -40,8 +48,10 @@ __global__ void id_sizes_kernel(int base, int count, const int* __restrict__ is_
   xbar_n[i] = nx;
   int mn = nx < ny ? nx : ny;
   // workspace: M (ny*nx doubles) + nrm2 (nx) + v (ny) + piv/xbar (2*nx ints, as doubles)
-  wsz[t] = nx > 0 ? (int64_t)ny * nx + nx + ny + nx + 2 : 0;
+  const bool fits = id_smem_bytes(ny, nx) <= kIdSmemMax;
+  wsz[t] = nx > 0 && !fits ? (int64_t)ny * nx + nx + ny + nx + 2 : 0;
   usz[t] = (int64_t)nx * mn;
+  if (nx > 0 && fits) atomicMax(smax, (int)id_smem_bytes(ny, nx));
 }
 
 __global__ void __launch_bounds__(kIdThreads) id_kernel(
@@ -60,6 +70,7 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
     if (tid == 0) kout[i] = 0;
     return;
   }
+  if (id_smem_bytes(ny, nx) <= kIdSmemMax) return;  // handled by id_kernel_smem
   double* M = work + woff[t];
   double* nrm2 = M + (int64_t)ny * nx;
   double* v = nrm2 + nx;
@@ -101,6 +112,58 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
   }
 }
 
+// shared-memory path: the whole block and the CPQR live in shared memory (cpqr.cuh, row-major)
+__global__ void __launch_bounds__(kIdSmemThreads) id_kernel_smem(
+    int base, int kid, double p2, double tol, const double* __restrict__ X, int64_t n, int d, int r,
+    const int* __restrict__ is_leaf, const int* __restrict__ nbegin, const int* __restrict__ first_child,
+    const int* __restrict__ nchild, const int* __restrict__ ys_cnt, const int* __restrict__ ys,
+    const int* __restrict__ xbar_n, const int64_t* __restrict__ uoff, double* U, int* kout, int* sk,
+    unsigned long long* evals) {
+  extern __shared__ double sh[];
+  __shared__ CpqrRmSmem<kIdSmemThreads> csm;
+  const int i = base + blockIdx.x;
+  const int nx = xbar_n[i];
+  const int ny = ys_cnt[i];
+  const int tid = threadIdx.x;
+  if (nx == 0 || id_smem_bytes(ny, nx) > kIdSmemMax) return;
+  double* M = sh;
+  double* nrm2 = M + (int64_t)ny * nx;
+  double* v = nrm2 + nx;
+  int* piv = reinterpret_cast<int*>(v + ny);
+  int* xb = piv + nx;
+  if (is_leaf[i]) {
+    for (int b = tid; b < nx; b += kIdSmemThreads) xb[b] = nbegin[i] + b;
+  } else {
+    int o = 0;
+    for (int c = 0; c < nchild[i]; c++) {
+      const int ch = first_child[i] + c;
+      const int kc = kout[ch];
+      for (int a = tid; a < kc; a += kIdSmemThreads) xb[o + a] = sk[(int64_t)ch * r + a];
+      o += kc;
+    }
+  }
+  __syncthreads();
+  // A^T row-major: M[a*nx + b] = K(Xbar[b], Y^*[a]), Y^* ascending
+  const int* yv = ys + (int64_t)i * r;
+  for (int e = tid; e < ny * nx; e += kIdSmemThreads) {
+    const int a = e / nx, b = e - a * nx;
+    M[e] = kernel_pts_d(kid, p2, X, n, d, xb[b], yv[a]);
+  }
+  __syncthreads();
+  const int k = cta_cpqr_rm<kIdSmemThreads>(M, ny, nx, nx, tol, piv, nrm2, v, csm);
+  double* Ui = U + uoff[blockIdx.x];
+  for (int a = tid; a < k; a += kIdSmemThreads) sk[(int64_t)i * r + a] = xb[piv[a]];
+  for (int e = tid; e < nx * k; e += kIdSmemThreads) {
+    const int c = e % nx, tt = e / nx;
+    const double val = c < k ? (c == tt ? 1.0 : 0.0) : M[tt * nx + c];
+    Ui[piv[c] + (int64_t)nx * tt] = val;
+  }
+  if (tid == 0) {
+    kout[i] = k;
+    atomicAdd(evals, (unsigned long long)nx * ny);
+  }
+}
+
 __global__ void uoff_scatter_kernel(int base, int count, const int64_t* __restrict__ off, int64_t shift,
                                     int64_t* u_off) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -133,18 +196,22 @@ void id_sweep(h2_handle* h) {
   for (int l = h->depth; l >= 1; l--) {
     int base = h->lvl_start[l], count = h->lvl_start[l + 1] - base;
     if (count == 0) continue;
-    Scratch sz(sizeof(int64_t) * 2 * (count + 1), s), off(sizeof(int64_t) * 2 * (count + 1), s);
+    Scratch sz(sizeof(int64_t) * 2 * (count + 1) + 16, s), off(sizeof(int64_t) * 2 * (count + 1), s);
+    int* smax = reinterpret_cast<int*>(sz.as<int64_t>() + 2 * (count + 1));
+    H2_CUDA_TRY(cudaMemsetAsync(smax, 0, sizeof(int), s));
     int64_t *wsz = sz.as<int64_t>(), *usz = wsz + count + 1;
     int64_t *woff = off.as<int64_t>(), *uo = woff + count + 1;
     id_sizes_kernel<<<(count + 1 + 255) / 256, 256, 0, s>>>(base, count, h->is_leaf, h->nbegin, h->nend,
                                                             h->first_child, h->nchild, h->ys_cnt, h->k, h->xbar_n,
-                                                            h->child_off, wsz, usz);
+                                                            h->child_off, wsz, usz, smax);
     scan_excl_i64(wsz, woff, count + 1, s);
     scan_excl_i64(usz, uo, count + 1, s);
     H2_CHECK_LAUNCH();
     int64_t tot[2];
+    int smem_bytes = 0;
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[0], woff + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[1], uo + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    H2_CUDA_TRY(cudaMemcpyAsync(&smem_bytes, smax, sizeof(int), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaStreamSynchronize(s));
     if (uused + tot[1] > ucap) {
       int64_t nc = uused + tot[1];
@@ -162,6 +229,18 @@ void id_sweep(h2_handle* h) {
                                            work.as<double>(), h->u_off + base, U, h->k, h->sk,
                                            ev.as<unsigned long long>());
     H2_CHECK_LAUNCH();
+    if (smem_bytes > 0) {
+      static bool attr_set = false;
+      if (!attr_set) {
+        H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kIdSmemMax));
+        attr_set = true;
+      }
+      id_kernel_smem<<<count, kIdSmemThreads, smem_bytes, s>>>(
+          base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child, h->nchild,
+          h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>());
+      H2_CHECK_LAUNCH();
+      h->gpu_launches += 1;
+    }
     h->gpu_launches += 5;
     uused += tot[1];  // u_off[] holds global offsets into the arena
   }
