@@ -285,7 +285,7 @@ def run_ours(args):
     fp64_peak = 148 * FP64_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic,
-                "kernel": "fill_kernel<D=2,MATERN32,NEARFIELD> (a10)", "kernel_ms": round(nf_ms, 3),
+                "kernel": "nf_fill_kernel<D=2,MATERN32> (a10, nearfield fill)", "kernel_ms": round(nf_ms, 3),
                 "step_share": round(nf_ms / t_step, 4),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650 GB/s",
                 "fp64_peak_tflops_at_sm_clock": round(fp64_peak, 2)}
@@ -320,7 +320,7 @@ def _rank_points(cfg, n, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=4)
