@@ -138,64 +138,75 @@ int calibrate(h2_handle* h) {
   int has[64];
   H2_CUDA_TRY(cudaMemcpyAsync(has, hasd.p, sizeof(int) * 64, cudaMemcpyDeviceToHost, s));
   H2_CUDA_TRY(cudaStreamSynchronize(s));
-  std::vector<double> wl;
-  std::vector<int> lv, mv;
-  for (int l = 0; l <= h->depth; l++) {
-    if (!has[l]) continue;
-    for (int m = 1;; m++) {
-      long long G = 1;
-      for (int c = 0; c < d; c++) G *= m;
-      wl.push_back(ldexp(h->W, -l));
-      lv.push_back(l);
-      mv.push_back(m);
-      if (G >= N) break;
-    }
-  }
+  // Trials in two phases: first every m with m^d <= 64 (cheap blocks) for all levels, then the
+  // larger m only for levels that have not passed yet.  The chosen m is the first passing one
+  // either way (the phases only avoid evaluating trials beyond it).
+  std::vector<int> levels;
+  for (int l = 0; l <= h->depth; l++)
+    if (has[l]) levels.push_back(l);
   int r = 1;
-  if (wl.empty()) return r;
+  if (levels.empty()) return r;
   const double p2 = kernel_p2(h->kid, h->kp);
-  const int T = (int)wl.size();
-  const int batch = 256;
-  std::vector<int> pass(T);
-  std::vector<double> errs(T);
-  Scratch work(sizeof(CalWork) * (T < batch ? T : batch), s);
-  Scratch params(sizeof(double) * T + sizeof(int) * 2 * T, s), outs(sizeof(double) * T + sizeof(int) * T, s);
-  double* dw = params.as<double>();
-  int* dl = reinterpret_cast<int*>(dw + T);
-  int* dm = dl + T;
-  double* derr = outs.as<double>();
-  int* dpass = reinterpret_cast<int*>(derr + T);
-  H2_CUDA_TRY(cudaMemcpyAsync(dw, wl.data(), sizeof(double) * T, cudaMemcpyHostToDevice, s));
-  H2_CUDA_TRY(cudaMemcpyAsync(dl, lv.data(), sizeof(int) * T, cudaMemcpyHostToDevice, s));
-  H2_CUDA_TRY(cudaMemcpyAsync(dm, mv.data(), sizeof(int) * T, cudaMemcpyHostToDevice, s));
-  for (int b0 = 0; b0 < T; b0 += batch) {
-    int nb = T - b0 < batch ? T - b0 : batch;
-    switch (d) {
+  auto Gof = [&](int m) {
+    long long G = 1;
+    for (int c = 0; c < d; c++) G *= m;
+    return G;
+  };
+  std::vector<int> chosen_m(levels.size(), 0);
+  for (int phase = 0; phase < 2; phase++) {
+    std::vector<double> wl;
+    std::vector<int> lv, mv, li;
+    for (size_t q = 0; q < levels.size(); q++) {
+      if (chosen_m[q]) continue;
+      for (int m = 1;; m++) {
+        const long long G = Gof(m);
+        const bool in_phase = phase == 0 ? (G <= 64 || m == 1) : (G > 64 || m == 1);
+        if (in_phase && !(phase == 1 && G <= 64)) {
+          wl.push_back(ldexp(h->W, -levels[q]));
+          lv.push_back(levels[q]);
+          mv.push_back(m);
+          li.push_back((int)q);
+        }
+        if (G >= N || (phase == 0 && G > 64)) break;
+      }
+    }
+    const int T = (int)wl.size();
+    if (T == 0) break;
+    const int batch = 256;
+    Scratch work(sizeof(CalWork) * (T < batch ? T : batch), s);
+    Scratch params(sizeof(double) * T + sizeof(int) * 2 * T, s), outs(sizeof(double) * T + sizeof(int) * T, s);
+    double* dw = params.as<double>();
+    int* dl = reinterpret_cast<int*>(dw + T);
+    int* dm = dl + T;
+    double* derr = outs.as<double>();
+    int* dpass = reinterpret_cast<int*>(derr + T);
+    H2_CUDA_TRY(cudaMemcpyAsync(dw, wl.data(), sizeof(double) * T, cudaMemcpyHostToDevice, s));
+    H2_CUDA_TRY(cudaMemcpyAsync(dl, lv.data(), sizeof(int) * T, cudaMemcpyHostToDevice, s));
+    H2_CUDA_TRY(cudaMemcpyAsync(dm, mv.data(), sizeof(int) * T, cudaMemcpyHostToDevice, s));
+    for (int b0 = 0; b0 < T; b0 += batch) {
+      int nb = T - b0 < batch ? T - b0 : batch;
+      switch (d) {
 #define H2_CAL_CASE(DD)                                                                                  \
   case DD:                                                                                               \
     calib_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, h->id_tol, h->tau, dw + b0, dl + b0, dm + b0, \
                                                 work.as<CalWork>(), derr + b0, dpass + b0);               \
     break;
-      H2_CAL_CASE(1) H2_CAL_CASE(2) H2_CAL_CASE(3) H2_CAL_CASE(4)
-      H2_CAL_CASE(5) H2_CAL_CASE(6) H2_CAL_CASE(7) H2_CAL_CASE(8)
+        H2_CAL_CASE(1) H2_CAL_CASE(2) H2_CAL_CASE(3) H2_CAL_CASE(4)
+        H2_CAL_CASE(5) H2_CAL_CASE(6) H2_CAL_CASE(7) H2_CAL_CASE(8)
 #undef H2_CAL_CASE
+      }
+      H2_CHECK_LAUNCH();
+      h->gpu_launches += 1;
     }
-    H2_CHECK_LAUNCH();
-    h->gpu_launches += 1;
+    std::vector<int> pass(T);
+    H2_CUDA_TRY(cudaMemcpyAsync(pass.data(), dpass, sizeof(int) * T, cudaMemcpyDeviceToHost, s));
+    H2_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int t = 0; t < T; t++)  // trials of a level are in increasing m: keep the first pass
+      if (pass[t] && (!chosen_m[li[t]] || mv[t] < chosen_m[li[t]])) chosen_m[li[t]] = mv[t];
   }
-  H2_CUDA_TRY(cudaMemcpyAsync(pass.data(), dpass, sizeof(int) * T, cudaMemcpyDeviceToHost, s));
-  H2_CUDA_TRY(cudaMemcpyAsync(errs.data(), derr, sizeof(double) * T, cudaMemcpyDeviceToHost, s));
-  H2_CUDA_TRY(cudaStreamSynchronize(s));
-  for (int t = 0; t < T;) {
-    int l = lv[t];
-    int chosen = -1;
-    int u = t;
-    for (; u < T && lv[u] == l; u++)
-      if (chosen < 0 && pass[u]) chosen = u;
-    long long G = 1;
-    for (int c = 0; c < d; c++) G *= mv[chosen];
+  for (size_t q = 0; q < levels.size(); q++) {
+    const long long G = Gof(chosen_m[q]);
     if (G > r) r = (int)G;
-    t = u;
   }
   return r;
 }

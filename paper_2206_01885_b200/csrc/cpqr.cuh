@@ -262,20 +262,38 @@ __device__ int cta_cpqr_rm(double* __restrict__ M, int ny, int nx, int ld, doubl
     __syncthreads();
     const double vtv = sm.vtv;
     for (int j = t + 1 + tid; j < nx; j += NT) {
-      double nn = 0.0;
+      // independent partial sums (4-way) break the serial FMA chains
+      double nn0 = 0.0, nn1 = 0.0;
       if (vtv > 0.0) {
-        double s = 0.0;
-        for (int i = t; i < ny; i++) s += v[i] * M[i * ld + j];
-        const double f = 2.0 * s / vtv;
-        for (int i = t; i < ny; i++) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int i = t;
+        for (; i + 3 < ny; i += 4) {
+          s0 += v[i] * M[i * ld + j];
+          s1 += v[i + 1] * M[(i + 1) * ld + j];
+          s2 += v[i + 2] * M[(i + 2) * ld + j];
+          s3 += v[i + 3] * M[(i + 3) * ld + j];
+        }
+        for (; i < ny; i++) s0 += v[i] * M[i * ld + j];
+        const double f = 2.0 * ((s0 + s1) + (s2 + s3)) / vtv;
+        const double a0 = M[t * ld + j] - f * v[t];  // row t joins R, not the residual norm
+        M[t * ld + j] = a0;
+        i = t + 1;
+        for (; i + 1 < ny; i += 2) {
+          const double a = M[i * ld + j] - f * v[i], b = M[(i + 1) * ld + j] - f * v[i + 1];
+          M[i * ld + j] = a;
+          M[(i + 1) * ld + j] = b;
+          nn0 += a * a;
+          nn1 += b * b;
+        }
+        for (; i < ny; i++) {
           const double a = M[i * ld + j] - f * v[i];
           M[i * ld + j] = a;
-          if (i > t) nn += a * a;
+          nn0 += a * a;
         }
       } else {
-        for (int i = t + 1; i < ny; i++) nn += M[i * ld + j] * M[i * ld + j];
+        for (int i = t + 1; i < ny; i++) nn0 += M[i * ld + j] * M[i * ld + j];
       }
-      nrm2[j] = nn;
+      nrm2[j] = nn0 + nn1;
     }
     k = t + 1;
     __syncthreads();

@@ -14,9 +14,13 @@ constexpr int kIdThreads = 256;
 constexpr int kIdSmemThreads = 128;
 constexpr int kIdSmemMax = 100 * 1024;  // dynamic shared memory budget of the shared-memory path
 
+// shared-memory size classes: nodes are launched per class so small nodes get high occupancy
+__host__ __device__ __forceinline__ int id_class(int64_t bytes) { return bytes <= 24576 ? 0 : (bytes <= 49152 ? 1 : 2); }
+
 // shared-memory footprint of one node's ID: M (ny x nx) + nrm2 (nx) + v (ny) + piv, Xbar (2 nx ints)
+// (+ staged coordinates of Xbar and Y^*: 8 (nx + ny) kMaxD bytes at most, + the exp table)
 __host__ __device__ __forceinline__ int64_t id_smem_bytes(int ny, int nx) {
-  return 8LL * ((int64_t)ny * nx + nx + ny) + 8LL * nx;
+  return 8LL * ((int64_t)ny * nx + nx + ny) + 8LL * nx + 8LL * kMaxD * (nx + ny) + 512;
 }
 
 // per node of one level: |Xbar| (and child offsets), workspace and U sizes
@@ -51,7 +55,7 @@ __global__ void id_sizes_kernel(int base, int count, const int* __restrict__ is_
   const bool fits = id_smem_bytes(ny, nx) <= kIdSmemMax;
   wsz[t] = nx > 0 && !fits ? (int64_t)ny * nx + nx + ny + nx + 2 : 0;
   usz[t] = (int64_t)nx * mn;
-  if (nx > 0 && fits) atomicMax(smax, (int)id_smem_bytes(ny, nx));
+  if (nx > 0 && fits) atomicMax(smax + id_class(id_smem_bytes(ny, nx)), (int)id_smem_bytes(ny, nx));
 }
 
 __global__ void __launch_bounds__(kIdThreads) id_kernel(
@@ -113,24 +117,29 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
 }
 
 // shared-memory path: the whole block and the CPQR live in shared memory (cpqr.cuh, row-major)
+template <int D>
 __global__ void __launch_bounds__(kIdSmemThreads) id_kernel_smem(
-    int base, int kid, double p2, double tol, const double* __restrict__ X, int64_t n, int d, int r,
+    int base, int kid, double p2, double tol, const double* __restrict__ X, int64_t n, int d_unused, int r,
     const int* __restrict__ is_leaf, const int* __restrict__ nbegin, const int* __restrict__ first_child,
     const int* __restrict__ nchild, const int* __restrict__ ys_cnt, const int* __restrict__ ys,
     const int* __restrict__ xbar_n, const int64_t* __restrict__ uoff, double* U, int* kout, int* sk,
-    unsigned long long* evals) {
+    unsigned long long* evals, int cls) {
   extern __shared__ double sh[];
   __shared__ CpqrRmSmem<kIdSmemThreads> csm;
   const int i = base + blockIdx.x;
   const int nx = xbar_n[i];
   const int ny = ys_cnt[i];
   const int tid = threadIdx.x;
-  if (nx == 0 || id_smem_bytes(ny, nx) > kIdSmemMax) return;
+  if (nx == 0 || id_smem_bytes(ny, nx) > kIdSmemMax || id_class(id_smem_bytes(ny, nx)) != cls) return;
   double* M = sh;
   double* nrm2 = M + (int64_t)ny * nx;
   double* v = nrm2 + nx;
-  int* piv = reinterpret_cast<int*>(v + ny);
+  double* cx = v + ny;           // Xbar coordinates, [c * nx + b]
+  double* cy = cx + D * nx;      // Y^* coordinates, [c * ny + a]
+  double* tab = cy + D * ny;     // exp table
+  int* piv = reinterpret_cast<int*>(tab + 64);
   int* xb = piv + nx;
+  if (tid < 64) tab[tid] = kExp2Tab64[tid];
   if (is_leaf[i]) {
     for (int b = tid; b < nx; b += kIdSmemThreads) xb[b] = nbegin[i] + b;
   } else {
@@ -142,12 +151,30 @@ __global__ void __launch_bounds__(kIdSmemThreads) id_kernel_smem(
       o += kc;
     }
   }
-  __syncthreads();
-  // A^T row-major: M[a*nx + b] = K(Xbar[b], Y^*[a]), Y^* ascending
   const int* yv = ys + (int64_t)i * r;
-  for (int e = tid; e < ny * nx; e += kIdSmemThreads) {
-    const int a = e / nx, b = e - a * nx;
-    M[e] = kernel_pts_d(kid, p2, X, n, d, xb[b], yv[a]);
+  for (int a = tid; a < ny; a += kIdSmemThreads)
+#pragma unroll
+    for (int c = 0; c < D; c++) cy[c * ny + a] = X[c * n + yv[a]];
+  __syncthreads();
+  for (int b = tid; b < nx; b += kIdSmemThreads)
+#pragma unroll
+    for (int c = 0; c < D; c++) cx[c * nx + b] = X[c * n + xb[b]];
+  __syncthreads();
+  // A^T row-major: M[a*nx + b] = K(Xbar[b], Y^*[a]), Y^* ascending; thread per column b, the
+  // column's point in registers, rows' points broadcast from shared memory
+  for (int b = tid; b < nx; b += kIdSmemThreads) {
+    double xr[D];
+#pragma unroll
+    for (int c = 0; c < D; c++) xr[c] = cx[c * nx + b];
+    for (int a = 0; a < ny; a++) {
+      double sq = 0.0;
+#pragma unroll
+      for (int c = 0; c < D; c++) {
+        const double df = xr[c] - cy[c * ny + a];
+        sq = fma(df, df, sq);
+      }
+      M[a * nx + b] = kernel_s(kid, p2, sq, tab);
+    }
   }
   __syncthreads();
   const int k = cta_cpqr_rm<kIdSmemThreads>(M, ny, nx, nx, tol, piv, nrm2, v, csm);
@@ -197,8 +224,8 @@ void id_sweep(h2_handle* h) {
     int base = h->lvl_start[l], count = h->lvl_start[l + 1] - base;
     if (count == 0) continue;
     Scratch sz(sizeof(int64_t) * 2 * (count + 1) + 16, s), off(sizeof(int64_t) * 2 * (count + 1), s);
-    int* smax = reinterpret_cast<int*>(sz.as<int64_t>() + 2 * (count + 1));
-    H2_CUDA_TRY(cudaMemsetAsync(smax, 0, sizeof(int), s));
+    int* smax = reinterpret_cast<int*>(sz.as<int64_t>() + 2 * (count + 1));  // one max per class
+    H2_CUDA_TRY(cudaMemsetAsync(smax, 0, 3 * sizeof(int), s));
     int64_t *wsz = sz.as<int64_t>(), *usz = wsz + count + 1;
     int64_t *woff = off.as<int64_t>(), *uo = woff + count + 1;
     id_sizes_kernel<<<(count + 1 + 255) / 256, 256, 0, s>>>(base, count, h->is_leaf, h->nbegin, h->nend,
@@ -208,10 +235,10 @@ void id_sweep(h2_handle* h) {
     scan_excl_i64(usz, uo, count + 1, s);
     H2_CHECK_LAUNCH();
     int64_t tot[2];
-    int smem_bytes = 0;
+    int smem_bytes[3] = {0, 0, 0};
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[0], woff + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[1], uo + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    H2_CUDA_TRY(cudaMemcpyAsync(&smem_bytes, smax, sizeof(int), cudaMemcpyDeviceToHost, s));
+    H2_CUDA_TRY(cudaMemcpyAsync(smem_bytes, smax, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaStreamSynchronize(s));
     if (uused + tot[1] > ucap) {
       int64_t nc = uused + tot[1];
@@ -229,15 +256,25 @@ void id_sweep(h2_handle* h) {
                                            work.as<double>(), h->u_off + base, U, h->k, h->sk,
                                            ev.as<unsigned long long>());
     H2_CHECK_LAUNCH();
-    if (smem_bytes > 0) {
-      static bool attr_set = false;
-      if (!attr_set) {
-        H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kIdSmemMax));
-        attr_set = true;
+    for (int cls = 0; cls < 3; cls++) {
+      if (smem_bytes[cls] == 0) continue;
+      switch (h->d) {
+#define H2_ID_CASE(DD)                                                                                        \
+  case DD: {                                                                                                  \
+    static bool attr_set = false;                                                                             \
+    if (!attr_set) {                                                                                          \
+      H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_smem<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                       kIdSmemMax));                                                          \
+      attr_set = true;                                                                                        \
+    }                                                                                                         \
+    id_kernel_smem<DD><<<count, kIdSmemThreads, smem_bytes[cls], s>>>(                                        \
+        base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child, h->nchild, \
+        h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>(), cls);       \
+  } break;
+        H2_ID_CASE(1) H2_ID_CASE(2) H2_ID_CASE(3) H2_ID_CASE(4)
+        H2_ID_CASE(5) H2_ID_CASE(6) H2_ID_CASE(7) H2_ID_CASE(8)
+#undef H2_ID_CASE
       }
-      id_kernel_smem<<<count, kIdSmemThreads, smem_bytes, s>>>(
-          base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child, h->nchild,
-          h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>());
       H2_CHECK_LAUNCH();
       h->gpu_launches += 1;
     }
