@@ -93,6 +93,8 @@ typedef struct h2_options {
   void* stream;            /* cudaStream_t for all work; NULL = legacy default stream               */
   int32_t points_on_host;  /* 1: `points` is a HOST pointer; the H2D copy is part of the call       */
   int32_t timing;          /* 1: record per-stage CUDA-event times (h2_info stage_ms)               */
+  int32_t hidr_brute;      /* 1: brute-force top-down Vol instead of the pruned exact kernel (same  */
+                           /*    result bit for bit; for A/B checks)                                */
 } h2_options;
 
 /* h2_options with the defaults listed above (r calibrated, AUTO, whole-device budget, timing off) */
@@ -135,6 +137,7 @@ typedef struct h2_info_t {
    * [2] calibration a5, [3] HiDR up a6, [4] HiDR down a7, [5] ID sweep a8, [6] coupling fill a9,
    * [7] nearfield fill a10, [8] whole build                                                     */
   float stage_ms[9];
+  int64_t hidr_dist_done;                    /* distances the pruned top-down Vol evaluated        */
 } h2_info_t;
 
 int h2_info(const h2_handle* h, h2_info_t* out);

@@ -31,7 +31,8 @@ EXPORTED_SYMBOLS = ["h2_build", "h2_build_ex", "h2_options_default", "h2_matvec"
 
 class h2_options(C.Structure):
     _fields_ = [("r_override", C.c_int32), ("storage", C.c_int32), ("mem_budget_bytes", C.c_int64),
-                ("stream", C.c_void_p), ("points_on_host", C.c_int32), ("timing", C.c_int32)]
+                ("stream", C.c_void_p), ("points_on_host", C.c_int32), ("timing", C.c_int32),
+                ("hidr_brute", C.c_int32)]
 
 
 class h2_info_t(C.Structure):
@@ -40,7 +41,7 @@ class h2_info_t(C.Structure):
                 ("n_nf", C.c_int64), ("coupling_entries", C.c_int64), ("nearfield_entries", C.c_int64),
                 ("stored_bytes", C.c_int64), ("coupling_stored", C.c_int32), ("nearfield_stored", C.c_int32),
                 ("hidr_dist_evals", C.c_int64), ("id_kernel_evals", C.c_int64), ("kmax", C.c_int32),
-                ("gpu_launches", C.c_int32), ("stage_ms", C.c_float * 9)]
+                ("gpu_launches", C.c_int32), ("stage_ms", C.c_float * 9), ("hidr_dist_done", C.c_int64)]
 
 
 STAGES = ["tree", "lists", "calibrate", "hidr_up", "hidr_down", "id_sweep", "coupling_fill", "nearfield_fill",
@@ -162,9 +163,10 @@ class H2Matrix:
 
     def __init__(self, points, kernel_id: int, kernel_params=(), id_tol: float = 1e-6, leaf_size: int = 64,
                  admissibility: float = 0.5, r: int = 0, storage: int = H2_STORE_AUTO, stream=None,
-                 timing: bool = False, mem_budget_bytes: int = 0):
+                 timing: bool = False, mem_budget_bytes: int = 0, hidr_brute: bool = False):
         import torch
         o = h2_options_default()
+        o.hidr_brute = int(bool(hidr_brute))
         o.r_override = int(r)
         o.storage = int(storage)
         o.timing = int(bool(timing))

@@ -85,6 +85,7 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
   h->tau = admissibility;
   h->stream = static_cast<cudaStream_t>(o.stream);
   h->timing = o.timing;
+  h->hidr_prune = o.hidr_brute ? 0 : 1;
   cudaEvent_t ev[8];
   int nev = 0;
   try {
@@ -184,6 +185,7 @@ int h2_info(const h2_handle* h, h2_info_t* out) {
   out->coupling_stored = h->cp_stored;
   out->nearfield_stored = h->np_stored;
   out->hidr_dist_evals = h->hidr_dist_evals;
+  out->hidr_dist_done = h->hidr_dist_done;
   out->id_kernel_evals = h->id_kernel_evals;
   out->kmax = h->kmax;
   out->gpu_launches = h->gpu_launches;

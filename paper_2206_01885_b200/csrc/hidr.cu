@@ -6,7 +6,7 @@
 // Level-synchronous: per level, (1) a size kernel, (2) an exclusive scan, (3) a gather kernel
 // writing every node's S_i / T_i index list contiguously (the union is disjoint by the tiling of
 // the block partition, so it is a concatenation), (4) one CTA per node runs Vol.
-#include "vol.cuh"
+#include "hidr_down.cuh"
 
 namespace h2 {
 
@@ -120,6 +120,48 @@ static void launch_vol(int d, unsigned grid, cudaStream_t s, const double* X, in
   }
 }
 
+static void launch_sel_box(h2_handle* h, int base, int count, const int* cnt, const int* slots, double* box) {
+  const unsigned grid = (unsigned)((count * 32LL + 255) / 256);
+  switch (h->d) {
+#define H2_BOX_CASE(DD) \
+  case DD: sel_box_kernel<DD><<<grid, 256, 0, h->stream>>>(base, count, cnt, slots, h->r, h->X, h->n, box); break;
+    H2_BOX_CASE(1) H2_BOX_CASE(2) H2_BOX_CASE(3) H2_BOX_CASE(4)
+    H2_BOX_CASE(5) H2_BOX_CASE(6) H2_BOX_CASE(7) H2_BOX_CASE(8)
+#undef H2_BOX_CASE
+  }
+  H2_CHECK_LAUNCH();
+  h->gpu_launches += 1;
+}
+
+// pruned down level; false when the group boxes do not fit shared memory (brute-force path then)
+static bool hidr_down_level_pruned(h2_handle* h, int l, unsigned long long* ev, unsigned long long* ev_done) {
+  const int base = h->lvl_start[l], count = h->lvl_start[l + 1] - base;
+  const int ngmax = (h->csp + 1 + 31) / 32;
+  const size_t smem = sizeof(double) * 2 * h->d * (size_t)ngmax;
+  if (smem > (size_t)kDownSmemMax) return false;
+  cudaStream_t s = h->stream;
+  switch (h->d) {
+#define H2_DOWN_CASE(DD)                                                                                         \
+  case DD: {                                                                                                     \
+    static bool attr = false;                                                                                    \
+    if (!attr) {                                                                                                 \
+      H2_CUDA_TRY(cudaFuncSetAttribute(hidr_down_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                                       kDownSmemMax));                                                           \
+      attr = true;                                                                                               \
+    }                                                                                                            \
+    hidr_down_kernel<DD><<<count, kDownThreads, smem, s>>>(h->X, h->n, base, h->r, h->parent, h->il_off,           \
+                                                           h->il_idx, h->xs_cnt, h->xs, h->xbox, h->ybox,        \
+                                                           h->ys_cnt, h->ys, ev, ev_done);                       \
+  } break;
+    H2_DOWN_CASE(1) H2_DOWN_CASE(2) H2_DOWN_CASE(3) H2_DOWN_CASE(4)
+    H2_DOWN_CASE(5) H2_DOWN_CASE(6) H2_DOWN_CASE(7) H2_DOWN_CASE(8)
+#undef H2_DOWN_CASE
+  }
+  H2_CHECK_LAUNCH();
+  h->gpu_launches += 1;
+  return true;
+}
+
 static void hidr_level(h2_handle* h, int mode, int l, unsigned long long* ev) {
   cudaStream_t s = h->stream;
   int base = h->lvl_start[l], count = h->lvl_start[l + 1] - base;
@@ -140,6 +182,8 @@ static void hidr_level(h2_handle* h, int mode, int l, unsigned long long* ev) {
              mode == 0 ? h->xs_cnt : h->ys_cnt, mode == 0 ? h->xs : h->ys, ev);
   H2_CHECK_LAUNCH();
   h->gpu_launches += 4;
+  if (mode == 0) launch_sel_box(h, base, count, h->xs_cnt, h->xs, h->xbox);
+  else launch_sel_box(h, base, count, h->ys_cnt, h->ys, h->ybox);
 }
 
 void hidr_up(h2_handle* h) {
@@ -148,6 +192,8 @@ void hidr_up(h2_handle* h) {
   h->xs = halloc<int>(h, (size_t)h->nnodes * h->r);
   h->ys_cnt = halloc<int>(h, h->nnodes);
   h->ys = halloc<int>(h, (size_t)h->nnodes * h->r);
+  h->xbox = halloc<double>(h, (size_t)h->nnodes * kBox);
+  h->ybox = halloc<double>(h, (size_t)h->nnodes * kBox);
   H2_CUDA_TRY(cudaMemsetAsync(h->ys_cnt, 0, sizeof(int) * h->nnodes, h->stream));
   Scratch ev(sizeof(unsigned long long), h->stream);
   H2_CUDA_TRY(cudaMemsetAsync(ev.p, 0, sizeof(unsigned long long), h->stream));
@@ -158,8 +204,20 @@ void hidr_up(h2_handle* h) {
 void hidr_down(h2_handle* h) {
   Scratch ev(sizeof(unsigned long long), h->stream);
   H2_CUDA_TRY(cudaMemsetAsync(ev.p, 0, sizeof(unsigned long long), h->stream));
-  for (int l = 1; l <= h->depth; l++) hidr_level(h, 1, l, ev.as<unsigned long long>());
+  Scratch evd(sizeof(unsigned long long), h->stream);
+  H2_CUDA_TRY(cudaMemsetAsync(evd.p, 0, sizeof(unsigned long long), h->stream));
+  // the root's Y^* is empty (reading D1): its box is the empty box
+  launch_sel_box(h, 0, 1, h->ys_cnt, h->ys, h->ybox);
+  for (int l = 1; l <= h->depth; l++) {
+    const int base = h->lvl_start[l], count = h->lvl_start[l + 1] - base;
+    if (count == 0) continue;
+    if (h->hidr_prune && hidr_down_level_pruned(h, l, ev.as<unsigned long long>(), evd.as<unsigned long long>()))
+      launch_sel_box(h, base, count, h->ys_cnt, h->ys, h->ybox);
+    else
+      hidr_level(h, 1, l, ev.as<unsigned long long>());
+  }
   h->hidr_dist_evals += (int64_t)read1(ev.as<unsigned long long>(), h->stream);
+  h->hidr_dist_done = (int64_t)read1(evd.as<unsigned long long>(), h->stream);
 }
 
 }  // namespace h2

@@ -1,0 +1,352 @@
+// hidr_down.cuh -- selection boxes and the pruned exact top-down Vol of HiDR (a7; Algorithm 1
+// lines 14-21; Vol as in vol.cuh, readings C2-C5).  Included by hidr.cu.
+#pragma once
+#include "vol.cuh"
+
+namespace h2 {
+
+// ------------------------------------------------------------------------------------------
+// Selection boxes: the tight bounding box of every node's X_i^* (after its up level) and Y_i^*
+// (after its down level): box[i * kBox + c] = lo_c, box[i * kBox + kMaxD + c] = hi_c; an empty
+// selection gets lo = +inf, hi = -inf.  One warp per node.  min / max are exact, so the union of
+// the segment boxes is the bounding box of T_i bit for bit.
+// ------------------------------------------------------------------------------------------
+constexpr int kBox = 2 * kMaxD;
+
+template <int D>
+__global__ void sel_box_kernel(int base, int count, const int* __restrict__ cnt, const int* __restrict__ slots, int r,
+                               const double* __restrict__ X, int64_t n, double* __restrict__ box) {
+  const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (w >= count) return;
+  const int i = base + w;
+  const int c = cnt[i];
+  double lo[D], hi[D];
+#pragma unroll
+  for (int k = 0; k < D; k++) {
+    lo[k] = INFINITY;
+    hi[k] = -INFINITY;
+  }
+  for (int a = lane; a < c; a += 32) {
+    const int idx = slots[(int64_t)i * r + a];
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+      const double v = X[k * n + idx];
+      lo[k] = fmin(lo[k], v);
+      hi[k] = fmax(hi[k], v);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < D; k++)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[k] = fmin(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+      hi[k] = fmax(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+    }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+      box[(int64_t)i * kBox + k] = lo[k];
+      box[(int64_t)i * kBox + kMaxD + k] = hi[k];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Pruned exact top-down Vol.  Same result as the brute-force argmin of cta_vol, bit for bit.
+// T_i is the union of segments -- Y_p^* and X_j^* for j in IL(i) -- whose bounding boxes are
+// known.  For a grid node q and a box B, with the operations of the point distance
+// s(x) = sum_c fl(fl(x_c - q_c)^2) (each rounded separately, summed in c order):
+//   lb(q,B) = that expression on g_c = max(0, fl(lo_c - q_c), fl(q_c - hi_c))  <=  s(x),  x in B
+//   ub(q,B) = that expression on g_c = max(fl(hi_c - q_c), fl(q_c - lo_c))     >=  s(x),  x in B
+// because rounding to nearest is monotone and odd (fl(x - q) = -fl(q - x)).  A segment is
+// skipped only when lb > delta, delta an upper bound of the best s found so far (an evaluated s
+// or the ub of a non-empty box), so the minimiser and every tie with it are always evaluated;
+// ties go to the lowest index (reading C4) as in the brute-force kernel.
+// Segments are grouped 32 at a time (one per lane); the group boxes live in shared memory.
+// One CTA per node, one warp per grid node.
+// ------------------------------------------------------------------------------------------
+constexpr int kDownThreads = 256;
+constexpr int kDownWarps = kDownThreads / 32;
+constexpr int kDownSmemMax = 96 * 1024;
+
+template <int D>
+__device__ __forceinline__ double box_lb(const double* q, const double* lo, const double* hi) {
+  double g = fmax(fmax(__dsub_rn(lo[0], q[0]), __dsub_rn(q[0], hi[0])), 0.0);
+  double s = __dmul_rn(g, g);
+#pragma unroll
+  for (int c = 1; c < D; c++) {
+    g = fmax(fmax(__dsub_rn(lo[c], q[c]), __dsub_rn(q[c], hi[c])), 0.0);
+    s = __dadd_rn(s, __dmul_rn(g, g));
+  }
+  return s;
+}
+
+template <int D>
+__device__ __forceinline__ double box_ub(const double* q, const double* lo, const double* hi) {
+  double g = fmax(__dsub_rn(hi[0], q[0]), __dsub_rn(q[0], lo[0]));
+  double s = __dmul_rn(g, g);
+#pragma unroll
+  for (int c = 1; c < D; c++) {
+    g = fmax(__dsub_rn(hi[c], q[c]), __dsub_rn(q[c], lo[c]));
+    s = __dadd_rn(s, __dmul_rn(g, g));
+  }
+  return s;
+}
+
+__device__ __forceinline__ double warp_min_d(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kDownThreads) hidr_down_kernel(
+    const double* __restrict__ X, int64_t n, int base, int r, const int* __restrict__ parent,
+    const int64_t* __restrict__ il_off, const int* __restrict__ il_idx, const int* __restrict__ xs_cnt,
+    const int* __restrict__ xs, const double* __restrict__ xbox, const double* __restrict__ ybox, int* ys_cnt,
+    int* ys, unsigned long long* evals_alg, unsigned long long* evals_done) {
+  extern __shared__ double gbox[];  // group g: lo at gbox[g*2D + c], hi at gbox[g*2D + D + c]
+  __shared__ int sel[kVolSelCap];
+  __shared__ typename cub::BlockScan<int, kDownThreads>::TempStorage scan;
+  __shared__ double wlo[D][kDownWarps], whi[D][kDownWarps];
+  __shared__ long long wcnt[kDownWarps];
+  __shared__ double s_lo[D], s_hi[D], s_h[D];
+  __shared__ long long s_tot;
+  __shared__ int s_fill;
+  const int i = base + blockIdx.x, p = parent[i];
+  const int64_t e0 = il_off[i];
+  const int nseg = 1 + (int)(il_off[i + 1] - e0);
+  const int ng = (nseg + 31) >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+  int* out = ys + (int64_t)i * r;
+  const int* yp = ys + (int64_t)p * r;
+  // segment s: 0 = Y_p^*, s >= 1 = X_j^* of the (s-1)-th entry of IL(i)
+  auto seg_node = [&](int s) { return s == 0 ? p : il_idx[e0 + s - 1]; };
+  auto seg_cnt = [&](int s, int nd) { return s == 0 ? ys_cnt[nd] : xs_cnt[nd]; };
+  auto seg_box = [&](int s, int nd) { return (s == 0 ? ybox : xbox) + (int64_t)nd * kBox; };
+  auto seg_slots = [&](int s, int nd) { return s == 0 ? yp : xs + (int64_t)nd * r; };
+
+  // 1. group boxes, bbox(T_i), |T_i|
+  double tlo[D], thi[D];
+#pragma unroll
+  for (int c = 0; c < D; c++) {
+    tlo[c] = INFINITY;
+    thi[c] = -INFINITY;
+  }
+  long long tcnt = 0;
+  for (int g = warp; g < ng; g += kDownWarps) {
+    const int s = g * 32 + lane;
+    double blo[D], bhi[D];
+#pragma unroll
+    for (int c = 0; c < D; c++) {
+      blo[c] = INFINITY;
+      bhi[c] = -INFINITY;
+    }
+    int cnt = 0;
+    if (s < nseg) {
+      const int nd = seg_node(s);
+      cnt = seg_cnt(s, nd);
+      if (cnt > 0) {
+        const double* b = seg_box(s, nd);
+#pragma unroll
+        for (int c = 0; c < D; c++) {
+          blo[c] = b[c];
+          bhi[c] = b[kMaxD + c];
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < D; c++)
+      for (int o = 16; o > 0; o >>= 1) {
+        blo[c] = fmin(blo[c], __shfl_xor_sync(0xffffffffu, blo[c], o));
+        bhi[c] = fmax(bhi[c], __shfl_xor_sync(0xffffffffu, bhi[c], o));
+      }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < D; c++) {
+        gbox[g * 2 * D + c] = blo[c];
+        gbox[g * 2 * D + D + c] = bhi[c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < D; c++) {
+      tlo[c] = fmin(tlo[c], blo[c]);
+      thi[c] = fmax(thi[c], bhi[c]);
+    }
+    tcnt += cnt;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < D; c++) {
+      wlo[c][warp] = tlo[c];
+      whi[c][warp] = thi[c];
+    }
+    wcnt[warp] = tcnt;
+  }
+  if (tid == 0) s_fill = 0;
+  __syncthreads();
+  if (tid == 0) {
+    long long t = 0;
+    for (int w = 0; w < kDownWarps; w++) t += wcnt[w];
+    s_tot = t;
+  }
+  if (tid < D) {
+    double a = INFINITY, b = -INFINITY;
+    for (int w = 0; w < kDownWarps; w++) {
+      a = fmin(a, wlo[tid][w]);
+      b = fmax(b, whi[tid][w]);
+    }
+    s_lo[tid] = a;
+    s_hi[tid] = b;
+  }
+  __syncthreads();
+  const long long tot = s_tot;
+  if (tot == 0) {
+    if (tid == 0) ys_cnt[i] = 0;
+    return;
+  }
+  if (tot <= r) {  // pass-through (reading C5): gather, sort, de-duplicate
+    for (int s = tid; s < nseg; s += kDownThreads) {
+      const int nd = seg_node(s);
+      const int cnt = seg_cnt(s, nd);
+      if (cnt > 0) {
+        const int pos = atomicAdd(&s_fill, cnt);
+        const int* src = seg_slots(s, nd);
+        for (int a = 0; a < cnt; a++) sel[pos + a] = src[a];
+      }
+    }
+    __syncthreads();
+    const int c = cta_sort_unique_write<kDownThreads>(scan, sel, (int)tot, out);
+    if (tid == 0) ys_cnt[i] = c;
+    return;
+  }
+  // 2. the grid: the same arithmetic as cta_vol
+  int m = 1;
+  for (;;) {
+    long long pw = 1;
+    for (int c = 0; c < D; c++) pw *= (m + 1);
+    if (pw > r) break;
+    m++;
+  }
+  int G = 1;
+  for (int c = 0; c < D; c++) G *= m;
+  if (tid < D) s_h[tid] = __ddiv_rn(__dsub_rn(s_hi[tid], s_lo[tid]), (double)m);
+  __syncthreads();
+  // 3. one warp per grid node
+  unsigned long long done = 0;
+  for (int g = warp; g < G; g += kDownWarps) {
+    double q[D];
+    {
+      int rem = g;
+#pragma unroll
+      for (int c = 0; c < D; c++) {
+        const int j = rem % m;
+        rem /= m;
+        q[c] = __dadd_rn(s_lo[c], __dmul_rn((double)j + 0.5, s_h[c]));
+      }
+    }
+    // pass A: delta = min over the non-empty groups of ub; g0 = a group attaining it
+    double dl = INFINITY;
+    int g0 = -1;
+    for (int gg = lane; gg < ng; gg += 32) {
+      const double* b = gbox + gg * 2 * D;
+      if (b[0] <= b[D]) {
+        const double u = box_ub<D>(q, b, b + D);
+        if (u < dl) {
+          dl = u;
+          g0 = gg;
+        }
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, dl, o);
+      const int og = __shfl_xor_sync(0xffffffffu, g0, o);
+      if (od < dl || (od == dl && og > g0)) {  // any attaining group will do; make it uniform
+        dl = od;
+        g0 = og;
+      }
+    }
+    double best = INFINITY;
+    int bi = INT_MAX;
+    auto process_group = [&](int gg) {
+      const int s = gg * 32 + lane;
+      int nd = 0, cnt = 0;
+      double lbs = INFINITY, u = INFINITY;
+      if (s < nseg) {
+        nd = seg_node(s);
+        cnt = seg_cnt(s, nd);
+        if (cnt > 0) {
+          const double* b = seg_box(s, nd);
+          double blo[D], bhi[D];
+#pragma unroll
+          for (int c = 0; c < D; c++) {
+            blo[c] = b[c];
+            bhi[c] = b[kMaxD + c];
+          }
+          lbs = box_lb<D>(q, blo, bhi);
+          u = box_ub<D>(q, blo, bhi);
+        }
+      }
+      dl = fmin(dl, warp_min_d(u));
+      unsigned mask = __ballot_sync(0xffffffffu, cnt > 0 && lbs <= dl);
+      while (mask) {
+        const int t = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const double lbt = __shfl_sync(0xffffffffu, lbs, t);
+        const int ct = __shfl_sync(0xffffffffu, cnt, t);
+        const int ndt = __shfl_sync(0xffffffffu, nd, t);
+        if (lbt > dl) continue;  // uniform
+        const int* sl = seg_slots(gg * 32 + t, ndt);
+        for (int a = lane; a < ct; a += 32) {
+          const int idx = sl[a];
+          double df = __dsub_rn(X[idx], q[0]);
+          double sd = __dmul_rn(df, df);
+#pragma unroll
+          for (int c = 1; c < D; c++) {
+            df = __dsub_rn(X[c * n + idx], q[c]);
+            sd = __dadd_rn(sd, __dmul_rn(df, df));
+          }
+          if (sd < best || (sd == best && idx < bi)) {
+            best = sd;
+            bi = idx;
+          }
+        }
+        done += (unsigned long long)ct;
+        dl = fmin(dl, warp_min_d(best));
+      }
+    };
+    if (g0 >= 0) process_group(g0);
+    for (int gg0 = 0; gg0 < ng; gg0 += 32) {
+      const int gg = gg0 + lane;
+      bool cand = false;
+      if (gg < ng && gg != g0) {
+        const double* b = gbox + gg * 2 * D;
+        cand = box_lb<D>(q, b, b + D) <= dl;
+      }
+      unsigned mask = __ballot_sync(0xffffffffu, cand);
+      while (mask) {
+        const int t = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const double* b = gbox + (gg0 + t) * 2 * D;
+        if (box_lb<D>(q, b, b + D) <= dl) process_group(gg0 + t);  // uniform
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob < best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (lane == 0) out[g] = bi;  // parked in the output slot (capacity r >= G)
+  }
+  if (lane == 0 && evals_done) atomicAdd(evals_done, done);
+  if (tid == 0 && evals_alg) atomicAdd(evals_alg, (unsigned long long)G * (unsigned long long)tot);
+  __syncthreads();
+  for (int g = tid; g < G; g += kDownThreads) sel[g] = out[g];
+  __syncthreads();
+  const int c = cta_sort_unique_write<kDownThreads>(scan, sel, G, out);
+  if (tid == 0) ys_cnt[i] = c;
+}
+
+}  // namespace h2

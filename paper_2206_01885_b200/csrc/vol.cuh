@@ -63,8 +63,9 @@ __device__ void cta_bitonic(int* a, int P) {
 // sort sel[0..cnt) and write the distinct values to out; returns the distinct count.
 // cnt <= 64: warp 0 sorts two keys per lane with shuffles and compacts with ballots (no CTA
 // barrier inside); larger: CTA bitonic sort + block-scan compaction.
-template <int D, int NT>
-__device__ int cta_sort_unique_write(VolSmem<D, NT>& sm, int* sel, int cnt, int* out) {
+template <int NT>
+__device__ int cta_sort_unique_write(typename cub::BlockScan<int, NT>::TempStorage& scan, int* sel, int cnt,
+                                     int* out) {
   __shared__ int s_cnt;
   if (cnt <= 64) {
     if (threadIdx.x < 32) {
@@ -116,7 +117,7 @@ __device__ int cta_sort_unique_write(VolSmem<D, NT>& sm, int* sel, int cnt, int*
     int i = c0 + threadIdx.x;
     int keep = (i < cnt) && (i == 0 || sel[i] != sel[i - 1]);
     int pos, agg;
-    cub::BlockScan<int, NT>(sm.scan).ExclusiveSum(keep, pos, agg);
+    cub::BlockScan<int, NT>(scan).ExclusiveSum(keep, pos, agg);
     if (keep) out[base + pos] = sel[i];
     base += agg;
     __syncthreads();
@@ -135,7 +136,7 @@ __device__ int cta_vol(const Acc& acc, int ns, int k, int* out, VolSmem<D, NT>& 
   if (ns <= k) {
     for (int i = tid; i < ns; i += NT) sm.u.out.sel[i] = acc.index(i);
     __syncthreads();
-    return cta_sort_unique_write<D, NT>(sm, sm.u.out.sel, ns, out);
+    return cta_sort_unique_write<NT>(sm.scan, sm.u.out.sel, ns, out);
   }
   int m = 1;
   for (;;) {
@@ -298,7 +299,7 @@ __device__ int cta_vol(const Acc& acc, int ns, int k, int* out, VolSmem<D, NT>& 
   int* sel = sm.u.out.sel;
   for (int g = tid; g < G; g += NT) sel[g] = out[g];
   __syncthreads();
-  return cta_sort_unique_write<D, NT>(sm, sel, G, out);
+  return cta_sort_unique_write<NT>(sm.scan, sel, G, out);
 }
 
 }  // namespace h2

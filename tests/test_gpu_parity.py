@@ -224,3 +224,40 @@ def test_parity_bench_config_full_size():
     print(f"full cfg4: err_gpu={eg:.3e} err_oracle={eo:.3e}")
     assert eg <= 2.0 * eo + 1e-15
     assert np.linalg.norm(yg - yo) / np.linalg.norm(yo) <= 10 * c["id_tol"]
+
+
+@pytest.mark.parametrize("cfg,n,q", [(1, 8192, None), (2, 262144, None), (3, 262144, None), (4, 1 << 20, None),
+                                     (5, 65536, None)])
+def test_pruned_down_equals_brute_force(cfg, n, q):
+    """a7: the pruned exact top-down Vol (hidr_down.cuh) selects exactly the brute-force argmin
+    set Y_i^* on every node (bit-exact indices), at sizes well beyond the oracle's reach."""
+    c = synth.CONFIGS[cfg]
+    pts = synth.points(cfg, n)
+    kp = list(c["params"])
+    a = gpu_build(pts, c["kernel"], kp, c["id_tol"], q or c["q"], c["tau"], storage=P.H2_STORE_ON_THE_FLY)
+    X = torch.from_numpy(np.ascontiguousarray(pts)).cuda()
+    b = P.H2Matrix(X, c["kernel"], kp, c["id_tol"], q or c["q"], c["tau"], storage=P.H2_STORE_ON_THE_FLY,
+                   timing=True, hidr_brute=True)
+    for name in ("XS_OFF", "XS_IDX", "YS_OFF", "YS_IDX"):
+        assert np.array_equal(a.export(name), b.export(name)), name
+    ia, ib = a.info(), b.info()
+    assert ia["hidr_dist_evals"] == ib["hidr_dist_evals"]
+    print(f"cfg{cfg} n={n}: down ms pruned {ia['stage_ms']['hidr_down']:.2f} brute {ib['stage_ms']['hidr_down']:.2f}"
+          f" evaluated {ia['hidr_dist_done']:.3e} of {ia['hidr_dist_evals']:.3e}")
+    a.close()
+    b.close()
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_pruned_down_lattice_ties(d):
+    """Points on a dyadic lattice (with duplicates): grid nodes fall exactly half-way between
+    lattice points, so the argmin has exact distance ties everywhere -- the lowest tree-order
+    index must win, identically to the oracle."""
+    side = {1: 4096, 2: 64, 3: 16}[d]
+    g1 = np.arange(side) / side
+    pts = np.stack(np.meshgrid(*([g1] * d), indexing="ij"), -1).reshape(-1, d)
+    pts = np.concatenate([pts, pts[::7]])
+    o, r = oracle_build(pts, 2, [0.3], 1e-5, 8)
+    g = gpu_build(pts, 2, [0.3], 1e-5, 8)
+    assert g.info()["r"] == r
+    assert_structure_equal(g, o)
