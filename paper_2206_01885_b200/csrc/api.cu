@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of include/h2.h: argument validation, the Algorithm 2 stage sequence
 // (PAPER.md P:459-506), per-stage timing, export hooks and error reporting.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -26,6 +27,36 @@ static void free_handle(h2_handle* h) {
     if (p) dev_free(p, h->stream);
   cudaStreamSynchronize(h->stream);
   delete h;
+}
+
+// The build's two internal streams on the current device (per host thread, created once, never
+// destroyed: cached allocator blocks stay tagged with them).  `main` carries a1-a9 at the
+// highest priority; `side` carries the nearfield fill (a10) at the lowest, so the latency-bound
+// level kernels take SMs first whenever a fill CTA retires.
+struct BuildStreams {
+  cudaStream_t main = nullptr, side = nullptr;
+};
+static BuildStreams& build_streams() {
+  thread_local BuildStreams per_dev[64];
+  int dev = 0;
+  H2_CUDA_TRY(cudaGetDevice(&dev));
+  BuildStreams& b = per_dev[dev & 63];
+  if (!b.main) {
+    int least = 0, greatest = 0;
+    H2_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    H2_CUDA_TRY(cudaStreamCreateWithPriority(&b.main, cudaStreamNonBlocking, greatest));
+    H2_CUDA_TRY(cudaStreamCreateWithPriority(&b.side, cudaStreamNonBlocking, least));
+  }
+  return b;
+}
+
+// H2_SERIAL=1: run the nearfield fill after the coupling fill on the main stream (A/B knob)
+static bool serial_fill() {
+  static const bool v = [] {
+    const char* e = getenv("H2_SERIAL");
+    return e && atoi(e) != 0;
+  }();
+  return v;
 }
 
 template <class T>
@@ -88,7 +119,16 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
   h->hidr_prune = o.hidr_brute ? 0 : 1;
   cudaEvent_t ev[8];
   int nev = 0;
+  cudaStream_t user = h->stream;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   try {
+    BuildStreams& bs = build_streams();
+    H2_CUDA_TRY(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    H2_CUDA_TRY(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
+    // all work runs on the internal streams, ordered after what the caller queued on `user`
+    H2_CUDA_TRY(cudaEventRecord(fork_ev, user));
+    H2_CUDA_TRY(cudaStreamWaitEvent(bs.main, fork_ev, 0));
+    h->stream = bs.main;
     if (h->timing) {
       for (auto& e : ev) H2_CUDA_TRY(cudaEventCreate(&e));
       nev = 8;
@@ -104,11 +144,15 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
                                   h->stream));
       pts = staged.as<double>();
     }
+    NfJob nf;
     mark(0);
     build_tree(h, pts);  // a1-a3
     mark(1);
     build_lists(h);  // a4
     mark(2);
+    // a10 needs only the tree and the nearfield list: it starts now on the side stream and
+    // overlaps a5-a9 (serial_fill(): after a9 on the main stream instead)
+    if (!serial_fill()) fill_nearfield_begin(h, bs.side, o.storage, o.mem_budget_bytes, nf);
     h->r = o.r_override > 0 ? o.r_override : calibrate(h);  // a5
     mark(3);
     hidr_up(h);  // a6
@@ -117,25 +161,43 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
     mark(5);
     id_sweep(h);  // a8
     mark(6);
-    fill_blocks(h, o.storage, o.mem_budget_bytes);  // a9, a10
+    fill_coupling(h, o.storage, o.mem_budget_bytes, nf);  // a9
+    if (serial_fill()) fill_nearfield_begin(h, h->stream, o.storage, o.mem_budget_bytes, nf);
+    fill_nearfield_join(h, nf);
     mark(7);
+    H2_CUDA_TRY(cudaEventRecord(join_ev, h->stream));
+    H2_CUDA_TRY(cudaStreamWaitEvent(user, join_ev, 0));
+    h->stream = user;
     H2_CUDA_TRY(cudaStreamSynchronize(h->stream));
     if (h->timing) {
+      nf.finish_timing(h);
       for (int i = 0; i < 6; i++) cudaEventElapsedTime(&h->stage_ms[i], ev[i], ev[i + 1]);
       cudaEventElapsedTime(&h->stage_ms[8], ev[0], ev[7]);
     }
   } catch (const Error& e) {
     set_error(e.code, e.msg);
     cudaGetLastError();
+    cudaDeviceSynchronize();  // the internal streams may still use the handle's buffers
+    cudaGetLastError();
+    h->stream = user;
     for (int i = 0; i < nev; i++) cudaEventDestroy(ev[i]);
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    if (join_ev) cudaEventDestroy(join_ev);
     free_handle(h);
     return nullptr;
   } catch (const std::exception& e) {
     set_error(H2_ERR_INTERNAL, e.what());
+    cudaDeviceSynchronize();
+    cudaGetLastError();
+    h->stream = user;
     for (int i = 0; i < nev; i++) cudaEventDestroy(ev[i]);
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    if (join_ev) cudaEventDestroy(join_ev);
     free_handle(h);
     return nullptr;
   }
+  cudaEventDestroy(fork_ev);
+  cudaEventDestroy(join_ev);
   for (int i = 0; i < nev; i++) cudaEventDestroy(ev[i]);
   return h;
 }

@@ -107,10 +107,11 @@ __global__ void unit_map_kernel(int64_t np, const int64_t* __restrict__ uoff, in
 }
 
 // one unit's rows [r0, r1) over NS column slots: NS independent evaluation chains per row, no
-// control flow between them (so the compiler interleaves them), next row's point prefetched
+// control flow between them (so the compiler interleaves them), next row's point prefetched.
+// Coordinates are pre-scaled (kernel_cscale), so sq is the kernel's own argument.
 template <int D, int KID, int NS>
 __device__ __forceinline__ void nf_unit_rows(const double* __restrict__ xr, int64_t n, const double (&xb)[8][D],
-                                             const bool (&ok)[8], int r0, int r1, int nj, double* o, double p2,
+                                             const bool (&ok)[8], int r0, int r1, int nj, double* o,
                                              const double* __restrict__ tab) {
   double xa[D];
 #pragma unroll
@@ -129,7 +130,7 @@ __device__ __forceinline__ void nf_unit_rows(const double* __restrict__ xr, int6
         const double df = xa[c] - xb[s][c];
         sq = fma(df, df, sq);
       }
-      v[s] = kernel_s(KID, p2, sq, tab);
+      v[s] = kernel_fill<KID>(sq, tab);
     }
 #pragma unroll
     for (int s = 0; s < NS; s++)
@@ -147,11 +148,11 @@ __global__ void __launch_bounds__(kFillThreads, MINB) nf_fill_kernel(int64_t nun
                                                                      const int* __restrict__ nbegin,
                                                                      const int* __restrict__ nend,
                                                                      const double* __restrict__ X, int64_t n,
-                                                                     double p2, double* __restrict__ out) {
+                                                                     double* __restrict__ out) {
   static_assert(CW >= 1 && CW <= 8, "1..8 column slots");
   constexpr int WC = 32 * CW;
-  __shared__ double tab[64];
-  if (threadIdx.x < 64) tab[threadIdx.x] = kExp2Tab64[threadIdx.x];
+  __shared__ double tab[256];
+  tab[threadIdx.x] = kExp2Tab256[threadIdx.x];
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -180,14 +181,14 @@ __global__ void __launch_bounds__(kFillThreads, MINB) nf_fill_kernel(int64_t nun
     int nslot = (nj - c0 + 31) >> 5;  // warp-uniform: slots with at least one column
     if (nslot > CW) nslot = CW;
     switch (nslot) {
-      case 1: nf_unit_rows<D, KID, 1>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
-      case 2: nf_unit_rows<D, KID, (CW < 2 ? CW : 2)>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
-      case 3: nf_unit_rows<D, KID, (CW < 3 ? CW : 3)>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
-      case 4: nf_unit_rows<D, KID, (CW < 4 ? CW : 4)>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
-      case 5: nf_unit_rows<D, KID, (CW < 5 ? CW : 5)>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
-      case 6: nf_unit_rows<D, KID, (CW < 6 ? CW : 6)>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
-      case 7: nf_unit_rows<D, KID, (CW < 7 ? CW : 7)>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
-      default: nf_unit_rows<D, KID, CW>(xr, n, xb, ok, r0, r1, nj, o, p2, tab); break;
+      case 1: nf_unit_rows<D, KID, 1>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
+      case 2: nf_unit_rows<D, KID, (CW < 2 ? CW : 2)>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
+      case 3: nf_unit_rows<D, KID, (CW < 3 ? CW : 3)>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
+      case 4: nf_unit_rows<D, KID, (CW < 4 ? CW : 4)>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
+      case 5: nf_unit_rows<D, KID, (CW < 5 ? CW : 5)>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
+      case 6: nf_unit_rows<D, KID, (CW < 6 ? CW : 6)>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
+      case 7: nf_unit_rows<D, KID, (CW < 7 ? CW : 7)>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
+      default: nf_unit_rows<D, KID, CW>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
     }
   }
 }
@@ -198,7 +199,10 @@ __global__ void __launch_bounds__(kFillThreads) cp_fill_kernel(int64_t np, const
                                                                const int64_t* __restrict__ voff,
                                                                const int* __restrict__ k, const int* __restrict__ sk,
                                                                int r, const double* __restrict__ X, int64_t n,
-                                                               double p2, double* __restrict__ out) {
+                                                               double cs, double* __restrict__ out) {
+  __shared__ double tab[256];
+  tab[threadIdx.x] = kExp2Tab256[threadIdx.x];
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -214,30 +218,51 @@ __global__ void __launch_bounds__(kFillThreads) cp_fill_kernel(int64_t np, const
       if (col < kj) {
         const int b = sj[col];
 #pragma unroll
-        for (int c = 0; c < D; c++) xb[c] = X[c * n + b];
+        for (int c = 0; c < D; c++) xb[c] = X[c * n + b] * cs;
       }
       for (int row = 0; row < ki; row++) {
         const int a = si[row];
         double s = 0.0;
 #pragma unroll
         for (int c = 0; c < D; c++) {
-          double df = X[c * n + a] - (col < kj ? xb[c] : 0.0);
+          double df = X[c * n + a] * cs - (col < kj ? xb[c] : 0.0);
           s = fma(df, df, s);
         }
-        if (col < kj) __stcs(o + (int64_t)row * kj + col, kernel_s(KID, p2, s));
+        if (col < kj) __stcs(o + (int64_t)row * kj + col, kernel_fill<KID>(s, tab));
       }
     }
   }
 }
 
+// coordinates pre-scaled by kernel_cscale for the nearfield fill (SoA, like h->X)
+__global__ void scale_coords_kernel(int64_t m, const double* __restrict__ X, double cs, double* __restrict__ Xs) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x)
+    Xs[t] = X[t] * cs;
+}
+
+// H2_NF_UPW (tuning knob, read once): nearfield units per warp of one CTA's lifetime.  The
+// nearfield fill runs CONCURRENTLY with the HiDR / ID stages (api.cu), on a low-priority stream:
+// its grid is made of many short-lived CTAs (default 8 units per warp, ~0.1 ms each) so that
+// the latency-bound level kernels on the high-priority stream get SMs as soon as a fill CTA
+// retires; 0 = one persistent wave (148 x 8 CTAs).
+static int nf_units_per_warp() {
+  static const int v = [] {
+    const char* e = getenv("H2_NF_UPW");
+    return e ? atoi(e) : 8;
+  }();
+  return v;
+}
+
 template <int KID>
-static void launch_fill_kid(const h2_handle* h, int mode, int64_t nwork, int64_t np, const int* umap, const int64_t* uoff,
-                            const int2* pairs, const int64_t* voff, double p2, double* out) {
-  cudaStream_t s = h->stream;
+static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_t nwork, int64_t np, const int* umap,
+                            const int64_t* uoff, const int2* pairs, const int64_t* voff, const double* Xs, double cs,
+                            double* out) {
   if (mode == 1) {
-    const int64_t blocks = (nwork + 7) / 8;  // one warp per unit, 8 warps per CTA
-    unsigned g = (unsigned)(blocks < 148 * 8 ? blocks : 148 * 8);
-#define H2_NF_ARGS nwork, umap, uoff, pairs, voff, h->nbegin, h->nend, h->X, h->n, p2, out
+    const int upw = nf_units_per_warp();
+    int64_t blocks = upw > 0 ? (nwork + 8 * upw - 1) / (8 * upw) : (nwork + 7) / 8;  // 8 warps per CTA
+    const int64_t cap = upw > 0 ? (int64_t)1 << 30 : 148 * 8;
+    unsigned g = (unsigned)(blocks < cap ? blocks : cap);
+#define H2_NF_ARGS nwork, umap, uoff, pairs, voff, h->nbegin, h->nend, Xs, h->n, out
     switch (h->d) {
       case 2:
         switch (nf_variant()) {  // tuning variants of the D = 2 kernel (CW, RU, MINB)
@@ -263,7 +288,7 @@ static void launch_fill_kid(const h2_handle* h, int mode, int64_t nwork, int64_t
     switch (h->d) {
 #define H2_CP_CASE(DD)                                                                                        \
   case DD:                                                                                                    \
-    cp_fill_kernel<DD, KID><<<g, kFillThreads, 0, s>>>(np, pairs, voff, h->k, h->sk, h->r, h->X, h->n, p2, out); \
+    cp_fill_kernel<DD, KID><<<g, kFillThreads, 0, s>>>(np, pairs, voff, h->k, h->sk, h->r, h->X, h->n, cs, out);   \
     break;
       H2_CP_CASE(1) H2_CP_CASE(2) H2_CP_CASE(3) H2_CP_CASE(4)
       H2_CP_CASE(5) H2_CP_CASE(6) H2_CP_CASE(7) H2_CP_CASE(8)
@@ -272,19 +297,20 @@ static void launch_fill_kid(const h2_handle* h, int mode, int64_t nwork, int64_t
   }
 }
 
-static void launch_fill(const h2_handle* h, int mode, int64_t nwork, int64_t np, const int* umap, const int64_t* uoff,
-                        const int2* pairs, const int64_t* voff, double* out) {
+static void launch_fill(const h2_handle* h, cudaStream_t s, int mode, int64_t nwork, int64_t np, const int* umap,
+                        const int64_t* uoff, const int2* pairs, const int64_t* voff, const double* Xs, double* out) {
   if (nwork < 1) return;
-  const double p2 = kernel_p2(h->kid, h->kp);
-  if (h->kid == H2_KERNEL_COULOMB) launch_fill_kid<H2_KERNEL_COULOMB>(h, mode, nwork, np, umap, uoff, pairs, voff, p2, out);
+  const double cs = kernel_cscale(h->kid, h->kp);
+  if (h->kid == H2_KERNEL_COULOMB)
+    launch_fill_kid<H2_KERNEL_COULOMB>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
   else if (h->kid == H2_KERNEL_GAUSSIAN)
-    launch_fill_kid<H2_KERNEL_GAUSSIAN>(h, mode, nwork, np, umap, uoff, pairs, voff, p2, out);
-  else launch_fill_kid<H2_KERNEL_MATERN32>(h, mode, nwork, np, umap, uoff, pairs, voff, p2, out);
+    launch_fill_kid<H2_KERNEL_GAUSSIAN>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
+  else launch_fill_kid<H2_KERNEL_MATERN32>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
 }
 
-// builds the symmetric-once pair list of one class (CSR order) with entry offsets
-static void make_pairs(h2_handle* h, int mode, int64_t& np, int2*& pairs, int64_t*& voff, int64_t& entries) {
-  cudaStream_t s = h->stream;
+// builds the symmetric-once pair list of one class (CSR order) with entry offsets, on stream s
+static void make_pairs(h2_handle* h, cudaStream_t s, int mode, int64_t& np, int2*& pairs, int64_t*& voff,
+                       int64_t& entries) {
   const int nn = h->nnodes;
   const int64_t* off = mode == 0 ? h->il_off : h->nf_off;
   const int* idx = mode == 0 ? h->il_idx : h->nf_idx;
@@ -313,77 +339,114 @@ static int64_t pool_available() {
   return (int64_t)fr + (int64_t)cached_free_bytes();
 }
 
-void fill_blocks(h2_handle* h, int storage, int64_t budget) {
-  cudaStream_t s = h->stream;
-  make_pairs(h, 0, h->n_cp, h->cp_pairs, h->cp_off, h->cp_entries);
-  make_pairs(h, 1, h->n_np, h->np_pairs, h->np_off, h->np_entries);
-  const int64_t cb = h->cp_entries * 8, nb = h->np_entries * 8;
-  bool store_cp = false, store_np = false;
-  if (storage == H2_STORE_ALL) {
-    store_cp = store_np = true;
-  } else if (storage == H2_STORE_AUTO) {
-    int64_t avail = budget > 0 ? budget : pool_available() - ((int64_t)4 << 30);
-    // greedy: the smaller class first
-    if (cb <= nb) {
-      if (cb <= avail) store_cp = true, avail -= cb;
-      if (nb <= avail) store_np = true;
-    } else {
-      if (nb <= avail) store_np = true, avail -= nb;
-      if (cb <= avail) store_cp = true;
-    }
+static int64_t store_budget(int64_t budget) { return budget > 0 ? budget : pool_available() - ((int64_t)4 << 30); }
+
+// a10, issued right after the lists (it needs only the tree and the nearfield list) on the side
+// stream `side`, which first waits for everything already queued on h->stream.  Storage policy
+// AUTO stores the nearfield class first when it fits the budget (it is the class a matvec
+// re-evaluates at the highest cost per entry), then the coupling class in what remains.
+void fill_nearfield_begin(h2_handle* h, cudaStream_t side, int storage, int64_t budget, NfJob& job) {
+  job.side = side;
+  H2_CUDA_TRY(cudaEventCreateWithFlags(&job.forked, cudaEventDisableTiming));
+  H2_CUDA_TRY(cudaEventCreateWithFlags(&job.done, cudaEventDisableTiming));
+  if (h->timing) {
+    H2_CUDA_TRY(cudaEventCreate(&job.t0));
+    H2_CUDA_TRY(cudaEventCreate(&job.t1));
   }
-  cudaEvent_t ev[4];
+  H2_CUDA_TRY(cudaEventRecord(job.forked, h->stream));
+  H2_CUDA_TRY(cudaStreamWaitEvent(side, job.forked, 0));
+  make_pairs(h, side, 1, h->n_np, h->np_pairs, h->np_off, h->np_entries);
+  const int64_t nb = h->np_entries * 8;
+  const bool store_np = storage == H2_STORE_ALL || (storage == H2_STORE_AUTO && nb <= store_budget(budget));
+  if (store_np) {
+    h->np_val = halloc<double>(h, h->np_entries);
+    h->np_stored = 1;
+    job.stored_bytes = nb;
+  }
+  int64_t nunits = 0;
+  if (store_np && h->n_np > 0) {
+    const int64_t np = h->n_np;
+    Scratch units(sizeof(int64_t) * (np + 1), side);
+    job.uoff = Scratch(sizeof(int64_t) * (np + 1), side);
+    nf_units_kernel<<<grid_for(np + 1, 256), 256, 0, side>>>(32 * nf_slots(h->d), np, h->np_pairs, h->nbegin,
+                                                             h->nend, units.as<int64_t>());
+    scan_excl_i64(units.as<int64_t>(), job.uoff.as<int64_t>(), np + 1, side);
+    H2_CHECK_LAUNCH();
+    nunits = read1(job.uoff.as<int64_t>() + np, side);
+    job.umap = Scratch(sizeof(int) * (nunits > 0 ? nunits : 1), side);
+    unit_map_kernel<<<grid_for(np, 256), 256, 0, side>>>(np, job.uoff.as<int64_t>(), job.umap.as<int>());
+    H2_CHECK_LAUNCH();
+    h->gpu_launches += 3;
+  }
+  if (h->timing) H2_CUDA_TRY(cudaEventRecord(job.t0, side));
+  if (nunits > 0) {
+    job.xs = Scratch(sizeof(double) * (size_t)h->n * h->d, side);
+    scale_coords_kernel<<<grid_for((int64_t)h->n * h->d, 256), 256, 0, side>>>(
+        (int64_t)h->n * h->d, h->X, kernel_cscale(h->kid, h->kp), job.xs.as<double>());
+    launch_fill(h, side, 1, nunits, h->n_np, job.umap.as<int>(), job.uoff.as<int64_t>(), h->np_pairs, h->np_off,
+                job.xs.as<double>(), h->np_val);
+    h->gpu_launches += 1;
+    H2_CHECK_LAUNCH();
+    h->gpu_launches += 1;
+  }
+  if (h->timing) H2_CUDA_TRY(cudaEventRecord(job.t1, side));
+  H2_CUDA_TRY(cudaEventRecord(job.done, side));
+  job.active = true;
+}
+
+// a9 on h->stream (needs the skeletons of the ID sweep)
+void fill_coupling(h2_handle* h, int storage, int64_t budget, const NfJob& job) {
+  cudaStream_t s = h->stream;
+  make_pairs(h, s, 0, h->n_cp, h->cp_pairs, h->cp_off, h->cp_entries);
+  const int64_t cb = h->cp_entries * 8;
+  const bool store_cp = storage == H2_STORE_ALL || (storage == H2_STORE_AUTO && cb <= store_budget(budget) -
+                                                                                    (budget > 0 ? job.stored_bytes : 0));
+  cudaEvent_t ev[2];
   if (h->timing)
     for (auto& e : ev) H2_CUDA_TRY(cudaEventCreate(&e));
   if (store_cp) {
     h->cp_val = halloc<double>(h, h->cp_entries);
     h->cp_stored = 1;
   }
-  if (store_np) {
-    h->np_val = halloc<double>(h, h->np_entries);
-    h->np_stored = 1;
-  }
-  // a9 coupling
   if (h->timing) H2_CUDA_TRY(cudaEventRecord(ev[0], s));
   if (store_cp && h->n_cp > 0) {
-    launch_fill(h, 0, h->n_cp, h->n_cp, nullptr, nullptr, h->cp_pairs, h->cp_off, h->cp_val);
-    H2_CHECK_LAUNCH();
-    h->gpu_launches += 1;
-  }
-  if (h->timing) H2_CUDA_TRY(cudaEventRecord(ev[1], s));
-  // a10 nearfield
-  Scratch units, uoff, umap;
-  int64_t nunits = 0;
-  if (store_np && h->n_np > 0) {
-    const int64_t np = h->n_np;
-    units = Scratch(sizeof(int64_t) * (np + 1), s);
-    uoff = Scratch(sizeof(int64_t) * (np + 1), s);
-    nf_units_kernel<<<grid_for(np + 1, 256), 256, 0, s>>>(32 * nf_slots(h->d), np, h->np_pairs, h->nbegin, h->nend,
-                                                          units.as<int64_t>());
-    scan_excl_i64(units.as<int64_t>(), uoff.as<int64_t>(), np + 1, s);
-    H2_CHECK_LAUNCH();
-    nunits = read1(uoff.as<int64_t>() + np, s);
-    umap = Scratch(sizeof(int) * (nunits > 0 ? nunits : 1), s);
-    unit_map_kernel<<<grid_for(np, 256), 256, 0, s>>>(np, uoff.as<int64_t>(), umap.as<int>());
-    H2_CHECK_LAUNCH();
-    h->gpu_launches += 3;
-  }
-  if (h->timing) H2_CUDA_TRY(cudaEventRecord(ev[2], s));
-  if (nunits > 0) {
-    launch_fill(h, 1, nunits, h->n_np, umap.as<int>(), uoff.as<int64_t>(), h->np_pairs, h->np_off, h->np_val);
+    launch_fill(h, s, 0, h->n_cp, h->n_cp, nullptr, nullptr, h->cp_pairs, h->cp_off, h->X, h->cp_val);
     H2_CHECK_LAUNCH();
     h->gpu_launches += 1;
   }
   if (h->timing) {
-    H2_CUDA_TRY(cudaEventRecord(ev[3], s));
-    H2_CUDA_TRY(cudaEventSynchronize(ev[3]));
-    float a = 0, b = 0;
+    H2_CUDA_TRY(cudaEventRecord(ev[1], s));
+    H2_CUDA_TRY(cudaEventSynchronize(ev[1]));
+    float a = 0;
     cudaEventElapsedTime(&a, ev[0], ev[1]);
-    cudaEventElapsedTime(&b, ev[2], ev[3]);
     h->stage_ms[6] = a;
-    h->stage_ms[7] = b;
     for (auto& e : ev) cudaEventDestroy(e);
   }
+}
+
+// joins the side stream into h->stream; the nearfield scratch is released on h->stream after
+// the join (so no later allocation ever waits on the fill)
+void fill_nearfield_join(h2_handle* h, NfJob& job) {
+  if (!job.active) return;
+  H2_CUDA_TRY(cudaStreamWaitEvent(h->stream, job.done, 0));
+  job.uoff.s = job.umap.s = job.xs.s = h->stream;
+  job.uoff = Scratch();
+  job.umap = Scratch();
+  job.xs = Scratch();
+  job.active = false;
+}
+
+void NfJob::finish_timing(h2_handle* h) {
+  if (h->timing && t0 && t1) {
+    float b = 0;
+    if (cudaEventElapsedTime(&b, t0, t1) == cudaSuccess) h->stage_ms[7] = b;
+  }
+}
+
+NfJob::~NfJob() {
+  if (active && side) cudaStreamSynchronize(side);  // error path: nothing may still use the scratch
+  for (cudaEvent_t e : {forked, done, t0, t1})
+    if (e) cudaEventDestroy(e);
 }
 
 // ---- sampled reads of stored entries for the parity tests ----------------------------------

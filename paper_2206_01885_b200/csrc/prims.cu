@@ -12,12 +12,16 @@ namespace h2 {
 // earlier builds when one of a close size exists (the sizes repeat exactly from build to build),
 // otherwise from cudaMalloc.  Freed blocks are kept (never cudaFree'd except to recover from an
 // out-of-memory), so steady-state builds make no driver allocation calls at all.  A block is
-// tagged with the stream that freed it; handing it to another stream first synchronises that one.
+// tagged with the stream that freed it and an event recorded there at the free: another stream
+// may take it only once that event has completed (no host or device wait is ever introduced --
+// the build runs two streams concurrently, and a wait on the busy one would serialise them);
+// otherwise a fresh block is allocated, so steady state keeps per-stream blocks.
 struct CachedBlock {
   void* p;
   size_t size;
   cudaStream_t stream;
   int dev;
+  cudaEvent_t freed;  // recorded on `stream` when the block was freed (its last use precedes it)
 };
 static std::mutex g_mu;
 static std::multimap<size_t, CachedBlock> g_free;
@@ -34,6 +38,7 @@ static void release_cached(int dev) {  // caller holds g_mu
   for (auto it = g_free.begin(); it != g_free.end();) {
     if (it->second.dev == dev) {
       cudaFree(it->second.p);
+      cudaEventDestroy(it->second.freed);
       it = g_free.erase(it);
     } else {
       ++it;
@@ -49,9 +54,16 @@ void* dev_alloc(size_t bytes, cudaStream_t s) {
   for (auto it = g_free.lower_bound(size); it != g_free.end() && it->first <= size + size / 4 + (size_t(2) << 20);
        ++it) {
     if (it->second.dev != dev) continue;
+    if (it->second.stream != s) {
+      const cudaError_t q = cudaEventQuery(it->second.freed);
+      if (q == cudaErrorNotReady) {
+        cudaGetLastError();
+        continue;
+      }
+      H2_CUDA_TRY(q);
+    }
     CachedBlock b = it->second;
     g_free.erase(it);
-    if (b.stream != s) H2_CUDA_TRY(cudaStreamSynchronize(b.stream));
     b.stream = s;
     g_live[b.p] = b;
     return b.p;
@@ -68,7 +80,9 @@ void* dev_alloc(size_t bytes, cudaStream_t s) {
     throw Error{H2_ERR_OOM, "device allocation of " + std::to_string(bytes) + " bytes failed: " +
                                 cudaGetErrorString(e)};
   }
-  g_live[p] = CachedBlock{p, size, s, dev};
+  cudaEvent_t ev = nullptr;
+  H2_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  g_live[p] = CachedBlock{p, size, s, dev, ev};
   return p;
 }
 
@@ -80,6 +94,7 @@ void dev_free(void* p, cudaStream_t s) {
   CachedBlock b = it->second;
   g_live.erase(it);
   b.stream = s;
+  cudaEventRecord(b.freed, s);
   g_free.emplace(b.size, b);
 }
 
