@@ -95,6 +95,9 @@ typedef struct h2_options {
   int32_t timing;          /* 1: record per-stage CUDA-event times (h2_info stage_ms)               */
   int32_t hidr_brute;      /* 1: brute-force top-down Vol instead of the pruned exact kernel (same  */
                            /*    result bit for bit; for A/B checks)                                */
+  struct h2_comm* comm;    /* NULL: single GPU.  Otherwise a sharded build over comm's ranks (see   */
+                           /*    "sharded build" below): every rank calls h2_build_ex with the same */
+                           /*    points and parameters; the comm must outlive the handle.           */
 } h2_options;
 
 /* h2_options with the defaults listed above (r calibrated, AUTO, whole-device budget, timing off) */
@@ -120,6 +123,42 @@ void h2_free(h2_handle* h);
 /* thread-local status / message of the last failing call on this thread (H2_OK if none). */
 int h2_last_error(void);
 const char* h2_last_error_message(void);
+
+/* ---- sharded build (BASELINE north_star) -------------------------------------
+ * One rank per GPU.  Every rank builds the tree, the lists and the calibration redundantly (they are
+ * deterministic, hence identical).  The cut level c is the shallowest level with >= 64 nodes per
+ * rank; its nodes are split into contiguous Morton runs balanced by an integer work estimate
+ * (h2_shard_split).  HiDR (Algorithm 1) and the ID sweep (Algorithm 2 lines 10-14,
+ * P:474-495) run at levels >= c on the rank's own subtrees and at levels < c on every rank; the
+ * X_i^* of every level >= c are exchanged (one allgather) after HiDR up below the cut, and the
+ * skeletons X^_i (with k_i) after the ID sweep below the cut.  A rank stores the coupling and
+ * nearfield blocks of the rows it owns (nodes whose first point lies in its point range).
+ * Per-node results are bit-identical to a single-GPU build.  h2_matvec on a sharded handle is
+ * collective (same x on every rank; every rank receives the whole y).
+ *
+ * Transports (h2_comm):
+ *   h2_comm_nccl_unique_id / h2_comm_init_nccl: NCCL over NVLink, one process per GPU (rank 0 makes
+ *     the id, the caller broadcasts it, e.g. with torch.distributed).  libnccl is resolved at run
+ *     time: the copy the process already loaded (import torch first), or $H2_NCCL_LIB.
+ *   h2_comm_init_local: nranks host threads of ONE process (same or different devices) whose
+ *     comms share group_key; the exchange is a host barrier + device copies (tests).
+ * All return NULL / an H2_ERR_* code on failure (h2_last_error).                                   */
+typedef struct h2_comm h2_comm;
+int h2_comm_nccl_unique_id(unsigned char id[128]);
+h2_comm* h2_comm_init_nccl(int32_t nranks, int32_t rank, const unsigned char id[128]);
+h2_comm* h2_comm_init_local(int32_t nranks, int32_t rank, int64_t group_key);
+void h2_comm_free(h2_comm* comm);  /* NULL-safe; after every handle built on it is freed */
+int32_t h2_comm_size(const h2_comm* comm);
+int32_t h2_comm_rank(const h2_comm* comm);
+
+/* Host-only planning helpers (no device work; usable without a GPU).
+ * h2_shard_cut_level: the shallowest level l with level_counts[l] >= 64*nranks, else the most
+ *   populous level (shallowest on ties).
+ * h2_shard_split: first[q] (q = 0..nranks) = the smallest t with (w[0]+...+w[t-1])*nranks >=
+ *   q*total, first[nranks] = ncut: rank q owns cut nodes [first[q], first[q+1]).  Weights must be
+ *   >= 0.  Returns H2_OK or H2_ERR_INVALID_ARG.                                                    */
+int32_t h2_shard_cut_level(const int64_t* level_counts, int32_t nlevels, int32_t nranks);
+int h2_shard_split(const int64_t* weights, int64_t ncut, int32_t nranks, int64_t* first);
 
 /* ---- introspection --------------------------------------------------------------------------- */
 typedef struct h2_info_t {
@@ -161,6 +200,8 @@ enum {
   H2_EXPORT_U = 16,       /* double[...]                                                         */
   H2_EXPORT_XBAR_N = 17,  /* int32[nnodes] |Xbar_i|                                              */
   H2_EXPORT_TREE_X = 18,  /* double[n*d] tree-order coordinates, point-major                     */
+  H2_EXPORT_SHARD = 19,   /* int64[5 + 2*(depth+1)]: nranks, rank, cut level, p_lo, p_hi, then per */
+                          /* level l the node range [lo_l, hi_l) this rank computed               */
   H2_EXPORT_BLOCK_SAMPLE = 20 /* see h2_sample_blocks                                            */
 };
 

@@ -19,20 +19,22 @@ H2_KERNEL_COULOMB, H2_KERNEL_GAUSSIAN, H2_KERNEL_MATERN32 = 1, 2, 3
 H2_STORE_AUTO, H2_STORE_ALL, H2_STORE_ON_THE_FLY = 0, 1, 2
 
 EXPORT = dict(PERM=1, NODES=2, IL_OFF=4, IL_IDX=5, NF_OFF=6, NF_IDX=7, XS_OFF=8, XS_IDX=9, YS_OFF=10,
-              YS_IDX=11, K=12, SK_OFF=13, SK_IDX=14, U_OFF=15, U=16, XBAR_N=17, TREE_X=18)
+              YS_IDX=11, K=12, SK_OFF=13, SK_IDX=14, U_OFF=15, U=16, XBAR_N=17, TREE_X=18, SHARD=19)
 _EXPORT_DTYPE = dict(PERM=np.int32, NODES=np.int32, IL_OFF=np.int64, IL_IDX=np.int32, NF_OFF=np.int64,
                      NF_IDX=np.int32, XS_OFF=np.int64, XS_IDX=np.int32, YS_OFF=np.int64, YS_IDX=np.int32,
                      K=np.int32, SK_OFF=np.int64, SK_IDX=np.int32, U_OFF=np.int64, U=np.float64,
-                     XBAR_N=np.int32, TREE_X=np.float64)
+                     XBAR_N=np.int32, TREE_X=np.float64, SHARD=np.int64)
 
 EXPORTED_SYMBOLS = ["h2_build", "h2_build_ex", "h2_options_default", "h2_matvec", "h2_free", "h2_last_error",
-                    "h2_last_error_message", "h2_info", "h2_export", "h2_sample_blocks"]
+                    "h2_last_error_message", "h2_info", "h2_export", "h2_sample_blocks", "h2_comm_nccl_unique_id",
+                    "h2_comm_init_nccl", "h2_comm_init_local", "h2_comm_free", "h2_comm_size", "h2_comm_rank",
+                    "h2_shard_cut_level", "h2_shard_split"]
 
 
 class h2_options(C.Structure):
     _fields_ = [("r_override", C.c_int32), ("storage", C.c_int32), ("mem_budget_bytes", C.c_int64),
                 ("stream", C.c_void_p), ("points_on_host", C.c_int32), ("timing", C.c_int32),
-                ("hidr_brute", C.c_int32)]
+                ("hidr_brute", C.c_int32), ("comm", C.c_void_p)]
 
 
 class h2_info_t(C.Structure):
@@ -80,6 +82,21 @@ def lib():
         L.h2_export.argtypes = [vp, C.c_int, vp, C.c_size_t, C.POINTER(C.c_size_t)]
         L.h2_sample_blocks.restype = C.c_int
         L.h2_sample_blocks.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp]
+        L.h2_comm_nccl_unique_id.restype = C.c_int
+        L.h2_comm_nccl_unique_id.argtypes = [vp]
+        L.h2_comm_init_nccl.restype = vp
+        L.h2_comm_init_nccl.argtypes = [i32, i32, vp]
+        L.h2_comm_init_local.restype = vp
+        L.h2_comm_init_local.argtypes = [i32, i32, i64]
+        L.h2_comm_free.argtypes = [vp]
+        L.h2_comm_size.restype = i32
+        L.h2_comm_size.argtypes = [vp]
+        L.h2_comm_rank.restype = i32
+        L.h2_comm_rank.argtypes = [vp]
+        L.h2_shard_cut_level.restype = i32
+        L.h2_shard_cut_level.argtypes = [vp, i32, i32]
+        L.h2_shard_split.restype = C.c_int
+        L.h2_shard_split.argtypes = [vp, i64, i32, vp]
         _lib = L
     return _lib
 
@@ -158,14 +175,92 @@ def h2_sample_blocks(h: int, kind, pair, entry):
     return val, rp, cp
 
 
+def _nccl_hint():
+    """Points the library's run-time NCCL lookup at the copy PyTorch ships (if the env is unset)."""
+    if os.environ.get("H2_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl
+        for d in nvidia.nccl.__path__:
+            so = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(so):
+                os.environ["H2_NCCL_LIB"] = so
+                return
+    except Exception:
+        pass
+
+
+class H2Comm:
+    """Exchange transport of a sharded build (include/h2.h "sharded build").
+
+    H2Comm.nccl(nranks, rank, uid): one process per GPU; uid from H2Comm.nccl_unique_id() on rank 0,
+    broadcast by the caller (e.g. torch.distributed.broadcast_object_list).
+    H2Comm.local(nranks, rank, key): ranks are host threads of this process sharing `key`."""
+
+    def __init__(self, ptr: int):
+        if not ptr:
+            _raise()
+        self.ptr = ptr
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        _nccl_hint()
+        buf = (C.c_ubyte * 128)()
+        if lib().h2_comm_nccl_unique_id(buf) != 0:
+            _raise()
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, nranks: int, rank: int, uid: bytes) -> "H2Comm":
+        _nccl_hint()
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        return cls(lib().h2_comm_init_nccl(nranks, rank, buf))
+
+    @classmethod
+    def local(cls, nranks: int, rank: int, key: int) -> "H2Comm":
+        return cls(lib().h2_comm_init_local(nranks, rank, key))
+
+    @property
+    def size(self) -> int:
+        return int(lib().h2_comm_size(C.c_void_p(self.ptr)))
+
+    @property
+    def rank(self) -> int:
+        return int(lib().h2_comm_rank(C.c_void_p(self.ptr)))
+
+    def close(self):
+        if getattr(self, "ptr", None):
+            lib().h2_comm_free(C.c_void_p(self.ptr))
+            self.ptr = None
+
+
+def shard_cut_level(level_counts, nranks: int) -> int:
+    """h2_shard_cut_level (host only)."""
+    c = np.ascontiguousarray(level_counts, np.int64)
+    return int(lib().h2_shard_cut_level(c.ctypes.data_as(C.c_void_p), len(c), nranks))
+
+
+def shard_split(weights, nranks: int) -> np.ndarray:
+    """h2_shard_split (host only): first[q], q = 0..nranks."""
+    w = np.ascontiguousarray(weights, np.int64)
+    first = np.empty(nranks + 1, np.int64)
+    if lib().h2_shard_split(w.ctypes.data_as(C.c_void_p), len(w), nranks, first.ctypes.data_as(C.c_void_p)) != 0:
+        _raise()
+    return first
+
+
 class H2Matrix:
     """Owning wrapper: builds on the GPU from a torch CUDA tensor (n x d fp64) or a numpy array."""
 
     def __init__(self, points, kernel_id: int, kernel_params=(), id_tol: float = 1e-6, leaf_size: int = 64,
                  admissibility: float = 0.5, r: int = 0, storage: int = H2_STORE_AUTO, stream=None,
-                 timing: bool = False, mem_budget_bytes: int = 0, hidr_brute: bool = False):
+                 timing: bool = False, mem_budget_bytes: int = 0, hidr_brute: bool = False,
+                 comm: H2Comm | None = None):
         import torch
         o = h2_options_default()
+        if comm is not None:
+            o.comm = C.c_void_p(comm.ptr)
+            self._comm = comm
         o.hidr_brute = int(bool(hidr_brute))
         o.r_override = int(r)
         o.storage = int(storage)

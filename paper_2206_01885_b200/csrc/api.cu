@@ -117,6 +117,10 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
   h->stream = static_cast<cudaStream_t>(o.stream);
   h->timing = o.timing;
   h->hidr_prune = o.hidr_brute ? 0 : 1;
+  h->comm = o.comm;
+  h->nranks = h2_comm_size(o.comm);
+  h->rank = h2_comm_rank(o.comm);
+  h->p_hi = h->n;
   cudaEvent_t ev[8];
   int nev = 0;
   cudaStream_t user = h->stream;
@@ -149,6 +153,7 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
     build_tree(h, pts);  // a1-a3
     mark(1);
     build_lists(h);  // a4
+    if (h->nranks > 1) shard_plan(h);  // cut level, owned subtrees and block rows (shard.cu)
     mark(2);
     // a10 needs only the tree and the nearfield list: it starts now on the side stream and
     // overlaps a5-a9 (serial_fill(): after a9 on the main stream instead)
@@ -176,6 +181,7 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
     }
   } catch (const Error& e) {
     set_error(e.code, e.msg);
+    comm_abort(o.comm);  // LOCAL transport: release the other ranks' barriers
     cudaGetLastError();
     cudaDeviceSynchronize();  // the internal streams may still use the handle's buffers
     cudaGetLastError();
@@ -187,6 +193,7 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
     return nullptr;
   } catch (const std::exception& e) {
     set_error(H2_ERR_INTERNAL, e.what());
+    comm_abort(o.comm);
     cudaDeviceSynchronize();
     cudaGetLastError();
     h->stream = user;
@@ -217,6 +224,7 @@ int h2_matvec(const h2_handle* h, const double* x, double* y) {
     matvec(h, x, y);
   } catch (const Error& e) {
     set_error(e.code, e.msg);
+    comm_abort(h->comm);
     cudaGetLastError();
     return e.code;
   }
@@ -331,6 +339,15 @@ static std::vector<char> export_bytes(const h2_handle* h, int what) {
       for (int i = 0; i < nn; i++)
         if (off[i + 1] > off[i]) std::memcpy(&out[off[i]], &U[uo[i]], 8 * (off[i + 1] - off[i]));
       return bytes(out.data(), 8 * out.size());
+    }
+    case H2_EXPORT_SHARD: {
+      std::vector<int64_t> v = {h->nranks, h->rank, h->cut, h->p_lo, h->p_hi};
+      for (int l = 0; l <= h->depth; l++) {
+        const LevelRange lr = level_range(h, l);
+        v.push_back(lr.begin);
+        v.push_back(lr.end);
+      }
+      return bytes(v.data(), 8 * v.size());
     }
     case H2_EXPORT_TREE_X: {
       auto v = d2h(h->X, (size_t)n * d, s);

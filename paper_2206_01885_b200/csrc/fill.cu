@@ -31,15 +31,18 @@ __device__ __forceinline__ int row_of(const int64_t* __restrict__ off, int nnode
   return lo;
 }
 
+// a pair is stored (and applied by the matvec) by the rank owning its row: nbegin[i] in [p_lo, p_hi)
 __global__ void pair_flag_kernel(int mode, int nnodes, int64_t m, const int64_t* __restrict__ off,
-                                 const int* __restrict__ idx, const int* __restrict__ k, int64_t* flag) {
+                                 const int* __restrict__ idx, const int* __restrict__ k,
+                                 const int* __restrict__ nbegin, int p_lo, int p_hi, int64_t* flag) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= m; e += (int64_t)gridDim.x * blockDim.x) {
     if (e == m) {
       flag[e] = 0;
       continue;
     }
     int i = row_of(off, nnodes, e), j = idx[e];
-    flag[e] = mode == 0 ? (j > i && k[i] > 0 && k[j] > 0) : (j >= i);
+    const bool own = nbegin[i] >= p_lo && nbegin[i] < p_hi;
+    flag[e] = own && (mode == 0 ? (j > i && k[i] > 0 && k[j] > 0) : (j >= i));
   }
 }
 
@@ -316,7 +319,8 @@ static void make_pairs(h2_handle* h, cudaStream_t s, int mode, int64_t& np, int2
   const int* idx = mode == 0 ? h->il_idx : h->nf_idx;
   const int64_t m = mode == 0 ? h->n_il : h->n_nf;
   Scratch flag(sizeof(int64_t) * (m + 1), s), pos(sizeof(int64_t) * (m + 1), s);
-  pair_flag_kernel<<<grid_for(m + 1, 256), 256, 0, s>>>(mode, nn, m, off, idx, h->k, flag.as<int64_t>());
+  pair_flag_kernel<<<grid_for(m + 1, 256), 256, 0, s>>>(mode, nn, m, off, idx, h->k, h->nbegin, h->p_lo, h->p_hi,
+                                                        flag.as<int64_t>());
   scan_excl_i64(flag.as<int64_t>(), pos.as<int64_t>(), m + 1, s);
   H2_CHECK_LAUNCH();
   np = read1(pos.as<int64_t>() + m, s);

@@ -135,7 +135,8 @@ static void launch_sel_box(h2_handle* h, int base, int count, const int* cnt, co
 
 // pruned down level; false when the group boxes do not fit shared memory (brute-force path then)
 static bool hidr_down_level_pruned(h2_handle* h, int l, unsigned long long* ev, unsigned long long* ev_done) {
-  const int base = h->lvl_start[l], count = h->lvl_start[l + 1] - base;
+  const LevelRange lr = level_range(h, l);
+  const int base = lr.begin, count = lr.end - lr.begin;
   const int ngmax = (h->csp + 1 + 31) / 32;
   const size_t smem = sizeof(double) * 2 * h->d * (size_t)ngmax;
   if (smem > (size_t)kDownSmemMax) return false;
@@ -143,12 +144,8 @@ static bool hidr_down_level_pruned(h2_handle* h, int l, unsigned long long* ev, 
   switch (h->d) {
 #define H2_DOWN_CASE(DD)                                                                                         \
   case DD: {                                                                                                     \
-    static bool attr = false;                                                                                    \
-    if (!attr) {                                                                                                 \
-      H2_CUDA_TRY(cudaFuncSetAttribute(hidr_down_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+        H2_CUDA_TRY(cudaFuncSetAttribute(hidr_down_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                                        kDownSmemMax));                                                           \
-      attr = true;                                                                                               \
-    }                                                                                                            \
     hidr_down_kernel<DD><<<count, kDownThreads, smem, s>>>(h->X, h->n, base, h->r, h->parent, h->il_off,           \
                                                            h->il_idx, h->xs_cnt, h->xs, h->xbox, h->ybox,        \
                                                            h->ys_cnt, h->ys, ev, ev_done);                       \
@@ -164,7 +161,8 @@ static bool hidr_down_level_pruned(h2_handle* h, int l, unsigned long long* ev, 
 
 static void hidr_level(h2_handle* h, int mode, int l, unsigned long long* ev) {
   cudaStream_t s = h->stream;
-  int base = h->lvl_start[l], count = h->lvl_start[l + 1] - base;
+  const LevelRange lr = level_range(h, l);
+  int base = lr.begin, count = lr.end - lr.begin;
   if (count == 0) return;
   Scratch sizes(sizeof(int64_t) * (count + 1), s), off(sizeof(int64_t) * (count + 1), s);
   hidr_sizes_kernel<<<(count + 1 + 255) / 256, 256, 0, s>>>(mode, base, count, h->is_leaf, h->nbegin, h->nend,
@@ -197,7 +195,17 @@ void hidr_up(h2_handle* h) {
   H2_CUDA_TRY(cudaMemsetAsync(h->ys_cnt, 0, sizeof(int) * h->nnodes, h->stream));
   Scratch ev(sizeof(unsigned long long), h->stream);
   H2_CUDA_TRY(cudaMemsetAsync(ev.p, 0, sizeof(unsigned long long), h->stream));
-  for (int l = h->depth; l >= 0; l--) hidr_level(h, 0, l, ev.as<unsigned long long>());
+  for (int l = h->depth; l >= 0; l--) {
+    hidr_level(h, 0, l, ev.as<unsigned long long>());
+    if (h->nranks > 1 && l == h->cut) {
+      // sharded: every rank's X^* of the levels >= cut, then their boxes (hidr_down.cuh)
+      exchange_slots(h, h->xs_cnt, h->xs);
+      for (int m = h->cut; m <= h->depth; m++) {
+        const int b = h->lvl_start[m], c = h->lvl_start[m + 1] - b;
+        if (c > 0) launch_sel_box(h, b, c, h->xs_cnt, h->xs, h->xbox);
+      }
+    }
+  }
   h->hidr_dist_evals = (int64_t)read1(ev.as<unsigned long long>(), h->stream);
 }
 
@@ -209,7 +217,8 @@ void hidr_down(h2_handle* h) {
   // the root's Y^* is empty (reading D1): its box is the empty box
   launch_sel_box(h, 0, 1, h->ys_cnt, h->ys, h->ybox);
   for (int l = 1; l <= h->depth; l++) {
-    const int base = h->lvl_start[l], count = h->lvl_start[l + 1] - base;
+    const LevelRange lr = level_range(h, l);
+    const int base = lr.begin, count = lr.end - lr.begin;
     if (count == 0) continue;
     if (h->hidr_prune && hidr_down_level_pruned(h, l, ev.as<unsigned long long>(), evd.as<unsigned long long>()))
       launch_sel_box(h, base, count, h->ys_cnt, h->ys, h->ybox);

@@ -220,8 +220,14 @@ void id_sweep(h2_handle* h) {
   // U arena grows level by level (sizes depend on the children's ranks)
   double* U = nullptr;
   int64_t ucap = 0, uused = 0;
+  bool exchanged = h->nranks == 1;
   for (int l = h->depth; l >= 1; l--) {
-    int base = h->lvl_start[l], count = h->lvl_start[l + 1] - base;
+    if (!exchanged && l < h->cut) {  // sharded: every rank's skeletons of the levels >= cut
+      exchange_slots(h, h->k, h->sk);
+      exchanged = true;
+    }
+    const LevelRange lr = level_range(h, l);
+    int base = lr.begin, count = lr.end - lr.begin;
     if (count == 0) continue;
     Scratch sz(sizeof(int64_t) * 2 * (count + 1) + 16, s), off(sizeof(int64_t) * 2 * (count + 1), s);
     int* smax = reinterpret_cast<int*>(sz.as<int64_t>() + 2 * (count + 1));  // one max per class
@@ -261,12 +267,8 @@ void id_sweep(h2_handle* h) {
       switch (h->d) {
 #define H2_ID_CASE(DD)                                                                                        \
   case DD: {                                                                                                  \
-    static bool attr_set = false;                                                                             \
-    if (!attr_set) {                                                                                          \
-      H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_smem<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+        H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_smem<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                                        kIdSmemMax));                                                          \
-      attr_set = true;                                                                                        \
-    }                                                                                                         \
     id_kernel_smem<DD><<<count, kIdSmemThreads, smem_bytes[cls], s>>>(                                        \
         base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child, h->nchild, \
         h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>(), cls);       \
@@ -281,6 +283,7 @@ void id_sweep(h2_handle* h) {
     h->gpu_launches += 5;
     uused += tot[1];  // u_off[] holds global offsets into the arena
   }
+  if (!exchanged) exchange_slots(h, h->k, h->sk);
   h->U = U ? U : static_cast<double*>(dev_alloc(8, s));
   h->allocs.push_back(h->U);
   h->u_total = uused;

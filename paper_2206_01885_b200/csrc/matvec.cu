@@ -79,10 +79,11 @@ __global__ void coupling_kernel(int64_t np, const int2* __restrict__ pairs, cons
   }
 }
 
+// leaf outputs only for leaves whose first point lies in [p_lo, p_hi) (sharded: the row owner)
 __global__ void down_kernel(int base, int r, const int* __restrict__ is_leaf, const int* __restrict__ nbegin,
                             const int* __restrict__ parent, const int* __restrict__ k, const int* __restrict__ xbar_n,
                             const int* __restrict__ child_off, const int64_t* __restrict__ u_off,
-                            const double* __restrict__ U, double* yh, double* yt) {
+                            const double* __restrict__ U, int p_lo, int p_hi, double* yh, double* yt) {
   const int i = base + blockIdx.x;
   const int ki = k[i];
   if (ki == 0) return;
@@ -99,7 +100,7 @@ __global__ void down_kernel(int base, int r, const int* __restrict__ is_leaf, co
     }
   }
   __syncthreads();
-  if (is_leaf[i]) {
+  if (is_leaf[i] && nbegin[i] >= p_lo && nbegin[i] < p_hi) {
     const int nx = xbar_n[i];
     const double* Ui = U + u_off[i];
     for (int a = threadIdx.x; a < nx; a += blockDim.x) {
@@ -166,31 +167,44 @@ static void far_near(const h2_handle* h, double p2, const double* zh, double* yh
   }
 }
 
+// Sharded handles (shard.cu): the upward pass runs on the owned subtrees, the z^ of the levels
+// >= cut are summed over the ranks (each node is non-zero on its owner only), and the levels
+// above the cut are then computed by every rank; coupling and nearfield apply the rank's own
+// (row-owned) blocks in both directions, so y^ and y are partial sums completed by allreduces.
 void matvec(const h2_handle* h, const double* x, double* y) {
   cudaStream_t s = h->stream;
   const int64_t n = h->n;
   const int nn = h->nnodes, r = h->r;
+  const bool sharded = h->nranks > 1;
   Scratch xt(sizeof(double) * n, s), yt(sizeof(double) * n, s), zh(sizeof(double) * (size_t)nn * r, s),
       yh(sizeof(double) * (size_t)nn * r, s);
   H2_CUDA_TRY(cudaMemsetAsync(yt.p, 0, sizeof(double) * n, s));
   H2_CUDA_TRY(cudaMemsetAsync(yh.p, 0, sizeof(double) * (size_t)nn * r, s));
   H2_CUDA_TRY(cudaMemsetAsync(zh.p, 0, sizeof(double) * (size_t)nn * r, s));
   permute_in_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, h->perm, n, xt.as<double>());
-  for (int l = h->depth; l >= 1; l--) {
-    int base = h->lvl_start[l], cnt = h->lvl_start[l + 1] - base;
-    if (cnt > 0)
-      up_kernel<<<cnt, kMvThreads, 0, s>>>(base, r, h->is_leaf, h->nbegin, h->first_child, h->nchild, h->k,
-                                           h->xbar_n, h->child_off, h->u_off, h->U, xt.as<double>(), zh.as<double>());
-  }
+  auto up = [&](int l) {
+    const LevelRange lr = level_range(h, l);
+    if (lr.end > lr.begin)
+      up_kernel<<<lr.end - lr.begin, kMvThreads, 0, s>>>(lr.begin, r, h->is_leaf, h->nbegin, h->first_child,
+                                                         h->nchild, h->k, h->xbar_n, h->child_off, h->u_off, h->U,
+                                                         xt.as<double>(), zh.as<double>());
+  };
+  const int cut = sharded ? (h->cut > 1 ? h->cut : 1) : 1;
+  for (int l = h->depth; l >= cut; l--) up(l);
+  if (sharded) comm_allreduce_sum(h->comm, zh.as<double>(), zh.as<double>(), (int64_t)nn * r, s);
+  for (int l = cut - 1; l >= 1; l--) up(l);
   const double p2 = kernel_p2(h->kid, h->kp);
   far_near(h, p2, zh.as<double>(), yh.as<double>(), xt.as<double>(), yt.as<double>(), 0);
+  if (sharded) comm_allreduce_sum(h->comm, yh.as<double>(), yh.as<double>(), (int64_t)nn * r, s);
   for (int l = 1; l <= h->depth; l++) {
-    int base = h->lvl_start[l], cnt = h->lvl_start[l + 1] - base;
-    if (cnt > 0)
-      down_kernel<<<cnt, kMvThreads, 0, s>>>(base, r, h->is_leaf, h->nbegin, h->parent, h->k, h->xbar_n,
-                                             h->child_off, h->u_off, h->U, yh.as<double>(), yt.as<double>());
+    const LevelRange lr = level_range(h, l);
+    if (lr.end > lr.begin)
+      down_kernel<<<lr.end - lr.begin, kMvThreads, 0, s>>>(lr.begin, r, h->is_leaf, h->nbegin, h->parent, h->k,
+                                                           h->xbar_n, h->child_off, h->u_off, h->U, h->p_lo, h->p_hi,
+                                                           yh.as<double>(), yt.as<double>());
   }
   far_near(h, p2, zh.as<double>(), yh.as<double>(), xt.as<double>(), yt.as<double>(), 1);
+  if (sharded) comm_allreduce_sum(h->comm, yt.as<double>(), yt.as<double>(), n, s);
   permute_out_kernel<<<grid_for(n, 256), 256, 0, s>>>(yt.as<double>(), h->perm, n, y);
   H2_CHECK_LAUNCH();
   H2_CUDA_TRY(cudaStreamSynchronize(s));
