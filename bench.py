@@ -12,8 +12,9 @@ blocks and configs[4] ~198 GB, so neither fits; they are parity cases, not bench
 Timing: W untimed warm-up builds, then K timed builds, each bracketed by CUDA events on the
 library's stream with a barrier + synchronize on both sides of the timed region; L2 is flushed
 (512 MiB write) before every timed build; max over ranks.  value = total points built by all
-ranks / time (Mpoints/s).  Multi-GPU (torchrun): every rank builds its own independent problem
-instance of the same config (weak scaling, no data-path collective).
+ranks / time (Mpoints/s).  Multi-GPU (torchrun, N > 1): ONE problem of the same config built by the
+sharded path (subtree sharding below a cut level, X^* / skeleton allgathers over
+NCCL, row-owned block fill; include/h2.h "sharded build") -- strong scaling, value = n / time.
 --impl reference times the fp64 CPU oracle (the reference for this tier) on the host cores.
 """
 from __future__ import annotations
@@ -192,9 +193,15 @@ def run_ours(args):
     cfg = args.config
     c = synth.CONFIGS[cfg]
     n = c["n"] if args.n is None else args.n
-    # every rank builds its own independent instance (weak scaling); rank 0 uses the config's seed
-    pts_np = synth.points(cfg, n) if rank == 0 else _rank_points(cfg, n, rank)
+    # N > 1: every rank holds the same points (replicated) and builds its share of one H^2
+    pts_np = synth.points(cfg, n)
     pts = torch.from_numpy(pts_np).cuda()
+    comm = None
+    if ws > 1:
+        import torch.distributed as dist
+        uid = [P.H2Comm.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = P.H2Comm.nccl(ws, rank, uid[0])
     stream = torch.cuda.Stream()
     kp = list(c["params"])
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
@@ -205,6 +212,8 @@ def run_ours(args):
         o.timing = 1
         o.stream = stream.cuda_stream
         o.points_on_host = 1 if host else 0
+        if comm is not None:
+            o.comm = comm.ptr
         return o
 
     def one(host=False, src=None):
@@ -244,7 +253,7 @@ def run_ours(args):
     clocks = sampler.stop()
 
     t_step = max_over_ranks(float(np.mean(times)), ws)
-    value = ws * n / (t_step * 1e-3) / 1e6
+    value = n / (t_step * 1e-3) / 1e6
 
     # e2e: same build through the C ABI from pinned HOST memory (H2D inside the call) plus the
     # device->host read of the step's result (the skeleton ranks k_i of every node)
@@ -264,7 +273,7 @@ def run_ours(args):
         e2e_times.append(t1 - t0)
         P.h2_free(h)
     e2e_t = max_over_ranks(float(np.mean(e2e_times)), ws)
-    e2e = {"value": round(ws * n / e2e_t / 1e6, 4), "unit": UNIT, "h2d_bytes_per_step": h2d,
+    e2e = {"value": round(n / e2e_t / 1e6, 4), "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": int(d2h)}
 
     # roofline of the dominant kernel (nearfield fill, a10): algorithmic bytes = 8 B per stored entry
@@ -294,11 +303,12 @@ def run_ours(args):
         mean_stages = {k: round(float(np.mean([s[k] for s in stages])), 3) for k in stages[0]}
         line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(t_step, 3), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload_desc(cfg), "n_per_gpu": n, "r": info["r"], "nnodes": info["nnodes"],
                            "stored_bytes": info["stored_bytes"], "coupling_entries": info["coupling_entries"],
                            "nearfield_entries": info["nearfield_entries"],
-                           "parallelism": "single GPU" if ws == 1 else f"{ws} independent instances (weak)",
+                           "parallelism": "single GPU" if ws == 1 else
+                           f"sharded over {ws} GPUs (subtrees below the cut level; NCCL allgathers)",
                            "l2": "flushed (512 MiB write) before every timed step",
                            "wall_s_timed_region": round(t_wall, 3)},
                 "stages_ms": mean_stages, "clocks": clocks, "e2e": e2e, "gpu_launches": launches,
@@ -308,13 +318,10 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
+        dist.barrier()
+        comm.close()
         dist.destroy_process_group()
     return 0
-
-
-def _rank_points(cfg, n, rank):
-    """Independent instance per rank: same distribution, seed offset by the rank."""
-    return synth.points(cfg, n, seed_offset=10_000 * rank)
 
 
 def main():

@@ -34,7 +34,7 @@ static void free_handle(h2_handle* h) {
 // highest priority; `side` carries the nearfield fill (a10) at the lowest, so the latency-bound
 // level kernels take SMs first whenever a fill CTA retires.
 struct BuildStreams {
-  cudaStream_t main = nullptr, side = nullptr;
+  cudaStream_t main = nullptr, side = nullptr, calib = nullptr;
 };
 static BuildStreams& build_streams() {
   thread_local BuildStreams per_dev[64];
@@ -46,6 +46,7 @@ static BuildStreams& build_streams() {
     H2_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     H2_CUDA_TRY(cudaStreamCreateWithPriority(&b.main, cudaStreamNonBlocking, greatest));
     H2_CUDA_TRY(cudaStreamCreateWithPriority(&b.side, cudaStreamNonBlocking, least));
+    H2_CUDA_TRY(cudaStreamCreateWithPriority(&b.calib, cudaStreamNonBlocking, greatest));
   }
   return b;
 }
@@ -149,16 +150,23 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
       pts = staged.as<double>();
     }
     NfJob nf;
+    CalibJob cal;
     mark(0);
     build_tree(h, pts);  // a1-a3
     mark(1);
+    const bool calibrated = o.r_override <= 0;
+    if (calibrated) {  // a5 phase 0 overlaps a4 (calib.cu)
+      H2_CUDA_TRY(cudaEventRecord(fork_ev, h->stream));
+      H2_CUDA_TRY(cudaStreamWaitEvent(bs.calib, fork_ev, 0));
+      calibrate_begin(h, bs.calib, cal);
+    }
     build_lists(h);  // a4
     if (h->nranks > 1) shard_plan(h);  // cut level, owned subtrees and block rows (shard.cu)
     mark(2);
     // a10 needs only the tree and the nearfield list: it starts now on the side stream and
     // overlaps a5-a9 (serial_fill(): after a9 on the main stream instead)
     if (!serial_fill()) fill_nearfield_begin(h, bs.side, o.storage, o.mem_budget_bytes, nf);
-    h->r = o.r_override > 0 ? o.r_override : calibrate(h);  // a5
+    h->r = calibrated ? calibrate_end(h, cal) : o.r_override;  // a5
     mark(3);
     hidr_up(h);  // a6
     mark(4);

@@ -6,6 +6,9 @@
 // K(Z1, Z2*) at tolerance 1e-3 eps, e = ||K(Z1,Z2) - U K(Z1^,Z2)||_F / ||K(Z1,Z2)||_F; the level's
 // budget is the first m^d with e < 1e-2 eps, or m^d >= 256 (pass-through); r = max over levels.
 // All (level, m) trials run as one batched launch: one CTA per trial.
+#include <algorithm>
+#include <cstring>
+
 #include "cpqr.cuh"
 #include "vol.cuh"
 
@@ -127,9 +130,98 @@ __global__ void level_has_il_kernel(int nnodes, const int* __restrict__ level, c
   if (i < nnodes && il_off[i + 1] > il_off[i]) has[level[i]] = 1;
 }
 
-int calibrate(h2_handle* h) {
-  cudaStream_t s = h->stream;
+// Page-locked host staging for the trial parameters and pass flags (per host thread; slot 0 =
+// phase 0, slot 1 = phase 1): asynchronous copies to / from pageable memory would make the host
+// wait for the trials and serialise phase 0 with the lists.
+static char* pinned_slot(int slot, size_t bytes) {
+  thread_local char* p[2] = {nullptr, nullptr};
+  thread_local size_t cap[2] = {0, 0};
+  if (cap[slot] < bytes) {
+    if (p[slot]) cudaFreeHost(p[slot]);
+    p[slot] = nullptr;
+    cap[slot] = 0;
+    const size_t c = std::max<size_t>(bytes, 64 << 10);
+    H2_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&p[slot]), c));
+    cap[slot] = c;
+  }
+  return p[slot];
+}
+
+// One batch of (level, m) trials on stream s; the per-trial pass flags land in job.pass_h
+// (page-locked) once the stream has reached the end of the batch.
+static void launch_trials(h2_handle* h, cudaStream_t s, int slot, const std::vector<double>& wl,
+                          const std::vector<int>& lv, const std::vector<int>& mv, CalibJob& job) {
+  const int T = (int)wl.size();
+  job.T = T;
+  if (T == 0) return;
   const int d = h->d;
+  const double p2 = kernel_p2(h->kid, h->kp);
+  const int batch = 256;
+  job.work = Scratch(sizeof(CalWork) * (T < batch ? T : batch), s);
+  job.params = Scratch(sizeof(double) * T + sizeof(int) * 2 * T, s);
+  job.outs = Scratch(sizeof(double) * T + sizeof(int) * T, s);
+  double* dw = job.params.as<double>();
+  int* dl = reinterpret_cast<int*>(dw + T);
+  int* dm = dl + T;
+  double* derr = job.outs.as<double>();
+  int* dpass = reinterpret_cast<int*>(derr + T);
+  const size_t in_bytes = sizeof(double) * T + sizeof(int) * 2 * T;
+  char* hin = pinned_slot(slot, in_bytes + sizeof(int) * T);
+  std::memcpy(hin, wl.data(), sizeof(double) * T);
+  std::memcpy(hin + sizeof(double) * T, lv.data(), sizeof(int) * T);
+  std::memcpy(hin + sizeof(double) * T + sizeof(int) * T, mv.data(), sizeof(int) * T);
+  H2_CUDA_TRY(cudaMemcpyAsync(dw, hin, in_bytes, cudaMemcpyHostToDevice, s));
+  for (int b0 = 0; b0 < T; b0 += batch) {
+    int nb = T - b0 < batch ? T - b0 : batch;
+    switch (d) {
+#define H2_CAL_CASE(DD)                                                                                  \
+  case DD:                                                                                               \
+    calib_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, h->id_tol, h->tau, dw + b0, dl + b0, dm + b0, \
+                                                job.work.as<CalWork>(), derr + b0, dpass + b0);           \
+    break;
+      H2_CAL_CASE(1) H2_CAL_CASE(2) H2_CAL_CASE(3) H2_CAL_CASE(4)
+      H2_CAL_CASE(5) H2_CAL_CASE(6) H2_CAL_CASE(7) H2_CAL_CASE(8)
+#undef H2_CAL_CASE
+    }
+    H2_CHECK_LAUNCH();
+    h->gpu_launches += 1;
+  }
+  job.pass_h = reinterpret_cast<int*>(hin + in_bytes);
+  H2_CUDA_TRY(cudaMemcpyAsync(job.pass_h, dpass, sizeof(int) * T, cudaMemcpyDeviceToHost, s));
+  job.lv = lv;
+  job.mv = mv;
+}
+
+static long long grid_size(int d, int m) {
+  long long G = 1;
+  for (int c = 0; c < d; c++) G *= m;
+  return G;
+}
+
+// Phase 0, issued right after the tree (a1-a3) on the stream `s`: the trials with m^d <= 64 for
+// EVERY level 1..depth.  A trial depends only on the level's box width W 2^-l, not on the lists,
+// so it overlaps a4; calibrate_end keeps the levels that hold an admissible pair.
+void calibrate_begin(h2_handle* h, cudaStream_t s, CalibJob& job) {
+  job.stream = s;
+  std::vector<double> wl;
+  std::vector<int> lv, mv;
+  for (int l = 1; l <= h->depth; l++)
+    for (int m = 1;; m++) {
+      const long long G = grid_size(h->d, m);
+      if (G > 64 && m > 1) break;
+      wl.push_back(ldexp(h->W, -l));
+      lv.push_back(l);
+      mv.push_back(m);
+      if (G >= N) break;
+    }
+  launch_trials(h, s, 0, wl, lv, mv, job);
+  job.active = true;
+}
+
+// r = max over the levels holding an admissible pair of the first passing m^d (phase 0 results,
+// then phase 1 -- m^d > 64 -- on h->stream for the levels still open).
+int calibrate_end(h2_handle* h, CalibJob& job) {
+  cudaStream_t s = h->stream;
   Scratch hasd(sizeof(int) * 64, s);
   H2_CUDA_TRY(cudaMemsetAsync(hasd.p, 0, sizeof(int) * 64, s));
   level_has_il_kernel<<<(h->nnodes + 255) / 256, 256, 0, s>>>(h->nnodes, h->level, h->il_off, hasd.as<int>());
@@ -138,77 +230,45 @@ int calibrate(h2_handle* h) {
   int has[64];
   H2_CUDA_TRY(cudaMemcpyAsync(has, hasd.p, sizeof(int) * 64, cudaMemcpyDeviceToHost, s));
   H2_CUDA_TRY(cudaStreamSynchronize(s));
-  // Trials in two phases: first every m with m^d <= 64 (cheap blocks) for all levels, then the
-  // larger m only for levels that have not passed yet.  The chosen m is the first passing one
-  // either way (the phases only avoid evaluating trials beyond it).
-  std::vector<int> levels;
-  for (int l = 0; l <= h->depth; l++)
-    if (has[l]) levels.push_back(l);
-  int r = 1;
-  if (levels.empty()) return r;
-  const double p2 = kernel_p2(h->kid, h->kp);
-  auto Gof = [&](int m) {
-    long long G = 1;
-    for (int c = 0; c < d; c++) G *= m;
-    return G;
-  };
-  std::vector<int> chosen_m(levels.size(), 0);
-  for (int phase = 0; phase < 2; phase++) {
-    std::vector<double> wl;
-    std::vector<int> lv, mv, li;
-    for (size_t q = 0; q < levels.size(); q++) {
-      if (chosen_m[q]) continue;
-      for (int m = 1;; m++) {
-        const long long G = Gof(m);
-        const bool in_phase = phase == 0 ? (G <= 64 || m == 1) : (G > 64 || m == 1);
-        if (in_phase && !(phase == 1 && G <= 64)) {
-          wl.push_back(ldexp(h->W, -levels[q]));
-          lv.push_back(levels[q]);
-          mv.push_back(m);
-          li.push_back((int)q);
-        }
-        if (G >= N || (phase == 0 && G > 64)) break;
+  if (job.active) H2_CUDA_TRY(cudaStreamSynchronize(job.stream));
+  std::vector<int> chosen(h->depth + 1, 0);
+  for (int t = 0; t < job.T; t++)  // trials of a level are in increasing m: keep the first pass
+    if (job.pass_h[t] && !chosen[job.lv[t]]) chosen[job.lv[t]] = job.mv[t];
+  // release phase 0's buffers on h->stream (ordered after the synchronisation above)
+  job.work.s = job.params.s = job.outs.s = s;
+  job.work = Scratch();
+  job.params = Scratch();
+  job.outs = Scratch();
+  job.active = false;
+  std::vector<double> wl;
+  std::vector<int> lv, mv;
+  for (int l = 1; l <= h->depth; l++) {
+    if (!has[l] || chosen[l]) continue;
+    for (int m = 1;; m++) {
+      const long long G = grid_size(h->d, m);
+      if (G > 64) {
+        wl.push_back(ldexp(h->W, -l));
+        lv.push_back(l);
+        mv.push_back(m);
       }
+      if (G >= N) break;
     }
-    const int T = (int)wl.size();
-    if (T == 0) break;
-    const int batch = 256;
-    Scratch work(sizeof(CalWork) * (T < batch ? T : batch), s);
-    Scratch params(sizeof(double) * T + sizeof(int) * 2 * T, s), outs(sizeof(double) * T + sizeof(int) * T, s);
-    double* dw = params.as<double>();
-    int* dl = reinterpret_cast<int*>(dw + T);
-    int* dm = dl + T;
-    double* derr = outs.as<double>();
-    int* dpass = reinterpret_cast<int*>(derr + T);
-    H2_CUDA_TRY(cudaMemcpyAsync(dw, wl.data(), sizeof(double) * T, cudaMemcpyHostToDevice, s));
-    H2_CUDA_TRY(cudaMemcpyAsync(dl, lv.data(), sizeof(int) * T, cudaMemcpyHostToDevice, s));
-    H2_CUDA_TRY(cudaMemcpyAsync(dm, mv.data(), sizeof(int) * T, cudaMemcpyHostToDevice, s));
-    for (int b0 = 0; b0 < T; b0 += batch) {
-      int nb = T - b0 < batch ? T - b0 : batch;
-      switch (d) {
-#define H2_CAL_CASE(DD)                                                                                  \
-  case DD:                                                                                               \
-    calib_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, h->id_tol, h->tau, dw + b0, dl + b0, dm + b0, \
-                                                work.as<CalWork>(), derr + b0, dpass + b0);               \
-    break;
-        H2_CAL_CASE(1) H2_CAL_CASE(2) H2_CAL_CASE(3) H2_CAL_CASE(4)
-        H2_CAL_CASE(5) H2_CAL_CASE(6) H2_CAL_CASE(7) H2_CAL_CASE(8)
-#undef H2_CAL_CASE
-      }
-      H2_CHECK_LAUNCH();
-      h->gpu_launches += 1;
-    }
-    std::vector<int> pass(T);
-    H2_CUDA_TRY(cudaMemcpyAsync(pass.data(), dpass, sizeof(int) * T, cudaMemcpyDeviceToHost, s));
+  }
+  if (!wl.empty()) {
+    CalibJob p1;
+    launch_trials(h, s, 1, wl, lv, mv, p1);
     H2_CUDA_TRY(cudaStreamSynchronize(s));
-    for (int t = 0; t < T; t++)  // trials of a level are in increasing m: keep the first pass
-      if (pass[t] && (!chosen_m[li[t]] || mv[t] < chosen_m[li[t]])) chosen_m[li[t]] = mv[t];
+    for (int t = 0; t < p1.T; t++)
+      if (p1.pass_h[t] && !chosen[p1.lv[t]]) chosen[p1.lv[t]] = p1.mv[t];
   }
-  for (size_t q = 0; q < levels.size(); q++) {
-    const long long G = Gof(chosen_m[q]);
-    if (G > r) r = (int)G;
-  }
+  int r = 1;
+  for (int l = 1; l <= h->depth; l++)
+    if (has[l] && chosen[l]) r = (int)std::max<long long>(r, grid_size(h->d, chosen[l]));
   return r;
+}
+
+CalibJob::~CalibJob() {
+  if (active && stream) cudaStreamSynchronize(stream);  // error path: the trials may still run
 }
 
 }  // namespace h2

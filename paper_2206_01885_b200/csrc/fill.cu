@@ -11,6 +11,7 @@
 //    small blocks are balanced alike (unit -> pair map precomputed).
 //  * coupling (a9): k_i x k_j blocks are small (ranks <= r): one warp per pair, lanes over columns
 //    (column skeleton coordinates in registers), rows broadcast.
+#include <climits>
 #include <cstdlib>
 #include <cub/block/block_scan.cuh>
 
@@ -196,7 +197,14 @@ __global__ void __launch_bounds__(kFillThreads, MINB) nf_fill_kernel(int64_t nun
   }
 }
 
-// ---- coupling: one warp per pair ------------------------------------------------------------
+// ---- coupling: one warp per 32 consecutive pairs, entries flattened ---------------------------
+// Coupling blocks are small (k_i x k_j, ranks of a few to a few tens), so per-pair work is a
+// chain of dependent loads (pair -> ranks, offset -> skeleton indices -> coordinates).  A warp
+// takes 32 consecutive pairs at once: lane t loads pair t's metadata (one round of latency for
+// all 32), a warp scan gives the pairs' entry prefix, then the warp walks the concatenated
+// entries -- which are also consecutive in the output (blocks are stored in pair order), so every
+// store instruction writes 256 contiguous bytes -- each lane gathering its entry's two skeleton
+// points (L2-resident) and evaluating the kernel.
 template <int D, int KID>
 __global__ void __launch_bounds__(kFillThreads) cp_fill_kernel(int64_t np, const int2* __restrict__ pairs,
                                                                const int64_t* __restrict__ voff,
@@ -207,32 +215,50 @@ __global__ void __launch_bounds__(kFillThreads) cp_fill_kernel(int64_t np, const
   tab[threadIdx.x] = kExp2Tab256[threadIdx.x];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nunits = (np + 31) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t p = gw; p < np; p += nw) {
-    const int2 pr = pairs[p];
-    const int ki = k[pr.x], kj = k[pr.y];
-    const int* si = sk + (int64_t)pr.x * r;
-    const int* sj = sk + (int64_t)pr.y * r;
-    double* o = out + voff[p];
-    for (int c0 = 0; c0 < kj; c0 += 32) {
-      const int col = c0 + lane;
-      double xb[D];
-      if (col < kj) {
-        const int b = sj[col];
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < nunits; u += nw) {
+    const int64_t p = (u << 5) + lane;
+    int pi = 0, pj = 0, ki = 0, kj = 0;
+    if (p < np) {
+      const int2 pr = pairs[p];
+      pi = pr.x;
+      pj = pr.y;
+      ki = k[pi];
+      kj = k[pj];
+    }
+    int sz = ki * kj, pre = sz;  // inclusive scan of the pairs' sizes
 #pragma unroll
-        for (int c = 0; c < D; c++) xb[c] = X[c * n + b] * cs;
-      }
-      for (int row = 0; row < ki; row++) {
-        const int a = si[row];
-        double s = 0.0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, pre, 31);
+    pre -= sz;  // exclusive
+    double* o = out + voff[u << 5];
+    for (int e0 = 0; e0 < total; e0 += 32) {  // warp-uniform trip count: every shuffle is converged
+      const int e = e0 + lane;
+      // this entry's pair: the largest q with pre[q] <= e (size-0 pairs never win)
+      int q = 0;
 #pragma unroll
-        for (int c = 0; c < D; c++) {
-          double df = X[c * n + a] * cs - (col < kj ? xb[c] : 0.0);
-          s = fma(df, df, s);
-        }
-        if (col < kj) __stcs(o + (int64_t)row * kj + col, kernel_fill<KID>(s, tab));
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int cand = q + step;
+        const int pc = __shfl_sync(0xffffffffu, pre, cand & 31);
+        if (cand < 32 && pc <= e) q = cand;
       }
+      const int pre_q = __shfl_sync(0xffffffffu, pre, q);
+      const int i_q = __shfl_sync(0xffffffffu, pi, q), j_q = __shfl_sync(0xffffffffu, pj, q);
+      const int kj_q = __shfl_sync(0xffffffffu, kj, q);
+      if (e >= total) continue;
+      const int loc = e - pre_q, row = loc / kj_q, col = loc - row * kj_q;
+      const int a = sk[(int64_t)i_q * r + row], b = sk[(int64_t)j_q * r + col];
+      double sq = 0.0;
+#pragma unroll
+      for (int c = 0; c < D; c++) {
+        const double df = X[c * n + a] * cs - X[c * n + b] * cs;
+        sq = fma(df, df, sq);
+      }
+      __stcs(o + e, kernel_fill<KID>(sq, tab));
     }
   }
 }
@@ -256,6 +282,24 @@ static int nf_units_per_warp() {
   return v;
 }
 
+// H2_NF_SMEM (tuning knob, read once): dynamic shared memory requested by (and unused in) the
+// nearfield kernel, to cap how many of its CTAs an SM holds and leave room for the concurrent
+// level kernels of the main stream.
+static int nf_smem_reserve() {
+  static const int v = [] {
+    const char* e = getenv("H2_NF_SMEM");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <class K, class... A>
+static void launch_nf(K kernel, unsigned g, cudaStream_t s, A... args) {
+  const int sm = nf_smem_reserve();
+  if (sm > 48 * 1024) H2_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  kernel<<<g, kFillThreads, sm, s>>>(args...);
+}
+
 template <int KID>
 static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_t nwork, int64_t np, const int* umap,
                             const int64_t* uoff, const int2* pairs, const int64_t* voff, const double* Xs, double cs,
@@ -269,25 +313,25 @@ static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_
     switch (h->d) {
       case 2:
         switch (nf_variant()) {  // tuning variants of the D = 2 kernel (CW, RU, MINB)
-          case 1: nf_fill_kernel<2, KID, 4, 1, 4><<<g, kFillThreads, 0, s>>>(H2_NF_ARGS); break;
-          case 2: nf_fill_kernel<2, KID, 4, 1, 2><<<g, kFillThreads, 0, s>>>(H2_NF_ARGS); break;
-          case 3: nf_fill_kernel<2, KID, 6, 1, 2><<<g, kFillThreads, 0, s>>>(H2_NF_ARGS); break;
-          case 4: nf_fill_kernel<2, KID, 8, 1, 1><<<g, kFillThreads, 0, s>>>(H2_NF_ARGS); break;
-          case 5: nf_fill_kernel<2, KID, 2, 1, 4><<<g, kFillThreads, 0, s>>>(H2_NF_ARGS); break;
-          default: nf_fill_kernel<2, KID, 8, 1, 2><<<g, kFillThreads, 0, s>>>(H2_NF_ARGS); break;
+          case 1: launch_nf(nf_fill_kernel<2, KID, 4, 1, 4>, g, s, H2_NF_ARGS); break;
+          case 2: launch_nf(nf_fill_kernel<2, KID, 4, 1, 2>, g, s, H2_NF_ARGS); break;
+          case 3: launch_nf(nf_fill_kernel<2, KID, 6, 1, 2>, g, s, H2_NF_ARGS); break;
+          case 4: launch_nf(nf_fill_kernel<2, KID, 8, 1, 1>, g, s, H2_NF_ARGS); break;
+          case 5: launch_nf(nf_fill_kernel<2, KID, 2, 1, 4>, g, s, H2_NF_ARGS); break;
+          default: launch_nf(nf_fill_kernel<2, KID, 8, 1, 2>, g, s, H2_NF_ARGS); break;
         }
         break;
 #define H2_NF_CASE(DD) \
   case DD:             \
-    nf_fill_kernel<DD, KID, warp_slots(DD), 1, 2><<<g, kFillThreads, 0, s>>>(H2_NF_ARGS); break;
+    launch_nf(nf_fill_kernel<DD, KID, warp_slots(DD), 1, 2>, g, s, H2_NF_ARGS); break;
       H2_NF_CASE(1) H2_NF_CASE(3) H2_NF_CASE(4)
       H2_NF_CASE(5) H2_NF_CASE(6) H2_NF_CASE(7) H2_NF_CASE(8)
 #undef H2_NF_CASE
 #undef H2_NF_ARGS
     }
   } else {
-    int64_t blocks = (np + 7) / 8;
-    unsigned g = (unsigned)(blocks < 148 * 8 ? blocks : 148 * 8);
+    const int64_t blocks = ((np + 31) / 32 + 7) / 8;  // one warp per 32 pairs, 8 warps per CTA
+    unsigned g = (unsigned)(blocks < ((int64_t)1 << 30) ? blocks : ((int64_t)1 << 30));
     switch (h->d) {
 #define H2_CP_CASE(DD)                                                                                        \
   case DD:                                                                                                    \
