@@ -115,7 +115,7 @@ __global__ void unit_map_kernel(int64_t np, const int64_t* __restrict__ uoff, in
 // Coordinates are pre-scaled (kernel_cscale), so sq is the kernel's own argument.
 template <int D, int KID, int NS>
 __device__ __forceinline__ void nf_unit_rows(const double* __restrict__ xr, int64_t n, const double (&xb)[8][D],
-                                             const bool (&ok)[8], int r0, int r1, int nj, double* o,
+                                             bool last_ok, int r0, int r1, int nj, double* o,
                                              const double* __restrict__ tab) {
   double xa[D];
 #pragma unroll
@@ -137,8 +137,8 @@ __device__ __forceinline__ void nf_unit_rows(const double* __restrict__ xr, int6
       v[s] = kernel_fill<KID>(sq, tab);
     }
 #pragma unroll
-    for (int s = 0; s < NS; s++)
-      if (ok[s]) __stcs(o + 32 * s, v[s]);
+    for (int s = 0; s < NS; s++)  // slots before the last are full (see nslot)
+      if (s < NS - 1 || last_ok) __stcs(o + 32 * s, v[s]);
 #pragma unroll
     for (int c = 0; c < D; c++) xa[c] = xn[c];
   }
@@ -172,27 +172,28 @@ __global__ void __launch_bounds__(kFillThreads, MINB) nf_fill_kernel(int64_t nun
     const int r0 = rb * R, c0 = cb * WC;
     const int r1 = ni < r0 + R ? ni : r0 + R;
     double xb[8][D];
-    bool ok[8];
+
 #pragma unroll
     for (int s = 0; s < 8; s++) {
       const int col = c0 + lane + 32 * s;
-      ok[s] = s < CW && col < nj;
+      const bool ok = s < CW && col < nj;
 #pragma unroll
-      for (int c = 0; c < D; c++) xb[s][c] = ok[s] ? X[c * n + bj + col] : 0.0;
+      for (int c = 0; c < D; c++) xb[s][c] = ok ? X[c * n + bj + col] : 0.0;
     }
     double* o = out + voff[p] + (int64_t)r0 * nj + c0 + lane;
     const double* xr = X + bi;
     int nslot = (nj - c0 + 31) >> 5;  // warp-uniform: slots with at least one column
     if (nslot > CW) nslot = CW;
+    const bool last_ok = c0 + lane + 32 * (nslot - 1) < nj;  // only the last slot can be partial
     switch (nslot) {
-      case 1: nf_unit_rows<D, KID, 1>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
-      case 2: nf_unit_rows<D, KID, (CW < 2 ? CW : 2)>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
-      case 3: nf_unit_rows<D, KID, (CW < 3 ? CW : 3)>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
-      case 4: nf_unit_rows<D, KID, (CW < 4 ? CW : 4)>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
-      case 5: nf_unit_rows<D, KID, (CW < 5 ? CW : 5)>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
-      case 6: nf_unit_rows<D, KID, (CW < 6 ? CW : 6)>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
-      case 7: nf_unit_rows<D, KID, (CW < 7 ? CW : 7)>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
-      default: nf_unit_rows<D, KID, CW>(xr, n, xb, ok, r0, r1, nj, o, tab); break;
+      case 1: nf_unit_rows<D, KID, 1>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
+      case 2: nf_unit_rows<D, KID, (CW < 2 ? CW : 2)>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
+      case 3: nf_unit_rows<D, KID, (CW < 3 ? CW : 3)>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
+      case 4: nf_unit_rows<D, KID, (CW < 4 ? CW : 4)>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
+      case 5: nf_unit_rows<D, KID, (CW < 5 ? CW : 5)>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
+      case 6: nf_unit_rows<D, KID, (CW < 6 ? CW : 6)>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
+      case 7: nf_unit_rows<D, KID, (CW < 7 ? CW : 7)>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
+      default: nf_unit_rows<D, KID, CW>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
     }
   }
 }

@@ -14,17 +14,27 @@ constexpr int kIdThreads = 256;
 constexpr int kIdSmemThreads = 128;
 constexpr int kIdSmemMax = 100 * 1024;  // dynamic shared memory budget of the shared-memory path
 
-// shared-memory size classes: nodes are launched per class so small nodes get high occupancy
-__host__ __device__ __forceinline__ int id_class(int64_t bytes) { return bytes <= 24576 ? 0 : (bytes <= 49152 ? 1 : 2); }
+// shared-memory size classes: nodes are launched per class so small nodes get high occupancy;
+// the bounds are ~228 KB / {9, 7, 6, 5, 4, 3, 2} CTAs per SM (minus the static part)
+constexpr int kIdClasses = 7;
+__host__ __device__ __forceinline__ int id_class_bound(int c) {
+  return c == 0 ? 24 * 1024 : c == 1 ? 31 * 1024 : c == 2 ? 36 * 1024 : c == 3 ? 44 * 1024
+       : c == 4 ? 55 * 1024 : c == 5 ? 74 * 1024 : kIdSmemMax;
+}
+__host__ __device__ __forceinline__ int id_class(int64_t bytes) {
+  int c = 0;
+  while (c < kIdClasses - 1 && bytes > id_class_bound(c)) c++;
+  return c;
+}
 
 // shared-memory footprint of one node's ID: M (ny x nx) + nrm2 (nx) + v (ny) + piv, Xbar (2 nx ints)
-// (+ staged coordinates of Xbar and Y^*: 8 (nx + ny) kMaxD bytes at most, + the exp table)
-__host__ __device__ __forceinline__ int64_t id_smem_bytes(int ny, int nx) {
-  return 8LL * ((int64_t)ny * nx + nx + ny) + 8LL * nx + 8LL * kMaxD * (nx + ny) + 512;
+// (+ staged coordinates of Xbar and Y^*: 8 (nx + ny) d bytes, + the exp table)
+__host__ __device__ __forceinline__ int64_t id_smem_bytes(int ny, int nx, int d) {
+  return 8LL * ((int64_t)ny * nx + nx + ny) + 8LL * nx + 8LL * d * (nx + ny) + 512;
 }
 
 // per node of one level: |Xbar| (and child offsets), workspace and U sizes
-__global__ void id_sizes_kernel(int base, int count, const int* __restrict__ is_leaf, const int* __restrict__ nbegin,
+__global__ void id_sizes_kernel(int base, int count, int d, const int* __restrict__ is_leaf, const int* __restrict__ nbegin,
                                 const int* __restrict__ nend, const int* __restrict__ first_child,
                                 const int* __restrict__ nchild, const int* __restrict__ ys_cnt,
                                 const int* __restrict__ k, int* xbar_n, int* child_off, int64_t* wsz, int64_t* usz,
@@ -52,10 +62,10 @@ __global__ void id_sizes_kernel(int base, int count, const int* __restrict__ is_
   xbar_n[i] = nx;
   int mn = nx < ny ? nx : ny;
   // workspace: M (ny*nx doubles) + nrm2 (nx) + v (ny) + piv/xbar (2*nx ints, as doubles)
-  const bool fits = id_smem_bytes(ny, nx) <= kIdSmemMax;
+  const bool fits = id_smem_bytes(ny, nx, d) <= kIdSmemMax;
   wsz[t] = nx > 0 && !fits ? (int64_t)ny * nx + nx + ny + nx + 2 : 0;
   usz[t] = (int64_t)nx * mn;
-  if (nx > 0 && fits) atomicMax(smax + id_class(id_smem_bytes(ny, nx)), (int)id_smem_bytes(ny, nx));
+  if (nx > 0 && fits) atomicMax(smax + id_class(id_smem_bytes(ny, nx, d)), (int)id_smem_bytes(ny, nx, d));
 }
 
 __global__ void __launch_bounds__(kIdThreads) id_kernel(
@@ -74,7 +84,7 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
     if (tid == 0) kout[i] = 0;
     return;
   }
-  if (id_smem_bytes(ny, nx) <= kIdSmemMax) return;  // handled by id_kernel_smem
+  if (id_smem_bytes(ny, nx, d) <= kIdSmemMax) return;  // handled by id_kernel_smem
   double* M = work + woff[t];
   double* nrm2 = M + (int64_t)ny * nx;
   double* v = nrm2 + nx;
@@ -130,7 +140,7 @@ __global__ void __launch_bounds__(kIdSmemThreads) id_kernel_smem(
   const int nx = xbar_n[i];
   const int ny = ys_cnt[i];
   const int tid = threadIdx.x;
-  if (nx == 0 || id_smem_bytes(ny, nx) > kIdSmemMax || id_class(id_smem_bytes(ny, nx)) != cls) return;
+  if (nx == 0 || id_smem_bytes(ny, nx, D) > kIdSmemMax || id_class(id_smem_bytes(ny, nx, D)) != cls) return;
   double* M = sh;
   double* nrm2 = M + (int64_t)ny * nx;
   double* v = nrm2 + nx;
@@ -229,22 +239,22 @@ void id_sweep(h2_handle* h) {
     const LevelRange lr = level_range(h, l);
     int base = lr.begin, count = lr.end - lr.begin;
     if (count == 0) continue;
-    Scratch sz(sizeof(int64_t) * 2 * (count + 1) + 16, s), off(sizeof(int64_t) * 2 * (count + 1), s);
+    Scratch sz(sizeof(int64_t) * 2 * (count + 1) + 4 * kIdClasses, s), off(sizeof(int64_t) * 2 * (count + 1), s);
     int* smax = reinterpret_cast<int*>(sz.as<int64_t>() + 2 * (count + 1));  // one max per class
-    H2_CUDA_TRY(cudaMemsetAsync(smax, 0, 3 * sizeof(int), s));
+    H2_CUDA_TRY(cudaMemsetAsync(smax, 0, kIdClasses * sizeof(int), s));
     int64_t *wsz = sz.as<int64_t>(), *usz = wsz + count + 1;
     int64_t *woff = off.as<int64_t>(), *uo = woff + count + 1;
-    id_sizes_kernel<<<(count + 1 + 255) / 256, 256, 0, s>>>(base, count, h->is_leaf, h->nbegin, h->nend,
+    id_sizes_kernel<<<(count + 1 + 255) / 256, 256, 0, s>>>(base, count, h->d, h->is_leaf, h->nbegin, h->nend,
                                                             h->first_child, h->nchild, h->ys_cnt, h->k, h->xbar_n,
                                                             h->child_off, wsz, usz, smax);
     scan_excl_i64(wsz, woff, count + 1, s);
     scan_excl_i64(usz, uo, count + 1, s);
     H2_CHECK_LAUNCH();
     int64_t tot[2];
-    int smem_bytes[3] = {0, 0, 0};
+    int smem_bytes[kIdClasses] = {0};
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[0], woff + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[1], uo + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    H2_CUDA_TRY(cudaMemcpyAsync(smem_bytes, smax, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    H2_CUDA_TRY(cudaMemcpyAsync(smem_bytes, smax, kIdClasses * sizeof(int), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaStreamSynchronize(s));
     if (uused + tot[1] > ucap) {
       int64_t nc = uused + tot[1];
@@ -262,7 +272,7 @@ void id_sweep(h2_handle* h) {
                                            work.as<double>(), h->u_off + base, U, h->k, h->sk,
                                            ev.as<unsigned long long>());
     H2_CHECK_LAUNCH();
-    for (int cls = 0; cls < 3; cls++) {
+    for (int cls = 0; cls < kIdClasses; cls++) {
       if (smem_bytes[cls] == 0) continue;
       switch (h->d) {
 #define H2_ID_CASE(DD)                                                                                        \

@@ -98,13 +98,16 @@ def test_parity_config_shapes(name, cfg, n, q):
     g.close()
 
 
-def test_stored_blocks_sampled_against_kernel():
-    c = synth.CONFIGS[4]
-    pts = synth.points(4, 30000)
+@pytest.mark.parametrize("cfg,n", [(4, 30000), (3, 20000), (1, 8192), (5, 30000)])
+def test_stored_blocks_sampled_against_kernel(cfg, n):
+    """a9/a10 values (the fill's own fp64 kernel evaluation, kernel_fill) against the oracle's
+    kernel at the recorded points, for Matern, Gaussian (3-D and 5-D) and Coulomb."""
+    c = synth.CONFIGS[cfg]
+    pts = synth.points(cfg, n)
     g = gpu_build(pts, c["kernel"], list(c["params"]), c["id_tol"], c["q"])
     info = g.info()
     assert info["coupling_stored"] and info["nearfield_stored"]
-    Xt = g.export("TREE_X").reshape(-1, 2)
+    Xt = g.export("TREE_X").reshape(-1, c["d"])
     assert np.array_equal(Xt, pts[g.export("PERM")])
     rng = np.random.default_rng(0)
     # pair counts from the symmetric-once lists (i < j coupling with ranks, i <= j nearfield)
@@ -128,7 +131,8 @@ def test_stored_blocks_sampled_against_kernel():
             sz = (nodes[i, 2] - nodes[i, 1]) * (nodes[j, 2] - nodes[j, 1])
             kinds.append(1); pairs.append(p); entries.append(rng.integers(sz))
     val, rp, colp = P.h2_sample_blocks(g.h, kinds, pairs, entries)
-    ref = np.array([oracle.kernel(c["kernel"], c["params"][0], Xt[a], Xt[b]) for a, b in zip(rp, colp)])
+    kp = c["params"][0] if c["params"] else 0.0
+    ref = np.array([oracle.kernel(c["kernel"], kp, Xt[a], Xt[b]) for a, b in zip(rp, colp)])
     np.testing.assert_allclose(val, ref, rtol=1e-13, atol=1e-300)
     # the sampled rows / columns are the declared points of the pair
     so, si = g.export("SK_OFF"), g.export("SK_IDX")
