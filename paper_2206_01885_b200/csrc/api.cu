@@ -149,6 +149,7 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
                                   h->stream));
       pts = staged.as<double>();
     }
+    const int64_t prims0 = prim_launches();
     NfJob nf;
     CalibJob cal;
     mark(0);
@@ -180,6 +181,7 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
     mark(7);
     H2_CUDA_TRY(cudaEventRecord(join_ev, h->stream));
     H2_CUDA_TRY(cudaStreamWaitEvent(user, join_ev, 0));
+    h->gpu_launches += (int)(prim_launches() - prims0);
     h->stream = user;
     H2_CUDA_TRY(cudaStreamSynchronize(h->stream));
     if (h->timing) {

@@ -13,7 +13,6 @@
 //    (column skeleton coordinates in registers), rows broadcast.
 #include <climits>
 #include <cstdlib>
-#include <cub/block/block_scan.cuh>
 
 #include "h2_internal.cuh"
 
@@ -378,7 +377,7 @@ static void make_pairs(h2_handle* h, cudaStream_t s, int mode, int64_t& np, int2
                                                       pos.as<int64_t>(), pairs, size.as<int64_t>());
   scan_excl_i64(size.as<int64_t>(), voff, np + 1, s);
   H2_CHECK_LAUNCH();
-  h->gpu_launches += 5;
+  h->gpu_launches += 2;  // + the scans (prims.cu counts its own launches)
   entries = read1(voff + np, s);
 }
 
@@ -425,7 +424,7 @@ void fill_nearfield_begin(h2_handle* h, cudaStream_t side, int storage, int64_t 
     job.umap = Scratch(sizeof(int) * (nunits > 0 ? nunits : 1), side);
     unit_map_kernel<<<grid_for(np, 256), 256, 0, side>>>(np, job.uoff.as<int64_t>(), job.umap.as<int>());
     H2_CHECK_LAUNCH();
-    h->gpu_launches += 3;
+    h->gpu_launches += 2;
   }
   if (h->timing) H2_CUDA_TRY(cudaEventRecord(job.t0, side));
   if (nunits > 0) {

@@ -45,8 +45,7 @@ __global__ void __launch_bounds__(kHidrThreads) hidr_gather_kernel(
     const int* __restrict__ parent, const int64_t* __restrict__ il_off, const int* __restrict__ il_idx,
     const int* __restrict__ xs_cnt, const int* __restrict__ xs, const int* __restrict__ ys_cnt,
     const int* __restrict__ ys, int r, int* list) {
-  using Scan = cub::BlockScan<int, kHidrThreads>;
-  __shared__ typename Scan::TempStorage scan;
+  __shared__ BlockScanSmem<kHidrThreads> scan;
   const int t = blockIdx.x;
   const int i = base + t;
   int* out = list + off[t];
@@ -78,8 +77,8 @@ __global__ void __launch_bounds__(kHidrThreads) hidr_gather_kernel(
         cnt = xs_cnt[node];
       }
     }
-    int pos, agg;
-    Scan(scan).ExclusiveSum(cnt, pos, agg);
+    int agg;
+    const int pos = block_excl_sum<kHidrThreads>(cnt, &agg, scan);
     for (int a = 0; a < cnt; a++) out[pos0 + pos + a] = src[a];
     pos0 += agg;
     __syncthreads();
@@ -179,7 +178,7 @@ static void hidr_level(h2_handle* h, int mode, int l, unsigned long long* ev) {
   launch_vol(h->d, count, s, h->X, h->n, base, off.as<int64_t>(), list.as<int>(), h->r,
              mode == 0 ? h->xs_cnt : h->ys_cnt, mode == 0 ? h->xs : h->ys, ev);
   H2_CHECK_LAUNCH();
-  h->gpu_launches += 4;
+  h->gpu_launches += 3;
   if (mode == 0) launch_sel_box(h, base, count, h->xs_cnt, h->xs, h->xbox);
   else launch_sel_box(h, base, count, h->ys_cnt, h->ys, h->ybox);
 }

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kDownThreads) hidr_down_kernel(
     int* ys, unsigned long long* evals_alg, unsigned long long* evals_done) {
   extern __shared__ double gbox[];  // group g: lo at gbox[g*2D + c], hi at gbox[g*2D + D + c]
   __shared__ int sel[kVolSelCap];
-  __shared__ typename cub::BlockScan<int, kDownThreads>::TempStorage scan;
+  __shared__ BlockScanSmem<kDownThreads> scan;
   __shared__ double wlo[D][kDownWarps], whi[D][kDownWarps];
   __shared__ long long wcnt[kDownWarps];
   __shared__ double s_lo[D], s_hi[D], s_h[D];

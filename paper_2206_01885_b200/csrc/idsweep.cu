@@ -290,7 +290,7 @@ void id_sweep(h2_handle* h) {
       H2_CHECK_LAUNCH();
       h->gpu_launches += 1;
     }
-    h->gpu_launches += 5;
+    h->gpu_launches += 3;
     uused += tot[1];  // u_off[] holds global offsets into the arena
   }
   if (!exchanged) exchange_slots(h, h->k, h->sk);

@@ -71,12 +71,20 @@ __global__ void emit_kernel(const int2* __restrict__ fr, int64_t nf, const int64
   }
 }
 
-__global__ void row_count_kernel(const unsigned long long* __restrict__ keys, int64_t m, unsigned long long* cnt,
-                                 int* idx) {
+// (i << 32 | j) -> (i << bits | j): the sort then needs 2 bits key bits instead of 32 + bits
+__global__ void repack_kernel(unsigned long long* keys, int64_t m, int bits) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[e];
+    keys[e] = ((k >> 32) << bits) | (k & 0xffffffffULL);
+  }
+}
+
+__global__ void row_count_kernel(const unsigned long long* __restrict__ keys, int64_t m, int bits,
+                                 unsigned long long* cnt, int* idx) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
     unsigned long long k = keys[e];
-    atomicAdd(&cnt[k >> 32], 1ULL);
-    idx[e] = (int)(k & 0xffffffffULL);
+    atomicAdd(&cnt[k >> bits], 1ULL);
+    idx[e] = (int)(k & ((1ULL << bits) - 1ULL));
   }
 }
 
@@ -111,17 +119,20 @@ static void to_csr(h2_handle* h, unsigned long long* keys, int64_t m, int64_t*& 
   int bits = 1;
   while ((1LL << bits) <= h->nnodes) bits++;
   Scratch sorted(sizeof(unsigned long long) * (m > 0 ? m : 1), s);
-  if (m > 0) sort_keys_u64(keys, sorted.as<unsigned long long>(), m, 32 + bits, s);
+  if (m > 0) {
+    repack_kernel<<<grid_for(m, 256), 256, 0, s>>>(keys, m, bits);
+    sort_keys_u64(keys, sorted.as<unsigned long long>(), m, 2 * bits, s);
+  }
   off = halloc<int64_t>(h, h->nnodes + 1);
   idx = halloc<int>(h, m);
   Scratch cnt(sizeof(int64_t) * (h->nnodes + 1), s);
   H2_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, sizeof(int64_t) * (h->nnodes + 1), s));
   if (m > 0)
-    row_count_kernel<<<grid_for(m, 256), 256, 0, s>>>(sorted.as<unsigned long long>(), m,
+    row_count_kernel<<<grid_for(m, 256), 256, 0, s>>>(sorted.as<unsigned long long>(), m, bits,
                                                       cnt.as<unsigned long long>(), idx);
   scan_excl_i64(cnt.as<int64_t>(), off, h->nnodes + 1, s);
   H2_CHECK_LAUNCH();
-  h->gpu_launches += 6;
+  h->gpu_launches += 2;
 }
 
 void build_lists(h2_handle* h) {
@@ -146,7 +157,7 @@ void build_lists(h2_handle* h) {
     scan_excl_i64(cnear, onear, nf + 1, s);
     scan_excl_i64(cexp, oexp, nf + 1, s);
     H2_CHECK_LAUNCH();
-    h->gpu_launches += 4;
+    h->gpu_launches += 1;
     int64_t tot[3];
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[0], ofar + nf, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[1], onear + nf, sizeof(int64_t), cudaMemcpyDeviceToHost, s));

@@ -1,10 +1,11 @@
-// prims.cu -- device memory pool and the CUB primitives (scan, radix sort) used by the stages.
-#include <cub/cub.cuh>
+// prims.cu -- device memory pool and the device-wide primitives used by the stages: a single-pass
+// prefix sum (decoupled look-back) and a stable LSD radix sort (8-bit digits, one count / scan /
+// scatter round per digit) -- both written here, no library kernels.
 #include <map>
 #include <mutex>
 #include <unordered_map>
 
-#include "h2_internal.cuh"
+#include "prims.cuh"
 
 namespace h2 {
 
@@ -119,33 +120,235 @@ void hfree(h2_handle* h, void* p) {
     }
 }
 
-void scan_incl_i32(const int* in, int* out, int64_t n, cudaStream_t s) {
-  size_t tmp = 0;
-  H2_CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, tmp, in, out, n, s));
-  Scratch t(tmp, s);
-  H2_CUDA_TRY(cub::DeviceScan::InclusiveSum(t.p, tmp, in, out, n, s));
+// ==========================================================================================
+// Prefix sum in two launches, no inter-CTA waiting: (1) every tile of kScanTile items writes its
+// sum; (2) every tile adds up the sums of the tiles before it (a block reduction over at most a
+// few thousand values -- cheaper than a serial look-back chain at these sizes) and scans its
+// items.  Tiles are read warp-striped: warp w owns 32 kScanIPT consecutive items, read in
+// kScanIPT coalesced rounds of 32 and scanned round after round with a carry.
+// ==========================================================================================
+constexpr int kScanNT = 256, kScanIPT = 16, kScanTile = kScanNT * kScanIPT;
+
+static thread_local int64_t g_prim_launches = 0;  // kernels launched by the primitives (this thread)
+int64_t prim_launches() { return g_prim_launches; }
+
+template <typename T>
+__global__ void __launch_bounds__(kScanNT) scan_reduce_kernel(const T* __restrict__ in, int64_t n,
+                                                              long long* __restrict__ tile_sum) {
+  __shared__ long long s_warp[kScanNT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t base = blockIdx.x * (int64_t)kScanTile;
+  long long acc = 0;
+#pragma unroll
+  for (int k = 0; k < kScanIPT; k++) {
+    const int64_t p = base + k * kScanNT + tid;
+    if (p < n) acc += (long long)in[p];
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) s_warp[w] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    long long t = 0;
+    for (int q = 0; q < kScanNT / 32; q++) t += s_warp[q];
+    tile_sum[blockIdx.x] = t;
+  }
 }
+
+template <typename T, bool INCLUSIVE>
+__global__ void __launch_bounds__(kScanNT) scan_apply_kernel(const T* __restrict__ in, T* __restrict__ out,
+                                                             int64_t n, const long long* __restrict__ tile_sum) {
+  __shared__ long long s_warp[kScanNT / 32];
+  __shared__ long long s_red[kScanNT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t tile = blockIdx.x;
+  // prefix of this tile: sum of the tile sums before it
+  long long pre_t = 0;
+  for (int64_t q = tid; q < tile; q += kScanNT) pre_t += tile_sum[q];
+  for (int o = 16; o > 0; o >>= 1) pre_t += __shfl_xor_sync(0xffffffffu, pre_t, o);
+  if (lane == 0) s_red[w] = pre_t;
+  const int64_t wbase = tile * kScanTile + (int64_t)w * (32 * kScanIPT) + lane;
+  long long v[kScanIPT], pre[kScanIPT];
+#pragma unroll
+  for (int k = 0; k < kScanIPT; k++) {
+    const int64_t p = wbase + 32 * k;
+    v[k] = p < n ? (long long)in[p] : 0;
+  }
+  long long carry = 0;
+#pragma unroll
+  for (int k = 0; k < kScanIPT; k++) {
+    long long incl = v[k];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    pre[k] = carry + incl - v[k];
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) s_warp[w] = carry;
+  __syncthreads();
+  long long off = 0;
+#pragma unroll
+  for (int q = 0; q < kScanNT / 32; q++) off += s_red[q] + (q < w ? s_warp[q] : 0);
+#pragma unroll
+  for (int k = 0; k < kScanIPT; k++) {
+    const int64_t p = wbase + 32 * k;
+    if (p < n) out[p] = (T)(off + pre[k] + (INCLUSIVE ? v[k] : 0));
+  }
+}
+
+template <typename T, bool INCLUSIVE>
+static void device_scan(const T* in, T* out, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  Scratch ts(sizeof(long long) * tiles, s);
+  if (tiles > 1) scan_reduce_kernel<T><<<(unsigned)tiles, kScanNT, 0, s>>>(in, n, ts.as<long long>());
+  scan_apply_kernel<T, INCLUSIVE><<<(unsigned)tiles, kScanNT, 0, s>>>(in, out, n, ts.as<long long>());
+  H2_CHECK_LAUNCH();
+  g_prim_launches += tiles > 1 ? 2 : 1;
+}
+
+void scan_incl_i32(const int* in, int* out, int64_t n, cudaStream_t s) { device_scan<int, true>(in, out, n, s); }
 
 void scan_excl_i64(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s) {
-  size_t tmp = 0;
-  H2_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, s));
-  Scratch t(tmp, s);
-  H2_CUDA_TRY(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, n, s));
+  device_scan<int64_t, false>(in, out, n, s);
 }
 
+// ==========================================================================================
+// Stable LSD radix sort of 64-bit keys (optionally carrying 32-bit values), 8-bit digits.
+// Per digit: (1) count -- per-tile digit histograms, digit-major [digit][tile]; (2) the prefix
+// sum above over that matrix gives every (digit, tile) its output offset; (3) scatter -- each
+// tile ranks its keys stably (warps take consecutive 384-key spans in 12 rounds of 32, in-warp
+// ranks by __match_any_sync, warp spans combined per digit), reorders them in shared memory and
+// writes each digit's run contiguously.
+// ==========================================================================================
+constexpr int kSortNT = 256, kSortIPT = 12, kSortTile = kSortNT * kSortIPT, kSortWarps = kSortNT / 32;
+
+__global__ void __launch_bounds__(kSortNT) radix_count_kernel(const unsigned long long* __restrict__ keys, int64_t n,
+                                                            int shift, int64_t ntiles, int64_t* counts) {
+  __shared__ int hist[256];
+  hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = blockIdx.x * (int64_t)kSortTile;
+#pragma unroll 4
+  for (int k = 0; k < kSortIPT; k++) {
+    const int64_t p = base + k * kSortNT + threadIdx.x;
+    if (p < n) atomicAdd(&hist[(int)((keys[p] >> shift) & 255ULL)], 1);
+  }
+  __syncthreads();
+  counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = hist[threadIdx.x];
+}
+
+template <bool VALS>
+__global__ void __launch_bounds__(kSortNT) radix_scatter_kernel(const unsigned long long* __restrict__ kin,
+                                                              const int* __restrict__ vin, int64_t n, int shift,
+                                                              int64_t ntiles, const int64_t* __restrict__ offsets,
+                                                              unsigned long long* __restrict__ kout,
+                                                              int* __restrict__ vout) {
+  __shared__ unsigned long long sk[kSortTile];
+  __shared__ int sv[VALS ? kSortTile : 1];
+  __shared__ int wcnt[kSortWarps][256];  // per warp digit counts, then per warp digit prefixes
+  __shared__ int dstart[256];             // tile-local start of every digit
+  __shared__ long long gofs[256];         // this tile's output offset of every digit
+  __shared__ BlockScanSmem<kSortNT> scan;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t base = blockIdx.x * (int64_t)kSortTile;
+  for (int d = tid; d < kSortWarps * 256; d += kSortNT) (&wcnt[0][0])[d] = 0;
+  gofs[tid] = offsets[(int64_t)tid * ntiles + blockIdx.x];
+  __syncthreads();
+  unsigned long long key[kSortIPT];
+  int val[kSortIPT], rank[kSortIPT];
+  auto digit_of = [&](int k, int64_t p) { return p < n ? (int)((key[k] >> shift) & 255ULL) : 256; };
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int k = 0; k < kSortIPT; k++) {
+    // warp w's span is positions [w, w + 1) * 32 kSortIPT of the tile; round k covers 32 of them
+    const int64_t p = base + w * (32 * kSortIPT) + k * 32 + lane;
+    const bool ok = p < n;
+    key[k] = ok ? kin[p] : ~0ULL;
+    if (VALS) val[k] = ok ? vin[p] : 0;
+    const int dg = digit_of(k, p);  // padding: a 257th digit, never written
+    const unsigned peers = __match_any_sync(0xffffffffu, dg);
+    const int before = dg < 256 ? wcnt[w][dg] : 0;
+    rank[k] = before + __popc(peers & lt);
+    __syncwarp();
+    if (dg < 256 && (peers & lt) == 0) wcnt[w][dg] = before + __popc(peers);  // group leader
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit (thread = digit): exclusive prefix over the warps, tile count
+  int tcount = 0;
+  {
+    const int d = tid;
+    for (int q = 0; q < kSortWarps; q++) {
+      const int c = wcnt[q][d];
+      wcnt[q][d] = tcount;
+      tcount += c;
+    }
+  }
+  int total;
+  const int start = block_excl_sum<kSortNT>(tcount, &total, scan);
+  dstart[tid] = start;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kSortIPT; k++) {
+    const int64_t p = base + w * (32 * kSortIPT) + k * 32 + lane;
+    const int dg = digit_of(k, p);
+    if (dg < 256) {
+      const int pos = dstart[dg] + wcnt[w][dg] + rank[k];
+      sk[pos] = key[k];
+      if (VALS) sv[pos] = val[k];
+    }
+  }
+  __syncthreads();
+  const int valid = (int)(n - base < kSortTile ? n - base : kSortTile);
+  for (int pos = tid; pos < valid; pos += kSortNT) {
+    const unsigned long long kk = sk[pos];
+    const int d = (int)((kk >> shift) & 255ULL);
+    const int64_t o = gofs[d] + (pos - dstart[d]);
+    kout[o] = kk;
+    if (VALS) vout[o] = sv[pos];
+  }
+}
+
+static void radix_sort(unsigned long long* kin, unsigned long long* kout, int* vin, int* vout, int64_t n, int end_bit,
+                       cudaStream_t s) {
+  if (n <= 0) return;
+  const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
+  const int passes = (end_bit + 7) / 8;
+  Scratch counts(sizeof(int64_t) * 256 * ntiles, s), offs(sizeof(int64_t) * 256 * ntiles, s);
+  Scratch kt(passes > 1 ? sizeof(unsigned long long) * n : 8, s), vt(passes > 1 && vin ? sizeof(int) * n : 8, s);
+  // ping-pong so that the last pass writes kout / vout
+  const unsigned long long* ksrc = kin;
+  const int* vsrc = vin;
+  for (int p = 0; p < passes; p++) {
+    const bool to_out = ((passes - 1 - p) % 2) == 0;
+    unsigned long long* kdst = to_out ? kout : kt.as<unsigned long long>();
+    int* vdst = vin ? (to_out ? vout : vt.as<int>()) : nullptr;
+    radix_count_kernel<<<(unsigned)ntiles, kSortNT, 0, s>>>(ksrc, n, 8 * p, ntiles, counts.as<int64_t>());
+    H2_CHECK_LAUNCH();
+    scan_excl_i64(counts.as<int64_t>(), offs.as<int64_t>(), 256 * ntiles, s);
+    if (vin)
+      radix_scatter_kernel<true><<<(unsigned)ntiles, kSortNT, 0, s>>>(ksrc, vsrc, n, 8 * p, ntiles,
+                                                                      offs.as<int64_t>(), kdst, vdst);
+    else
+      radix_scatter_kernel<false><<<(unsigned)ntiles, kSortNT, 0, s>>>(ksrc, nullptr, n, 8 * p, ntiles,
+                                                                       offs.as<int64_t>(), kdst, nullptr);
+    H2_CHECK_LAUNCH();
+    g_prim_launches += 2;  // count + scatter (the scan counts itself)
+    ksrc = kdst;
+    vsrc = vdst;
+  }
+}
+
+// keys_out / vals_out receive the stable sort of (keys_in, vals_in) by the key's bits [0, end_bit)
 void sort_pairs_u64_i32(unsigned long long* kin, unsigned long long* kout, int* vin, int* vout, int64_t n,
                         int end_bit, cudaStream_t s) {
-  size_t tmp = 0;
-  H2_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, n, 0, end_bit, s));
-  Scratch t(tmp, s);
-  H2_CUDA_TRY(cub::DeviceRadixSort::SortPairs(t.p, tmp, kin, kout, vin, vout, n, 0, end_bit, s));
+  radix_sort(kin, kout, vin, vout, n, end_bit, s);
 }
 
 void sort_keys_u64(unsigned long long* kin, unsigned long long* kout, int64_t n, int end_bit, cudaStream_t s) {
-  size_t tmp = 0;
-  H2_CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp, kin, kout, n, 0, end_bit, s));
-  Scratch t(tmp, s);
-  H2_CUDA_TRY(cub::DeviceRadixSort::SortKeys(t.p, tmp, kin, kout, n, 0, end_bit, s));
+  radix_sort(kin, kout, nullptr, nullptr, n, end_bit, s);
 }
 
 }  // namespace h2

@@ -227,7 +227,6 @@ void build_tree(h2_handle* h, const double* pts) {
   h->gpu_launches += 1;
   int end_bit = d * L > 0 ? d * L : 1;
   sort_pairs_u64_i32(kin.as<unsigned long long>(), h->key, iin.as<int>(), h->perm, n, end_bit, s);
-  h->gpu_launches += (end_bit + 7) / 8 + 2;
   h->X = halloc<double>(h, (size_t)n * d);
   gather_soa_kernel<<<grid_for(n, 256), 256, 0, s>>>(pts, h->perm, n, d, h->X);
   H2_CHECK_LAUNCH();
@@ -252,7 +251,7 @@ void build_tree(h2_handle* h, const double* pts) {
                                                         flag.as<int>(), nid_b.as<int>());
     H2_CHECK_LAUNCH();
     scan_incl_i32(flag.as<int>(), cnt.as<int>(), n, s);
-    h->gpu_launches += 2;
+    h->gpu_launches += 1;
     int total = read1(cnt.as<int>() + n - 1, s);
     if (total == 0) break;
     grow_nodes(h, cap, h->nnodes + total);

@@ -12,9 +12,8 @@
 #pragma once
 #include <cfloat>
 #include <climits>
-#include <cub/block/block_scan.cuh>
 
-#include "h2_internal.cuh"
+#include "prims.cuh"
 
 namespace h2 {
 
@@ -37,7 +36,7 @@ struct VolSmem {
   } u;
   double lo[D], hi[D], hstep[D];
   double rlo[D][NT / 32], rhi[D][NT / 32];
-  typename cub::BlockScan<int, NT>::TempStorage scan;
+  BlockScanSmem<NT> scan;
 };
 
 // bitonic sort of a[0..P), P a power of two, by the whole CTA
@@ -64,7 +63,7 @@ __device__ void cta_bitonic(int* a, int P) {
 // cnt <= 64: warp 0 sorts two keys per lane with shuffles and compacts with ballots (no CTA
 // barrier inside); larger: CTA bitonic sort + block-scan compaction.
 template <int NT>
-__device__ int cta_sort_unique_write(typename cub::BlockScan<int, NT>::TempStorage& scan, int* sel, int cnt,
+__device__ int cta_sort_unique_write(BlockScanSmem<NT>& scan, int* sel, int cnt,
                                      int* out) {
   __shared__ int s_cnt;
   if (cnt <= 64) {
@@ -116,8 +115,8 @@ __device__ int cta_sort_unique_write(typename cub::BlockScan<int, NT>::TempStora
   for (int c0 = 0; c0 < cnt; c0 += NT) {
     int i = c0 + threadIdx.x;
     int keep = (i < cnt) && (i == 0 || sel[i] != sel[i - 1]);
-    int pos, agg;
-    cub::BlockScan<int, NT>(scan).ExclusiveSum(keep, pos, agg);
+    int agg;
+    const int pos = block_excl_sum<NT>(keep, &agg, scan);
     if (keep) out[base + pos] = sel[i];
     base += agg;
     __syncthreads();
