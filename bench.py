@@ -145,9 +145,11 @@ def oracle_sample_run(cfg: int, n_sample: int):
 def cpu_baseline(cfg: int, n_sample: int) -> dict:
     import oracle
     dt, entries = oracle_sample_run(cfg, n_sample)
+    what = ("the whole workload" if n_sample == synth.CONFIGS[cfg]["n"]
+            else "points of the same distribution as the workload")
     return {"value": round(n_sample / dt / 1e6, 6), "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"oracle a1-a8 + evaluate-only a9/a10 ({entries} block entries) on n={n_sample} points "
-                      f"of the same distribution as the workload; wall {dt:.2f} s"}
+            "sample": f"oracle a1-a8 + evaluate-only a9/a10 ({entries} block entries) on n={n_sample} ({what}); "
+                      f"wall {dt:.2f} s"}
 
 
 def run_reference(args):
@@ -156,7 +158,7 @@ def run_reference(args):
         return 0
     import oracle
     cfg = args.config
-    n_s = args.cpu_sample
+    n_s = args.ref_sample
     for _ in range(args.warmup):
         oracle_sample_run(cfg, n_s // 4)
     times = []
@@ -166,7 +168,7 @@ def run_reference(args):
     t = float(np.mean(times))
     v = n_s / t / 1e6
     line = {"metric": METRIC, "value": round(v, 6), "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": workload_desc(cfg), "sample_n": n_s,
                        "note": "reference = the fp64 CPU oracle (oracle/h2_oracle.c) on the host cores"},
@@ -206,19 +208,20 @@ def run_ours(args):
     kp = list(c["params"])
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
-    def opts(host=False):
+    def opts(host=False, serial=False):
         o = P.h2_options_default()
         o.storage = P.H2_STORE_ALL
         o.timing = 1
         o.stream = stream.cuda_stream
         o.points_on_host = 1 if host else 0
+        o.serial_fill = 1 if serial else 0
         if comm is not None:
             o.comm = comm.ptr
         return o
 
-    def one(host=False, src=None):
+    def one(host=False, src=None, serial=False):
         ptr = src if src is not None else pts.data_ptr()
-        return P.h2_build(ptr, n, c["d"], c["kernel"], kp, c["id_tol"], c["q"], c["tau"], opts(host))
+        return P.h2_build(ptr, n, c["d"], c["kernel"], kp, c["id_tol"], c["q"], c["tau"], opts(host, serial))
 
     for _ in range(args.warmup):
         h = one()
@@ -276,6 +279,15 @@ def run_ours(args):
     e2e = {"value": round(n / e2e_t / 1e6, 4), "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": int(d2h)}
 
+    # the same build with the nearfield fill run alone (serial_fill): the kernel's own roofline
+    iso_ms = []
+    for _ in range(2):
+        with torch.cuda.stream(stream):
+            flush.fill_(3)
+        h = one(serial=True)
+        iso_ms.append(P.h2_info(h)["stage_ms"]["nearfield_fill"])
+        P.h2_free(h)
+
     # roofline of the dominant kernel (nearfield fill, a10): algorithmic bytes = 8 B per stored entry
     peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
     hbm = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
@@ -296,8 +308,15 @@ def run_ours(args):
                 "frac": round(achieved / hbm, 4), "traffic": traffic,
                 "kernel": "nf_fill_kernel<D=2,MATERN32> (a10, nearfield fill)", "kernel_ms": round(nf_ms, 3),
                 "step_share": round(nf_ms / t_step, 4),
+                "note": "live: the kernel runs concurrently with a5-a9 (side stream), sharing the SMs",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650 GB/s",
                 "fp64_peak_tflops_at_sm_clock": round(fp64_peak, 2)}
+    iso = float(np.mean(iso_ms))
+    roofline_isolated = {"bound": "hbm", "achieved": round(nf_bytes / (iso * 1e-3) / 1e9, 1), "peak": hbm,
+                         "unit": "GB/s", "frac": round(nf_bytes / (iso * 1e-3) / 1e9 / hbm, 4),
+                         "kernel_ms": round(iso, 3), "traffic": traffic,
+                         "note": "same kernel, same build, fill run alone after a9 (h2_options.serial_fill = 1); "
+                                 "2 builds after the timed region, L2 flushed before each"}
 
     if rank == 0:
         mean_stages = {k: round(float(np.mean([s[k] for s in stages])), 3) for k in stages[0]}
@@ -312,7 +331,7 @@ def run_ours(args):
                            "l2": "flushed (512 MiB write) before every timed step",
                            "wall_s_timed_region": round(t_wall, 3)},
                 "stages_ms": mean_stages, "clocks": clocks, "e2e": e2e, "gpu_launches": launches,
-                "roofline": roofline}
+                "roofline": roofline, "roofline_isolated": roofline_isolated}
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample)
         print(json.dumps(line), flush=True)
@@ -332,7 +351,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--n", type=int, default=None, help="override n (not a bench line)")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 19)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 22,
+                    help="points of the oracle's cpu_baseline run (default: the whole workload)")
+    ap.add_argument("--ref-sample", type=int, default=1 << 22,
+                    help="points per step of --impl reference (default: the whole workload, ~6 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -98,6 +98,9 @@ typedef struct h2_options {
   struct h2_comm* comm;    /* NULL: single GPU.  Otherwise a sharded build over comm's ranks (see   */
                            /*    "sharded build" below): every rank calls h2_build_ex with the same */
                            /*    points and parameters; the comm must outlive the handle.           */
+  int32_t serial_fill;     /* 1: run the nearfield fill (a10) after a9 on the main stream instead of */
+                           /*    concurrently with a5-a9 on a low-priority side stream (default 0;  */
+                           /*    same result; for measuring the fill kernel in isolation)           */
 } h2_options;
 
 /* h2_options with the defaults listed above (r calibrated, AUTO, whole-device budget, timing off) */

@@ -34,7 +34,7 @@ EXPORTED_SYMBOLS = ["h2_build", "h2_build_ex", "h2_options_default", "h2_matvec"
 class h2_options(C.Structure):
     _fields_ = [("r_override", C.c_int32), ("storage", C.c_int32), ("mem_budget_bytes", C.c_int64),
                 ("stream", C.c_void_p), ("points_on_host", C.c_int32), ("timing", C.c_int32),
-                ("hidr_brute", C.c_int32), ("comm", C.c_void_p)]
+                ("hidr_brute", C.c_int32), ("comm", C.c_void_p), ("serial_fill", C.c_int32)]
 
 
 class h2_info_t(C.Structure):

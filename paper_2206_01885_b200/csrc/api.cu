@@ -51,8 +51,8 @@ static BuildStreams& build_streams() {
   return b;
 }
 
-// H2_SERIAL=1: run the nearfield fill after the coupling fill on the main stream (A/B knob)
-static bool serial_fill() {
+// H2_SERIAL=1 (A/B knob, read once) forces h2_options.serial_fill for every build
+static bool serial_fill_env() {
   static const bool v = [] {
     const char* e = getenv("H2_SERIAL");
     return e && atoi(e) != 0;
@@ -165,8 +165,9 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
     if (h->nranks > 1) shard_plan(h);  // cut level, owned subtrees and block rows (shard.cu)
     mark(2);
     // a10 needs only the tree and the nearfield list: it starts now on the side stream and
-    // overlaps a5-a9 (serial_fill(): after a9 on the main stream instead)
-    if (!serial_fill()) fill_nearfield_begin(h, bs.side, o.storage, o.mem_budget_bytes, nf);
+    // overlaps a5-a9 (serial_fill: after a9 on the main stream instead)
+    const bool serial = o.serial_fill || serial_fill_env();
+    if (!serial) fill_nearfield_begin(h, bs.side, o.storage, o.mem_budget_bytes, nf);
     h->r = calibrated ? calibrate_end(h, cal) : o.r_override;  // a5
     mark(3);
     hidr_up(h);  // a6
@@ -176,7 +177,7 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
     id_sweep(h);  // a8
     mark(6);
     fill_coupling(h, o.storage, o.mem_budget_bytes, nf);  // a9
-    if (serial_fill()) fill_nearfield_begin(h, h->stream, o.storage, o.mem_budget_bytes, nf);
+    if (serial) fill_nearfield_begin(h, h->stream, o.storage, o.mem_budget_bytes, nf);
     fill_nearfield_join(h, nf);
     mark(7);
     H2_CUDA_TRY(cudaEventRecord(join_ev, h->stream));
