@@ -112,7 +112,7 @@ __global__ void unit_map_kernel(int64_t np, const int64_t* __restrict__ uoff, in
 // one unit's rows [r0, r1) over NS column slots: NS independent evaluation chains per row, no
 // control flow between them (so the compiler interleaves them), next row's point prefetched.
 // Coordinates are pre-scaled (kernel_cscale), so sq is the kernel's own argument.
-template <int D, int KID, int NS>
+template <int D, int KID, int NS, bool CL>
 __device__ __forceinline__ void nf_unit_rows(const double* __restrict__ xr, int64_t n, const double (&xb)[8][D],
                                              bool last_ok, int r0, int r1, int nj, double* o,
                                              const double* __restrict__ tab) {
@@ -127,13 +127,13 @@ __device__ __forceinline__ void nf_unit_rows(const double* __restrict__ xr, int6
     double v[NS];
 #pragma unroll
     for (int s = 0; s < NS; s++) {
-      double sq = 0.0;
+      double sq = kFillBias;
 #pragma unroll
       for (int c = 0; c < D; c++) {
         const double df = xa[c] - xb[s][c];
         sq = fma(df, df, sq);
       }
-      v[s] = kernel_fill<KID>(sq, tab);
+      v[s] = kernel_fill<KID, CL>(sq, tab);
     }
 #pragma unroll
     for (int s = 0; s < NS; s++)  // slots before the last are full (see nslot)
@@ -143,7 +143,7 @@ __device__ __forceinline__ void nf_unit_rows(const double* __restrict__ xr, int6
   }
 }
 
-template <int D, int KID, int CW, int RU, int MINB>
+template <int D, int KID, int CW, int CL, int MINB>
 __global__ void __launch_bounds__(kFillThreads, MINB) nf_fill_kernel(int64_t nunits, const int* __restrict__ umap,
                                                                      const int64_t* __restrict__ uoff,
                                                                      const int2* __restrict__ pairs,
@@ -185,14 +185,14 @@ __global__ void __launch_bounds__(kFillThreads, MINB) nf_fill_kernel(int64_t nun
     if (nslot > CW) nslot = CW;
     const bool last_ok = c0 + lane + 32 * (nslot - 1) < nj;  // only the last slot can be partial
     switch (nslot) {
-      case 1: nf_unit_rows<D, KID, 1>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
-      case 2: nf_unit_rows<D, KID, (CW < 2 ? CW : 2)>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
-      case 3: nf_unit_rows<D, KID, (CW < 3 ? CW : 3)>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
-      case 4: nf_unit_rows<D, KID, (CW < 4 ? CW : 4)>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
-      case 5: nf_unit_rows<D, KID, (CW < 5 ? CW : 5)>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
-      case 6: nf_unit_rows<D, KID, (CW < 6 ? CW : 6)>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
-      case 7: nf_unit_rows<D, KID, (CW < 7 ? CW : 7)>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
-      default: nf_unit_rows<D, KID, CW>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
+      case 1: nf_unit_rows<D, KID, 1, CL != 0>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
+      case 2: nf_unit_rows<D, KID, (CW < 2 ? CW : 2), CL != 0>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
+      case 3: nf_unit_rows<D, KID, (CW < 3 ? CW : 3), CL != 0>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
+      case 4: nf_unit_rows<D, KID, (CW < 4 ? CW : 4), CL != 0>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
+      case 5: nf_unit_rows<D, KID, (CW < 5 ? CW : 5), CL != 0>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
+      case 6: nf_unit_rows<D, KID, (CW < 6 ? CW : 6), CL != 0>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
+      case 7: nf_unit_rows<D, KID, (CW < 7 ? CW : 7), CL != 0>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
+      default: nf_unit_rows<D, KID, CW, CL != 0>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
     }
   }
 }
@@ -252,13 +252,13 @@ __global__ void __launch_bounds__(kFillThreads) cp_fill_kernel(int64_t np, const
       if (e >= total) continue;
       const int loc = e - pre_q, row = loc / kj_q, col = loc - row * kj_q;
       const int a = sk[(int64_t)i_q * r + row], b = sk[(int64_t)j_q * r + col];
-      double sq = 0.0;
+      double sq = kFillBias;
 #pragma unroll
       for (int c = 0; c < D; c++) {
         const double df = X[c * n + a] * cs - X[c * n + b] * cs;
         sq = fma(df, df, sq);
       }
-      __stcs(o + e, kernel_fill<KID>(sq, tab));
+      __stcs(o + e, kernel_fill<KID, true>(sq, tab));
     }
   }
 }
@@ -305,6 +305,7 @@ static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_
                             const int64_t* uoff, const int2* pairs, const int64_t* voff, const double* Xs, double cs,
                             double* out) {
   if (mode == 1) {
+    const bool clamp = fill_needs_clamp(h->kid, h->d, h->W, cs);
     const int upw = nf_units_per_warp();
     int64_t blocks = upw > 0 ? (nwork + 8 * upw - 1) / (8 * upw) : (nwork + 7) / 8;  // 8 warps per CTA
     const int64_t cap = upw > 0 ? (int64_t)1 << 30 : 148 * 8;
@@ -312,13 +313,16 @@ static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_
 #define H2_NF_ARGS nwork, umap, uoff, pairs, voff, h->nbegin, h->nend, Xs, h->n, out
     switch (h->d) {
       case 2:
-        switch (nf_variant()) {  // tuning variants of the D = 2 kernel (CW, RU, MINB)
+        switch (nf_variant()) {  // tuning variants of the D = 2 kernel (CW, clamp, MINB)
           case 1: launch_nf(nf_fill_kernel<2, KID, 4, 1, 4>, g, s, H2_NF_ARGS); break;
           case 2: launch_nf(nf_fill_kernel<2, KID, 4, 1, 2>, g, s, H2_NF_ARGS); break;
           case 3: launch_nf(nf_fill_kernel<2, KID, 6, 1, 2>, g, s, H2_NF_ARGS); break;
           case 4: launch_nf(nf_fill_kernel<2, KID, 8, 1, 1>, g, s, H2_NF_ARGS); break;
           case 5: launch_nf(nf_fill_kernel<2, KID, 2, 1, 4>, g, s, H2_NF_ARGS); break;
-          default: launch_nf(nf_fill_kernel<2, KID, 8, 1, 2>, g, s, H2_NF_ARGS); break;
+          default:
+            if (clamp) launch_nf(nf_fill_kernel<2, KID, 8, 1, 2>, g, s, H2_NF_ARGS);
+            else launch_nf(nf_fill_kernel<2, KID, 8, 0, 2>, g, s, H2_NF_ARGS);
+            break;
         }
         break;
 #define H2_NF_CASE(DD) \

@@ -1,11 +1,7 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; echo tests_rc=$? >> gpurun_out/gpu_tests.log
-timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo smoke_rc=$? >> gpurun_out/smoke.log
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/smi.txt
-timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo bench_rc=$? >> gpurun_out/bench.log
-timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo ref_rc=$? >> gpurun_out/bench_ref.log
-CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline"
-$CMD > gpurun_out/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_l.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:nf_fill -s 1 -c 1 -o gpurun_out/prof_nf $CMD > gpurun_out/ncu_f.log 2>&1
-echo ncu_rc=$?
+rm -f gpurun_out/ab.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests_rc=$? >> gpurun_out/gpu_tests.log
+for v in "H2_SERIAL=1" "H2_NF_UPW=8"; do
+  echo "== $v" >> gpurun_out/ab.log
+  env $v timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline >> gpurun_out/ab.log 2>&1
+done
