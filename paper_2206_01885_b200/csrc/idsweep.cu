@@ -140,7 +140,9 @@ __global__ void __launch_bounds__(kIdSmemThreads) id_kernel_smem(
   const int nx = xbar_n[i];
   const int ny = ys_cnt[i];
   const int tid = threadIdx.x;
-  if (nx == 0 || id_smem_bytes(ny, nx, D) > kIdSmemMax || id_class(id_smem_bytes(ny, nx, D)) != cls) return;
+  // cls < 0: every node of the shared-memory path (merged launch)
+  if (nx == 0 || id_smem_bytes(ny, nx, D) > kIdSmemMax || (cls >= 0 && id_class(id_smem_bytes(ny, nx, D)) != cls))
+    return;
   double* M = sh;
   double* nrm2 = M + (int64_t)ny * nx;
   double* v = nrm2 + nx;
@@ -267,19 +269,33 @@ void id_sweep(h2_handle* h) {
     }
     uoff_scatter_kernel<<<(count + 255) / 256, 256, 0, s>>>(base, count, uo, uused, h->u_off);
     Scratch work(sizeof(double) * (tot[0] > 0 ? tot[0] : 1), s);
-    id_kernel<<<count, kIdThreads, 0, s>>>(base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf,
-                                           h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
-                                           work.as<double>(), h->u_off + base, U, h->k, h->sk,
-                                           ev.as<unsigned long long>());
-    H2_CHECK_LAUNCH();
+    if (tot[0] > 0) {  // some node's block exceeds the shared-memory path: global-memory CPQR
+      id_kernel<<<count, kIdThreads, 0, s>>>(base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf,
+                                             h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
+                                             work.as<double>(), h->u_off + base, U, h->k, h->sk,
+                                             ev.as<unsigned long long>());
+      H2_CHECK_LAUNCH();
+      h->gpu_launches += 1;
+    }
+    // Small levels: one launch for all classes (sized by the largest): the class launches of a
+    // level run one after the other, and with few nodes each costs a node's full CPQR latency.
+    // Merged when the level fits in about two waves at the largest class's occupancy.
+    int smax_all = 0, ncls = 0;
     for (int cls = 0; cls < kIdClasses; cls++) {
-      if (smem_bytes[cls] == 0) continue;
+      smax_all = smem_bytes[cls] > smax_all ? smem_bytes[cls] : smax_all;
+      ncls += smem_bytes[cls] > 0;
+    }
+    const int per_sm = smax_all > 0 ? (228 * 1024) / (smax_all + 1024) : 0;
+    const bool merge = ncls > 1 && count <= 2 * 148 * (per_sm > 0 ? per_sm : 1);
+    for (int cls = merge ? -1 : 0; cls < (merge ? 0 : kIdClasses); cls++) {
+      const int smem = cls < 0 ? smax_all : smem_bytes[cls];
+      if (smem == 0) continue;
       switch (h->d) {
 #define H2_ID_CASE(DD)                                                                                        \
   case DD: {                                                                                                  \
         H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_smem<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                                        kIdSmemMax));                                                          \
-    id_kernel_smem<DD><<<count, kIdSmemThreads, smem_bytes[cls], s>>>(                                        \
+    id_kernel_smem<DD><<<count, kIdSmemThreads, smem, s>>>(                                                   \
         base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child, h->nchild, \
         h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>(), cls);       \
   } break;
@@ -290,7 +306,7 @@ void id_sweep(h2_handle* h) {
       H2_CHECK_LAUNCH();
       h->gpu_launches += 1;
     }
-    h->gpu_launches += 3;
+    h->gpu_launches += 2;
     uused += tot[1];  // u_off[] holds global offsets into the arena
   }
   if (!exchanged) exchange_slots(h, h->k, h->sk);
