@@ -97,6 +97,15 @@ __device__ __forceinline__ double warp_min_d(double v) {
   return v;
 }
 
+// An upper bound of the warp minimum of v >= 0 (distances) in ONE instruction: high words of
+// non-negative doubles order like the doubles, so the least high word with an all-ones low word
+// bounds the minimum from above (at most 2^-20 relative above it).  The pruning only needs
+// delta >= the true best; the result is warp-uniform.  +inf stays +inf.
+__device__ __forceinline__ double warp_min_ub(double v) {
+  const unsigned hi = __reduce_min_sync(0xffffffffu, (unsigned)__double2hiint(v));
+  return hi >= 0x7FF00000u ? INFINITY : __hiloint2double((int)hi, (int)0xFFFFFFFFu);
+}
+
 template <int D>
 __global__ void __launch_bounds__(kDownThreads) hidr_down_kernel(
     const double* __restrict__ X, int64_t n, int base, int r, const int* __restrict__ parent,
@@ -233,7 +242,10 @@ __global__ void __launch_bounds__(kDownThreads) hidr_down_kernel(
   __syncthreads();
   // 3. one warp per grid node
   unsigned long long done = 0;
-  for (int g = warp; g < G; g += kDownWarps) {
+  // grid nodes are taken dynamically (their search costs differ): a CTA-local counter
+  if (tid == 0) s_fill = kDownWarps;
+  __syncthreads();
+  for (int g = warp; g < G;) {
     double q[D];
     {
       int rem = g;
@@ -286,7 +298,7 @@ __global__ void __launch_bounds__(kDownThreads) hidr_down_kernel(
           u = box_ub<D>(q, blo, bhi);
         }
       }
-      dl = fmin(dl, warp_min_d(u));
+      dl = fmin(dl, warp_min_ub(u));
       unsigned mask = __ballot_sync(0xffffffffu, cnt > 0 && lbs <= dl);
       while (mask) {
         const int t = __ffs(mask) - 1;
@@ -311,7 +323,7 @@ __global__ void __launch_bounds__(kDownThreads) hidr_down_kernel(
           }
         }
         done += (unsigned long long)ct;
-        dl = fmin(dl, warp_min_d(best));
+        dl = fmin(dl, warp_min_ub(best));
       }
     };
     if (g0 >= 0) process_group(g0);
@@ -339,6 +351,9 @@ __global__ void __launch_bounds__(kDownThreads) hidr_down_kernel(
       }
     }
     if (lane == 0) out[g] = bi;  // parked in the output slot (capacity r >= G)
+    int nxt = 0;
+    if (lane == 0) nxt = atomicAdd(&s_fill, 1);
+    g = __shfl_sync(0xffffffffu, nxt, 0);
   }
   if (lane == 0 && evals_done) atomicAdd(evals_done, done);
   if (tid == 0 && evals_alg) atomicAdd(evals_alg, (unsigned long long)G * (unsigned long long)tot);
