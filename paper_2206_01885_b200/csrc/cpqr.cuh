@@ -180,6 +180,36 @@ struct CpqrRmSmem {
 };
 
 template <int NT>
+__device__ __forceinline__ void cta_cpqr_rm_argmax(const double* __restrict__ nrm2, int t, int nx,
+                                                   CpqrRmSmem<NT>& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double best = -1.0;
+  int bj = INT_MAX;
+  for (int j = t + tid; j < nx; j += NT) {
+    const double x = sqrt(nrm2[j]);
+    if (x > best) {
+      best = x;
+      bj = j;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double b2 = __shfl_xor_sync(0xffffffffu, best, o);
+    const int j2 = __shfl_xor_sync(0xffffffffu, bj, o);
+    if (b2 > best || (b2 == best && j2 < bj)) {
+      best = b2;
+      bj = j2;
+    }
+  }
+  if (lane == 0) {
+    sm.wb[warp] = best;
+    sm.wj[warp] = bj;
+  }
+}
+
+// Two barriers per step: the warps' argmax candidates for step t+1 are published at the end of
+// step t's update (each thread owns its columns, so it scans the norms it just computed), the
+// barrier closing the update also publishes them.
+template <int NT>
 __device__ int cta_cpqr_rm(double* __restrict__ M, int ny, int nx, int ld, double tol, int* __restrict__ piv,
                            double* __restrict__ nrm2, double* __restrict__ v, CpqrRmSmem<NT>& sm) {
   constexpr int NW = NT / 32;
@@ -190,33 +220,12 @@ __device__ int cta_cpqr_rm(double* __restrict__ M, int ny, int nx, int ld, doubl
     for (int i = 0; i < ny; i++) s += M[i * ld + j] * M[i * ld + j];
     nrm2[j] = s;
   }
+  cta_cpqr_rm_argmax<NT>(nrm2, 0, nx, sm);  // each thread scans only the norms it wrote
   __syncthreads();
   const int kmax = ny < nx ? ny : nx;
   double r11 = 0.0;
   int k = 0;
   for (int t = 0; t < kmax; t++) {
-    double best = -1.0;
-    int bj = INT_MAX;
-    for (int j = t + tid; j < nx; j += NT) {
-      const double x = sqrt(nrm2[j]);
-      if (x > best) {
-        best = x;
-        bj = j;
-      }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double b2 = __shfl_xor_sync(0xffffffffu, best, o);
-      const int j2 = __shfl_xor_sync(0xffffffffu, bj, o);
-      if (b2 > best || (b2 == best && j2 < bj)) {
-        best = b2;
-        bj = j2;
-      }
-    }
-    if (lane == 0) {
-      sm.wb[warp] = best;
-      sm.wj[warp] = bj;
-    }
-    __syncthreads();
     double nrm = sm.wb[0];
     int p = sm.wj[0];
 #pragma unroll
@@ -259,7 +268,7 @@ __device__ int cta_cpqr_rm(double* __restrict__ M, int ny, int nx, int ld, doubl
         nrm2[p] = nrm2[t];
       }
     }
-    __syncthreads();
+    __syncthreads();  // (every thread read this step's winners before it)
     const double vtv = sm.vtv;
     for (int j = t + 1 + tid; j < nx; j += NT) {
       // independent partial sums (4-way) break the serial FMA chains
@@ -296,6 +305,7 @@ __device__ int cta_cpqr_rm(double* __restrict__ M, int ny, int nx, int ld, doubl
       nrm2[j] = nn0 + nn1;
     }
     k = t + 1;
+    cta_cpqr_rm_argmax<NT>(nrm2, t + 1, nx, sm);  // next step's candidates (own columns only)
     __syncthreads();
   }
   __syncthreads();
