@@ -35,6 +35,7 @@ static void free_handle(h2_handle* h) {
 // level kernels take SMs first whenever a fill CTA retires.
 struct BuildStreams {
   cudaStream_t main = nullptr, side = nullptr, calib = nullptr;
+  cudaStream_t aux[h2_handle::kAux] = {};
 };
 static BuildStreams& build_streams() {
   thread_local BuildStreams per_dev[64];
@@ -47,6 +48,7 @@ static BuildStreams& build_streams() {
     H2_CUDA_TRY(cudaStreamCreateWithPriority(&b.main, cudaStreamNonBlocking, greatest));
     H2_CUDA_TRY(cudaStreamCreateWithPriority(&b.side, cudaStreamNonBlocking, least));
     H2_CUDA_TRY(cudaStreamCreateWithPriority(&b.calib, cudaStreamNonBlocking, greatest));
+    for (auto& a : b.aux) H2_CUDA_TRY(cudaStreamCreateWithPriority(&a, cudaStreamNonBlocking, greatest));
   }
   return b;
 }
@@ -134,6 +136,7 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
     H2_CUDA_TRY(cudaEventRecord(fork_ev, user));
     H2_CUDA_TRY(cudaStreamWaitEvent(bs.main, fork_ev, 0));
     h->stream = bs.main;
+    for (int a = 0; a < h2_handle::kAux; a++) h->aux[a] = bs.aux[a];
     if (h->timing) {
       for (auto& e : ev) H2_CUDA_TRY(cudaEventCreate(&e));
       nev = 8;
@@ -184,6 +187,7 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
     H2_CUDA_TRY(cudaStreamWaitEvent(user, join_ev, 0));
     h->gpu_launches += (int)(prim_launches() - prims0);
     h->stream = user;
+    for (auto& a : h->aux) a = nullptr;
     H2_CUDA_TRY(cudaStreamSynchronize(h->stream));
     if (h->timing) {
       nf.finish_timing(h);

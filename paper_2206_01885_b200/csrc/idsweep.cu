@@ -287,15 +287,31 @@ void id_sweep(h2_handle* h) {
     }
     const int per_sm = smax_all > 0 ? (228 * 1024) / (smax_all + 1024) : 0;
     const bool merge = ncls > 1 && count <= 2 * 148 * (per_sm > 0 ? per_sm : 1);
+    // the class launches of a level are independent (disjoint nodes): they run concurrently on the
+    // build's auxiliary streams, joined back into the main stream before the next level
+    int used = 0;
+    cudaEvent_t lev_ev[h2_handle::kAux + 1];
+    const bool fan = !merge && h->aux[0] != nullptr;
+    if (fan) {
+      for (auto& e : lev_ev) H2_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      H2_CUDA_TRY(cudaEventRecord(lev_ev[h2_handle::kAux], s));
+    }
     for (int cls = merge ? -1 : 0; cls < (merge ? 0 : kIdClasses); cls++) {
       const int smem = cls < 0 ? smax_all : smem_bytes[cls];
       if (smem == 0) continue;
+      cudaStream_t cs = s;
+      if (fan) {
+        const int a = used % h2_handle::kAux;
+        cs = h->aux[a];
+        if (used < h2_handle::kAux) H2_CUDA_TRY(cudaStreamWaitEvent(cs, lev_ev[h2_handle::kAux], 0));
+        used++;
+      }
       switch (h->d) {
 #define H2_ID_CASE(DD)                                                                                        \
   case DD: {                                                                                                  \
         H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_smem<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                                        kIdSmemMax));                                                          \
-    id_kernel_smem<DD><<<count, kIdSmemThreads, smem, s>>>(                                                   \
+    id_kernel_smem<DD><<<count, kIdSmemThreads, smem, cs>>>(                                                  \
         base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child, h->nchild, \
         h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>(), cls);       \
   } break;
@@ -305,6 +321,13 @@ void id_sweep(h2_handle* h) {
       }
       H2_CHECK_LAUNCH();
       h->gpu_launches += 1;
+    }
+    if (fan) {
+      for (int a = 0; a < h2_handle::kAux && a < used; a++) {
+        H2_CUDA_TRY(cudaEventRecord(lev_ev[a], h->aux[a]));
+        H2_CUDA_TRY(cudaStreamWaitEvent(s, lev_ev[a], 0));
+      }
+      for (auto& e : lev_ev) cudaEventDestroy(e);
     }
     h->gpu_launches += 2;
     uused += tot[1];  // u_off[] holds global offsets into the arena
