@@ -46,7 +46,9 @@ static BuildStreams& build_streams() {
     int least = 0, greatest = 0;
     H2_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     H2_CUDA_TRY(cudaStreamCreateWithPriority(&b.main, cudaStreamNonBlocking, greatest));
-    H2_CUDA_TRY(cudaStreamCreateWithPriority(&b.side, cudaStreamNonBlocking, least));
+    // H2_SIDE_PRIORITY=1 (A/B knob): the nearfield fill at the highest priority instead
+    const char* sp = getenv("H2_SIDE_PRIORITY");
+    H2_CUDA_TRY(cudaStreamCreateWithPriority(&b.side, cudaStreamNonBlocking, sp && atoi(sp) ? greatest : least));
     H2_CUDA_TRY(cudaStreamCreateWithPriority(&b.calib, cudaStreamNonBlocking, greatest));
     for (auto& a : b.aux) H2_CUDA_TRY(cudaStreamCreateWithPriority(&a, cudaStreamNonBlocking, greatest));
   }
