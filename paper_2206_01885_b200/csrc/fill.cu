@@ -65,7 +65,6 @@ __global__ void pair_emit_kernel(int mode, int nnodes, int64_t m, const int64_t*
 // registers; rows are streamed with warp-uniform (broadcast) loads; slot s stores at a fixed
 // offset of 256 s bytes from the lane's row pointer.  The inner loop is the kernel evaluation.
 __host__ __device__ constexpr int warp_slots(int D) { return D <= 2 ? 8 : (D <= 3 ? 5 : (D <= 5 ? 3 : 2)); }
-constexpr int kWarpUnitEntries = 4096;
 
 // H2_FILL_VARIANT (tuning knob, read once): selects the (slots, rows per iteration, min blocks)
 // instantiation of the D = 2 nearfield kernel; 0 = default (8 slots, 2 CTAs/SM: fastest measured).
@@ -82,13 +81,6 @@ static int nf_slots(int d) {
   return v == 1 || v == 2 ? 4 : (v == 3 ? 6 : (v == 5 ? 2 : 8));
 }
 
-__host__ __device__ __forceinline__ void unit_shape(int ni, int nj, int wc, int& R, int& nrb, int& ncb) {
-  int nc = nj < wc ? nj : wc;
-  R = kWarpUnitEntries / (nc > 0 ? nc : 1);
-  if (R < 1) R = 1;
-  nrb = (ni + R - 1) / R;
-  ncb = (nj + wc - 1) / wc;
-}
 
 __global__ void nf_units_kernel(int wc, int64_t np, const int2* __restrict__ pairs, const int* __restrict__ nbegin,
                                 const int* __restrict__ nend, int64_t* units) {
@@ -419,14 +411,16 @@ void fill_nearfield_begin(h2_handle* h, cudaStream_t side, int storage, int64_t 
   if (store_np && h->n_np > 0) {
     const int64_t np = h->n_np;
     Scratch units(sizeof(int64_t) * (np + 1), side);
-    job.uoff = Scratch(sizeof(int64_t) * (np + 1), side);
-    nf_units_kernel<<<grid_for(np + 1, 256), 256, 0, side>>>(32 * nf_slots(h->d), np, h->np_pairs, h->nbegin,
-                                                             h->nend, units.as<int64_t>());
-    scan_excl_i64(units.as<int64_t>(), job.uoff.as<int64_t>(), np + 1, side);
+    h->nf_wc = 32 * nf_slots(h->d);
+    h->nf_uoff = halloc_on<int64_t>(h, np + 1, side);
+    nf_units_kernel<<<grid_for(np + 1, 256), 256, 0, side>>>(h->nf_wc, np, h->np_pairs, h->nbegin, h->nend,
+                                                             units.as<int64_t>());
+    scan_excl_i64(units.as<int64_t>(), h->nf_uoff, np + 1, side);
     H2_CHECK_LAUNCH();
-    nunits = read1(job.uoff.as<int64_t>() + np, side);
-    job.umap = Scratch(sizeof(int) * (nunits > 0 ? nunits : 1), side);
-    unit_map_kernel<<<grid_for(np, 256), 256, 0, side>>>(np, job.uoff.as<int64_t>(), job.umap.as<int>());
+    nunits = read1(h->nf_uoff + np, side);
+    h->nf_nunits = nunits;
+    h->nf_umap = halloc_on<int>(h, nunits > 0 ? nunits : 1, side);
+    unit_map_kernel<<<grid_for(np, 256), 256, 0, side>>>(np, h->nf_uoff, h->nf_umap);
     H2_CHECK_LAUNCH();
     h->gpu_launches += 2;
   }
@@ -435,8 +429,8 @@ void fill_nearfield_begin(h2_handle* h, cudaStream_t side, int storage, int64_t 
     job.xs = Scratch(sizeof(double) * (size_t)h->n * h->d, side);
     scale_coords_kernel<<<grid_for((int64_t)h->n * h->d, 256), 256, 0, side>>>(
         (int64_t)h->n * h->d, h->X, kernel_cscale(h->kid, h->kp), job.xs.as<double>());
-    launch_fill(h, side, 1, nunits, h->n_np, job.umap.as<int>(), job.uoff.as<int64_t>(), h->np_pairs, h->np_off,
-                job.xs.as<double>(), h->np_val);
+    launch_fill(h, side, 1, nunits, h->n_np, h->nf_umap, h->nf_uoff, h->np_pairs, h->np_off, job.xs.as<double>(),
+                h->np_val);
     h->gpu_launches += 1;
     H2_CHECK_LAUNCH();
     h->gpu_launches += 1;
@@ -481,9 +475,7 @@ void fill_coupling(h2_handle* h, int storage, int64_t budget, const NfJob& job) 
 void fill_nearfield_join(h2_handle* h, NfJob& job) {
   if (!job.active) return;
   H2_CUDA_TRY(cudaStreamWaitEvent(h->stream, job.done, 0));
-  job.uoff.s = job.umap.s = job.xs.s = h->stream;
-  job.uoff = Scratch();
-  job.umap = Scratch();
+  job.xs.s = h->stream;
   job.xs = Scratch();
   job.active = false;
 }

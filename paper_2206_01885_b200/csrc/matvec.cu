@@ -139,6 +139,98 @@ __global__ void nearfield_kernel(int64_t np, const int2* __restrict__ pairs, con
   }
 }
 
+// ---- stored nearfield blocks: one pass over each entry, both directions ---------------------
+// Warp per nearfield unit (the fill's units: R rows x up to 32 CW columns of one block).  Lane l
+// owns the columns c0 + l + 32 s: x_j of those columns and the D^T x_i accumulators stay in
+// registers; each row contributes one FMA per entry to the row partial and one to the column
+// accumulator, the entries streamed once with coalesced 256-byte loads issued kMvPf rows ahead
+// (the loop is otherwise latency-bound: 16 FMAs per row per lane).  The row partials of 16 rows
+// are summed across the warp by a transposing butterfly (31 shuffles; lane l ends with row
+// l & 15), then one atomic per row; the column sums go out once per unit.  Diagonal blocks
+// (i = j) are stored whole and only multiply forward.
+template <int CW>
+__global__ void __launch_bounds__(256, (CW >= 8 ? 1 : 2)) nf_matvec_kernel(int64_t nunits, const int* __restrict__ umap,
+                                                           const int64_t* __restrict__ uoff,
+                                                           const int2* __restrict__ pairs,
+                                                           const int64_t* __restrict__ voff,
+                                                           const int* __restrict__ nbegin, const int* __restrict__ nend,
+                                                           const double* __restrict__ Dv, const double* __restrict__ xt,
+                                                           double* yt) {
+  constexpr int WC = 32 * CW, G = 16, PF = CW >= 6 ? 4 : (CW >= 3 ? 6 : 8);
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < nunits; u += nw) {
+    const int p = umap[u];
+    const int2 pr = pairs[p];
+    const bool diag = pr.x == pr.y;
+    const int bi = nbegin[pr.x], bj = nbegin[pr.y];
+    const int ni = nend[pr.x] - bi, nj = nend[pr.y] - bj;
+    int R, nrb, ncb;
+    unit_shape(ni, nj, WC, R, nrb, ncb);
+    const int loc = (int)(u - uoff[p]);
+    const int rb = loc / ncb, cb = loc - rb * ncb;
+    const int r0 = rb * R, c0 = cb * WC;
+    const int r1 = ni < r0 + R ? ni : r0 + R;
+    double xj[CW], acc[CW];
+    bool ok[CW];
+#pragma unroll
+    for (int s = 0; s < CW; s++) {
+      const int col = c0 + lane + 32 * s;
+      ok[s] = col < nj;
+      xj[s] = ok[s] ? xt[bj + col] : 0.0;
+      acc[s] = 0.0;
+    }
+    const double* Dp = Dv + voff[p] + c0 + lane;
+    auto load_row = [&](int a, double (&b)[CW], double& xa) {
+      if (a < r1) {  // warp-uniform
+        const double* row = Dp + (int64_t)a * nj;
+#pragma unroll
+        for (int s = 0; s < CW; s++) b[s] = ok[s] ? __ldcs(row + 32 * s) : 0.0;
+        xa = diag ? 0.0 : xt[bi + a];
+      } else {
+#pragma unroll
+        for (int s = 0; s < CW; s++) b[s] = 0.0;
+        xa = 0.0;
+      }
+    };
+    for (int a0 = r0; a0 < r1; a0 += G) {
+      double buf[PF][CW], xbuf[PF], part[G];
+#pragma unroll
+      for (int q = 0; q < PF; q++) load_row(a0 + q, buf[q], xbuf[q]);
+#pragma unroll
+      for (int q = 0; q < G; q++) {
+        double pq = 0.0;
+#pragma unroll
+        for (int s = 0; s < CW; s++) {
+          pq = fma(buf[q % PF][s], xj[s], pq);
+          acc[s] = fma(buf[q % PF][s], xbuf[q % PF], acc[s]);
+        }
+        part[q] = pq;
+        if (q + PF < G) load_row(a0 + q + PF, buf[q % PF], xbuf[q % PF]);
+      }
+      // lanes l and l ^ 16 first add up, then the transposing butterfly over 16 rows: after the
+      // step with offset o a lane keeps the half of its rows selected by bit o of its lane id
+#pragma unroll
+      for (int q = 0; q < G; q++) part[q] += __shfl_xor_sync(0xffffffffu, part[q], 16);
+#pragma unroll
+      for (int o = 8, w = 8; o > 0; o >>= 1, w >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int q = 0; q < w; q++) {
+          const double lo = part[q], hi = part[q + w];
+          const double send = up ? lo : hi, keep = up ? hi : lo;
+          part[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if (lane < 16 && a0 + lane < r1) atomicAdd(yt + bi + a0 + lane, part[0]);
+    }
+    if (!diag)
+#pragma unroll
+      for (int s = 0; s < CW; s++)
+        if (ok[s]) atomicAdd(yt + bj + c0 + lane + 32 * s, acc[s]);
+  }
+}
+
 template <int D>
 static void launch_far_near(const h2_handle* h, double p2, const double* zh, double* yh, const double* xt, double* yt,
                             int which) {
@@ -148,7 +240,19 @@ static void launch_far_near(const h2_handle* h, double p2, const double* zh, dou
     coupling_kernel<D><<<g, kMvThreads, 0, s>>>(h->n_cp, h->cp_pairs, h->cp_off, h->cp_stored ? h->cp_val : nullptr,
                                                 h->kid, p2, h->X, h->n, h->k, h->sk, h->r, zh, yh);
   }
-  if (which == 1 && h->n_np > 0) {
+  if (which == 1 && h->n_np > 0 && h->np_stored && h->nf_nunits > 0) {
+    const int cw = h->nf_wc / 32;
+    const int64_t blocks = (h->nf_nunits + 7) / 8;
+    const unsigned g = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
+    switch (cw) {
+#define H2_NFMV_CASE(C) \
+  case C: nf_matvec_kernel<C><<<g, 256, 0, s>>>(h->nf_nunits, h->nf_umap, h->nf_uoff, h->np_pairs, h->np_off, \
+                                                h->nbegin, h->nend, h->np_val, xt, yt); break;
+      H2_NFMV_CASE(2) H2_NFMV_CASE(3) H2_NFMV_CASE(4) H2_NFMV_CASE(5) H2_NFMV_CASE(6) H2_NFMV_CASE(8)
+#undef H2_NFMV_CASE
+      default: throw Error{H2_ERR_INTERNAL, "nearfield matvec: unexpected unit width"};
+    }
+  } else if (which == 1 && h->n_np > 0) {
     unsigned g = (unsigned)(h->n_np < 148 * 64 ? h->n_np : 148 * 64);
     nearfield_kernel<D><<<g, kMvThreads, 0, s>>>(h->n_np, h->np_pairs, h->np_off, h->np_stored ? h->np_val : nullptr,
                                                  h->kid, p2, h->X, h->n, h->nbegin, h->nend, xt, yt);
