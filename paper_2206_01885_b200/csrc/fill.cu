@@ -96,6 +96,13 @@ __global__ void nf_units_kernel(int wc, int64_t np, const int2* __restrict__ pai
   }
 }
 
+// matvec items (matvec.cu): one per column chunk of a nearfield block, covering all its rows
+__global__ void nf_items_kernel(int wc, int64_t np, const int2* __restrict__ pairs, const int* __restrict__ nbegin,
+                                const int* __restrict__ nend, int64_t* items) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p <= np; p += (int64_t)gridDim.x * blockDim.x)
+    items[p] = p == np ? 0 : (int64_t)((nend[pairs[p].y] - nbegin[pairs[p].y] + wc - 1) / wc);
+}
+
 __global__ void unit_map_kernel(int64_t np, const int64_t* __restrict__ uoff, int* umap) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np; p += (int64_t)gridDim.x * blockDim.x)
     for (int64_t u = uoff[p]; u < uoff[p + 1]; u++) umap[u] = (int)p;
@@ -403,7 +410,7 @@ void fill_nearfield_begin(h2_handle* h, cudaStream_t side, int storage, int64_t 
   const int64_t nb = h->np_entries * 8;
   const bool store_np = storage == H2_STORE_ALL || (storage == H2_STORE_AUTO && nb <= store_budget(budget));
   if (store_np) {
-    h->np_val = halloc<double>(h, h->np_entries);
+    h->np_val = halloc<double>(h, h->np_entries + 2);  // +2: the matvec's 16-byte-aligned bulk copies
     h->np_stored = 1;
     job.stored_bytes = nb;
   }
@@ -422,7 +429,16 @@ void fill_nearfield_begin(h2_handle* h, cudaStream_t side, int storage, int64_t 
     h->nf_umap = halloc_on<int>(h, nunits > 0 ? nunits : 1, side);
     unit_map_kernel<<<grid_for(np, 256), 256, 0, side>>>(np, h->nf_uoff, h->nf_umap);
     H2_CHECK_LAUNCH();
-    h->gpu_launches += 2;
+    h->nf_ioff = halloc_on<int64_t>(h, np + 1, side);
+    nf_items_kernel<<<grid_for(np + 1, 256), 256, 0, side>>>(h->nf_wc, np, h->np_pairs, h->nbegin, h->nend,
+                                                             units.as<int64_t>());
+    scan_excl_i64(units.as<int64_t>(), h->nf_ioff, np + 1, side);
+    H2_CHECK_LAUNCH();
+    h->nf_nitems = read1(h->nf_ioff + np, side);
+    h->nf_imap = halloc_on<int>(h, h->nf_nitems > 0 ? h->nf_nitems : 1, side);
+    unit_map_kernel<<<grid_for(np, 256), 256, 0, side>>>(np, h->nf_ioff, h->nf_imap);
+    H2_CHECK_LAUNCH();
+    h->gpu_launches += 4;
   }
   if (h->timing) H2_CUDA_TRY(cudaEventRecord(job.t0, side));
   if (nunits > 0) {

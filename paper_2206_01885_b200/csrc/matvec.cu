@@ -4,6 +4,8 @@
 //   downward  y^_c += R_c y^_p, then y_i += U_i y^_i at leaves          (levels 1 -> deepest)
 //   nearfield y_i += D_ij x_j and y_j += D_ij^T x_i, i <= j              (stored or on the fly)
 // Accumulation uses fp64 atomics (order-dependent rounding only).  Used for accuracy checks.
+#include <cstdlib>
+
 #include "h2_internal.cuh"
 
 namespace h2 {
@@ -140,37 +142,36 @@ __global__ void nearfield_kernel(int64_t np, const int2* __restrict__ pairs, con
 }
 
 // ---- stored nearfield blocks: one pass over each entry, both directions ---------------------
-// Warp per nearfield unit (the fill's units: R rows x up to 32 CW columns of one block).  Lane l
-// owns the columns c0 + l + 32 s: x_j of those columns and the D^T x_i accumulators stay in
-// registers; each row contributes one FMA per entry to the row partial and one to the column
-// accumulator, the entries streamed once with coalesced 256-byte loads issued kMvPf rows ahead
-// (the loop is otherwise latency-bound: 16 FMAs per row per lane).  The row partials of 16 rows
-// are summed across the warp by a transposing butterfly (31 shuffles; lane l ends with row
-// l & 15), then one atomic per row; the column sums go out once per unit.  Diagonal blocks
-// (i = j) are stored whole and only multiply forward.
-template <int CW>
-__global__ void __launch_bounds__(256, (CW >= 8 ? 1 : 2)) nf_matvec_kernel(int64_t nunits, const int* __restrict__ umap,
-                                                           const int64_t* __restrict__ uoff,
+// Warp per ITEM: one 32 CW-column slice of one nearfield block (a 32 CW SPLIT-column chunk is
+// split over SPLIT warps), all rows.  Lane l owns the columns c0 + l + 32 s: x_j of those columns
+// and the D^T x_i accumulators stay in registers for the whole block (flushed with one atomic per
+// column), each row contributes one FMA per entry to the row partial and one to the column
+// accumulator; the entries stream once with coalesced 256-byte loads issued PF rows ahead.  The
+// row partials of 16 rows are summed across the warp by a transposing butterfly (31 shuffles;
+// lane l ends with row l & 15), one atomic per row.  Diagonal blocks (i = j) are stored whole and
+// only multiply forward.
+template <int CW, int SPLIT>
+__global__ void __launch_bounds__(256, 2) nf_matvec_kernel(int64_t nitems, const int* __restrict__ imap,
+                                                           const int64_t* __restrict__ ioff,
                                                            const int2* __restrict__ pairs,
                                                            const int64_t* __restrict__ voff,
                                                            const int* __restrict__ nbegin, const int* __restrict__ nend,
                                                            const double* __restrict__ Dv, const double* __restrict__ xt,
                                                            double* yt) {
-  constexpr int WC = 32 * CW, G = 16, PF = CW >= 6 ? 4 : (CW >= 3 ? 6 : 8);
+  constexpr int WC = 32 * CW * SPLIT, G = 16, PF = CW >= 3 ? 4 : 8;
+  static_assert(G % PF == 0, "the prefetch ring must wrap with the row groups");
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < nunits; u += nw) {
-    const int p = umap[u];
+  for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < nitems * SPLIT; v += nw) {
+    const int64_t it = v / SPLIT;
+    const int half = (int)(v - it * SPLIT);
+    const int p = imap[it];
     const int2 pr = pairs[p];
     const bool diag = pr.x == pr.y;
     const int bi = nbegin[pr.x], bj = nbegin[pr.y];
     const int ni = nend[pr.x] - bi, nj = nend[pr.y] - bj;
-    int R, nrb, ncb;
-    unit_shape(ni, nj, WC, R, nrb, ncb);
-    const int loc = (int)(u - uoff[p]);
-    const int rb = loc / ncb, cb = loc - rb * ncb;
-    const int r0 = rb * R, c0 = cb * WC;
-    const int r1 = ni < r0 + R ? ni : r0 + R;
+    const int c0 = (int)(it - ioff[p]) * WC + half * 32 * CW;
+    if (c0 >= nj) continue;  // warp-uniform: an empty slice of a narrow last chunk
     double xj[CW], acc[CW];
     bool ok[CW];
 #pragma unroll
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(256, (CW >= 8 ? 1 : 2)) nf_matvec_kernel(int64
     }
     const double* Dp = Dv + voff[p] + c0 + lane;
     auto load_row = [&](int a, double (&b)[CW], double& xa) {
-      if (a < r1) {  // warp-uniform
+      if (a < ni) {  // warp-uniform
         const double* row = Dp + (int64_t)a * nj;
 #pragma unroll
         for (int s = 0; s < CW; s++) b[s] = ok[s] ? __ldcs(row + 32 * s) : 0.0;
@@ -193,10 +194,12 @@ __global__ void __launch_bounds__(256, (CW >= 8 ? 1 : 2)) nf_matvec_kernel(int64
         xa = 0.0;
       }
     };
-    for (int a0 = r0; a0 < r1; a0 += G) {
-      double buf[PF][CW], xbuf[PF], part[G];
+    // a continuous ring: row a lives in buf[a % PF] from PF rows before its use (across groups)
+    double buf[PF][CW], xbuf[PF];
 #pragma unroll
-      for (int q = 0; q < PF; q++) load_row(a0 + q, buf[q], xbuf[q]);
+    for (int q = 0; q < PF; q++) load_row(q, buf[q], xbuf[q]);
+    for (int a0 = 0; a0 < ni; a0 += G) {
+      double part[G];
 #pragma unroll
       for (int q = 0; q < G; q++) {
         double pq = 0.0;
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(256, (CW >= 8 ? 1 : 2)) nf_matvec_kernel(int64
           acc[s] = fma(buf[q % PF][s], xbuf[q % PF], acc[s]);
         }
         part[q] = pq;
-        if (q + PF < G) load_row(a0 + q + PF, buf[q % PF], xbuf[q % PF]);
+        load_row(a0 + q + PF, buf[q % PF], xbuf[q % PF]);
       }
       // lanes l and l ^ 16 first add up, then the transposing butterfly over 16 rows: after the
       // step with offset o a lane keeps the half of its rows selected by bit o of its lane id
@@ -222,13 +225,191 @@ __global__ void __launch_bounds__(256, (CW >= 8 ? 1 : 2)) nf_matvec_kernel(int64
           part[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
         }
       }
-      if (lane < 16 && a0 + lane < r1) atomicAdd(yt + bi + a0 + lane, part[0]);
+      if (lane < 16 && a0 + lane < ni) atomicAdd(yt + bi + a0 + lane, part[0]);
     }
     if (!diag)
 #pragma unroll
       for (int s = 0; s < CW; s++)
         if (ok[s]) atomicAdd(yt + bj + c0 + lane + 32 * s, acc[s]);
   }
+}
+
+// ---- stored nearfield blocks, bulk-staged (the default) --------------------------------------
+// A CTA walks its nearfield units with a two-deep ring of shared-memory buffers: one elected
+// thread arms an mbarrier with the unit's byte count and issues cp.async.bulk copies (the TMA
+// bulk engine: a unit of a block with nj <= 32 CW columns is ONE contiguous range; wider blocks
+// copy row by row) of the NEXT unit while the CTA computes the current one from shared memory.
+// Nothing is staged through registers, so HBM sees up to two units (2 x ~32 KB) in flight per
+// CTA without the register cost of a deep software prefetch.  Compute: warp w takes rows
+// r0 + w, r0 + w + 8, ...; lanes over columns; row sums by warp shuffles (one atomic per row),
+// the D^T x_i column partials reduced across the 8 warps in shared memory (one atomic per column
+// per unit).  Diagonal blocks multiply forward only.
+constexpr int kMvBulkThreads = 256, kMvBulkWarps = kMvBulkThreads / 32, kMvBulkBuf = 4160;
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done)
+                 : "r"(a), "r"(parity)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+
+struct MvUnit {
+  int pi, pj, bi, bj, r0, r1, c0, nc, nj;
+  int64_t base;  // global index (doubles) of the unit's first entry
+  bool contig;   // nj <= WC: the unit's rows are one contiguous range
+};
+
+template <int WC>
+__device__ __forceinline__ MvUnit mv_unit(int64_t u, const int* __restrict__ umap, const int64_t* __restrict__ uoff,
+                                          const int2* __restrict__ pairs, const int64_t* __restrict__ voff,
+                                          const int* __restrict__ nbegin, const int* __restrict__ nend) {
+  MvUnit m;
+  const int p = umap[u];
+  const int2 pr = pairs[p];
+  m.pi = pr.x;
+  m.pj = pr.y;
+  m.bi = nbegin[pr.x];
+  m.bj = nbegin[pr.y];
+  const int ni = nend[pr.x] - m.bi;
+  m.nj = nend[pr.y] - m.bj;
+  int R, nrb, ncb;
+  unit_shape(ni, m.nj, WC, R, nrb, ncb);
+  const int loc = (int)(u - uoff[p]);
+  const int rb = loc / ncb, cb = loc - rb * ncb;
+  m.r0 = rb * R;
+  m.r1 = ni < m.r0 + R ? ni : m.r0 + R;
+  m.c0 = cb * WC;
+  m.nc = m.nj - m.c0 < WC ? m.nj - m.c0 : WC;
+  m.base = voff[p] + (int64_t)m.r0 * m.nj + m.c0;
+  m.contig = m.nj <= WC;
+  return m;
+}
+
+// shared-memory position of (row a - r0, column b - c0) of a staged unit; copies start at an
+// even global index (16-byte alignment), hence the +1 when the range starts odd
+__device__ __forceinline__ int mv_pos(const MvUnit& m, int ra, int cb) {
+  if (m.contig) return (int)(m.base & 1) + ra * m.nj + cb;
+  const int64_t rs = m.base + (int64_t)ra * m.nj;
+  return ra * (m.nc + 4) + (int)(rs & 1) + cb;
+}
+
+template <int WC>
+__device__ __forceinline__ void mv_issue(const MvUnit& m, const double* __restrict__ Dv, double* buf, uint64_t* bar) {
+  if (m.contig) {
+    const int64_t s0 = m.base & ~1LL, e = m.base + (int64_t)(m.r1 - m.r0) * m.nj;
+    const unsigned bytes = (unsigned)(((e - s0 + 1) & ~1LL) * 8);
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(buf, Dv + s0, bytes, bar);
+  } else {
+    unsigned total = 0;
+    for (int ra = 0; ra < m.r1 - m.r0; ra++) {
+      const int64_t rs = m.base + (int64_t)ra * m.nj;
+      total += (unsigned)((((rs + m.nc) - (rs & ~1LL) + 1) & ~1LL) * 8);
+    }
+    mbar_expect_tx(bar, total);
+    for (int ra = 0; ra < m.r1 - m.r0; ra++) {
+      const int64_t rs = m.base + (int64_t)ra * m.nj;
+      const unsigned bytes = (unsigned)((((rs + m.nc) - (rs & ~1LL) + 1) & ~1LL) * 8);
+      bulk_g2s(buf + ra * (m.nc + 4), Dv + (rs & ~1LL), bytes, bar);
+    }
+  }
+}
+
+template <int CW>
+__global__ void __launch_bounds__(kMvBulkThreads) nf_matvec_bulk_kernel(
+    int64_t nunits, const int* __restrict__ umap, const int64_t* __restrict__ uoff, const int2* __restrict__ pairs,
+    const int64_t* __restrict__ voff, const int* __restrict__ nbegin, const int* __restrict__ nend,
+    const double* __restrict__ Dv, const double* __restrict__ xt, double* yt) {
+  constexpr int WC = 32 * CW;
+  extern __shared__ double sm[];  // buf[2][kMvBulkBuf], red[kMvBulkWarps][WC]
+  __shared__ __align__(8) uint64_t bar[2];
+  double* red = sm + 2 * kMvBulkBuf;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int64_t u = blockIdx.x;
+  if (tid == 0 && u < nunits) mv_issue<WC>(mv_unit<WC>(u, umap, uoff, pairs, voff, nbegin, nend), Dv, sm, &bar[0]);
+  for (int k = 0; u < nunits; k++, u += gridDim.x) {
+    const int cur = k & 1;
+    const int64_t un = u + gridDim.x;
+    if (tid == 0 && un < nunits) {  // the other buffer was released by the barrier ending step k-1
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mv_issue<WC>(mv_unit<WC>(un, umap, uoff, pairs, voff, nbegin, nend), Dv, sm + (cur ^ 1) * kMvBulkBuf,
+                   &bar[cur ^ 1]);
+    }
+    const MvUnit m = mv_unit<WC>(u, umap, uoff, pairs, voff, nbegin, nend);
+    const bool diag = m.pi == m.pj;
+    const double* buf = sm + cur * kMvBulkBuf;
+    double xj[CW], acc[CW];
+#pragma unroll
+    for (int s = 0; s < CW; s++) {
+      const int cb = lane + 32 * s;
+      xj[s] = cb < m.nc ? xt[m.bj + m.c0 + cb] : 0.0;
+      acc[s] = 0.0;
+    }
+    mbar_wait(&bar[cur], (unsigned)((k >> 1) & 1));
+    for (int ra = w; ra < m.r1 - m.r0; ra += kMvBulkWarps) {
+      const double xa = diag ? 0.0 : xt[m.bi + m.r0 + ra];
+      const int p0 = mv_pos(m, ra, 0);
+      double part = 0.0;
+#pragma unroll
+      for (int s = 0; s < CW; s++) {
+        const int cb = lane + 32 * s;
+        const double dv = cb < m.nc ? buf[p0 + cb] : 0.0;
+        part = fma(dv, xj[s], part);
+        acc[s] = fma(dv, xa, acc[s]);
+      }
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane == 0) atomicAdd(yt + m.bi + m.r0 + ra, part);
+    }
+    if (!diag) {
+#pragma unroll
+      for (int s = 0; s < CW; s++) red[w * WC + lane + 32 * s] = acc[s];
+    }
+    __syncthreads();  // buffer `cur` consumed, column partials published
+    if (!diag)
+      for (int cb = tid; cb < m.nc; cb += kMvBulkThreads) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < kMvBulkWarps; q++) t += red[q * WC + cb];
+        atomicAdd(yt + m.bj + m.c0 + cb, t);
+      }
+    __syncthreads();  // red free for the next unit
+  }
+}
+
+// H2_MV_BULK=1 (A/B knob, read once): the bulk-staged nearfield kernel instead of the
+// register-prefetch one (measured slower on config 4: 24.7 vs 14 ms -- the per-unit metadata
+// chain delays the next copy)
+static bool mv_bulk() {
+  static const bool v = [] {
+    const char* e = getenv("H2_MV_BULK");
+    return e && atoi(e) != 0;
+  }();
+  return v;
 }
 
 template <int D>
@@ -242,13 +423,32 @@ static void launch_far_near(const h2_handle* h, double p2, const double* zh, dou
   }
   if (which == 1 && h->n_np > 0 && h->np_stored && h->nf_nunits > 0) {
     const int cw = h->nf_wc / 32;
-    const int64_t blocks = (h->nf_nunits + 7) / 8;
+    const int64_t blocks = (2 * h->nf_nitems + 7) / 8;  // (split items: up to two warps per item)
     const unsigned g = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
+    if (mv_bulk()) {
+      const int smem = (int)(sizeof(double) * (2 * kMvBulkBuf + kMvBulkWarps * 32 * cw));
+      const unsigned gb = (unsigned)(h->nf_nunits < 148 * 2 ? h->nf_nunits : 148 * 2);
+      switch (cw) {
+#define H2_NFMVB_CASE(C)                                                                                         \
+  case C:                                                                                                        \
+    H2_CUDA_TRY(cudaFuncSetAttribute(nf_matvec_bulk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+    nf_matvec_bulk_kernel<C><<<gb, kMvBulkThreads, smem, s>>>(h->nf_nunits, h->nf_umap, h->nf_uoff, h->np_pairs,  \
+                                                              h->np_off, h->nbegin, h->nend, h->np_val, xt, yt); \
+    break;
+        H2_NFMVB_CASE(2) H2_NFMVB_CASE(3) H2_NFMVB_CASE(4) H2_NFMVB_CASE(5) H2_NFMVB_CASE(6) H2_NFMVB_CASE(8)
+#undef H2_NFMVB_CASE
+        default: throw Error{H2_ERR_INTERNAL, "nearfield matvec: unexpected unit width"};
+      }
+      return;
+    }
     switch (cw) {
-#define H2_NFMV_CASE(C) \
-  case C: nf_matvec_kernel<C><<<g, 256, 0, s>>>(h->nf_nunits, h->nf_umap, h->nf_uoff, h->np_pairs, h->np_off, \
-                                                h->nbegin, h->nend, h->np_val, xt, yt); break;
-      H2_NFMV_CASE(2) H2_NFMV_CASE(3) H2_NFMV_CASE(4) H2_NFMV_CASE(5) H2_NFMV_CASE(6) H2_NFMV_CASE(8)
+#define H2_NFMV_CASE(C, CWW, SP)                                                                              \
+  case C:                                                                                                    \
+    nf_matvec_kernel<CWW, SP><<<g, 256, 0, s>>>(h->nf_nitems, h->nf_imap, h->nf_ioff, h->np_pairs, h->np_off,     \
+                                                h->nbegin, h->nend, h->np_val, xt, yt);                      \
+    break;
+      H2_NFMV_CASE(2, 2, 1) H2_NFMV_CASE(3, 3, 1) H2_NFMV_CASE(4, 4, 1) H2_NFMV_CASE(5, 5, 1)
+      H2_NFMV_CASE(6, 3, 2) H2_NFMV_CASE(8, 4, 2)
 #undef H2_NFMV_CASE
       default: throw Error{H2_ERR_INTERNAL, "nearfield matvec: unexpected unit width"};
     }

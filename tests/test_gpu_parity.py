@@ -71,6 +71,7 @@ def matvec_check(g, o, pts, kid, kp, id_tol, cfg):
 CASES = [  # name, config, n, q override
     ("cfg1_full", 1, 8192, None),
     ("cfg2_shape", 2, 40000, 64),
+    ("cfg2_q200", 2, 40000, None),  # leaves of up to 200 points > a 160-column unit: row-wise bulk copies
     ("cfg3_shape", 3, 30000, None),
     ("cfg4_shape", 4, 60000, None),
     ("cfg5_shape", 5, 5000, 64),
