@@ -81,6 +81,40 @@ __global__ void coupling_kernel(int64_t np, const int2* __restrict__ pairs, cons
   }
 }
 
+// stored coupling blocks (k_i x k_j, small): warp per pair, lanes over columns; each row adds one
+// warp-reduced dot to y^_i (one atomic per row) and its column contributions to registers (one
+// atomic per column per pair): every entry read once, coalesced along the row
+__global__ void __launch_bounds__(256) coupling_mv_kernel(int64_t np, const int2* __restrict__ pairs,
+                                                          const int64_t* __restrict__ voff, const double* __restrict__ B,
+                                                          const int* __restrict__ k, int r,
+                                                          const double* __restrict__ zh, double* yh) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < np; p += nw) {
+    const int2 pr = pairs[p];
+    const int i = pr.x, j = pr.y, ki = k[i], kj = k[j];
+    const double* Bp = B + voff[p];
+    const double* zi = zh + (int64_t)i * r;
+    const double* zj = zh + (int64_t)j * r;
+    double* yi = yh + (int64_t)i * r;
+    double* yj = yh + (int64_t)j * r;
+    for (int c0 = 0; c0 < kj; c0 += 32) {
+      const int col = c0 + lane;
+      const bool ok = col < kj;
+      const double zc = ok ? zj[col] : 0.0;
+      double acc = 0.0;
+      for (int a = 0; a < ki; a++) {
+        const double v = ok ? Bp[(int64_t)a * kj + col] : 0.0;
+        double part = v * zc;
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) atomicAdd(yi + a, part);
+        acc = fma(v, zi[a], acc);
+      }
+      if (ok) atomicAdd(yj + col, acc);
+    }
+  }
+}
+
 // leaf outputs only for leaves whose first point lies in [p_lo, p_hi) (sharded: the row owner)
 __global__ void down_kernel(int base, int r, const int* __restrict__ is_leaf, const int* __restrict__ nbegin,
                             const int* __restrict__ parent, const int* __restrict__ k, const int* __restrict__ xbar_n,
@@ -416,7 +450,11 @@ template <int D>
 static void launch_far_near(const h2_handle* h, double p2, const double* zh, double* yh, const double* xt, double* yt,
                             int which) {
   cudaStream_t s = h->stream;
-  if (which == 0 && h->n_cp > 0) {
+  if (which == 0 && h->n_cp > 0 && h->cp_stored) {
+    const int64_t blocks = (h->n_cp + 7) / 8;
+    const unsigned g = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
+    coupling_mv_kernel<<<g, 256, 0, s>>>(h->n_cp, h->cp_pairs, h->cp_off, h->cp_val, h->k, h->r, zh, yh);
+  } else if (which == 0 && h->n_cp > 0) {
     unsigned g = (unsigned)(h->n_cp < 148 * 64 ? h->n_cp : 148 * 64);
     coupling_kernel<D><<<g, kMvThreads, 0, s>>>(h->n_cp, h->cp_pairs, h->cp_off, h->cp_stored ? h->cp_val : nullptr,
                                                 h->kid, p2, h->X, h->n, h->k, h->sk, h->r, zh, yh);
