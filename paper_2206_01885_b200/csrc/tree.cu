@@ -92,52 +92,69 @@ __global__ void gather_soa_kernel(const double* __restrict__ pts, const int* __r
 }
 
 // ---- a3: level-by-level node construction -------------------------------------------------
-// flag[p] = 1 iff point p starts a child of its (non-leaf) level-l node at level l+1
-__global__ void level_flags_kernel(const unsigned long long* __restrict__ key, const int* __restrict__ nid, int64_t n,
-                                   const int* __restrict__ is_leaf, const int* __restrict__ nbegin, int sh,
-                                   int* flag, int* nid_next) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-    int i = nid[p];
-    if (i < 0 || is_leaf[i]) {
-      flag[p] = 0;
-      nid_next[p] = -1;
+// The points are sorted by key, so the children of a node [b, e) at level l are the runs of its
+// points with equal child digit (key >> d(L - l - 1)) & (2^d - 1), in digit order -- level-order
+// ids with key order inside a level.  Per level: one thread per (node, digit) finds the digit's
+// run by two binary searches inside the node's range (O(nodes 2^d log n), not O(n)); a prefix
+// sum over the existence flags numbers the children; a third kernel writes them.
+__device__ __forceinline__ int digit_lower_bound(const unsigned long long* __restrict__ key, int b, int e, int sh,
+                                                 unsigned mask, unsigned g) {
+  while (b < e) {  // first position in [b, e) whose digit is >= g (digits are non-decreasing)
+    const int mid = (b + e) >> 1;
+    if ((unsigned)((key[mid] >> sh) & mask) < g) b = mid + 1;
+    else e = mid;
+  }
+  return b;
+}
+
+__global__ void split_count_kernel(const unsigned long long* __restrict__ key, int lb, int count, int d, int sh,
+                                   const int* __restrict__ nbegin, const int* __restrict__ nend,
+                                   const int* __restrict__ is_leaf, int64_t* exists, int2* range) {
+  const int64_t nd = (int64_t)1 << d;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= count * nd;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (t == count * nd) {
+      exists[t] = 0;
       continue;
     }
-    flag[p] = (p == nbegin[i]) || ((key[p] >> sh) != (key[p - 1] >> sh));
-  }
-}
-
-__global__ void level_create_kernel(const int* __restrict__ nid, const int* __restrict__ flag,
-                                    const int* __restrict__ cnt, int64_t n, const int* __restrict__ is_leaf,
-                                    int base, int lvl, int* nid_next, int* level, int* nbegin, int* nend,
-                                    int* parent) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-    int i = nid[p];
-    if (i < 0 || is_leaf[i]) continue;
-    int id = base + cnt[p] - 1;
-    nid_next[p] = id;
-    if (flag[p]) {
-      nbegin[id] = (int)p;
-      parent[id] = i;
-      level[id] = lvl;
+    const int i = lb + (int)(t >> d);
+    const unsigned g = (unsigned)(t & (nd - 1));
+    int lo = 0, hi = 0;
+    if (!is_leaf[i]) {
+      const unsigned mask = (unsigned)(nd - 1);
+      lo = digit_lower_bound(key, nbegin[i], nend[i], sh, mask, g);
+      hi = g + 1 < nd ? digit_lower_bound(key, lo, nend[i], sh, mask, g + 1) : nend[i];
     }
-    if (p == n - 1 || nid[p + 1] != i || flag[p + 1]) nend[id] = (int)(p + 1);
+    exists[t] = hi > lo;
+    range[t] = make_int2(lo, hi);
   }
 }
 
-__global__ void level_finalize_kernel(int base, int count, int q, int lvl, int L, const int* __restrict__ nbegin,
-                                      const int* __restrict__ nend, const int* __restrict__ parent, int* is_leaf,
-                                      int* first_child, int* nchild) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= count) return;
-  int id = base + t;
-  int c = nend[id] - nbegin[id];
-  is_leaf[id] = !(c > q && lvl < L);
-  first_child[id] = -1;
-  nchild[id] = 0;
-  int p = parent[id];
-  if (nbegin[id] == nbegin[p]) first_child[p] = id;
-  atomicAdd(&nchild[p], 1);
+__global__ void split_create_kernel(int lb, int count, int d, int base, int lvl, int q, int L,
+                                    const int64_t* __restrict__ pos, const int2* __restrict__ range, int* level,
+                                    int* nbegin, int* nend, int* parent, int* is_leaf, int* first_child,
+                                    int* nchild) {
+  const int64_t nd = (int64_t)1 << d;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count * nd;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = lb + (int)(t >> d);
+    const int64_t t0 = t & ~(nd - 1);  // the node's digit 0
+    if ((t & (nd - 1)) == 0) {         // one thread per parent: its child count and first child
+      const int nc = (int)(pos[t0 + nd] - pos[t0]);
+      nchild[i] = nc;
+      first_child[i] = nc > 0 ? base + (int)pos[t0] : -1;
+    }
+    if (pos[t + 1] == pos[t]) continue;  // this digit has no point
+    const int id = base + (int)pos[t];
+    const int2 rg = range[t];
+    level[id] = lvl;
+    nbegin[id] = rg.x;
+    nend[id] = rg.y;
+    parent[id] = i;
+    is_leaf[id] = !(rg.y - rg.x > q && lvl < L);
+    first_child[id] = -1;
+    nchild[id] = 0;
+  }
 }
 
 __global__ void root_init_kernel(int n, int q, int L, int* level, int* nbegin, int* nend, int* parent, int* is_leaf,
@@ -242,29 +259,27 @@ void build_tree(h2_handle* h, const double* pts) {
   h->nnodes = 1;
   h->lvl_start.assign(1, 0);
   h->lvl_start.push_back(1);
-  Scratch nid_a(sizeof(int) * n, s), nid_b(sizeof(int) * n, s), flag(sizeof(int) * n, s), cnt(sizeof(int) * n, s);
-  H2_CUDA_TRY(cudaMemsetAsync(nid_a.p, 0, sizeof(int) * n, s));
   int l = 0;
+  const int64_t nd = (int64_t)1 << d;
   while (l < L) {
-    int sh = d * (L - l - 1);
-    level_flags_kernel<<<grid_for(n, 256), 256, 0, s>>>(h->key, nid_a.as<int>(), n, h->is_leaf, h->nbegin, sh,
-                                                        flag.as<int>(), nid_b.as<int>());
+    const int lb = h->lvl_start[l], count = h->lvl_start[l + 1] - lb;
+    const int64_t m = count * nd;
+    Scratch ex(sizeof(int64_t) * (m + 1), s), pos(sizeof(int64_t) * (m + 1), s), rg(sizeof(int2) * (m + 1), s);
+    split_count_kernel<<<grid_for(m + 1, 256), 256, 0, s>>>(h->key, lb, count, d, d * (L - l - 1), h->nbegin, h->nend,
+                                                           h->is_leaf, ex.as<int64_t>(), rg.as<int2>());
+    scan_excl_i64(ex.as<int64_t>(), pos.as<int64_t>(), m + 1, s);
     H2_CHECK_LAUNCH();
-    scan_incl_i32(flag.as<int>(), cnt.as<int>(), n, s);
     h->gpu_launches += 1;
-    int total = read1(cnt.as<int>() + n - 1, s);
+    const int total = (int)read1(pos.as<int64_t>() + m, s);
     if (total == 0) break;
     grow_nodes(h, cap, h->nnodes + total);
-    level_create_kernel<<<grid_for(n, 256), 256, 0, s>>>(nid_a.as<int>(), flag.as<int>(), cnt.as<int>(), n,
-                                                         h->is_leaf, h->nnodes, l + 1, nid_b.as<int>(), h->level,
-                                                         h->nbegin, h->nend, h->parent);
-    level_finalize_kernel<<<(total + 255) / 256, 256, 0, s>>>(h->nnodes, total, h->q, l + 1, L, h->nbegin, h->nend,
-                                                             h->parent, h->is_leaf, h->first_child, h->nchild);
+    split_create_kernel<<<grid_for(m, 256), 256, 0, s>>>(lb, count, d, h->nnodes, l + 1, h->q, L, pos.as<int64_t>(),
+                                                        rg.as<int2>(), h->level, h->nbegin, h->nend, h->parent,
+                                                        h->is_leaf, h->first_child, h->nchild);
     H2_CHECK_LAUNCH();
-    h->gpu_launches += 2;
+    h->gpu_launches += 1;
     h->nnodes += total;
     h->lvl_start.push_back(h->nnodes);
-    std::swap(nid_a, nid_b);
     l++;
   }
   h->depth = (int)h->lvl_start.size() - 2;
