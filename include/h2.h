@@ -112,6 +112,20 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
                        double admissibility, const h2_options* opt);
 
 /*
+ * h2_rebuild_ex -- "HiDR once for all" (§6.1.3): the
+ * representor sets X_i^*, Y_i^* depend on the points and the budget r only, so an H^2 of the same
+ * points for ANOTHER kernel (or kernel parameter, or id_tol) reuses them.  The new handle copies
+ * base's tree, lists and HiDR sets (a1-a4, a6-a7, at base's r) and runs the skeleton sweep and the
+ * block fill (a8-a10) for kernel_id / kernel_params / id_tol.  The result equals h2_build_ex of
+ * the same points with opt->r_override = base's r, bit for bit in every index set.
+ *   base  a handle from h2_build / h2_build_ex / h2_rebuild_ex; only read; stays valid.
+ *   opt   as for h2_build_ex (r_override ignored; points_on_host meaningless); opt->comm must be
+ *         base's comm (NULL for a single-GPU base): a sharded rebuild is collective.
+ * Returns the new handle or NULL (h2_last_error).                                              */
+h2_handle* h2_rebuild_ex(const h2_handle* base, int32_t kernel_id, const double* kernel_params, double id_tol,
+                         const h2_options* opt);
+
+/*
  * h2_matvec -- y = K~ x, the four-pass H^2 product: upward (z^ = U^T x, z^_p = sum R_c^T z^_c),
  * coupling (y^_i += B_ij z^_j), downward (y^_c += R_c y^_p, y = U y^), nearfield (y_i += D_ij x_j).
  *   x, y   DEVICE, length n fp64, ORIGINAL point order; y is overwritten; x and y must not alias.

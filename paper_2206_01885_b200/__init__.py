@@ -25,7 +25,7 @@ _EXPORT_DTYPE = dict(PERM=np.int32, NODES=np.int32, IL_OFF=np.int64, IL_IDX=np.i
                      K=np.int32, SK_OFF=np.int64, SK_IDX=np.int32, U_OFF=np.int64, U=np.float64,
                      XBAR_N=np.int32, TREE_X=np.float64, SHARD=np.int64)
 
-EXPORTED_SYMBOLS = ["h2_build", "h2_build_ex", "h2_options_default", "h2_matvec", "h2_free", "h2_last_error",
+EXPORTED_SYMBOLS = ["h2_build", "h2_build_ex", "h2_rebuild_ex", "h2_options_default", "h2_matvec", "h2_free", "h2_last_error",
                     "h2_last_error_message", "h2_info", "h2_export", "h2_sample_blocks", "h2_comm_nccl_unique_id",
                     "h2_comm_init_nccl", "h2_comm_init_local", "h2_comm_free", "h2_comm_size", "h2_comm_rank",
                     "h2_shard_cut_level", "h2_shard_split"]
@@ -71,6 +71,8 @@ def lib():
         L.h2_build_ex.restype = vp
         L.h2_build_ex.argtypes = [vp, i64, i32, i32, vp, f64, i32, f64, C.POINTER(h2_options)]
         L.h2_options_default.argtypes = [C.POINTER(h2_options)]
+        L.h2_rebuild_ex.restype = vp
+        L.h2_rebuild_ex.argtypes = [vp, i32, vp, f64, C.POINTER(h2_options)]
         L.h2_matvec.restype = C.c_int
         L.h2_matvec.argtypes = [vp, vp, vp]
         L.h2_free.argtypes = [vp]
@@ -280,7 +282,29 @@ class H2Matrix:
             ptr = points.data_ptr()
         self.n, self.d = int(points.shape[0]), int(points.shape[1])
         self.stream = stream
+        self.id_tol = id_tol
         self.h = h2_build(ptr, self.n, self.d, kernel_id, list(kernel_params), id_tol, leaf_size, admissibility, o)
+
+    def rebuild(self, kernel_id: int, kernel_params=(), id_tol: float | None = None, storage: int = H2_STORE_AUTO,
+                timing: bool = False) -> "H2Matrix":
+        """h2_rebuild_ex: the same points, tree, lists and HiDR representor sets, another kernel."""
+        o = h2_options_default()
+        o.storage = int(storage)
+        o.timing = int(bool(timing))
+        o.stream = C.c_void_p(self.stream.cuda_stream)
+        if getattr(self, "_comm", None) is not None:
+            o.comm = C.c_void_p(self._comm.ptr)
+        kp = list(kernel_params)
+        kpa = (C.c_double * max(1, len(kp)))(*(kp or [0.0]))
+        tol = self.id_tol if id_tol is None else id_tol
+        h = lib().h2_rebuild_ex(C.c_void_p(self.h), kernel_id, kpa, tol, C.byref(o))
+        if not h:
+            _raise()
+        out = H2Matrix.__new__(H2Matrix)
+        out.h, out.n, out.d, out.stream, out._keep, out.id_tol = h, self.n, self.d, self.stream, self._keep, tol
+        if getattr(self, "_comm", None) is not None:
+            out._comm = self._comm
+        return out
 
     def matvec(self, x):
         import torch

@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "h2_internal.cuh"
@@ -72,6 +73,59 @@ static std::vector<T> d2h(const T* d, size_t count, cudaStream_t s) {
   return v;
 }
 
+// a1-a4 and a6-a7 of `base`, copied into the fresh handle h (device arrays duplicated on
+// h->stream; the base keeps its own): the geometry a rebuild for another kernel reuses
+static void clone_geometry(h2_handle* h, const h2_handle* b) {
+  cudaStream_t s = h->stream;
+  auto dup = [&](auto* src, size_t count) {
+    using T = std::remove_cv_t<std::remove_pointer_t<decltype(src)>>;
+    T* dst = halloc<T>(h, count);
+    if (count) H2_CUDA_TRY(cudaMemcpyAsync(dst, src, sizeof(T) * count, cudaMemcpyDeviceToDevice, s));
+    return dst;
+  };
+  const size_t n = b->n, nn = b->nnodes, d = b->d, r = b->r;
+  h->W = b->W;
+  std::memcpy(h->rlo, b->rlo, sizeof(h->rlo));
+  h->L = b->L;
+  h->X = dup(b->X, n * d);
+  h->perm = dup(b->perm, n);
+  h->key = dup(b->key, n);
+  h->nnodes = b->nnodes;
+  h->depth = b->depth;
+  h->nleaves = b->nleaves;
+  h->lvl_start = b->lvl_start;
+  h->level = dup(b->level, nn);
+  h->nbegin = dup(b->nbegin, nn);
+  h->nend = dup(b->nend, nn);
+  h->parent = dup(b->parent, nn);
+  h->first_child = dup(b->first_child, nn);
+  h->nchild = dup(b->nchild, nn);
+  h->is_leaf = dup(b->is_leaf, nn);
+  h->cell = dup(b->cell, nn * d);
+  h->n_il = b->n_il;
+  h->n_nf = b->n_nf;
+  h->il_off = dup(b->il_off, nn + 1);
+  h->nf_off = dup(b->nf_off, nn + 1);
+  h->il_idx = dup(b->il_idx, (size_t)b->n_il);
+  h->nf_idx = dup(b->nf_idx, (size_t)b->n_nf);
+  h->csp = b->csp;
+  h->r = b->r;
+  h->xs_cnt = dup(b->xs_cnt, nn);
+  h->xs = dup(b->xs, nn * r);
+  h->ys_cnt = dup(b->ys_cnt, nn);
+  h->ys = dup(b->ys, nn * r);
+  h->hidr_dist_evals = 0;  // nothing of HiDR ran for this handle
+  h->hidr_dist_done = 0;
+  h->nranks = b->nranks;
+  h->rank = b->rank;
+  h->cut = b->cut;
+  h->p_lo = b->p_lo;
+  h->p_hi = b->p_hi;
+  h->rng_lo = b->rng_lo;
+  h->rng_hi = b->rng_hi;
+  h->gpu_launches += 0;  // copies only
+}
+
 }  // namespace h2
 
 using namespace h2;
@@ -87,13 +141,16 @@ void h2_options_default(h2_options* o) {
   o->storage = H2_STORE_AUTO;
 }
 
-h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kernel_id, const double* kernel_params,
-                       double id_tol, int32_t leaf_size, double admissibility, const h2_options* opt) {
+// The build (h2_build_ex) and the rebuild from a base handle's geometry (h2_rebuild_ex: `base`
+// non-null -- a1-a7 are copied from it, only a8-a10 run for the new kernel).
+static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t kernel_id,
+                             const double* kernel_params, double id_tol, int32_t leaf_size, double admissibility,
+                             const h2_options* opt, const h2_handle* base) {
   clear_error();
   h2_options o;
   h2_options_default(&o);
   if (opt) o = *opt;
-  if (!points || n < 1 || n >= (1LL << 31) - 1 || d < 1 || d > kMaxD || leaf_size < 1 || !(admissibility > 0.0) ||
+  if ((!points && !base) || n < 1 || n >= (1LL << 31) - 1 || d < 1 || d > kMaxD || leaf_size < 1 || !(admissibility > 0.0) ||
       !(admissibility <= 0.7) || !(id_tol > 0.0) || !(id_tol < 1.0) || o.r_override < 0 || o.r_override > 4096 ||
       o.storage < 0 || o.storage > 2) {
     set_error(H2_ERR_INVALID_ARG, "invalid argument (n, d, leaf_size, admissibility, id_tol or options)");
@@ -148,7 +205,7 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
     };
     const double* pts = points;
     Scratch staged;
-    if (o.points_on_host) {
+    if (o.points_on_host && !base) {
       staged = Scratch(sizeof(double) * (size_t)n * d, h->stream);
       H2_CUDA_TRY(cudaMemcpyAsync(staged.p, points, sizeof(double) * (size_t)n * d, cudaMemcpyHostToDevice,
                                   h->stream));
@@ -158,26 +215,36 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
     NfJob nf;
     CalibJob cal;
     mark(0);
-    build_tree(h, pts);  // a1-a3
-    mark(1);
-    const bool calibrated = o.r_override <= 0;
-    if (calibrated) {  // a5 phase 0 overlaps a4 (calib.cu)
-      H2_CUDA_TRY(cudaEventRecord(fork_ev, h->stream));
-      H2_CUDA_TRY(cudaStreamWaitEvent(bs.calib, fork_ev, 0));
-      calibrate_begin(h, bs.calib, cal);
+    const bool calibrated = o.r_override <= 0 && !base;
+    if (base) {
+      clone_geometry(h, base);  // a1-a4, a6-a7 (and the shard plan) of the base handle
+      mark(1);
+    } else {
+      build_tree(h, pts);  // a1-a3
+      mark(1);
+      if (calibrated) {  // a5 phase 0 overlaps a4 (calib.cu)
+        H2_CUDA_TRY(cudaEventRecord(fork_ev, h->stream));
+        H2_CUDA_TRY(cudaStreamWaitEvent(bs.calib, fork_ev, 0));
+        calibrate_begin(h, bs.calib, cal);
+      }
+      build_lists(h);                    // a4
+      if (h->nranks > 1) shard_plan(h);  // cut level, owned subtrees and block rows (shard.cu)
     }
-    build_lists(h);  // a4
-    if (h->nranks > 1) shard_plan(h);  // cut level, owned subtrees and block rows (shard.cu)
     mark(2);
     // a10 needs only the tree and the nearfield list: it starts now on the side stream and
     // overlaps a5-a9 (serial_fill: after a9 on the main stream instead)
     const bool serial = o.serial_fill || serial_fill_env();
     if (!serial) fill_nearfield_begin(h, bs.side, o.storage, o.mem_budget_bytes, nf);
-    h->r = calibrated ? calibrate_end(h, cal) : o.r_override;  // a5
-    mark(3);
-    hidr_up(h);  // a6
-    mark(4);
-    hidr_down(h);  // a7
+    if (!base) {
+      h->r = calibrated ? calibrate_end(h, cal) : o.r_override;  // a5
+      mark(3);
+      hidr_up(h);  // a6
+      mark(4);
+      hidr_down(h);  // a7
+    } else {
+      mark(3);
+      mark(4);
+    }
     mark(5);
     id_sweep(h);  // a8
     mark(6);
@@ -224,6 +291,29 @@ h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kerne
   cudaEventDestroy(join_ev);
   for (int i = 0; i < nev; i++) cudaEventDestroy(ev[i]);
   return h;
+}
+
+h2_handle* h2_build_ex(const double* points, int64_t n, int32_t d, int32_t kernel_id, const double* kernel_params,
+                       double id_tol, int32_t leaf_size, double admissibility, const h2_options* opt) {
+  return build_impl(points, n, d, kernel_id, kernel_params, id_tol, leaf_size, admissibility, opt, nullptr);
+}
+
+h2_handle* h2_rebuild_ex(const h2_handle* base, int32_t kernel_id, const double* kernel_params, double id_tol,
+                         const h2_options* opt) {
+  clear_error();
+  if (!base || !base->xs || !base->ys) {
+    set_error(H2_ERR_INVALID_ARG, "h2_rebuild_ex: null base handle");
+    return nullptr;
+  }
+  h2_options o;
+  h2_options_default(&o);
+  if (opt) o = *opt;
+  if (o.comm != base->comm) {
+    set_error(H2_ERR_INVALID_ARG, "h2_rebuild_ex: opt->comm must be the base handle's comm");
+    return nullptr;
+  }
+  o.r_override = 0;  // the base's r and representor sets are reused
+  return build_impl(nullptr, base->n, base->d, kernel_id, kernel_params, id_tol, base->q, base->tau, &o, base);
 }
 
 h2_handle* h2_build(const double* points, int64_t n, int32_t d, int32_t kernel_id, const double* kernel_params,

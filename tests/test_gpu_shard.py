@@ -147,3 +147,32 @@ def test_sharded_on_the_fly_and_single_leaf():
     y_ref = ref.matvec(x).cpu().numpy()
     for y in collective_matvec(hs, x):
         np.testing.assert_allclose(y, y_ref, rtol=1e-13, atol=1e-13 * np.abs(y_ref).max())
+
+
+def test_sharded_rebuild_equals_single_gpu_rebuild():
+    """HiDR once for all on a sharded handle: every rank rebuilds for another kernel (collective)."""
+    c = synth.CONFIGS[1]
+    pts = synth.points(1, 8192)
+    X = torch.from_numpy(pts).cuda()
+    ref = P.H2Matrix(X, 1, [], 1e-6, c["q"], storage=P.H2_STORE_ALL).rebuild(2, [0.5], 1e-6, P.H2_STORE_ALL)
+    hs = build_sharded(pts, 2, 1, [], 1e-6, c["q"])
+    out, errs = [None, None], []
+
+    def run(r):
+        try:
+            with torch.cuda.stream(hs[r].stream):
+                out[r] = hs[r].rebuild(2, [0.5], 1e-6, P.H2_STORE_ALL)
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    assert all(np.array_equal(g.export("SK_IDX"), ref.export("SK_IDX")) for g in out)
+    x = torch.from_numpy(synth.matvec_vector(1, 8192)).cuda()
+    y_ref = ref.matvec(x).cpu().numpy()
+    for y in collective_matvec(out, x):
+        assert np.linalg.norm(y - y_ref) <= 1e-12 * np.linalg.norm(y_ref)
