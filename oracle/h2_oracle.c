@@ -85,7 +85,7 @@ static int64_t ipow_sat(int64_t m, int d) {
 /* kernel functions  (Table 1; Matern-3/2 from BASELINE.json configs[3])    */
 /* ------------------------------------------------------------------------------------------ */
 
-enum { ORC_COULOMB = 1, ORC_GAUSSIAN = 2, ORC_MATERN32 = 3 };
+enum { ORC_COULOMB = 1, ORC_GAUSSIAN = 2, ORC_MATERN32 = 3, ORC_LAPLACE = 4, ORC_BUMP = 5 };
 
 static double sqdist(const double* x, const double* y, int d) {
   double s = 0.0;
@@ -106,6 +106,13 @@ static double kernel_of_s(int kid, double p, double s) {
     case ORC_MATERN32: { /* (1 + sqrt3 r / l) exp(-sqrt3 r / l) */
       double a = sqrt(3.0) * sqrt(s) / p;
       return (1.0 + a) * exp(-a);
+    }
+    case ORC_LAPLACE: /* exp(-|x-y| / l): the Laplace kernel e^{-|x-y|} of P:91 at l = 1 */
+      return exp(-(sqrt(s) / p));
+    case ORC_BUMP: { /* kappa_4 of Table 1: exp(-1/(1 - 0.1|x-y|^2)); 0 where
+                        0.1|x-y|^2 >= 1 (reading K5: its limit at the edge of its domain) */
+      double t = 0.1 * s;
+      return t < 1.0 ? exp(-(1.0 / (1.0 - t))) : 0.0;
     }
     default:
       return NAN;

@@ -351,11 +351,23 @@ static void launch_fill(const h2_handle* h, cudaStream_t s, int mode, int64_t nw
                         const int64_t* uoff, const int2* pairs, const int64_t* voff, const double* Xs, double* out) {
   if (nwork < 1) return;
   const double cs = kernel_cscale(h->kid, h->kp);
-  if (h->kid == H2_KERNEL_COULOMB)
-    launch_fill_kid<H2_KERNEL_COULOMB>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
-  else if (h->kid == H2_KERNEL_GAUSSIAN)
-    launch_fill_kid<H2_KERNEL_GAUSSIAN>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
-  else launch_fill_kid<H2_KERNEL_MATERN32>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
+  switch (h->kid) {
+    case H2_KERNEL_COULOMB:
+      launch_fill_kid<H2_KERNEL_COULOMB>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
+      break;
+    case H2_KERNEL_GAUSSIAN:
+      launch_fill_kid<H2_KERNEL_GAUSSIAN>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
+      break;
+    case H2_KERNEL_MATERN32:
+      launch_fill_kid<H2_KERNEL_MATERN32>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
+      break;
+    case H2_KERNEL_LAPLACE:
+      launch_fill_kid<H2_KERNEL_LAPLACE>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
+      break;
+    default:
+      launch_fill_kid<H2_KERNEL_BUMP>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
+      break;
+  }
 }
 
 // builds the symmetric-once pair list of one class (CSR order) with entry offsets, on stream s

@@ -23,6 +23,8 @@ SEED_BASE = 20601885
 KERNEL_COULOMB = 1
 KERNEL_GAUSSIAN = 2
 KERNEL_MATERN32 = 3
+KERNEL_LAPLACE = 4
+KERNEL_BUMP = 5
 
 # (n, d, kernel_id, kernel_params, leaf_size, id_tol, tau, name)
 CONFIGS = {

@@ -146,6 +146,37 @@ def test_stored_blocks_sampled_against_kernel(cfg, n):
     g.close()
 
 
+@pytest.mark.parametrize("kid,kp,cfg,n", [(4, [0.3], 1, 8192), (4, [0.05], 4, 40000), (5, [], 1, 8192),
+                                         (5, [], 3, 20000)])
+def test_parity_laplace_and_bump(kid, kp, cfg, n):
+    """The Laplace kernel e^{-r/l} and Table 1's kappa_4 bump through the whole path:
+    bit-exact structure and r, matvec error within 2x of the oracle's, stored entries = kernel."""
+    c = synth.CONFIGS[cfg]
+    pts = synth.points(cfg, n)
+    o, r = oracle_build(pts, kid, kp, 1e-6, c["q"], c["tau"])
+    g = gpu_build(pts, kid, kp, 1e-6, c["q"], c["tau"])
+    assert g.info()["r"] == r
+    assert_structure_equal(g, o)
+    assert skeleton_agreement(g, o) >= 0.9
+    eg, eo, agree = matvec_check(g, o, pts, kid, kp, 1e-6, cfg)
+    print(f"kernel {kid}{kp} cfg{cfg}: r={r} err_gpu={eg:.3e} err_oracle={eo:.3e} gpu-vs-oracle={agree:.3e}")
+    assert eg <= 2.0 * eo + 1e-15
+    assert agree <= 10 * 1e-6
+    # stored nearfield entries against the oracle's kernel
+    nf_off, nf_idx = g.export("NF_OFF"), g.export("NF_IDX")
+    nfp = [(i, j) for i in range(len(nf_off) - 1) for j in nf_idx[nf_off[i]:nf_off[i + 1]] if j >= i]
+    nodes = g.export("NODES").reshape(-1, 7)
+    rng = np.random.default_rng(1)
+    pairs = rng.integers(len(nfp), size=500)
+    entries = [rng.integers((nodes[nfp[p][0], 2] - nodes[nfp[p][0], 1]) * (nodes[nfp[p][1], 2] - nodes[nfp[p][1], 1]))
+               for p in pairs]
+    val, rp, colp = P.h2_sample_blocks(g.h, np.ones(len(pairs)), pairs, entries)
+    Xt = g.export("TREE_X").reshape(-1, c["d"])
+    ref = np.array([oracle.kernel(kid, kp[0] if kp else 0.0, Xt[a], Xt[b]) for a, b in zip(rp, colp)])
+    np.testing.assert_allclose(val, ref, rtol=1e-13, atol=1e-300)
+    g.close()
+
+
 def test_on_the_fly_equals_stored():
     c = synth.CONFIGS[1]
     pts = synth.points(1, 8192)

@@ -166,6 +166,34 @@ def test_kernel_closed_forms(orc):
     assert orc.kernel(M, l, [0.0], [l / np.sqrt(3)]) == pytest.approx(2 * np.exp(-1), rel=1e-14)
 
 
+def test_kernel_closed_forms_laplace_and_bump(orc):
+    La, Bu = synth.KERNEL_LAPLACE, synth.KERNEL_BUMP
+    # Laplace e^{-|x-y|}: a 3-4-5 triangle gives |x-y| = 5 exactly
+    assert orc.kernel(La, 1.0, [0.0, 0.0], [3.0, 4.0]) == pytest.approx(np.exp(-5), rel=1e-15)
+    assert orc.kernel(La, 2.0, [1.0], [1.0]) == 1.0
+    assert orc.kernel(La, 0.5, [0.0], [1.0]) == pytest.approx(np.exp(-2), rel=1e-15)
+    # Table 1 kappa_4 = exp(-1/(1 - 0.1 r^2)): e^{-1} at r = 0, e^{-2} at r^2 = 5,
+    # vanishing at and beyond r^2 = 10 (reading K5), and continuous there from below
+    assert orc.kernel(Bu, 0.0, [0.5, 0.5], [0.5, 0.5]) == pytest.approx(np.exp(-1), rel=1e-15)
+    assert orc.kernel(Bu, 0.0, [0.0, 0.0], [1.0, 2.0]) == pytest.approx(np.exp(-2), rel=1e-15)
+    assert orc.kernel(Bu, 0.0, [0.0], [np.sqrt(10.0) * 1.0000001]) == 0.0
+    assert orc.kernel(Bu, 0.0, [0.0], [4.0]) == 0.0
+    assert 0.0 < orc.kernel(Bu, 0.0, [0.0], [np.sqrt(10.0) * 0.999]) < 1e-80
+
+
+@pytest.mark.parametrize("kid,param,tol", [(synth.KERNEL_LAPLACE, 0.3, 1e-6), (synth.KERNEL_BUMP, 0.0, 1e-6)])
+def test_new_kernels_full_pipeline_small(orc, kid, param, tol):
+    """The pipeline on the two added kernels: the error falls with id_tol (BASELINE north_star pin)."""
+    pts = synth.points(1, 3000)
+    x = synth.matvec_vector(1, 3000)
+    errs = []
+    for t in (1e-2, 1e-4, tol):
+        h, r = _build(orc, pts, kid, param, 32, t)
+        errs.append(_rel_err(orc, h, pts, kid, param, x))
+    assert errs[0] > errs[1] > errs[2], errs
+    assert errs[2] < 1e-4, errs
+
+
 def test_dense_rows_harmonic_numbers(orc):
     n = 500
     pts = np.arange(n, dtype=float).reshape(n, 1)
