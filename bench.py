@@ -261,6 +261,7 @@ def run_ours(args):
     # e2e: same build through the C ABI from pinned HOST memory (H2D inside the call) plus the
     # device->host read of the step's result (the skeleton ranks k_i of every node)
     pinned = torch.from_numpy(pts_np).pin_memory()
+    P.h2_free(one(host=True, src=pinned.data_ptr()))  # untimed: the host path's first staging allocation
     e2e_times = []
     h2d = n * c["d"] * 8
     d2h = 0
