@@ -5,7 +5,9 @@
 // (B3) and cross-level pairs on adaptive trees (B4).  The frontier of candidate pairs
 // starts at (root, root); each step classifies every pair: admissible -> IL, both leaves -> NF,
 // otherwise expand the non-leaf side (both sides when neither is a leaf).
-#include "h2_internal.cuh"
+#include <climits>
+
+#include "vol.cuh"
 
 namespace h2 {
 
@@ -71,21 +73,59 @@ __global__ void emit_kernel(const int2* __restrict__ fr, int64_t nf, const int64
   }
 }
 
-// (i << 32 | j) -> (i << bits | j): the sort then needs 2 bits key bits instead of 32 + bits
-__global__ void repack_kernel(unsigned long long* keys, int64_t m, int bits) {
+// ---- CSR from the unordered (i << 32 | j) pairs: counting sort by row, then each row sorted --
+__global__ void row_hist_kernel(const unsigned long long* __restrict__ keys, int64_t m, unsigned long long* cnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[keys[e] >> 32], 1ULL);
+}
+
+__global__ void row_scatter_kernel(const unsigned long long* __restrict__ keys, int64_t m,
+                                   const int64_t* __restrict__ off, int* fill, int* idx) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long k = keys[e];
-    keys[e] = ((k >> 32) << bits) | (k & 0xffffffffULL);
+    const int i = (int)(k >> 32);
+    idx[off[i] + atomicAdd(&fill[i], 1)] = (int)(k & 0xffffffffULL);
   }
 }
 
-__global__ void row_count_kernel(const unsigned long long* __restrict__ keys, int64_t m, int bits,
-                                 unsigned long long* cnt, int* idx) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-    unsigned long long k = keys[e];
-    atomicAdd(&cnt[k >> bits], 1ULL);
-    idx[e] = (int)(k & ((1ULL << bits) - 1ULL));
+// one CTA per row: a row of <= 64 entries is sorted by warp 0 with shuffles (two per lane, no
+// barrier), a longer one by a shared-memory bitonic network of its own power-of-two size
+constexpr int kRowSortThreads = 256;
+__global__ void __launch_bounds__(kRowSortThreads) row_sort_kernel(const int64_t* __restrict__ off, int* idx) {
+  extern __shared__ int rs[];
+  const int64_t b = off[blockIdx.x];
+  const int len = (int)(off[blockIdx.x + 1] - b);
+  if (len <= 1) return;
+  int* row = idx + b;
+  if (len <= 64) {
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    int a = lane < len ? row[lane] : INT_MAX, c = lane + 32 < len ? row[lane + 32] : INT_MAX;
+    for (int k = 2; k <= 64; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        if (j == 32) {
+          const bool up = (lane & k) == 0;
+          const int lo = min(a, c), hi = max(a, c);
+          a = up ? lo : hi;
+          c = up ? hi : lo;
+        } else {
+          const int pa = __shfl_xor_sync(0xffffffffu, a, j), pc = __shfl_xor_sync(0xffffffffu, c, j);
+          const bool lower = (lane & j) == 0;
+          const bool upa = (lane & k) == 0, upc = ((lane + 32) & k) == 0;
+          a = (lower == upa) ? min(a, pa) : max(a, pa);
+          c = (lower == upc) ? min(c, pc) : max(c, pc);
+        }
+      }
+    if (lane < len) row[lane] = a;
+    if (lane + 32 < len) row[lane + 32] = c;
+    return;
   }
+  int P = 128;
+  while (P < len) P <<= 1;
+  for (int t = threadIdx.x; t < P; t += kRowSortThreads) rs[t] = t < len ? row[t] : INT_MAX;
+  __syncthreads();
+  cta_bitonic<kRowSortThreads>(rs, P);
+  for (int t = threadIdx.x; t < len; t += kRowSortThreads) row[t] = rs[t];
 }
 
 __global__ void max_row_kernel(const int64_t* __restrict__ off, int nnodes, int* out) {
@@ -116,23 +156,28 @@ struct Grow {
 
 static void to_csr(h2_handle* h, unsigned long long* keys, int64_t m, int64_t*& off, int*& idx) {
   cudaStream_t s = h->stream;
-  int bits = 1;
-  while ((1LL << bits) <= h->nnodes) bits++;
-  Scratch sorted(sizeof(unsigned long long) * (m > 0 ? m : 1), s);
-  if (m > 0) {
-    repack_kernel<<<grid_for(m, 256), 256, 0, s>>>(keys, m, bits);
-    sort_keys_u64(keys, sorted.as<unsigned long long>(), m, 2 * bits, s);
-  }
-  off = halloc<int64_t>(h, h->nnodes + 1);
+  const int nn = h->nnodes;
+  off = halloc<int64_t>(h, nn + 1);
   idx = halloc<int>(h, m);
-  Scratch cnt(sizeof(int64_t) * (h->nnodes + 1), s);
-  H2_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, sizeof(int64_t) * (h->nnodes + 1), s));
-  if (m > 0)
-    row_count_kernel<<<grid_for(m, 256), 256, 0, s>>>(sorted.as<unsigned long long>(), m, bits,
-                                                      cnt.as<unsigned long long>(), idx);
-  scan_excl_i64(cnt.as<int64_t>(), off, h->nnodes + 1, s);
+  Scratch cnt(sizeof(int64_t) * (nn + 1), s), fill(sizeof(int) * nn, s), mx(sizeof(int), s);
+  H2_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, sizeof(int64_t) * (nn + 1), s));
+  H2_CUDA_TRY(cudaMemsetAsync(fill.p, 0, sizeof(int) * nn, s));
+  H2_CUDA_TRY(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
+  if (m > 0) row_hist_kernel<<<grid_for(m, 256), 256, 0, s>>>(keys, m, cnt.as<unsigned long long>());
+  scan_excl_i64(cnt.as<int64_t>(), off, nn + 1, s);
+  if (m == 0) return;
+  row_scatter_kernel<<<grid_for(m, 256), 256, 0, s>>>(keys, m, off, fill.as<int>(), idx);
+  max_row_kernel<<<(nn + 255) / 256, 256, 0, s>>>(off, nn, mx.as<int>());
   H2_CHECK_LAUNCH();
-  h->gpu_launches += 2;
+  const int maxlen = read1(mx.as<int>(), s);
+  int P = 128;
+  while (P < maxlen) P <<= 1;
+  const size_t smem = sizeof(int) * (size_t)P;
+  if (smem > 200 * 1024) throw Error{H2_ERR_INTERNAL, "list row longer than the row sort supports"};
+  H2_CUDA_TRY(cudaFuncSetAttribute(row_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  row_sort_kernel<<<nn, kRowSortThreads, smem, s>>>(off, idx);
+  H2_CHECK_LAUNCH();
+  h->gpu_launches += 4;
 }
 
 void build_lists(h2_handle* h) {
