@@ -28,48 +28,149 @@ __device__ __forceinline__ bool admissible(const int* __restrict__ cell, int nno
   return lhs <= __dmul_rn(tau2, S);
 }
 
-// classify: kind 0 far, 1 near, 2 expand; counts for the three output streams
-__global__ void classify_kernel(const int2* __restrict__ fr, int64_t nf, const int* __restrict__ cell, int nnodes,
-                                int d, double tau2, const int* __restrict__ level, const int* __restrict__ is_leaf,
-                                const int* __restrict__ nchild, int64_t* cfar, int64_t* cnear, int64_t* cexp) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nf; e += (int64_t)gridDim.x * blockDim.x) {
-    int2 pr = fr[e];
-    int i = pr.x, j = pr.y;
-    int64_t a = 0, b = 0, c = 0;
-    if (admissible(cell, nnodes, d, i, level[i], j, level[j], tau2)) {
-      a = 1;
-    } else {
-      int li = is_leaf[i], lj = is_leaf[j];
-      if (li && lj) b = 1;
-      else c = (int64_t)(li ? 1 : nchild[i]) * (lj ? 1 : nchild[j]);
-    }
-    cfar[e] = a;
-    cnear[e] = b;
-    cexp[e] = c;
+// ---- one traversal step in two launches ----------------------------------------------------
+// Tiles of kTravTile frontier pairs (each thread kTravIPT consecutive pairs).  trav_count:
+// classify every pair (far -> IL, both leaves -> NF, else expand), per-tile counts of the three
+// outputs, and their totals (atomics) for the host to size the outputs.  trav_emit: the same
+// classification again, each tile's offsets = the sums of the tiles before it plus an in-tile
+// exclusive scan (thread-blocked, so the output order is the frontier order), and the writes.
+constexpr int kTravThreads = 256, kTravIPT = 8, kTravTile = kTravThreads * kTravIPT;
+
+__device__ __forceinline__ void trav_classify(const int2 pr, const int* __restrict__ cell, int nnodes, int d,
+                                              double tau2, const int* __restrict__ level,
+                                              const int* __restrict__ is_leaf, const int* __restrict__ nchild,
+                                              long long& a, long long& b, long long& c) {
+  const int i = pr.x, j = pr.y;
+  a = b = c = 0;
+  if (admissible(cell, nnodes, d, i, level[i], j, level[j], tau2)) {
+    a = 1;
+  } else {
+    const int li = is_leaf[i], lj = is_leaf[j];
+    if (li && lj) b = 1;
+    else c = (long long)(li ? 1 : nchild[i]) * (lj ? 1 : nchild[j]);
   }
 }
 
-__global__ void emit_kernel(const int2* __restrict__ fr, int64_t nf, const int64_t* __restrict__ ofar,
-                            const int64_t* __restrict__ onear, const int64_t* __restrict__ oexp,
-                            const int* __restrict__ is_leaf, const int* __restrict__ first_child,
-                            const int* __restrict__ nchild, unsigned long long* il, int64_t il_base,
-                            unsigned long long* nl, int64_t nl_base, int2* next) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nf; e += (int64_t)gridDim.x * blockDim.x) {
-    int2 pr = fr[e];
-    int i = pr.x, j = pr.y;
-    unsigned long long key = ((unsigned long long)i << 32) | (unsigned)j;
-    if (ofar[e + 1] != ofar[e]) {
-      il[il_base + ofar[e]] = key;
-    } else if (onear[e + 1] != onear[e]) {
-      nl[nl_base + onear[e]] = key;
-    } else {
-      int li = is_leaf[i], lj = is_leaf[j];
-      int ci = li ? 1 : nchild[i], cj = lj ? 1 : nchild[j];
-      int fi = li ? i : first_child[i], fj = lj ? j : first_child[j];
-      int64_t o = oexp[e];
-      for (int a = 0; a < ci; a++)
-        for (int b = 0; b < cj; b++) next[o + (int64_t)a * cj + b] = make_int2(fi + a, fj + b);
+__global__ void __launch_bounds__(kTravThreads) trav_count_kernel(const int2* __restrict__ fr, int64_t nf,
+                                                                  const int* __restrict__ cell, int nnodes, int d,
+                                                                  double tau2, const int* __restrict__ level,
+                                                                  const int* __restrict__ is_leaf,
+                                                                  const int* __restrict__ nchild,
+                                                                  long long* __restrict__ tile_sum,
+                                                                  unsigned long long* totals) {
+  __shared__ long long red[3][kTravThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t base = blockIdx.x * (int64_t)kTravTile + (int64_t)tid * kTravIPT;
+  long long sa = 0, sb = 0, sc = 0;
+  for (int k = 0; k < kTravIPT; k++) {
+    if (base + k >= nf) break;
+    long long a, b, c;
+    trav_classify(fr[base + k], cell, nnodes, d, tau2, level, is_leaf, nchild, a, b, c);
+    sa += a;
+    sb += b;
+    sc += c;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    sc += __shfl_xor_sync(0xffffffffu, sc, o);
+  }
+  if (lane == 0) {
+    red[0][w] = sa;
+    red[1][w] = sb;
+    red[2][w] = sc;
+  }
+  __syncthreads();
+  if (tid < 3) {
+    long long t = 0;
+    for (int q = 0; q < kTravThreads / 32; q++) t += red[tid][q];
+    tile_sum[(int64_t)tid * gridDim.x + blockIdx.x] = t;
+    atomicAdd(totals + tid, (unsigned long long)t);
+  }
+}
+
+__global__ void __launch_bounds__(kTravThreads) trav_emit_kernel(
+    const int2* __restrict__ fr, int64_t nf, const int* __restrict__ cell, int nnodes, int d, double tau2,
+    const int* __restrict__ level, const int* __restrict__ is_leaf, const int* __restrict__ nchild,
+    const int* __restrict__ first_child, const long long* __restrict__ tile_sum, unsigned long long* il,
+    int64_t il_base, unsigned long long* nl, int64_t nl_base, int2* next) {
+  __shared__ long long red[3][kTravThreads / 32];
+  __shared__ long long wsum[3][kTravThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int ntiles = gridDim.x;
+  // offsets of this tile: the sums of the tiles before it (three channels)
+  long long pa = 0, pb = 0, pc = 0;
+  for (int q = tid; q < (int)blockIdx.x; q += kTravThreads) {
+    pa += tile_sum[q];
+    pb += tile_sum[ntiles + q];
+    pc += tile_sum[2 * ntiles + q];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    pa += __shfl_xor_sync(0xffffffffu, pa, o);
+    pb += __shfl_xor_sync(0xffffffffu, pb, o);
+    pc += __shfl_xor_sync(0xffffffffu, pc, o);
+  }
+  if (lane == 0) {
+    red[0][w] = pa;
+    red[1][w] = pb;
+    red[2][w] = pc;
+  }
+  // this thread's pairs: classification and thread totals
+  const int64_t base = blockIdx.x * (int64_t)kTravTile + (int64_t)tid * kTravIPT;
+  long long ca[kTravIPT], cb[kTravIPT], cc[kTravIPT];
+  long long ta = 0, tb = 0, tc = 0;
+#pragma unroll
+  for (int k = 0; k < kTravIPT; k++) {
+    ca[k] = cb[k] = cc[k] = 0;
+    if (base + k < nf) trav_classify(fr[base + k], cell, nnodes, d, tau2, level, is_leaf, nchild, ca[k], cb[k], cc[k]);
+    ta += ca[k];
+    tb += cb[k];
+    tc += cc[k];
+  }
+  // in-tile exclusive scan of the thread totals (warp scan + warp sums)
+  long long ia = ta, ib = tb, ic = tc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long ua = __shfl_up_sync(0xffffffffu, ia, o), ub = __shfl_up_sync(0xffffffffu, ib, o),
+                    uc = __shfl_up_sync(0xffffffffu, ic, o);
+    if (lane >= o) {
+      ia += ua;
+      ib += ub;
+      ic += uc;
     }
+  }
+  if (lane == 31) {
+    wsum[0][w] = ia;
+    wsum[1][w] = ib;
+    wsum[2][w] = ic;
+  }
+  __syncthreads();
+  long long oa = ia - ta, ob = ib - tb, oc = ic - tc;
+#pragma unroll
+  for (int q = 0; q < kTravThreads / 32; q++) {
+    oa += red[0][q] + (q < w ? wsum[0][q] : 0);
+    ob += red[1][q] + (q < w ? wsum[1][q] : 0);
+    oc += red[2][q] + (q < w ? wsum[2][q] : 0);
+  }
+#pragma unroll
+  for (int k = 0; k < kTravIPT; k++) {
+    if (base + k >= nf) break;
+    const int2 pr = fr[base + k];
+    const int i = pr.x, j = pr.y;
+    if (ca[k]) {
+      il[il_base + oa] = ((unsigned long long)i << 32) | (unsigned)j;
+    } else if (cb[k]) {
+      nl[nl_base + ob] = ((unsigned long long)i << 32) | (unsigned)j;
+    } else {
+      const int li = is_leaf[i], lj = is_leaf[j];
+      const int ci = li ? 1 : nchild[i], cj = lj ? 1 : nchild[j];
+      const int fi = li ? i : first_child[i], fj = lj ? j : first_child[j];
+      for (int a = 0; a < ci; a++)
+        for (int b = 0; b < cj; b++) next[oc + (int64_t)a * cj + b] = make_int2(fi + a, fj + b);
+    }
+    oa += ca[k];
+    ob += cb[k];
+    oc += cc[k];
   }
 }
 
@@ -174,7 +275,8 @@ static void to_csr(h2_handle* h, unsigned long long* keys, int64_t m, int64_t*& 
   while (P < maxlen) P <<= 1;
   const size_t smem = sizeof(int) * (size_t)P;
   if (smem > 200 * 1024) throw Error{H2_ERR_INTERNAL, "list row longer than the row sort supports"};
-  H2_CUDA_TRY(cudaFuncSetAttribute(row_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // one constant value: concurrent builds on other host threads set the same attribute
+  H2_CUDA_TRY(cudaFuncSetAttribute(row_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   row_sort_kernel<<<nn, kRowSortThreads, smem, s>>>(off, idx);
   H2_CHECK_LAUNCH();
   h->gpu_launches += 4;
@@ -189,32 +291,31 @@ void build_lists(h2_handle* h) {
   int2 root = make_int2(0, 0);
   H2_CUDA_TRY(cudaMemcpyAsync(fa.p, &root, sizeof(int2), cudaMemcpyHostToDevice, s));
   int64_t nf = 1, nil = 0, nnl = 0;
+  unsigned long long* tot_h = nullptr;  // page-locked totals (per host thread, reused)
+  {
+    thread_local unsigned long long* pinned = nullptr;
+    if (!pinned) H2_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&pinned), 4 * sizeof(unsigned long long)));
+    tot_h = pinned;
+  }
   while (nf > 0) {
-    Scratch c3(sizeof(int64_t) * 3 * (nf + 1), s), o3(sizeof(int64_t) * 3 * (nf + 1), s);
-    int64_t *cfar = c3.as<int64_t>(), *cnear = cfar + nf + 1, *cexp = cnear + nf + 1;
-    int64_t *ofar = o3.as<int64_t>(), *onear = ofar + nf + 1, *oexp = onear + nf + 1;
-    classify_kernel<<<grid_for(nf, 256), 256, 0, s>>>(fa.p, nf, h->cell, h->nnodes, h->d, tau2, h->level,
-                                                      h->is_leaf, h->nchild, cfar, cnear, cexp);
-    H2_CUDA_TRY(cudaMemsetAsync(cfar + nf, 0, sizeof(int64_t), s));
-    H2_CUDA_TRY(cudaMemsetAsync(cnear + nf, 0, sizeof(int64_t), s));
-    H2_CUDA_TRY(cudaMemsetAsync(cexp + nf, 0, sizeof(int64_t), s));
-    scan_excl_i64(cfar, ofar, nf + 1, s);
-    scan_excl_i64(cnear, onear, nf + 1, s);
-    scan_excl_i64(cexp, oexp, nf + 1, s);
+    const int64_t ntiles = (nf + kTravTile - 1) / kTravTile;
+    Scratch ts(sizeof(long long) * 3 * ntiles + sizeof(unsigned long long) * 4, s);
+    unsigned long long* tot_d = reinterpret_cast<unsigned long long*>(ts.as<long long>() + 3 * ntiles);
+    H2_CUDA_TRY(cudaMemsetAsync(tot_d, 0, 3 * sizeof(unsigned long long), s));
+    trav_count_kernel<<<(unsigned)ntiles, kTravThreads, 0, s>>>(fa.p, nf, h->cell, h->nnodes, h->d, tau2, h->level,
+                                                                 h->is_leaf, h->nchild, ts.as<long long>(), tot_d);
     H2_CHECK_LAUNCH();
-    h->gpu_launches += 1;
-    int64_t tot[3];
-    H2_CUDA_TRY(cudaMemcpyAsync(&tot[0], ofar + nf, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    H2_CUDA_TRY(cudaMemcpyAsync(&tot[1], onear + nf, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    H2_CUDA_TRY(cudaMemcpyAsync(&tot[2], oexp + nf, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    H2_CUDA_TRY(cudaMemcpyAsync(tot_h, tot_d, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaStreamSynchronize(s));
+    const int64_t tot[3] = {(int64_t)tot_h[0], (int64_t)tot_h[1], (int64_t)tot_h[2]};
     il.ensure(nil + tot[0], nil);
     nl.ensure(nnl + tot[1], nnl);
     fb.ensure(tot[2] > 0 ? tot[2] : 1, 0);
-    emit_kernel<<<grid_for(nf, 256), 256, 0, s>>>(fa.p, nf, ofar, onear, oexp, h->is_leaf, h->first_child, h->nchild,
-                                                  il.p, nil, nl.p, nnl, fb.p);
+    trav_emit_kernel<<<(unsigned)ntiles, kTravThreads, 0, s>>>(fa.p, nf, h->cell, h->nnodes, h->d, tau2, h->level,
+                                                                h->is_leaf, h->nchild, h->first_child,
+                                                                ts.as<long long>(), il.p, nil, nl.p, nnl, fb.p);
     H2_CHECK_LAUNCH();
-    h->gpu_launches += 1;
+    h->gpu_launches += 2;
     nil += tot[0];
     nnl += tot[1];
     nf = tot[2];

@@ -469,7 +469,8 @@ static void launch_far_near(const h2_handle* h, double p2, const double* zh, dou
       switch (cw) {
 #define H2_NFMVB_CASE(C)                                                                                         \
   case C:                                                                                                        \
-    H2_CUDA_TRY(cudaFuncSetAttribute(nf_matvec_bulk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+    H2_CUDA_TRY(cudaFuncSetAttribute(nf_matvec_bulk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                     200 * 1024));                                                               \
     nf_matvec_bulk_kernel<C><<<gb, kMvBulkThreads, smem, s>>>(h->nf_nunits, h->nf_umap, h->nf_uoff, h->np_pairs,  \
                                                               h->np_off, h->nbegin, h->nend, h->np_val, xt, yt); \
     break;
