@@ -210,7 +210,7 @@ def run_ours(args):
 
     def opts(host=False, serial=False):
         o = P.h2_options_default()
-        o.storage = P.H2_STORE_ALL
+        o.storage = {"all": P.H2_STORE_ALL, "fly": P.H2_STORE_ON_THE_FLY, "auto": P.H2_STORE_AUTO}[args.storage]
         o.timing = 1
         o.stream = stream.cuda_stream
         o.points_on_host = 1 if host else 0
@@ -282,14 +282,15 @@ def run_ours(args):
 
     # H^2 matvec on one stored build: y = K~ x, every pass on the GPU; the
     # stored blocks are read once (the nearfield pass dominates: 8 B per stored entry)
-    h = one()
+    stored = args.storage == "all"
+    h = one() if stored else None
     xv = torch.randn(n, dtype=torch.float64, device="cuda")
     yv = torch.empty_like(xv)
     torch.cuda.synchronize()
-    for _ in range(2):
+    for _ in range(2 if stored else 0):
         P.h2_matvec(h, xv.data_ptr(), yv.data_ptr())
     mv_ms = []
-    for _ in range(5):
+    for _ in range(5 if stored else 0):
         with torch.cuda.stream(stream):
             flush.fill_(4)
         m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -298,14 +299,15 @@ def run_ours(args):
         m1.record(stream)
         m1.synchronize()
         mv_ms.append(m0.elapsed_time(m1))
-    mv_info = P.h2_info(h)
-    P.h2_free(h)
-    mv_t = float(np.median(mv_ms))
-    mv_bytes = 8 * (mv_info["nearfield_entries"] + mv_info["coupling_entries"])
+    if stored:
+        mv_info = P.h2_info(h)
+        P.h2_free(h)
+        mv_t = float(np.median(mv_ms))
+        mv_bytes = 8 * (mv_info["nearfield_entries"] + mv_info["coupling_entries"])
 
     # the same build with the nearfield fill run alone (serial_fill): the kernel's own roofline
     iso_ms = []
-    for _ in range(2):
+    for _ in range(2 if stored else 0):
         with torch.cuda.stream(stream):
             flush.fill_(3)
         h = one(serial=True)
@@ -316,8 +318,8 @@ def run_ours(args):
     peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
     hbm = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
     nf_bytes = 8 * info["nearfield_entries"]
-    nf_ms = float(np.mean(fill_ms))
-    achieved = nf_bytes / (nf_ms * 1e-3) / 1e9
+    nf_ms = float(np.mean(fill_ms)) if stored else 0.0
+    achieved = nf_bytes / (nf_ms * 1e-3) / 1e9 if stored else 0.0
     traffic = None
     if os.path.exists(TRAFFIC_FILE):
         try:
@@ -335,7 +337,7 @@ def run_ours(args):
                 "note": "live: the kernel runs concurrently with a5-a9 (side stream), sharing the SMs",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650 GB/s",
                 "fp64_peak_tflops_at_sm_clock": round(fp64_peak, 2)}
-    iso = float(np.mean(iso_ms))
+    iso = float(np.mean(iso_ms)) if stored else 1.0
     roofline_isolated = {"bound": "hbm", "achieved": round(nf_bytes / (iso * 1e-3) / 1e9, 1), "peak": hbm,
                          "unit": "GB/s", "frac": round(nf_bytes / (iso * 1e-3) / 1e9 / hbm, 4),
                          "kernel_ms": round(iso, 3), "traffic": traffic,
@@ -355,12 +357,16 @@ def run_ours(args):
                            "l2": "flushed (512 MiB write) before every timed step",
                            "wall_s_timed_region": round(t_wall, 3)},
                 "stages_ms": mean_stages, "clocks": clocks, "e2e": e2e, "gpu_launches": launches,
-                "roofline": roofline, "roofline_isolated": roofline_isolated,
+                "roofline": roofline if stored else None,
+                "roofline_isolated": roofline_isolated if stored else None,
                 "matvec": {"ms": round(mv_t, 3), "stored_bytes_read": mv_bytes,
                            "achieved_gbs": round(mv_bytes / (mv_t * 1e-3) / 1e9, 1),
                            "frac_of_hbm": round(mv_bytes / (mv_t * 1e-3) / 1e9 / hbm, 4),
                            "note": "h2_matvec (all four passes, permutations, host sync) on one stored build; "
-                                   "median of 5, L2 flushed; not part of the construction metric"}}
+                                   "median of 5, L2 flushed; not part of the construction metric"} if stored
+                else None}
+        if not stored:
+            line["config"]["storage"] = "blocks not stored (skeleton build a1-a8; a9/a10 evaluated in the matvec)"
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample)
         print(json.dumps(line), flush=True)
@@ -380,6 +386,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--n", type=int, default=None, help="override n (not a bench line)")
+    ap.add_argument("--storage", choices=["all", "fly", "auto"], default="all",
+                    help="block storage (fly: skeleton build a1-a8, blocks evaluated in the matvec; for "
+                         "configs whose blocks exceed one GPU)")
     ap.add_argument("--cpu-sample", type=int, default=1 << 22,
                     help="points of the oracle's cpu_baseline run (default: the whole workload)")
     ap.add_argument("--ref-sample", type=int, default=1 << 22,
