@@ -10,7 +10,9 @@
 
 namespace h2 {
 
-constexpr int kIdThreads = 256;
+// global-memory path: one CTA per node; blocks of >= kIdBigBlock bytes get 1024 threads (they are
+// L2-latency-bound: more columns in flight), smaller ones 256 (more CTAs per SM)
+constexpr int kIdBigBlock = 256 << 10;
 constexpr int kIdSmemThreads = 128;
 constexpr int kIdSmemMax = 100 * 1024;  // dynamic shared memory budget of the shared-memory path
 
@@ -68,13 +70,17 @@ __global__ void id_sizes_kernel(int base, int count, int d, const int* __restric
   if (nx > 0 && fits) atomicMax(smax + id_class(id_smem_bytes(ny, nx, d)), (int)id_smem_bytes(ny, nx, d));
 }
 
+template <int kIdThreads>
 __global__ void __launch_bounds__(kIdThreads) id_kernel(
     int base, int kid, double p2, double tol, const double* __restrict__ X, int64_t n, int d, int r,
     const int* __restrict__ is_leaf, const int* __restrict__ nbegin, const int* __restrict__ first_child,
     const int* __restrict__ nchild, const int* __restrict__ ys_cnt, const int* __restrict__ ys,
     const int* __restrict__ xbar_n, const int64_t* __restrict__ woff, double* work, const int64_t* __restrict__ uoff,
-    double* U, int* kout, int* sk, unsigned long long* evals) {
+    double* U, int* kout, int* sk, unsigned long long* evals, int64_t min_block, int64_t max_block) {
   __shared__ CpqrSmem<kIdThreads> csm;
+  // the Householder vector in shared memory for the big-block variant (ny <= r <= 4096, the budget
+  // cap); the 256-thread variant keeps it in its global workspace (more CTAs per SM)
+  __shared__ double sv[kIdThreads >= 1024 ? 4096 : 1];
   const int t = blockIdx.x;
   const int i = base + t;
   const int nx = xbar_n[i];
@@ -85,6 +91,8 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
     return;
   }
   if (id_smem_bytes(ny, nx, d) <= kIdSmemMax) return;  // handled by id_kernel_smem
+  const int64_t blk = 8LL * nx * ny;
+  if (blk < min_block || blk >= max_block) return;  // the other thread-count variant
   double* M = work + woff[t];
   double* nrm2 = M + (int64_t)ny * nx;
   double* v = nrm2 + nx;
@@ -111,7 +119,7 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
     M[e] = kernel_pts_d(kid, p2, X, n, d, xb[b], yv[a]);
   }
   __syncthreads();
-  const int k = cta_cpqr<kIdThreads>(M, ny, nx, tol, piv, nrm2, v, csm);
+  const int k = cta_cpqr<kIdThreads>(M, ny, nx, tol, piv, nrm2, kIdThreads >= 1024 ? sv : v, csm);
   // outputs: k, skeleton (pivot order), U (nx x k column-major)
   double* Ui = U + uoff[t];
   for (int a = tid; a < k; a += kIdThreads) sk[(int64_t)i * r + a] = xb[piv[a]];
@@ -270,12 +278,28 @@ void id_sweep(h2_handle* h) {
     uoff_scatter_kernel<<<(count + 255) / 256, 256, 0, s>>>(base, count, uo, uused, h->u_off);
     Scratch work(sizeof(double) * (tot[0] > 0 ? tot[0] : 1), s);
     if (tot[0] > 0) {  // some node's block exceeds the shared-memory path: global-memory CPQR
-      id_kernel<<<count, kIdThreads, 0, s>>>(base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf,
+      // the two thread-count variants run concurrently on auxiliary streams (disjoint nodes)
+      cudaStream_t sa = h->aux[0] ? h->aux[0] : s, sb = h->aux[1] ? h->aux[1] : s;
+      cudaEvent_t gev[3];
+      for (auto& e : gev) H2_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      H2_CUDA_TRY(cudaEventRecord(gev[0], s));
+      H2_CUDA_TRY(cudaStreamWaitEvent(sa, gev[0], 0));
+      H2_CUDA_TRY(cudaStreamWaitEvent(sb, gev[0], 0));
+      id_kernel<256><<<count, 256, 0, sa>>>(base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf,
+                                           h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
+                                           work.as<double>(), h->u_off + base, U, h->k, h->sk,
+                                           ev.as<unsigned long long>(), 0, kIdBigBlock);
+      id_kernel<1024><<<count, 1024, 0, sb>>>(base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf,
                                              h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
                                              work.as<double>(), h->u_off + base, U, h->k, h->sk,
-                                             ev.as<unsigned long long>());
+                                             ev.as<unsigned long long>(), kIdBigBlock, INT64_MAX);
       H2_CHECK_LAUNCH();
-      h->gpu_launches += 1;
+      H2_CUDA_TRY(cudaEventRecord(gev[1], sa));
+      H2_CUDA_TRY(cudaEventRecord(gev[2], sb));
+      H2_CUDA_TRY(cudaStreamWaitEvent(s, gev[1], 0));
+      H2_CUDA_TRY(cudaStreamWaitEvent(s, gev[2], 0));
+      for (auto& e : gev) cudaEventDestroy(e);
+      h->gpu_launches += 2;
     }
     // Small levels: one launch for all classes (sized by the largest): the class launches of a
     // level run one after the other, and with few nodes each costs a node's full CPQR latency.
