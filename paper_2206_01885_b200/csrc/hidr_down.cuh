@@ -7,6 +7,9 @@ namespace h2 {
 
 // ------------------------------------------------------------------------------------------
 // Selection boxes: the tight bounding box of every node's X_i^* (after its up level) and Y_i^*
+// (the same pass packs the selection's coordinates next to its slots, xyz[(i r + a) D + c], so the
+// top-down search reads a segment's points with contiguous loads instead of an index load and D
+// scattered coordinate loads per point)
 // (after its down level): box[i * kBox + c] = lo_c, box[i * kBox + kMaxD + c] = hi_c; an empty
 // selection gets lo = +inf, hi = -inf.  One warp per node.  min / max are exact, so the union of
 // the segment boxes is the bounding box of T_i bit for bit.
@@ -15,7 +18,8 @@ constexpr int kBox = 2 * kMaxD;
 
 template <int D>
 __global__ void sel_box_kernel(int base, int count, const int* __restrict__ cnt, const int* __restrict__ slots, int r,
-                               const double* __restrict__ X, int64_t n, double* __restrict__ box) {
+                               const double* __restrict__ X, int64_t n, double* __restrict__ box,
+                               double* __restrict__ xyz) {
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (w >= count) return;
   const int i = base + w;
@@ -31,6 +35,7 @@ __global__ void sel_box_kernel(int base, int count, const int* __restrict__ cnt,
 #pragma unroll
     for (int k = 0; k < D; k++) {
       const double v = X[k * n + idx];
+      xyz[((int64_t)i * r + a) * D + k] = v;
       lo[k] = fmin(lo[k], v);
       hi[k] = fmax(hi[k], v);
     }
@@ -111,7 +116,8 @@ __global__ void __launch_bounds__(kDownThreads) hidr_down_kernel(
     const double* __restrict__ X, int64_t n, int base, int r, const int* __restrict__ parent,
     const int64_t* __restrict__ il_off, const int* __restrict__ il_idx, const int* __restrict__ xs_cnt,
     const int* __restrict__ xs, const double* __restrict__ xbox, const double* __restrict__ ybox, int* ys_cnt,
-    int* ys, unsigned long long* evals_alg, unsigned long long* evals_done) {
+    int* ys, const double* __restrict__ xs_xyz, const double* __restrict__ ys_xyz, unsigned long long* evals_alg,
+    unsigned long long* evals_done) {
   extern __shared__ double gbox[];  // group g: lo at gbox[g*2D + c], hi at gbox[g*2D + D + c]
   __shared__ int sel[kVolSelCap];
   __shared__ BlockScanSmem<kDownThreads> scan;
@@ -132,6 +138,7 @@ __global__ void __launch_bounds__(kDownThreads) hidr_down_kernel(
   auto seg_cnt = [&](int s, int nd) { return s == 0 ? ys_cnt[nd] : xs_cnt[nd]; };
   auto seg_box = [&](int s, int nd) { return (s == 0 ? ybox : xbox) + (int64_t)nd * kBox; };
   auto seg_slots = [&](int s, int nd) { return s == 0 ? yp : xs + (int64_t)nd * r; };
+  auto seg_xyz = [&](int s, int nd) { return (s == 0 ? ys_xyz : xs_xyz) + (int64_t)nd * r * D; };
 
   // 1. group boxes, bbox(T_i), |T_i|
   double tlo[D], thi[D];
@@ -308,13 +315,14 @@ __global__ void __launch_bounds__(kDownThreads) hidr_down_kernel(
         const int ndt = __shfl_sync(0xffffffffu, nd, t);
         if (lbt > dl) continue;  // uniform
         const int* sl = seg_slots(gg * 32 + t, ndt);
+        const double* px = seg_xyz(gg * 32 + t, ndt);
         for (int a = lane; a < ct; a += 32) {
           const int idx = sl[a];
-          double df = __dsub_rn(X[idx], q[0]);
+          double df = __dsub_rn(px[a * D], q[0]);
           double sd = __dmul_rn(df, df);
 #pragma unroll
           for (int c = 1; c < D; c++) {
-            df = __dsub_rn(X[c * n + idx], q[c]);
+            df = __dsub_rn(px[a * D + c], q[c]);
             sd = __dadd_rn(sd, __dmul_rn(df, df));
           }
           if (sd < best || (sd == best && idx < bi)) {
