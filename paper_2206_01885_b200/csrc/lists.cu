@@ -92,29 +92,16 @@ __global__ void __launch_bounds__(kTravThreads) trav_count_kernel(const int2* __
 __global__ void __launch_bounds__(kTravThreads) trav_emit_kernel(
     const int2* __restrict__ fr, int64_t nf, const int* __restrict__ cell, int nnodes, int d, double tau2,
     const int* __restrict__ level, const int* __restrict__ is_leaf, const int* __restrict__ nchild,
-    const int* __restrict__ first_child, const long long* __restrict__ tile_sum, unsigned long long* il,
+    const int* __restrict__ first_child, const long long* __restrict__ tile_pre, unsigned long long* il,
     int64_t il_base, unsigned long long* nl, int64_t nl_base, int2* next) {
-  __shared__ long long red[3][kTravThreads / 32];
   __shared__ long long wsum[3][kTravThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int ntiles = gridDim.x;
-  // offsets of this tile: the sums of the tiles before it (three channels)
-  long long pa = 0, pb = 0, pc = 0;
-  for (int q = tid; q < (int)blockIdx.x; q += kTravThreads) {
-    pa += tile_sum[q];
-    pb += tile_sum[ntiles + q];
-    pc += tile_sum[2 * ntiles + q];
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    pa += __shfl_xor_sync(0xffffffffu, pa, o);
-    pb += __shfl_xor_sync(0xffffffffu, pb, o);
-    pc += __shfl_xor_sync(0xffffffffu, pc, o);
-  }
-  if (lane == 0) {
-    red[0][w] = pa;
-    red[1][w] = pb;
-    red[2][w] = pc;
-  }
+  // offsets of this tile: tile_pre is the exclusive prefix sum of the channel-major tile sums, so
+  // channel c's offset is tile_pre[c ntiles + tile] - tile_pre[c ntiles]
+  const long long pa = tile_pre[blockIdx.x];
+  const long long pb = tile_pre[ntiles + blockIdx.x] - tile_pre[ntiles];
+  const long long pc = tile_pre[2 * ntiles + blockIdx.x] - tile_pre[2 * ntiles];
   // this thread's pairs: classification and thread totals
   const int64_t base = blockIdx.x * (int64_t)kTravTile + (int64_t)tid * kTravIPT;
   long long ca[kTravIPT], cb[kTravIPT], cc[kTravIPT];
@@ -145,12 +132,12 @@ __global__ void __launch_bounds__(kTravThreads) trav_emit_kernel(
     wsum[2][w] = ic;
   }
   __syncthreads();
-  long long oa = ia - ta, ob = ib - tb, oc = ic - tc;
+  long long oa = pa + ia - ta, ob = pb + ib - tb, oc = pc + ic - tc;
 #pragma unroll
   for (int q = 0; q < kTravThreads / 32; q++) {
-    oa += red[0][q] + (q < w ? wsum[0][q] : 0);
-    ob += red[1][q] + (q < w ? wsum[1][q] : 0);
-    oc += red[2][q] + (q < w ? wsum[2][q] : 0);
+    oa += q < w ? wsum[0][q] : 0;
+    ob += q < w ? wsum[1][q] : 0;
+    oc += q < w ? wsum[2][q] : 0;
   }
 #pragma unroll
   for (int k = 0; k < kTravIPT; k++) {
@@ -299,12 +286,13 @@ void build_lists(h2_handle* h) {
   }
   while (nf > 0) {
     const int64_t ntiles = (nf + kTravTile - 1) / kTravTile;
-    Scratch ts(sizeof(long long) * 3 * ntiles + sizeof(unsigned long long) * 4, s);
+    Scratch ts(sizeof(long long) * 3 * ntiles + sizeof(unsigned long long) * 4, s), tp(sizeof(long long) * 3 * ntiles, s);
     unsigned long long* tot_d = reinterpret_cast<unsigned long long*>(ts.as<long long>() + 3 * ntiles);
     H2_CUDA_TRY(cudaMemsetAsync(tot_d, 0, 3 * sizeof(unsigned long long), s));
     trav_count_kernel<<<(unsigned)ntiles, kTravThreads, 0, s>>>(fa.p, nf, h->cell, h->nnodes, h->d, tau2, h->level,
                                                                  h->is_leaf, h->nchild, ts.as<long long>(), tot_d);
     H2_CHECK_LAUNCH();
+    scan_excl_i64(reinterpret_cast<const int64_t*>(ts.as<long long>()), tp.as<int64_t>(), 3 * ntiles, s);
     H2_CUDA_TRY(cudaMemcpyAsync(tot_h, tot_d, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaStreamSynchronize(s));
     const int64_t tot[3] = {(int64_t)tot_h[0], (int64_t)tot_h[1], (int64_t)tot_h[2]};
@@ -313,7 +301,7 @@ void build_lists(h2_handle* h) {
     fb.ensure(tot[2] > 0 ? tot[2] : 1, 0);
     trav_emit_kernel<<<(unsigned)ntiles, kTravThreads, 0, s>>>(fa.p, nf, h->cell, h->nnodes, h->d, tau2, h->level,
                                                                 h->is_leaf, h->nchild, h->first_child,
-                                                                ts.as<long long>(), il.p, nil, nl.p, nnl, fb.p);
+                                                                tp.as<long long>(), il.p, nil, nl.p, nnl, fb.p);
     H2_CHECK_LAUNCH();
     h->gpu_launches += 2;
     nil += tot[0];
