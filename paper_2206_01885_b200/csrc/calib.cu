@@ -23,6 +23,7 @@ struct CalWork {  // per-trial global workspace
   double Ks[N * N];
   double nrm2[N], v[N];
   int piv[N], sel[N];
+  int ns, k;  // |Z2^*| and the ID rank, passed between the trial's launches
 };
 
 // k-th SplitMix64 output of the stream seeded with `seed` (counter form of the sequential
@@ -41,13 +42,15 @@ struct PtAcc {
   __device__ __forceinline__ int index(int pos) const { return pos; }
 };
 
+// A trial runs as three launches over the batch: prep (Z1, Z2, Vol(Z2, m^d), the block M; 256
+// threads), the CPQR ID of M (1024 threads: the block lives in global memory / L2 and the steps are
+// latency-bound, so more columns in flight), and the error of the interpolation (256 threads).
 template <int D>
-__global__ void __launch_bounds__(kCalThreads) calib_kernel(int kid, double p2, double eps, double tau,
-                                                            const double* __restrict__ wl, const int* __restrict__ lv,
-                                                            const int* __restrict__ mv, CalWork* work, double* err,
-                                                            int* pass) {
+__global__ void __launch_bounds__(kCalThreads) calib_prep_kernel(int kid, double p2, double tau,
+                                                                 const double* __restrict__ wl,
+                                                                 const int* __restrict__ lv, const int* __restrict__ mv,
+                                                                 CalWork* work) {
   __shared__ VolSmem<D, kCalThreads> vsm;
-  __shared__ CpqrSmem<kCalThreads> csm;
   __shared__ int s_ns;
   const int tid = threadIdx.x;
   CalWork& W = work[blockIdx.x];
@@ -74,6 +77,7 @@ __global__ void __launch_bounds__(kCalThreads) calib_kernel(int kid, double p2, 
   }
   __syncthreads();
   const int ns = s_ns;
+  if (tid == 0) W.ns = ns;
   // M = K(Z1, Z2*)^T : ns x N column-major (columns = Z1 candidates)
   for (int e = tid; e < ns * N; e += kCalThreads) {
     int a = e % ns, b = e / ns;
@@ -84,8 +88,27 @@ __global__ void __launch_bounds__(kCalThreads) calib_kernel(int kid, double p2, 
     }
     W.M[e] = kernel_s(kid, p2, s);
   }
-  __syncthreads();
-  const int k = cta_cpqr<kCalThreads>(W.M, ns, N, 1e-3 * eps, W.piv, W.nrm2, W.v, csm);
+}
+
+constexpr int kCalCpqrThreads = 1024;
+__global__ void __launch_bounds__(kCalCpqrThreads) calib_cpqr_kernel(double eps, CalWork* work) {
+  __shared__ CpqrSmem<kCalCpqrThreads> csm;
+  __shared__ double sv[N];
+  CalWork& W = work[blockIdx.x];
+  const int k = cta_cpqr<kCalCpqrThreads>(W.M, W.ns, N, 1e-3 * eps, W.piv, W.nrm2, sv, csm);
+  if (threadIdx.x == 0) W.k = k;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kCalThreads) calib_err_kernel(int kid, double p2, double eps,
+                                                                const int* __restrict__ mv, CalWork* work,
+                                                                double* err, int* pass) {
+  __shared__ CpqrSmem<kCalThreads> csm;
+  const int tid = threadIdx.x;
+  CalWork& W = work[blockIdx.x];
+  const int m = mv[blockIdx.x], ns = W.ns, k = W.k;
+  long long G = 1;
+  for (int c = 0; c < D; c++) G *= m;
   // Ks[t][e] = K(Z1[piv[t]], Z2[e]) for the k skeleton rows
   for (int x = tid; x < k * N; x += kCalThreads) {
     int t = x / N, e = x % N;
@@ -174,17 +197,20 @@ static void launch_trials(h2_handle* h, cudaStream_t s, int slot, const std::vec
   for (int b0 = 0; b0 < T; b0 += batch) {
     int nb = T - b0 < batch ? T - b0 : batch;
     switch (d) {
-#define H2_CAL_CASE(DD)                                                                                  \
-  case DD:                                                                                               \
-    calib_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, h->id_tol, h->tau, dw + b0, dl + b0, dm + b0, \
-                                                job.work.as<CalWork>(), derr + b0, dpass + b0);           \
+#define H2_CAL_CASE(DD)                                                                                   \
+  case DD:                                                                                                \
+    calib_prep_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, h->tau, dw + b0, dl + b0, dm + b0,         \
+                                                     job.work.as<CalWork>());                              \
+    calib_cpqr_kernel<<<nb, kCalCpqrThreads, 0, s>>>(h->id_tol, job.work.as<CalWork>());                  \
+    calib_err_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, h->id_tol, dm + b0, job.work.as<CalWork>(), \
+                                                    derr + b0, dpass + b0);                               \
     break;
       H2_CAL_CASE(1) H2_CAL_CASE(2) H2_CAL_CASE(3) H2_CAL_CASE(4)
       H2_CAL_CASE(5) H2_CAL_CASE(6) H2_CAL_CASE(7) H2_CAL_CASE(8)
 #undef H2_CAL_CASE
     }
     H2_CHECK_LAUNCH();
-    h->gpu_launches += 1;
+    h->gpu_launches += 3;
   }
   job.pass_h = reinterpret_cast<int*>(hin + in_bytes);
   H2_CUDA_TRY(cudaMemcpyAsync(job.pass_h, dpass, sizeof(int) * T, cudaMemcpyDeviceToHost, s));
