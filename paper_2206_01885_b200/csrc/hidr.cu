@@ -147,7 +147,7 @@ static bool hidr_down_level_pruned(h2_handle* h, int l, unsigned long long* ev, 
         H2_CUDA_TRY(cudaFuncSetAttribute(hidr_down_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                                        kDownSmemMax));                                                           \
     hidr_down_kernel<DD><<<count, kDownThreads, smem, s>>>(h->X, h->n, base, h->r, h->parent, h->il_off,           \
-                                                           h->il_idx, h->xs_cnt, h->xs, h->xbox, h->ybox,        \
+                                                           h->il_idx, h->xs, h->xbox, h->ybox,        \
                                                            h->ys_cnt, h->ys, h->xs_xyz, h->ys_xyz, ev, ev_done);                       \
   } break;
     H2_DOWN_CASE(1) H2_DOWN_CASE(2) H2_DOWN_CASE(3) H2_DOWN_CASE(4)

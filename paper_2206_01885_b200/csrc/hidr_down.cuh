@@ -7,14 +7,15 @@ namespace h2 {
 
 // ------------------------------------------------------------------------------------------
 // Selection boxes: the tight bounding box of every node's X_i^* (after its up level) and Y_i^*
-// (the same pass packs the selection's coordinates next to its slots, xyz[(i r + a) D + c], so the
-// top-down search reads a segment's points with contiguous loads instead of an index load and D
-// scattered coordinate loads per point)
-// (after its down level): box[i * kBox + c] = lo_c, box[i * kBox + kMaxD + c] = hi_c; an empty
-// selection gets lo = +inf, hi = -inf.  One warp per node.  min / max are exact, so the union of
-// the segment boxes is the bounding box of T_i bit for bit.
+// (after its down level): box[i * kBox + c] = lo_c, box[i * kBox + D + c] = hi_c and the selection
+// size at box[i * kBox + 2D] (one load gives the top-down search a segment's box and count); an
+// empty selection gets lo = +inf, hi = -inf.  The same pass packs the selection's coordinates per
+// slot, coordinate-major, xyz[(i D + c) r + a], so the top-down search reads a segment's points
+// with coalesced loads instead of an index load and D scattered loads per point.  One warp per
+// node.  min / max are exact, so the union of the segment boxes is the bounding box of T_i bit for
+// bit.
 // ------------------------------------------------------------------------------------------
-constexpr int kBox = 2 * kMaxD;
+constexpr int kBox = 2 * kMaxD + 2;
 
 template <int D>
 __global__ void sel_box_kernel(int base, int count, const int* __restrict__ cnt, const int* __restrict__ slots, int r,
@@ -35,7 +36,7 @@ __global__ void sel_box_kernel(int base, int count, const int* __restrict__ cnt,
 #pragma unroll
     for (int k = 0; k < D; k++) {
       const double v = X[k * n + idx];
-      xyz[((int64_t)i * r + a) * D + k] = v;
+      xyz[((int64_t)i * D + k) * r + a] = v;
       lo[k] = fmin(lo[k], v);
       hi[k] = fmax(hi[k], v);
     }
@@ -50,8 +51,9 @@ __global__ void sel_box_kernel(int base, int count, const int* __restrict__ cnt,
 #pragma unroll
     for (int k = 0; k < D; k++) {
       box[(int64_t)i * kBox + k] = lo[k];
-      box[(int64_t)i * kBox + kMaxD + k] = hi[k];
+      box[(int64_t)i * kBox + D + k] = hi[k];
     }
+    box[(int64_t)i * kBox + 2 * D] = (double)c;
   }
 }
 
@@ -112,9 +114,9 @@ __device__ __forceinline__ double warp_min_ub(double v) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(kDownThreads) hidr_down_kernel(
+__global__ void __launch_bounds__(kDownThreads, 4) hidr_down_kernel(
     const double* __restrict__ X, int64_t n, int base, int r, const int* __restrict__ parent,
-    const int64_t* __restrict__ il_off, const int* __restrict__ il_idx, const int* __restrict__ xs_cnt,
+    const int64_t* __restrict__ il_off, const int* __restrict__ il_idx,
     const int* __restrict__ xs, const double* __restrict__ xbox, const double* __restrict__ ybox, int* ys_cnt,
     int* ys, const double* __restrict__ xs_xyz, const double* __restrict__ ys_xyz, unsigned long long* evals_alg,
     unsigned long long* evals_done) {
@@ -135,10 +137,20 @@ __global__ void __launch_bounds__(kDownThreads) hidr_down_kernel(
   const int* yp = ys + (int64_t)p * r;
   // segment s: 0 = Y_p^*, s >= 1 = X_j^* of the (s-1)-th entry of IL(i)
   auto seg_node = [&](int s) { return s == 0 ? p : il_idx[e0 + s - 1]; };
-  auto seg_cnt = [&](int s, int nd) { return s == 0 ? ys_cnt[nd] : xs_cnt[nd]; };
   auto seg_box = [&](int s, int nd) { return (s == 0 ? ybox : xbox) + (int64_t)nd * kBox; };
   auto seg_slots = [&](int s, int nd) { return s == 0 ? yp : xs + (int64_t)nd * r; };
   auto seg_xyz = [&](int s, int nd) { return (s == 0 ? ys_xyz : xs_xyz) + (int64_t)nd * r * D; };
+  // a segment's box and count: lo, hi, |segment| (one contiguous run of 2D + 1 doubles)
+  auto load_seg = [&](int s, int& nd, double* blo, double* bhi) {
+    nd = seg_node(s);
+    const double* b = seg_box(s, nd);
+#pragma unroll
+    for (int c = 0; c < D; c++) {
+      blo[c] = b[c];
+      bhi[c] = b[D + c];
+    }
+    return (int)b[2 * D];
+  };
 
   // 1. group boxes, bbox(T_i), |T_i|
   double tlo[D], thi[D];
@@ -158,16 +170,8 @@ __global__ void __launch_bounds__(kDownThreads) hidr_down_kernel(
     }
     int cnt = 0;
     if (s < nseg) {
-      const int nd = seg_node(s);
-      cnt = seg_cnt(s, nd);
-      if (cnt > 0) {
-        const double* b = seg_box(s, nd);
-#pragma unroll
-        for (int c = 0; c < D; c++) {
-          blo[c] = b[c];
-          bhi[c] = b[kMaxD + c];
-        }
-      }
+      int nd;
+      cnt = load_seg(s, nd, blo, bhi);
     }
 #pragma unroll
     for (int c = 0; c < D; c++)
@@ -223,7 +227,7 @@ __global__ void __launch_bounds__(kDownThreads) hidr_down_kernel(
   if (tot <= r) {  // pass-through (reading C5): gather, sort, de-duplicate
     for (int s = tid; s < nseg; s += kDownThreads) {
       const int nd = seg_node(s);
-      const int cnt = seg_cnt(s, nd);
+      const int cnt = (int)seg_box(s, nd)[2 * D];
       if (cnt > 0) {
         const int pos = atomicAdd(&s_fill, cnt);
         const int* src = seg_slots(s, nd);
@@ -286,68 +290,91 @@ __global__ void __launch_bounds__(kDownThreads) hidr_down_kernel(
     }
     double best = INFINITY;
     int bi = INT_MAX;
+    auto eval_point = [&](const double* px, int idx) {  // px: coordinate c at px[c * r]
+      double df = __dsub_rn(px[0], q[0]);
+      double sd = __dmul_rn(df, df);
+#pragma unroll
+      for (int c = 1; c < D; c++) {
+        df = __dsub_rn(px[c * r], q[c]);
+        sd = __dadd_rn(sd, __dmul_rn(df, df));
+      }
+      if (sd < best || (sd == best && idx < bi)) {
+        best = sd;
+        bi = idx;
+      }
+    };
+    // A group: lane t holds segment gg*32+t.  The passing segment with the least lower bound is
+    // evaluated first (it tightens delta); the others that still pass are then evaluated together,
+    // their points flattened over the lanes so every load of an iteration is independent.
     auto process_group = [&](int gg) {
       const int s = gg * 32 + lane;
       int nd = 0, cnt = 0;
       double lbs = INFINITY, u = INFINITY;
       if (s < nseg) {
-        nd = seg_node(s);
-        cnt = seg_cnt(s, nd);
+        double blo[D], bhi[D];
+        cnt = load_seg(s, nd, blo, bhi);
         if (cnt > 0) {
-          const double* b = seg_box(s, nd);
-          double blo[D], bhi[D];
-#pragma unroll
-          for (int c = 0; c < D; c++) {
-            blo[c] = b[c];
-            bhi[c] = b[kMaxD + c];
-          }
           lbs = box_lb<D>(q, blo, bhi);
           u = box_ub<D>(q, blo, bhi);
         }
       }
       dl = fmin(dl, warp_min_ub(u));
-      unsigned mask = __ballot_sync(0xffffffffu, cnt > 0 && lbs <= dl);
-      while (mask) {
-        const int t = __ffs(mask) - 1;
-        mask &= mask - 1;
-        const double lbt = __shfl_sync(0xffffffffu, lbs, t);
+      bool pass = cnt > 0 && lbs <= dl;
+      const unsigned key = pass ? (unsigned)__double2hiint(lbs) : 0xFFFFFFFFu;
+      const unsigned kmin = __reduce_min_sync(0xffffffffu, key);
+      if (kmin == 0xFFFFFFFFu) return;
+      {
+        const int t = __ffs(__ballot_sync(0xffffffffu, key == kmin)) - 1;
         const int ct = __shfl_sync(0xffffffffu, cnt, t);
         const int ndt = __shfl_sync(0xffffffffu, nd, t);
-        if (lbt > dl) continue;  // uniform
         const int* sl = seg_slots(gg * 32 + t, ndt);
         const double* px = seg_xyz(gg * 32 + t, ndt);
-        for (int a = lane; a < ct; a += 32) {
-          const int idx = sl[a];
-          double df = __dsub_rn(px[a * D], q[0]);
-          double sd = __dmul_rn(df, df);
-#pragma unroll
-          for (int c = 1; c < D; c++) {
-            df = __dsub_rn(px[a * D + c], q[c]);
-            sd = __dadd_rn(sd, __dmul_rn(df, df));
-          }
-          if (sd < best || (sd == best && idx < bi)) {
-            best = sd;
-            bi = idx;
-          }
-        }
+        for (int a = lane; a < ct; a += 32) eval_point(px + a, sl[a]);
         done += (unsigned long long)ct;
         dl = fmin(dl, warp_min_ub(best));
+        if (lane == t) pass = false;
       }
+      pass = pass && lbs <= dl;
+      // flattened remainder: inclusive prefix of the passing counts over the lanes
+      int incl = pass ? cnt : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      const int excl = incl - (pass ? cnt : 0);
+      for (int a0 = 0; a0 < total; a0 += 32) {
+        const int a = a0 + lane;
+        int t = 0;  // the lane whose range holds a: the number of lanes with incl <= a
+#pragma unroll
+        for (int bb = 16; bb > 0; bb >>= 1)
+          if (__shfl_sync(0xffffffffu, incl, t + bb - 1) <= a) t += bb;
+        const int off = a - __shfl_sync(0xffffffffu, excl, t & 31);
+        const int ndt = __shfl_sync(0xffffffffu, nd, t & 31);
+        if (a < total) eval_point(seg_xyz(gg * 32 + t, ndt) + off, seg_slots(gg * 32 + t, ndt)[off]);
+      }
+      done += (unsigned long long)total;
+      dl = fmin(dl, warp_min_ub(best));
     };
     if (g0 >= 0) process_group(g0);
+    // the other groups, best-first (least lower bound) within each run of 32
     for (int gg0 = 0; gg0 < ng; gg0 += 32) {
       const int gg = gg0 + lane;
       bool cand = false;
+      double lbg = INFINITY;
       if (gg < ng && gg != g0) {
         const double* b = gbox + gg * 2 * D;
-        cand = box_lb<D>(q, b, b + D) <= dl;
+        lbg = box_lb<D>(q, b, b + D);
+        cand = lbg <= dl;
       }
-      unsigned mask = __ballot_sync(0xffffffffu, cand);
-      while (mask) {
-        const int t = __ffs(mask) - 1;
-        mask &= mask - 1;
-        const double* b = gbox + (gg0 + t) * 2 * D;
-        if (box_lb<D>(q, b, b + D) <= dl) process_group(gg0 + t);  // uniform
+      for (;;) {
+        const unsigned key = (cand && lbg <= dl) ? (unsigned)__double2hiint(lbg) : 0xFFFFFFFFu;
+        const unsigned kmin = __reduce_min_sync(0xffffffffu, key);
+        if (kmin == 0xFFFFFFFFu) break;
+        const int t = __ffs(__ballot_sync(0xffffffffu, key == kmin)) - 1;
+        if (lane == t) cand = false;
+        process_group(gg0 + t);
       }
     }
     for (int o = 16; o > 0; o >>= 1) {
