@@ -120,11 +120,11 @@ static void launch_vol(int d, unsigned grid, cudaStream_t s, const double* X, in
 }
 
 static void launch_sel_box(h2_handle* h, int base, int count, const int* cnt, const int* slots, double* box,
-                           double* xyz) {
+                           float* boxf, double* xyz) {
   const unsigned grid = (unsigned)((count * 32LL + 255) / 256);
   switch (h->d) {
 #define H2_BOX_CASE(DD) \
-  case DD: sel_box_kernel<DD><<<grid, 256, 0, h->stream>>>(base, count, cnt, slots, h->r, h->X, h->n, box, xyz); break;
+  case DD: sel_box_kernel<DD><<<grid, 256, 0, h->stream>>>(base, count, cnt, slots, h->r, h->X, h->n, box, boxf, xyz); break;
     H2_BOX_CASE(1) H2_BOX_CASE(2) H2_BOX_CASE(3) H2_BOX_CASE(4)
     H2_BOX_CASE(5) H2_BOX_CASE(6) H2_BOX_CASE(7) H2_BOX_CASE(8)
 #undef H2_BOX_CASE
@@ -138,7 +138,7 @@ static bool hidr_down_level_pruned(h2_handle* h, int l, unsigned long long* ev, 
   const LevelRange lr = level_range(h, l);
   const int base = lr.begin, count = lr.end - lr.begin;
   const int ngmax = (h->csp + 1 + 31) / 32;
-  const size_t smem = sizeof(double) * 2 * h->d * (size_t)ngmax;
+  const size_t smem = sizeof(float) * 2 * h->d * (size_t)ngmax;
   if (smem > (size_t)kDownSmemMax) return false;
   cudaStream_t s = h->stream;
   switch (h->d) {
@@ -147,7 +147,7 @@ static bool hidr_down_level_pruned(h2_handle* h, int l, unsigned long long* ev, 
         H2_CUDA_TRY(cudaFuncSetAttribute(hidr_down_kernel<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                                        kDownSmemMax));                                                           \
     hidr_down_kernel<DD><<<count, kDownThreads, smem, s>>>(h->X, h->n, base, h->r, h->parent, h->il_off,           \
-                                                           h->il_idx, h->xs, h->xbox, h->ybox,        \
+                                                           h->il_idx, h->xs, h->xbox, h->ybox, h->xboxf, h->yboxf,        \
                                                            h->ys_cnt, h->ys, h->xs_xyz, h->ys_xyz, ev, ev_done);                       \
   } break;
     H2_DOWN_CASE(1) H2_DOWN_CASE(2) H2_DOWN_CASE(3) H2_DOWN_CASE(4)
@@ -180,8 +180,8 @@ static void hidr_level(h2_handle* h, int mode, int l, unsigned long long* ev) {
              mode == 0 ? h->xs_cnt : h->ys_cnt, mode == 0 ? h->xs : h->ys, ev);
   H2_CHECK_LAUNCH();
   h->gpu_launches += 3;
-  if (mode == 0) launch_sel_box(h, base, count, h->xs_cnt, h->xs, h->xbox, h->xs_xyz);
-  else launch_sel_box(h, base, count, h->ys_cnt, h->ys, h->ybox, h->ys_xyz);
+  if (mode == 0) launch_sel_box(h, base, count, h->xs_cnt, h->xs, h->xbox, h->xboxf, h->xs_xyz);
+  else launch_sel_box(h, base, count, h->ys_cnt, h->ys, h->ybox, h->yboxf, h->ys_xyz);
 }
 
 void hidr_up(h2_handle* h) {
@@ -192,6 +192,8 @@ void hidr_up(h2_handle* h) {
   h->ys = halloc<int>(h, (size_t)h->nnodes * h->r);
   h->xbox = halloc<double>(h, (size_t)h->nnodes * kBox);
   h->ybox = halloc<double>(h, (size_t)h->nnodes * kBox);
+  h->xboxf = halloc<float>(h, (size_t)h->nnodes * kBoxF);
+  h->yboxf = halloc<float>(h, (size_t)h->nnodes * kBoxF);
   h->xs_xyz = halloc<double>(h, (size_t)h->nnodes * h->r * h->d);
   h->ys_xyz = halloc<double>(h, (size_t)h->nnodes * h->r * h->d);
   H2_CUDA_TRY(cudaMemsetAsync(h->ys_cnt, 0, sizeof(int) * h->nnodes, h->stream));
@@ -204,7 +206,7 @@ void hidr_up(h2_handle* h) {
       exchange_slots(h, h->xs_cnt, h->xs);
       for (int m = h->cut; m <= h->depth; m++) {
         const int b = h->lvl_start[m], c = h->lvl_start[m + 1] - b;
-        if (c > 0) launch_sel_box(h, b, c, h->xs_cnt, h->xs, h->xbox, h->xs_xyz);
+        if (c > 0) launch_sel_box(h, b, c, h->xs_cnt, h->xs, h->xbox, h->xboxf, h->xs_xyz);
       }
     }
   }
@@ -217,13 +219,13 @@ void hidr_down(h2_handle* h) {
   Scratch evd(sizeof(unsigned long long), h->stream);
   H2_CUDA_TRY(cudaMemsetAsync(evd.p, 0, sizeof(unsigned long long), h->stream));
   // the root's Y^* is empty (reading D1): its box is the empty box
-  launch_sel_box(h, 0, 1, h->ys_cnt, h->ys, h->ybox, h->ys_xyz);
+  launch_sel_box(h, 0, 1, h->ys_cnt, h->ys, h->ybox, h->yboxf, h->ys_xyz);
   for (int l = 1; l <= h->depth; l++) {
     const LevelRange lr = level_range(h, l);
     const int base = lr.begin, count = lr.end - lr.begin;
     if (count == 0) continue;
     if (h->hidr_prune && hidr_down_level_pruned(h, l, ev.as<unsigned long long>(), evd.as<unsigned long long>()))
-      launch_sel_box(h, base, count, h->ys_cnt, h->ys, h->ybox, h->ys_xyz);
+      launch_sel_box(h, base, count, h->ys_cnt, h->ys, h->ybox, h->yboxf, h->ys_xyz);
     else
       hidr_level(h, 1, l, ev.as<unsigned long long>());
   }

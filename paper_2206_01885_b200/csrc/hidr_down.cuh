@@ -13,14 +13,16 @@ namespace h2 {
 // slot, coordinate-major, xyz[(i D + c) r + a], so the top-down search reads a segment's points
 // with coalesced loads instead of an index load and D scattered loads per point.  One warp per
 // node.  min / max are exact, so the union of the segment boxes is the bounding box of T_i bit for
-// bit.
+// bit.  A float copy of each box, rounded outward (lo down, hi up, so it contains the double box),
+// with the count, serves the pruning tests (boxf[i * kBoxF + ...], same layout).
 // ------------------------------------------------------------------------------------------
 constexpr int kBox = 2 * kMaxD + 2;
+constexpr int kBoxF = 20;  // floats per node: 2 kMaxD + 1 rounded up to whole float4s
 
 template <int D>
 __global__ void sel_box_kernel(int base, int count, const int* __restrict__ cnt, const int* __restrict__ slots, int r,
                                const double* __restrict__ X, int64_t n, double* __restrict__ box,
-                               double* __restrict__ xyz) {
+                               float* __restrict__ boxf, double* __restrict__ xyz) {
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (w >= count) return;
   const int i = base + w;
@@ -54,49 +56,64 @@ __global__ void sel_box_kernel(int base, int count, const int* __restrict__ cnt,
       box[(int64_t)i * kBox + D + k] = hi[k];
     }
     box[(int64_t)i * kBox + 2 * D] = (double)c;
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+      boxf[(int64_t)i * kBoxF + k] = __double2float_rd(lo[k]);
+      boxf[(int64_t)i * kBoxF + D + k] = __double2float_ru(hi[k]);
+    }
+    boxf[(int64_t)i * kBoxF + 2 * D] = (float)c;
   }
 }
 
 // ------------------------------------------------------------------------------------------
 // Pruned exact top-down Vol.  Same result as the brute-force argmin of cta_vol, bit for bit.
 // T_i is the union of segments -- Y_p^* and X_j^* for j in IL(i) -- whose bounding boxes are
-// known.  For a grid node q and a box B, with the operations of the point distance
-// s(x) = sum_c fl(fl(x_c - q_c)^2) (each rounded separately, summed in c order):
-//   lb(q,B) = that expression on g_c = max(0, fl(lo_c - q_c), fl(q_c - hi_c))  <=  s(x),  x in B
-//   ub(q,B) = that expression on g_c = max(fl(hi_c - q_c), fl(q_c - lo_c))     >=  s(x),  x in B
-// because rounding to nearest is monotone and odd (fl(x - q) = -fl(q - x)).  A segment is
-// skipped only when lb > delta, delta an upper bound of the best s found so far (an evaluated s
-// or the ub of a non-empty box), so the minimiser and every tie with it are always evaluated;
-// ties go to the lowest index (reading C4) as in the brute-force kernel.
+// known.  The point distance s(x) = sum_c fl(fl(x_c - q_c)^2) (fp64, each operation rounded to
+// nearest, c order) is within a factor (1 +- 11 * 2^-53) of the exact sum of squares.  The box
+// tests run in fp32 with directed rounding on the outward-rounded float boxes and on q rounded
+// down (qd) and up (qu):
+//   lb(q,B) = rd(sum_c rd(g_c^2)) * (1 - 2^-20), g_c = max(0, rd(lo_c - qu_c), rd(qd_c - hi_c))
+//   ub(q,B) = ru(sum_c ru(u_c^2)) * (1 + 2^-20), u_c = max(ru(hi_c - qd_c), ru(qu_c - lo_c))
+// so lb <= s(x) <= ub for every x in B: each step only moves the bound away from the exact value,
+// and the slack covers the fp64 rounding of s.  A segment is skipped only when lb > delta, delta
+// an upper bound of the best s found so far (an evaluated s or the ub of a non-empty box), so the
+// minimiser and every tie with it are always evaluated; ties go to the lowest index (reading C4)
+// as in the brute-force kernel.  fp32 max / min / directed-rounding add and multiply are single
+// instructions (the fp64 max is a compare plus selects).
 // Segments are grouped 32 at a time (one per lane); the group boxes live in shared memory.
 // One CTA per node, one warp per grid node.
 // ------------------------------------------------------------------------------------------
 constexpr int kDownThreads = 256;
 constexpr int kDownWarps = kDownThreads / 32;
 constexpr int kDownSmemMax = 96 * 1024;
+constexpr float kLbSlack = 0x1.ffffep-1f;  // 1 - 2^-20
+constexpr float kUbSlack = 0x1.00001p+0f;  // 1 + 2^-20
 
 template <int D>
-__device__ __forceinline__ double box_lb(const double* q, const double* lo, const double* hi) {
-  double g = fmax(fmax(__dsub_rn(lo[0], q[0]), __dsub_rn(q[0], hi[0])), 0.0);
-  double s = __dmul_rn(g, g);
+__device__ __forceinline__ float box_lb(const float* qd, const float* qu, const float* lo, const float* hi) {
+  float s = 0.f;
 #pragma unroll
-  for (int c = 1; c < D; c++) {
-    g = fmax(fmax(__dsub_rn(lo[c], q[c]), __dsub_rn(q[c], hi[c])), 0.0);
-    s = __dadd_rn(s, __dmul_rn(g, g));
+  for (int c = 0; c < D; c++) {
+    const float g = fmaxf(fmaxf(__fsub_rd(lo[c], qu[c]), __fsub_rd(qd[c], hi[c])), 0.f);
+    s = __fadd_rd(s, __fmul_rd(g, g));
   }
-  return s;
+  return __fmul_rd(s, kLbSlack);
 }
 
 template <int D>
-__device__ __forceinline__ double box_ub(const double* q, const double* lo, const double* hi) {
-  double g = fmax(__dsub_rn(hi[0], q[0]), __dsub_rn(q[0], lo[0]));
-  double s = __dmul_rn(g, g);
+__device__ __forceinline__ float box_ub(const float* qd, const float* qu, const float* lo, const float* hi) {
+  float s = 0.f;
 #pragma unroll
-  for (int c = 1; c < D; c++) {
-    g = fmax(__dsub_rn(hi[c], q[c]), __dsub_rn(q[c], lo[c]));
-    s = __dadd_rn(s, __dmul_rn(g, g));
+  for (int c = 0; c < D; c++) {
+    const float u = fmaxf(__fsub_ru(hi[c], qd[c]), __fsub_ru(qu[c], lo[c]));
+    s = __fadd_ru(s, __fmul_ru(u, u));
   }
-  return s;
+  return __fmul_ru(s, kUbSlack);
+}
+
+// the warp minimum of v >= 0 (or +inf) in one instruction: non-negative floats order like their bits
+__device__ __forceinline__ float warp_min_f(float v) {
+  return __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(v)));
 }
 
 __device__ __forceinline__ double warp_min_d(double v) {
@@ -117,10 +134,11 @@ template <int D>
 __global__ void __launch_bounds__(kDownThreads, 4) hidr_down_kernel(
     const double* __restrict__ X, int64_t n, int base, int r, const int* __restrict__ parent,
     const int64_t* __restrict__ il_off, const int* __restrict__ il_idx,
-    const int* __restrict__ xs, const double* __restrict__ xbox, const double* __restrict__ ybox, int* ys_cnt,
+    const int* __restrict__ xs, const double* __restrict__ xbox, const double* __restrict__ ybox,
+    const float* __restrict__ xboxf, const float* __restrict__ yboxf, int* ys_cnt,
     int* ys, const double* __restrict__ xs_xyz, const double* __restrict__ ys_xyz, unsigned long long* evals_alg,
     unsigned long long* evals_done) {
-  extern __shared__ double gbox[];  // group g: lo at gbox[g*2D + c], hi at gbox[g*2D + D + c]
+  extern __shared__ float gbox[];  // group g (float, outward): lo at gbox[g*2D + c], hi at gbox[g*2D + D + c]
   __shared__ int sel[kVolSelCap];
   __shared__ BlockScanSmem<kDownThreads> scan;
   __shared__ double wlo[D][kDownWarps], whi[D][kDownWarps];
@@ -140,6 +158,27 @@ __global__ void __launch_bounds__(kDownThreads, 4) hidr_down_kernel(
   auto seg_box = [&](int s, int nd) { return (s == 0 ? ybox : xbox) + (int64_t)nd * kBox; };
   auto seg_slots = [&](int s, int nd) { return s == 0 ? yp : xs + (int64_t)nd * r; };
   auto seg_xyz = [&](int s, int nd) { return (s == 0 ? ys_xyz : xs_xyz) + (int64_t)nd * r * D; };
+  // a segment's float box and count in whole float4 loads
+  auto load_segf = [&](int s, int& nd, float* blo, float* bhi) {
+    nd = seg_node(s);
+    const float4* b = reinterpret_cast<const float4*>((s == 0 ? yboxf : xboxf) + (int64_t)nd * kBoxF);
+    constexpr int NV = (2 * D + 1 + 3) / 4;
+    float v[4 * NV];
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+      const float4 t = __ldg(b + k);
+      v[4 * k] = t.x;
+      v[4 * k + 1] = t.y;
+      v[4 * k + 2] = t.z;
+      v[4 * k + 3] = t.w;
+    }
+#pragma unroll
+    for (int c = 0; c < D; c++) {
+      blo[c] = v[c];
+      bhi[c] = v[D + c];
+    }
+    return (int)v[2 * D];
+  };
   // a segment's box and count: lo, hi, |segment| (one contiguous run of 2D + 1 doubles)
   auto load_seg = [&](int s, int& nd, double* blo, double* bhi) {
     nd = seg_node(s);
@@ -183,8 +222,8 @@ __global__ void __launch_bounds__(kDownThreads, 4) hidr_down_kernel(
     if (lane == 0) {
 #pragma unroll
       for (int c = 0; c < D; c++) {
-        gbox[g * 2 * D + c] = blo[c];
-        gbox[g * 2 * D + D + c] = bhi[c];
+        gbox[g * 2 * D + c] = __double2float_rd(blo[c]);
+        gbox[g * 2 * D + D + c] = __double2float_ru(bhi[c]);
       }
     }
 #pragma unroll
@@ -267,27 +306,32 @@ __global__ void __launch_bounds__(kDownThreads, 4) hidr_down_kernel(
         q[c] = __dadd_rn(s_lo[c], __dmul_rn((double)j + 0.5, s_h[c]));
       }
     }
+    float qd[D], qu[D];
+#pragma unroll
+    for (int c = 0; c < D; c++) {
+      qd[c] = __double2float_rd(q[c]);
+      qu[c] = __double2float_ru(q[c]);
+    }
     // pass A: delta = min over the non-empty groups of ub; g0 = a group attaining it
-    double dl = INFINITY;
+    float ua = INFINITY;
     int g0 = -1;
     for (int gg = lane; gg < ng; gg += 32) {
-      const double* b = gbox + gg * 2 * D;
+      const float* b = gbox + gg * 2 * D;
       if (b[0] <= b[D]) {
-        const double u = box_ub<D>(q, b, b + D);
-        if (u < dl) {
-          dl = u;
+        const float u = box_ub<D>(qd, qu, b, b + D);
+        if (u < ua) {
+          ua = u;
           g0 = gg;
         }
       }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double od = __shfl_xor_sync(0xffffffffu, dl, o);
-      const int og = __shfl_xor_sync(0xffffffffu, g0, o);
-      if (od < dl || (od == dl && og > g0)) {  // any attaining group will do; make it uniform
-        dl = od;
-        g0 = og;
-      }
+    {  // any attaining group will do; the highest-numbered lane's, uniform
+      const float um = warp_min_f(ua);
+      const unsigned who = __ballot_sync(0xffffffffu, ua == um && g0 >= 0);
+      g0 = who ? __shfl_sync(0xffffffffu, g0, 31 - __clz(who)) : -1;
+      ua = um;
     }
+    double dl = (double)ua;
     double best = INFINITY;
     int bi = INT_MAX;
     auto eval_point = [&](const double* px, int idx) {  // px: coordinate c at px[c * r]
@@ -309,18 +353,18 @@ __global__ void __launch_bounds__(kDownThreads, 4) hidr_down_kernel(
     auto process_group = [&](int gg) {
       const int s = gg * 32 + lane;
       int nd = 0, cnt = 0;
-      double lbs = INFINITY, u = INFINITY;
+      float lbs = INFINITY, u = INFINITY;
       if (s < nseg) {
-        double blo[D], bhi[D];
-        cnt = load_seg(s, nd, blo, bhi);
+        float blo[D], bhi[D];
+        cnt = load_segf(s, nd, blo, bhi);
         if (cnt > 0) {
-          lbs = box_lb<D>(q, blo, bhi);
-          u = box_ub<D>(q, blo, bhi);
+          lbs = box_lb<D>(qd, qu, blo, bhi);
+          u = box_ub<D>(qd, qu, blo, bhi);
         }
       }
-      dl = fmin(dl, warp_min_ub(u));
-      bool pass = cnt > 0 && lbs <= dl;
-      const unsigned key = pass ? (unsigned)__double2hiint(lbs) : 0xFFFFFFFFu;
+      dl = fmin(dl, (double)warp_min_f(u));
+      bool pass = cnt > 0 && (double)lbs <= dl;
+      const unsigned key = pass ? __float_as_uint(lbs) : 0xFFFFFFFFu;
       const unsigned kmin = __reduce_min_sync(0xffffffffu, key);
       if (kmin == 0xFFFFFFFFu) return;
       {
@@ -334,7 +378,7 @@ __global__ void __launch_bounds__(kDownThreads, 4) hidr_down_kernel(
         dl = fmin(dl, warp_min_ub(best));
         if (lane == t) pass = false;
       }
-      pass = pass && lbs <= dl;
+      pass = pass && (double)lbs <= dl;
       // flattened remainder: inclusive prefix of the passing counts over the lanes
       int incl = pass ? cnt : 0;
 #pragma unroll
@@ -362,14 +406,14 @@ __global__ void __launch_bounds__(kDownThreads, 4) hidr_down_kernel(
     for (int gg0 = 0; gg0 < ng; gg0 += 32) {
       const int gg = gg0 + lane;
       bool cand = false;
-      double lbg = INFINITY;
+      float lbg = INFINITY;
       if (gg < ng && gg != g0) {
-        const double* b = gbox + gg * 2 * D;
-        lbg = box_lb<D>(q, b, b + D);
-        cand = lbg <= dl;
+        const float* b = gbox + gg * 2 * D;
+        lbg = box_lb<D>(qd, qu, b, b + D);
+        cand = (double)lbg <= dl;
       }
       for (;;) {
-        const unsigned key = (cand && lbg <= dl) ? (unsigned)__double2hiint(lbg) : 0xFFFFFFFFu;
+        const unsigned key = (cand && (double)lbg <= dl) ? __float_as_uint(lbg) : 0xFFFFFFFFu;
         const unsigned kmin = __reduce_min_sync(0xffffffffu, key);
         if (kmin == 0xFFFFFFFFu) break;
         const int t = __ffs(__ballot_sync(0xffffffffu, key == kmin)) - 1;
