@@ -34,6 +34,29 @@ __host__ __device__ __forceinline__ int id_class(int64_t bytes) {
 __host__ __device__ __forceinline__ int64_t id_smem_bytes(int ny, int nx, int d) {
   return 8LL * ((int64_t)ny * nx + nx + ny) + 8LL * nx + 8LL * d * (nx + ny) + 512;
 }
+// the lean layout of the one-CTA-per-SM class: no staged coordinates (the block generation reads
+// them from global memory / L1)
+constexpr int kIdLeanThreads = 512;
+constexpr int kIdLeanMax = 226 * 1024;  // dynamic shared memory of that class (+ the small static part)
+constexpr int kIdLean = kIdClasses;      // its class number
+__host__ __device__ __forceinline__ int64_t id_smem_bytes_lean(int ny, int nx) {
+  return 8LL * ((int64_t)ny * nx + nx + ny) + 8LL * nx + 512;
+}
+// Layout of a shared-memory block: row-major with a thread per column (cta_cpqr_rm) unless the
+// block is tall enough that a warp per column (cta_cpqr, column-major) takes fewer serial steps:
+// per pivot step ~ceil(nx / NT) * ny smem accesses per thread against ceil(nx / (NT/32)) *
+// (ny / 32 + ~24 for the two warp reductions).
+__host__ __device__ __forceinline__ bool id_tall(int ny, int nx, int nt) {
+  const int64_t rm = (int64_t)((nx + nt - 1) / nt) * ny;
+  const int64_t cm = (int64_t)((nx + nt / 32 - 1) / (nt / 32)) * (ny / 32 + 24);
+  return cm < rm;
+}
+// the node's class: 0..kIdClasses-1 (staged, <= kIdSmemMax), kIdLean, or -1 (global-memory path)
+__host__ __device__ __forceinline__ int id_smem_class(int ny, int nx, int d) {
+  const int64_t b = id_smem_bytes(ny, nx, d);
+  if (b <= kIdSmemMax) return id_class(b);
+  return id_smem_bytes_lean(ny, nx) <= kIdLeanMax ? kIdLean : -1;
+}
 
 // per node of one level: |Xbar| (and child offsets), workspace and U sizes
 __global__ void id_sizes_kernel(int base, int count, int d, const int* __restrict__ is_leaf, const int* __restrict__ nbegin,
@@ -64,10 +87,11 @@ __global__ void id_sizes_kernel(int base, int count, int d, const int* __restric
   xbar_n[i] = nx;
   int mn = nx < ny ? nx : ny;
   // workspace: M (ny*nx doubles) + nrm2 (nx) + v (ny) + piv/xbar (2*nx ints, as doubles)
-  const bool fits = id_smem_bytes(ny, nx, d) <= kIdSmemMax;
-  wsz[t] = nx > 0 && !fits ? (int64_t)ny * nx + nx + ny + nx + 2 : 0;
+  const int cls = id_smem_class(ny, nx, d);
+  wsz[t] = nx > 0 && cls < 0 ? (int64_t)ny * nx + nx + ny + nx + 2 : 0;
   usz[t] = (int64_t)nx * mn;
-  if (nx > 0 && fits) atomicMax(smax + id_class(id_smem_bytes(ny, nx, d)), (int)id_smem_bytes(ny, nx, d));
+  if (nx > 0 && cls >= 0)
+    atomicMax(smax + cls, (int)(cls == kIdLean ? id_smem_bytes_lean(ny, nx) : id_smem_bytes(ny, nx, d)));
 }
 
 template <int kIdThreads>
@@ -90,7 +114,7 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
     if (tid == 0) kout[i] = 0;
     return;
   }
-  if (id_smem_bytes(ny, nx, d) <= kIdSmemMax) return;  // handled by id_kernel_smem
+  if (id_smem_class(ny, nx, d) >= 0) return;  // handled by id_kernel_smem
   const int64_t blk = 8LL * nx * ny;
   if (blk < min_block || blk >= max_block) return;  // the other thread-count variant
   double* M = work + woff[t];
@@ -134,75 +158,104 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
   }
 }
 
-// shared-memory path: the whole block and the CPQR live in shared memory (cpqr.cuh, row-major)
-template <int D>
-__global__ void __launch_bounds__(kIdSmemThreads) id_kernel_smem(
+// shared-memory path: the whole block and the CPQR live in shared memory (cpqr.cuh, row-major).
+// NT = kIdSmemThreads for the staged classes (several CTAs per SM), kIdLeanThreads for the lean
+// one-CTA-per-SM class (coordinates read from global memory, no staging).
+template <int D, int NT>
+__global__ void __launch_bounds__(NT) id_kernel_smem(
     int base, int kid, double p2, double tol, const double* __restrict__ X, int64_t n, int d_unused, int r,
     const int* __restrict__ is_leaf, const int* __restrict__ nbegin, const int* __restrict__ first_child,
     const int* __restrict__ nchild, const int* __restrict__ ys_cnt, const int* __restrict__ ys,
     const int* __restrict__ xbar_n, const int64_t* __restrict__ uoff, double* U, int* kout, int* sk,
     unsigned long long* evals, int cls) {
   extern __shared__ double sh[];
-  __shared__ CpqrRmSmem<kIdSmemThreads> csm;
+  __shared__ CpqrRmSmem<NT> csm;
+  __shared__ CpqrSmem<NT> csm_cm;
+  constexpr bool kLean = NT == kIdLeanThreads;
   const int i = base + blockIdx.x;
   const int nx = xbar_n[i];
   const int ny = ys_cnt[i];
   const int tid = threadIdx.x;
-  // cls < 0: every node of the shared-memory path (merged launch)
-  if (nx == 0 || id_smem_bytes(ny, nx, D) > kIdSmemMax || (cls >= 0 && id_class(id_smem_bytes(ny, nx, D)) != cls))
-    return;
+  if (nx == 0) return;
+  {  // cls < 0: every node of the staged classes (merged launch)
+    const int nc = id_smem_class(ny, nx, D);
+    if (kLean ? nc != kIdLean : (nc < 0 || nc == kIdLean || (cls >= 0 && nc != cls))) return;
+  }
   double* M = sh;
   double* nrm2 = M + (int64_t)ny * nx;
   double* v = nrm2 + nx;
-  double* cx = v + ny;           // Xbar coordinates, [c * nx + b]
-  double* cy = cx + D * nx;      // Y^* coordinates, [c * ny + a]
-  double* tab = cy + D * ny;     // exp table
+  double* cx = v + ny;                      // Xbar coordinates, [c * nx + b] (staged classes)
+  double* cy = cx + D * nx;                 // Y^* coordinates, [c * ny + a]
+  double* tab = kLean ? v + ny : cy + D * ny;  // exp table
   int* piv = reinterpret_cast<int*>(tab + 64);
   int* xb = piv + nx;
   if (tid < 64) tab[tid] = kExp2Tab64[tid];
   if (is_leaf[i]) {
-    for (int b = tid; b < nx; b += kIdSmemThreads) xb[b] = nbegin[i] + b;
+    for (int b = tid; b < nx; b += NT) xb[b] = nbegin[i] + b;
   } else {
     int o = 0;
     for (int c = 0; c < nchild[i]; c++) {
       const int ch = first_child[i] + c;
       const int kc = kout[ch];
-      for (int a = tid; a < kc; a += kIdSmemThreads) xb[o + a] = sk[(int64_t)ch * r + a];
+      for (int a = tid; a < kc; a += NT) xb[o + a] = sk[(int64_t)ch * r + a];
       o += kc;
     }
   }
   const int* yv = ys + (int64_t)i * r;
-  for (int a = tid; a < ny; a += kIdSmemThreads)
+  if (!kLean) {
+    for (int a = tid; a < ny; a += NT)
 #pragma unroll
-    for (int c = 0; c < D; c++) cy[c * ny + a] = X[c * n + yv[a]];
+      for (int c = 0; c < D; c++) cy[c * ny + a] = X[c * n + yv[a]];
+    __syncthreads();
+    for (int b = tid; b < nx; b += NT)
+#pragma unroll
+      for (int c = 0; c < D; c++) cx[c * nx + b] = X[c * n + xb[b]];
+  }
   __syncthreads();
-  for (int b = tid; b < nx; b += kIdSmemThreads)
+  const bool tall = id_tall(ny, nx, NT);
+  auto coord_x = [&](int c, int b) { return kLean ? X[c * n + xb[b]] : cx[c * nx + b]; };
+  auto coord_y = [&](int c, int a) { return kLean ? X[c * n + yv[a]] : cy[c * ny + a]; };
+  int k;
+  if (!tall) {
+    // A^T row-major: M[a*nx + b] = K(Xbar[b], Y^*[a]), Y^* ascending; thread per column b, the
+    // column's point in registers, rows' points broadcast from shared memory (or L1)
+    for (int b = tid; b < nx; b += NT) {
+      double xr[D];
 #pragma unroll
-    for (int c = 0; c < D; c++) cx[c * nx + b] = X[c * n + xb[b]];
-  __syncthreads();
-  // A^T row-major: M[a*nx + b] = K(Xbar[b], Y^*[a]), Y^* ascending; thread per column b, the
-  // column's point in registers, rows' points broadcast from shared memory
-  for (int b = tid; b < nx; b += kIdSmemThreads) {
-    double xr[D];
+      for (int c = 0; c < D; c++) xr[c] = coord_x(c, b);
+      for (int a = 0; a < ny; a++) {
+        double sq = 0.0;
 #pragma unroll
-    for (int c = 0; c < D; c++) xr[c] = cx[c * nx + b];
-    for (int a = 0; a < ny; a++) {
+        for (int c = 0; c < D; c++) {
+          const double df = xr[c] - coord_y(c, a);
+          sq = fma(df, df, sq);
+        }
+        M[a * nx + b] = kernel_s(kid, p2, sq, tab);
+      }
+    }
+    __syncthreads();
+    k = cta_cpqr_rm<NT>(M, ny, nx, nx, tol, piv, nrm2, v, csm);
+  } else {
+    // tall block (few candidates, many farfield rows): A^T column-major, M[a + ny*b], and the
+    // warp-per-column CPQR of cpqr.cuh on shared memory
+    for (int e = tid; e < ny * nx; e += NT) {
+      const int a = e % ny, b = e / ny;
       double sq = 0.0;
 #pragma unroll
       for (int c = 0; c < D; c++) {
-        const double df = xr[c] - cy[c * ny + a];
+        const double df = coord_x(c, b) - coord_y(c, a);
         sq = fma(df, df, sq);
       }
-      M[a * nx + b] = kernel_s(kid, p2, sq, tab);
+      M[e] = kernel_s(kid, p2, sq, tab);
     }
+    __syncthreads();
+    k = cta_cpqr<NT>(M, ny, nx, tol, piv, nrm2, v, csm_cm);
   }
-  __syncthreads();
-  const int k = cta_cpqr_rm<kIdSmemThreads>(M, ny, nx, nx, tol, piv, nrm2, v, csm);
   double* Ui = U + uoff[blockIdx.x];
-  for (int a = tid; a < k; a += kIdSmemThreads) sk[(int64_t)i * r + a] = xb[piv[a]];
-  for (int e = tid; e < nx * k; e += kIdSmemThreads) {
+  for (int a = tid; a < k; a += NT) sk[(int64_t)i * r + a] = xb[piv[a]];
+  for (int e = tid; e < nx * k; e += NT) {
     const int c = e % nx, tt = e / nx;
-    const double val = c < k ? (c == tt ? 1.0 : 0.0) : M[tt * nx + c];
+    const double val = c < k ? (c == tt ? 1.0 : 0.0) : (tall ? M[tt + ny * c] : M[tt * nx + c]);
     Ui[piv[c] + (int64_t)nx * tt] = val;
   }
   if (tid == 0) {
@@ -249,9 +302,9 @@ void id_sweep(h2_handle* h) {
     const LevelRange lr = level_range(h, l);
     int base = lr.begin, count = lr.end - lr.begin;
     if (count == 0) continue;
-    Scratch sz(sizeof(int64_t) * 2 * (count + 1) + 4 * kIdClasses, s), off(sizeof(int64_t) * 2 * (count + 1), s);
-    int* smax = reinterpret_cast<int*>(sz.as<int64_t>() + 2 * (count + 1));  // one max per class
-    H2_CUDA_TRY(cudaMemsetAsync(smax, 0, kIdClasses * sizeof(int), s));
+    Scratch sz(sizeof(int64_t) * 2 * (count + 1) + 4 * (kIdClasses + 1), s), off(sizeof(int64_t) * 2 * (count + 1), s);
+    int* smax = reinterpret_cast<int*>(sz.as<int64_t>() + 2 * (count + 1));  // one max per class (+ lean)
+    H2_CUDA_TRY(cudaMemsetAsync(smax, 0, (kIdClasses + 1) * sizeof(int), s));
     int64_t *wsz = sz.as<int64_t>(), *usz = wsz + count + 1;
     int64_t *woff = off.as<int64_t>(), *uo = woff + count + 1;
     id_sizes_kernel<<<(count + 1 + 255) / 256, 256, 0, s>>>(base, count, h->d, h->is_leaf, h->nbegin, h->nend,
@@ -261,10 +314,10 @@ void id_sweep(h2_handle* h) {
     scan_excl_i64(usz, uo, count + 1, s);
     H2_CHECK_LAUNCH();
     int64_t tot[2];
-    int smem_bytes[kIdClasses] = {0};
+    int smem_bytes[kIdClasses + 1] = {0};
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[0], woff + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[1], uo + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    H2_CUDA_TRY(cudaMemcpyAsync(smem_bytes, smax, kIdClasses * sizeof(int), cudaMemcpyDeviceToHost, s));
+    H2_CUDA_TRY(cudaMemcpyAsync(smem_bytes, smax, (kIdClasses + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaStreamSynchronize(s));
     if (uused + tot[1] > ucap) {
       int64_t nc = uused + tot[1];
@@ -313,14 +366,21 @@ void id_sweep(h2_handle* h) {
     const bool merge = ncls > 1 && count <= 2 * 148 * (per_sm > 0 ? per_sm : 1);
     // the class launches of a level are independent (disjoint nodes): they run concurrently on the
     // build's auxiliary streams, joined back into the main stream before the next level
+    int launches[kIdClasses + 2], nl = 0;
+    if (merge) launches[nl++] = -1;
+    else
+      for (int cls = 0; cls < kIdClasses; cls++)
+        if (smem_bytes[cls] > 0) launches[nl++] = cls;
+    if (smem_bytes[kIdLean] > 0) launches[nl++] = kIdLean;
     int used = 0;
     cudaEvent_t lev_ev[h2_handle::kAux + 1];
-    const bool fan = !merge && h->aux[0] != nullptr;
+    const bool fan = nl > 1 && h->aux[0] != nullptr;
     if (fan) {
       for (auto& e : lev_ev) H2_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       H2_CUDA_TRY(cudaEventRecord(lev_ev[h2_handle::kAux], s));
     }
-    for (int cls = merge ? -1 : 0; cls < (merge ? 0 : kIdClasses); cls++) {
+    for (int li = 0; li < nl; li++) {
+      const int cls = launches[li];
       const int smem = cls < 0 ? smax_all : smem_bytes[cls];
       if (smem == 0) continue;
       cudaStream_t cs = s;
@@ -330,15 +390,26 @@ void id_sweep(h2_handle* h) {
         if (used < h2_handle::kAux) H2_CUDA_TRY(cudaStreamWaitEvent(cs, lev_ev[h2_handle::kAux], 0));
         used++;
       }
+      const bool lean = cls == kIdLean;
       switch (h->d) {
-#define H2_ID_CASE(DD)                                                                                        \
-  case DD: {                                                                                                  \
-        H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_smem<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                                       kIdSmemMax));                                                          \
-    id_kernel_smem<DD><<<count, kIdSmemThreads, smem, cs>>>(                                                  \
-        base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child, h->nchild, \
-        h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>(), cls);       \
-  } break;
+#define H2_ID_CASE(DD)                                                                                          \
+  case DD:                                                                                                      \
+    if (lean) {                                                                                                 \
+      H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_smem<DD, kIdLeanThreads>,                                      \
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kIdLeanMax));               \
+      id_kernel_smem<DD, kIdLeanThreads><<<count, kIdLeanThreads, smem, cs>>>(                                  \
+          base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child,           \
+          h->nchild, h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>(), \
+          cls);                                                                                                 \
+    } else {                                                                                                    \
+      H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_smem<DD, kIdSmemThreads>,                                      \
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kIdSmemMax));               \
+      id_kernel_smem<DD, kIdSmemThreads><<<count, kIdSmemThreads, smem, cs>>>(                                  \
+          base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child,           \
+          h->nchild, h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>(), \
+          cls);                                                                                                 \
+    }                                                                                                           \
+    break;
         H2_ID_CASE(1) H2_ID_CASE(2) H2_ID_CASE(3) H2_ID_CASE(4)
         H2_ID_CASE(5) H2_ID_CASE(6) H2_ID_CASE(7) H2_ID_CASE(8)
 #undef H2_ID_CASE

@@ -38,3 +38,19 @@ for L in range(int(lvl.max()) + 1):
     big = tot > r
     print(f"L{L}: nodes {len(ids)} |IL| mean {nil.mean():.1f} max {nil.max()} |T| mean {tot.mean():.0f} "
           f"max {tot.max()} >r {big.sum()} alg(G*T>r) {float((tot[big]).sum()) * r:.3e}")
+# the ID sweep's blocks per level: |Y*| x |Xbar| and rank k
+yc_all = np.diff(g.export("YS_OFF"))
+xb = g.export("XBAR_N")
+kk = g.export("K")
+for L in range(int(lvl.max()) + 1):
+    ids = np.nonzero(lvl == L)[0]
+    e = yc_all[ids].astype(np.int64) * xb[ids]
+    ek = e * kk[ids]
+    big = e * 8 > 100 * 1024
+    print(f"ID L{L}: nodes {len(ids)} entries {e.sum():.3e} max {e.max()} |Y*| mean {yc_all[ids].mean():.0f} "
+          f"|Xbar| mean {xb[ids].mean():.0f} max {xb[ids].max()} k mean {kk[ids].mean():.1f} max {kk[ids].max()} "
+          f"sum k*entries {ek.sum():.3e} global-path nodes {big.sum()} their k*entries {ek[big].sum():.3e}")
+    if e.sum() > 0:
+        for lim in (12800, 28000, 100000, 200000, 400000, 800000):
+            sel = e <= lim
+            print(f"    entries <= {lim}: nodes {sel.sum()} share of k*entries {ek[sel].sum() / max(1, ek.sum()):.3f}")
