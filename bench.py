@@ -389,12 +389,18 @@ def main():
     ap.add_argument("--storage", choices=["all", "fly", "auto"], default="all",
                     help="block storage (fly: skeleton build a1-a8, blocks evaluated in the matvec; for "
                          "configs whose blocks exceed one GPU)")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 22,
-                    help="points of the oracle's cpu_baseline run (default: the whole workload)")
-    ap.add_argument("--ref-sample", type=int, default=1 << 22,
-                    help="points per step of --impl reference (default: the whole workload, ~6 s)")
+    ap.add_argument("--cpu-sample", type=int, default=None,
+                    help="points of the oracle's cpu_baseline run (default: the whole workload, ~6 s for "
+                         "configs[3]; configs[4]: 65536 points, ~20 s -- its 5-D HiDR is quadratic in the oracle)")
+    ap.add_argument("--ref-sample", type=int, default=None,
+                    help="points per step of --impl reference (default: as --cpu-sample)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    default_sample = min(synth.CONFIGS[args.config]["n"], 65536 if args.config == 5 else 1 << 22)
+    if args.cpu_sample is None:
+        args.cpu_sample = default_sample
+    if args.ref_sample is None:
+        args.ref_sample = default_sample
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
