@@ -150,15 +150,27 @@ __global__ void __launch_bounds__(kFillThreads, MINB) nf_fill_kernel(int64_t nun
                                                                      const int* __restrict__ nbegin,
                                                                      const int* __restrict__ nend,
                                                                      const double* __restrict__ X, int64_t n,
-                                                                     double* __restrict__ out) {
+                                                                     double* __restrict__ out, int upc,
+                                                                     unsigned long long* ctl) {
   static_assert(CW >= 1 && CW <= 8, "1..8 column slots");
   constexpr int WC = 32 * CW;
   __shared__ double tab[256];
   tab[threadIdx.x] = kExp2Tab256[threadIdx.x];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < nunits; u += nw) {
+  // Work is taken by warps in chunks of upc consecutive units from a global counter (ctl[0]).
+  // While the main stream's level kernels still run (ctl[1] == 0) a warp does one chunk and
+  // exits, so fill CTAs are short-lived and free their SM slots quickly; once the main stream has
+  // passed a9 (it sets ctl[1]) the resident warps keep taking chunks until the work is done and
+  // the CTAs launched after that find the counter exhausted and leave at once.
+  const int64_t nchunks = (nunits + upc - 1) / upc;
+  for (;;) {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(ctl, 1ull);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if ((int64_t)c >= nchunks) break;
+    const int64_t u_end = ((int64_t)c + 1) * upc < nunits ? ((int64_t)c + 1) * upc : nunits;
+  for (int64_t u = (int64_t)c * upc; u < u_end; u++) {
     const int p = umap[u];
     const int2 pr = pairs[p];
     const int bi = nbegin[pr.x], bj = nbegin[pr.y];
@@ -193,6 +205,8 @@ __global__ void __launch_bounds__(kFillThreads, MINB) nf_fill_kernel(int64_t nun
       case 7: nf_unit_rows<D, KID, (CW < 7 ? CW : 7), CL != 0>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
       default: nf_unit_rows<D, KID, CW, CL != 0>(xr, n, xb, last_ok, r0, r1, nj, o, tab); break;
     }
+  }
+    if (*reinterpret_cast<volatile unsigned long long*>(ctl + 1) == 0) break;
   }
 }
 
@@ -268,15 +282,15 @@ __global__ void scale_coords_kernel(int64_t m, const double* __restrict__ X, dou
     Xs[t] = X[t] * cs;
 }
 
-// H2_NF_UPW (tuning knob, read once): nearfield units per warp of one CTA's lifetime.  The
-// nearfield fill runs CONCURRENTLY with the HiDR / ID stages (api.cu), on a low-priority stream:
-// its grid is made of many short-lived CTAs (default 8 units per warp, ~0.1 ms each) so that
-// the latency-bound level kernels on the high-priority stream get SMs as soon as a fill CTA
-// retires; 0 = one persistent wave (148 x 8 CTAs).
+// H2_NF_UPW (tuning knob, read once): nearfield units per chunk (see nf_fill_kernel).  The
+// nearfield fill runs CONCURRENTLY with the HiDR / ID stages (api.cu), on a low-priority stream;
+// while they run, a fill warp does one chunk and its CTA retires (~0.05 ms), so the latency-bound
+// level kernels of the high-priority stream get SM slots quickly; after a9 the fill CTAs persist.
 static int nf_units_per_warp() {
   static const int v = [] {
     const char* e = getenv("H2_NF_UPW");
-    return e ? atoi(e) : 8;
+    const int u = e ? atoi(e) : 4;
+    return u > 0 ? u : 4;
   }();
   return v;
 }
@@ -302,14 +316,13 @@ static void launch_nf(K kernel, unsigned g, cudaStream_t s, A... args) {
 template <int KID>
 static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_t nwork, int64_t np, const int* umap,
                             const int64_t* uoff, const int2* pairs, const int64_t* voff, const double* Xs, double cs,
-                            double* out) {
+                            double* out, unsigned long long* ctl) {
   if (mode == 1) {
     const bool clamp = fill_needs_clamp(h->kid, h->d, h->W, cs);
     const int upw = nf_units_per_warp();
-    int64_t blocks = upw > 0 ? (nwork + 8 * upw - 1) / (8 * upw) : (nwork + 7) / 8;  // 8 warps per CTA
-    const int64_t cap = upw > 0 ? (int64_t)1 << 30 : 148 * 8;
-    unsigned g = (unsigned)(blocks < cap ? blocks : cap);
-#define H2_NF_ARGS nwork, umap, uoff, pairs, voff, h->nbegin, h->nend, Xs, h->n, out
+    const int64_t blocks = (nwork + 8 * upw - 1) / (8 * upw);  // one chunk per warp, 8 warps per CTA
+    unsigned g = (unsigned)(blocks < ((int64_t)1 << 30) ? blocks : ((int64_t)1 << 30));
+#define H2_NF_ARGS nwork, umap, uoff, pairs, voff, h->nbegin, h->nend, Xs, h->n, out, upw, ctl
     switch (h->d) {
       case 2:
         switch (nf_variant()) {  // tuning variants of the D = 2 kernel (CW, clamp, MINB)
@@ -348,24 +361,25 @@ static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_
 }
 
 static void launch_fill(const h2_handle* h, cudaStream_t s, int mode, int64_t nwork, int64_t np, const int* umap,
-                        const int64_t* uoff, const int2* pairs, const int64_t* voff, const double* Xs, double* out) {
+                        const int64_t* uoff, const int2* pairs, const int64_t* voff, const double* Xs, double* out,
+                        unsigned long long* ctl = nullptr) {
   if (nwork < 1) return;
   const double cs = kernel_cscale(h->kid, h->kp);
   switch (h->kid) {
     case H2_KERNEL_COULOMB:
-      launch_fill_kid<H2_KERNEL_COULOMB>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
+      launch_fill_kid<H2_KERNEL_COULOMB>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out, ctl);
       break;
     case H2_KERNEL_GAUSSIAN:
-      launch_fill_kid<H2_KERNEL_GAUSSIAN>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
+      launch_fill_kid<H2_KERNEL_GAUSSIAN>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out, ctl);
       break;
     case H2_KERNEL_MATERN32:
-      launch_fill_kid<H2_KERNEL_MATERN32>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
+      launch_fill_kid<H2_KERNEL_MATERN32>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out, ctl);
       break;
     case H2_KERNEL_LAPLACE:
-      launch_fill_kid<H2_KERNEL_LAPLACE>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
+      launch_fill_kid<H2_KERNEL_LAPLACE>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out, ctl);
       break;
     default:
-      launch_fill_kid<H2_KERNEL_BUMP>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out);
+      launch_fill_kid<H2_KERNEL_BUMP>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out, ctl);
       break;
   }
 }
@@ -457,8 +471,12 @@ void fill_nearfield_begin(h2_handle* h, cudaStream_t side, int storage, int64_t 
     job.xs = Scratch(sizeof(double) * (size_t)h->n * h->d, side);
     scale_coords_kernel<<<grid_for((int64_t)h->n * h->d, 256), 256, 0, side>>>(
         (int64_t)h->n * h->d, h->X, kernel_cscale(h->kid, h->kp), job.xs.as<double>());
+    // chunk counter + "main stream past a9" flag (set at once when the fill runs on the main stream)
+    job.ctl = Scratch(2 * sizeof(unsigned long long), side);
+    H2_CUDA_TRY(cudaMemsetAsync(job.ctl.p, 0, 2 * sizeof(unsigned long long), side));
+    if (side == h->stream) H2_CUDA_TRY(cudaMemsetAsync(job.ctl.as<unsigned long long>() + 1, 1, 1, side));
     launch_fill(h, side, 1, nunits, h->n_np, h->nf_umap, h->nf_uoff, h->np_pairs, h->np_off, job.xs.as<double>(),
-                h->np_val);
+                h->np_val, job.ctl.as<unsigned long long>());
     h->gpu_launches += 1;
     H2_CHECK_LAUNCH();
     h->gpu_launches += 1;
@@ -488,6 +506,9 @@ void fill_coupling(h2_handle* h, int storage, int64_t budget, const NfJob& job) 
     H2_CHECK_LAUNCH();
     h->gpu_launches += 1;
   }
+  // the main stream is past its level kernels: the concurrent nearfield fill may keep its SMs
+  if (job.ctl.p && job.side != s)
+    H2_CUDA_TRY(cudaMemsetAsync(static_cast<unsigned long long*>(job.ctl.p) + 1, 1, 1, s));
   if (h->timing) {
     H2_CUDA_TRY(cudaEventRecord(ev[1], s));
     H2_CUDA_TRY(cudaEventSynchronize(ev[1]));
@@ -505,6 +526,8 @@ void fill_nearfield_join(h2_handle* h, NfJob& job) {
   H2_CUDA_TRY(cudaStreamWaitEvent(h->stream, job.done, 0));
   job.xs.s = h->stream;
   job.xs = Scratch();
+  job.ctl.s = h->stream;
+  job.ctl = Scratch();
   job.active = false;
 }
 
