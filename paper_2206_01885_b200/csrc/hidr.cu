@@ -138,7 +138,11 @@ static bool hidr_down_level_pruned(h2_handle* h, int l, unsigned long long* ev, 
   const LevelRange lr = level_range(h, l);
   const int base = lr.begin, count = lr.end - lr.begin;
   const int ngmax = (h->csp + 1 + 31) / 32;
-  const size_t smem = sizeof(float) * 2 * h->d * (size_t)ngmax;
+  // group boxes + the segments' node ids, or the aliased selection buffer (next power of two >= r)
+  size_t sel_bytes = sizeof(int);
+  while (sel_bytes < sizeof(int) * (size_t)h->r) sel_bytes <<= 1;
+  size_t smem = sizeof(float) * 2 * h->d * (size_t)ngmax + sizeof(int) * (size_t)(h->csp + 1);
+  if (smem < sel_bytes) smem = sel_bytes;
   if (smem > (size_t)kDownSmemMax) return false;
   cudaStream_t s = h->stream;
   switch (h->d) {

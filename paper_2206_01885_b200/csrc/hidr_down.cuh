@@ -138,8 +138,11 @@ __global__ void __launch_bounds__(kDownThreads, 4) hidr_down_kernel(
     const float* __restrict__ xboxf, const float* __restrict__ yboxf, int* ys_cnt,
     int* ys, const double* __restrict__ xs_xyz, const double* __restrict__ ys_xyz, unsigned long long* evals_alg,
     unsigned long long* evals_done) {
-  extern __shared__ float gbox[];  // group g (float, outward): lo at gbox[g*2D + c], hi at gbox[g*2D + D + c]
-  __shared__ int sel[kVolSelCap];
+  // dynamic shared memory: during the search, the group boxes (float, outward: lo at
+  // gbox[g*2D + c], hi at gbox[g*2D + D + c]) and the segments' node ids; before and after it,
+  // the selection buffer `sel` (pass-through gather, final sort) aliased onto the same space
+  extern __shared__ float gbox[];
+  int* const sel = reinterpret_cast<int*>(gbox);
   __shared__ BlockScanSmem<kDownThreads> scan;
   __shared__ double wlo[D][kDownWarps], whi[D][kDownWarps];
   __shared__ long long wcnt[kDownWarps];
@@ -154,13 +157,14 @@ __global__ void __launch_bounds__(kDownThreads, 4) hidr_down_kernel(
   int* out = ys + (int64_t)i * r;
   const int* yp = ys + (int64_t)p * r;
   // segment s: 0 = Y_p^*, s >= 1 = X_j^* of the (s-1)-th entry of IL(i)
+  int* const seg_nd = reinterpret_cast<int*>(gbox + ng * 2 * D);  // filled in phase 1
   auto seg_node = [&](int s) { return s == 0 ? p : il_idx[e0 + s - 1]; };
   auto seg_box = [&](int s, int nd) { return (s == 0 ? ybox : xbox) + (int64_t)nd * kBox; };
   auto seg_slots = [&](int s, int nd) { return s == 0 ? yp : xs + (int64_t)nd * r; };
   auto seg_xyz = [&](int s, int nd) { return (s == 0 ? ys_xyz : xs_xyz) + (int64_t)nd * r * D; };
   // a segment's float box and count in whole float4 loads
   auto load_segf = [&](int s, int& nd, float* blo, float* bhi) {
-    nd = seg_node(s);
+    nd = seg_nd[s];
     const float4* b = reinterpret_cast<const float4*>((s == 0 ? yboxf : xboxf) + (int64_t)nd * kBoxF);
     constexpr int NV = (2 * D + 1 + 3) / 4;
     float v[4 * NV];
@@ -211,6 +215,7 @@ __global__ void __launch_bounds__(kDownThreads, 4) hidr_down_kernel(
     if (s < nseg) {
       int nd;
       cnt = load_seg(s, nd, blo, bhi);
+      seg_nd[s] = nd;
     }
 #pragma unroll
     for (int c = 0; c < D; c++)
