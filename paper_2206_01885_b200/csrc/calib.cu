@@ -24,7 +24,9 @@ struct CalWork {  // per-trial global workspace
   double nrm2[N], v[N];
   int piv[N], sel[N];
   int ns, k;  // |Z2^*| and the ID rank, passed between the trial's launches
+  double pnum[8], pden[8];  // the error's partial sums per column slice (calib_err_kernel)
 };
+constexpr int kErrSlices = 8;  // CTAs per trial of the error evaluation: N / 8 = 32 columns each
 
 // k-th SplitMix64 output of the stream seeded with `seed` (counter form of the sequential
 // generator: state_k = seed + (k+1) * golden gamma)
@@ -99,52 +101,101 @@ __global__ void __launch_bounds__(kCalCpqrThreads) calib_cpqr_kernel(double eps,
   if (threadIdx.x == 0) W.k = k;
 }
 
+// Ks[t][e] = K(Z1[piv[t]], Z2[e]) for the k skeleton rows
 template <int D>
-__global__ void __launch_bounds__(kCalThreads) calib_err_kernel(int kid, double p2, double eps,
-                                                                const int* __restrict__ mv, CalWork* work,
-                                                                double* err, int* pass) {
-  __shared__ CpqrSmem<kCalThreads> csm;
-  const int tid = threadIdx.x;
+__global__ void __launch_bounds__(kCalThreads) calib_ks_kernel(int kid, double p2, CalWork* work) {
   CalWork& W = work[blockIdx.x];
-  const int m = mv[blockIdx.x], ns = W.ns, k = W.k;
-  long long G = 1;
-  for (int c = 0; c < D; c++) G *= m;
-  // Ks[t][e] = K(Z1[piv[t]], Z2[e]) for the k skeleton rows
-  for (int x = tid; x < k * N; x += kCalThreads) {
-    int t = x / N, e = x % N;
+  const int k = W.k;
+  for (int x = threadIdx.x; x < k * N; x += kCalThreads) {
+    const int t = x / N, e = x % N;
     double s = 0.0;
     for (int c = 0; c < D; c++) {
-      double df = W.Z1[W.piv[t] * D + c] - W.Z2[e * D + c];
+      const double df = W.Z1[W.piv[t] * D + c] - W.Z2[e * D + c];
       s = fma(df, df, s);
     }
     W.Ks[x] = kernel_s(kid, p2, s);
   }
-  __syncthreads();
+}
+
+// Error of one trial, kErrSlices CTAs per trial: slice q takes the 32 columns (pivoted positions)
+// [32 q, 32 q + 32) x all N points of Z2.  A warp owns 4 columns (the same for all its lanes:
+// T and M loads are broadcasts) and a lane 8 points: a 4 x 8 register tile, 32 FMAs per 12 loads
+// in the k-long inner product U K^.  Partial sums per slice; calib_final_kernel adds them in a
+// fixed order.
+template <int D>
+__global__ void __launch_bounds__(kCalThreads) calib_err_kernel(int kid, double p2, CalWork* work) {
+  __shared__ CpqrSmem<kCalThreads> csm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  CalWork& W = work[blockIdx.x / kErrSlices];
+  const int q = blockIdx.x % kErrSlices;
+  const int ns = W.ns, k = W.k;
+  constexpr int CPW = 4, EPL = N / 32;  // columns per warp, points per lane
+  const int c0 = q * (N / kErrSlices) + warp * CPW;
   double num = 0.0, den = 0.0;
-  for (int x = tid; x < N * N; x += kCalThreads) {
-    int c = x / N, e = x % N;  // c = position in the pivoted order
-    int row = W.piv[c];
-    double s = 0.0;
-    for (int q = 0; q < D; q++) {
-      double df = W.Z1[row * D + q] - W.Z2[e * D + q];
-      s = fma(df, df, s);
+  double kv[CPW][EPL];
+#pragma unroll
+  for (int j = 0; j < CPW; j++) {
+    const int row = W.piv[c0 + j];
+#pragma unroll
+    for (int u = 0; u < EPL; u++) {
+      const int e = lane + 32 * u;
+      double s = 0.0;
+      for (int c = 0; c < D; c++) {
+        const double df = W.Z1[row * D + c] - W.Z2[e * D + c];
+        s = fma(df, df, s);
+      }
+      kv[j][u] = kernel_s(kid, p2, s);
+      den += kv[j][u] * kv[j][u];
     }
-    double kv = kernel_s(kid, p2, s);
-    den += kv * kv;
-    if (c >= k) {
-      double ap = 0.0;
-      for (int t = 0; t < k; t++) ap += W.M[t + ns * c] * W.Ks[t * N + e];
-      double df = kv - ap;
-      num += df * df;
+  }
+  if (c0 + CPW > k) {  // some of the warp's columns are outside the skeleton: K - U K^
+    double ap[CPW][EPL];
+#pragma unroll
+    for (int j = 0; j < CPW; j++)
+#pragma unroll
+      for (int u = 0; u < EPL; u++) ap[j][u] = 0.0;
+    for (int t = 0; t < k; t++) {
+      double tm[CPW], ks[EPL];
+#pragma unroll
+      for (int j = 0; j < CPW; j++) tm[j] = W.M[t + ns * (c0 + j)];
+#pragma unroll
+      for (int u = 0; u < EPL; u++) ks[u] = W.Ks[t * N + lane + 32 * u];
+#pragma unroll
+      for (int j = 0; j < CPW; j++)
+#pragma unroll
+        for (int u = 0; u < EPL; u++) ap[j][u] = fma(tm[j], ks[u], ap[j][u]);
     }
+#pragma unroll
+    for (int j = 0; j < CPW; j++)
+      if (c0 + j >= k)
+#pragma unroll
+        for (int u = 0; u < EPL; u++) {
+          const double df = kv[j][u] - ap[j][u];
+          num += df * df;
+        }
   }
   num = cta_sum<kCalThreads>(num, csm);
   den = cta_sum<kCalThreads>(den, csm);
   if (tid == 0) {
-    double e = den > 0.0 ? sqrt(num) / sqrt(den) : 0.0;
-    err[blockIdx.x] = e;
-    pass[blockIdx.x] = (e < 1e-2 * eps) || G >= N;
+    W.pnum[q] = num;
+    W.pden[q] = den;
   }
+}
+
+__global__ void calib_final_kernel(double eps, const int* __restrict__ mv, int d, CalWork* work, double* err,
+                                   int* pass) {
+  const int t = blockIdx.x;  // one thread per trial
+  CalWork& W = work[t];
+  double num = 0.0, den = 0.0;
+  for (int q = 0; q < kErrSlices; q++) {
+    num += W.pnum[q];
+    den += W.pden[q];
+  }
+  long long G = 1;
+  for (int c = 0; c < d; c++) G *= mv[t];
+  const double e = den > 0.0 ? sqrt(num) / sqrt(den) : 0.0;
+  err[t] = e;
+  pass[t] = (e < 1e-2 * eps) || G >= N;
 }
 
 __global__ void level_has_il_kernel(int nnodes, const int* __restrict__ level, const int64_t* __restrict__ il_off,
@@ -202,15 +253,16 @@ static void launch_trials(h2_handle* h, cudaStream_t s, int slot, const std::vec
     calib_prep_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, h->tau, dw + b0, dl + b0, dm + b0,         \
                                                      job.work.as<CalWork>());                              \
     calib_cpqr_kernel<<<nb, kCalCpqrThreads, 0, s>>>(h->id_tol, job.work.as<CalWork>());                  \
-    calib_err_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, h->id_tol, dm + b0, job.work.as<CalWork>(), \
-                                                    derr + b0, dpass + b0);                               \
+    calib_ks_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, job.work.as<CalWork>());                    \
+    calib_err_kernel<DD><<<nb * kErrSlices, kCalThreads, 0, s>>>(h->kid, p2, job.work.as<CalWork>());        \
     break;
       H2_CAL_CASE(1) H2_CAL_CASE(2) H2_CAL_CASE(3) H2_CAL_CASE(4)
       H2_CAL_CASE(5) H2_CAL_CASE(6) H2_CAL_CASE(7) H2_CAL_CASE(8)
 #undef H2_CAL_CASE
     }
+    calib_final_kernel<<<nb, 1, 0, s>>>(h->id_tol, dm + b0, d, job.work.as<CalWork>(), derr + b0, dpass + b0);
     H2_CHECK_LAUNCH();
-    h->gpu_launches += 3;
+    h->gpu_launches += 5;
   }
   job.pass_h = reinterpret_cast<int*>(hin + in_bytes);
   H2_CUDA_TRY(cudaMemcpyAsync(job.pass_h, dpass, sizeof(int) * T, cudaMemcpyDeviceToHost, s));
