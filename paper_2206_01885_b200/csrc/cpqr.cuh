@@ -124,16 +124,41 @@ __device__ int cta_cpqr(double* __restrict__ M, int rows, int cols, double tol, 
     if (vtv > 0.0) {
       for (int j = t + 1 + warp; j < cols; j += NW) {
         double* col = M + (int64_t)rows * j;
-        double s = 0.0;
-        for (int i = t + lane; i < rows; i += 32) s += v[i] * col[i];
+        // four rows per lane in flight (independent loads and partial sums): the column is in
+        // L2 / HBM, so memory-level parallelism sets the pace
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int i = t + lane;
+        for (; i + 96 < rows; i += 128) {
+          const double c0 = col[i], c1 = col[i + 32], c2 = col[i + 64], c3 = col[i + 96];
+          s0 += v[i] * c0;
+          s1 += v[i + 32] * c1;
+          s2 += v[i + 64] * c2;
+          s3 += v[i + 96] * c3;
+        }
+        for (; i < rows; i += 32) s0 += v[i] * col[i];
+        double s = (s0 + s1) + (s2 + s3);
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         const double f = 2.0 * s / vtv;
-        double nn = 0.0;
-        for (int i = t + lane; i < rows; i += 32) {
-          double a = col[i] - f * v[i];
-          col[i] = a;
-          if (i > t) nn += a * a;
+        double n0 = 0.0, n1 = 0.0, n2 = 0.0, n3 = 0.0;
+        i = t + lane;
+        for (; i + 96 < rows; i += 128) {
+          const double a0 = col[i] - f * v[i], a1 = col[i + 32] - f * v[i + 32];
+          const double a2 = col[i + 64] - f * v[i + 64], a3 = col[i + 96] - f * v[i + 96];
+          col[i] = a0;
+          col[i + 32] = a1;
+          col[i + 64] = a2;
+          col[i + 96] = a3;
+          if (i > t) n0 += a0 * a0;  // only row t itself is excluded (it joins R)
+          n1 += a1 * a1;
+          n2 += a2 * a2;
+          n3 += a3 * a3;
         }
+        for (; i < rows; i += 32) {
+          const double a = col[i] - f * v[i];
+          col[i] = a;
+          if (i > t) n0 += a * a;
+        }
+        double nn = (n0 + n1) + (n2 + n3);
         for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
         if (lane == 0) nrm2[j] = nn;
       }
@@ -147,8 +172,9 @@ __device__ int cta_cpqr(double* __restrict__ M, int rows, int cols, double tol, 
       }
     }
     __syncthreads();
+    // the pivot column joins R: row t = alpha; its rows below t are never read again (the back
+    // substitution and T read rows < k of R11 / R12 only), so they are left as they are
     if (tid == 0) ct[t] = alpha;
-    for (int i = t + 1 + tid; i < rows; i += NT) ct[i] = 0.0;
     k = t + 1;
     __syncthreads();
   }
