@@ -178,7 +178,7 @@ __global__ void row_scatter_kernel(const unsigned long long* __restrict__ keys, 
 
 // one CTA per row: a row of <= 64 entries is sorted by warp 0 with shuffles (two per lane, no
 // barrier), a longer one by a shared-memory bitonic network of its own power-of-two size
-constexpr int kRowSortThreads = 256;
+constexpr int kRowSortThreads = 512;
 __global__ void __launch_bounds__(kRowSortThreads) row_sort_kernel(const int64_t* __restrict__ off, int* idx) {
   extern __shared__ int rs[];
   const int64_t b = off[blockIdx.x];

@@ -42,17 +42,15 @@ struct VolSmem {
 // bitonic sort of a[0..P), P a power of two, by the whole CTA
 template <int NT>
 __device__ void cta_bitonic(int* a, int P) {
+  // every thread takes compare-exchange pairs (i, i + j) directly: P/2 pairs per stage
   for (int k = 2; k <= P; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P; i += NT) {
-        int l = i ^ j;
-        if (l > i) {
-          int x = a[i], y = a[l];
-          bool up = (i & k) == 0;
-          if ((x > y) == up) {
-            a[i] = y;
-            a[l] = x;
-          }
+      for (int q = threadIdx.x; q < (P >> 1); q += NT) {
+        const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1)), l = i + j;
+        const int x = a[i], y = a[l];
+        if ((x > y) == ((i & k) == 0)) {
+          a[i] = y;
+          a[l] = x;
         }
       }
       __syncthreads();
