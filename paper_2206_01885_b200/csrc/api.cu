@@ -196,6 +196,7 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
     H2_CUDA_TRY(cudaStreamWaitEvent(bs.main, fork_ev, 0));
     h->stream = bs.main;
     for (int a = 0; a < h2_handle::kAux; a++) h->aux[a] = bs.aux[a];
+    h->low = bs.side;
     if (h->timing) {
       for (auto& e : ev) H2_CUDA_TRY(cudaEventCreate(&e));
       nev = 8;

@@ -17,9 +17,16 @@ __global__ void permute_in_kernel(const double* __restrict__ x, const int* __res
     xt[t] = x[perm[t]];
 }
 
-__global__ void permute_out_kernel(const double* __restrict__ yt, const int* __restrict__ perm, int64_t n, double* y) {
+__global__ void add_kernel(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
-    y[perm[t]] = yt[t];
+    b[t] += a[t];
+}
+
+// y[perm[t]] = yt[t] + yf[t]: the nearfield and the farfield contributions (tree order)
+__global__ void permute_out_kernel(const double* __restrict__ yt, const double* __restrict__ yf,
+                                   const int* __restrict__ perm, int64_t n, double* y) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    y[perm[t]] = yt[t] + yf[t];
 }
 
 __global__ void up_kernel(int base, int r, const int* __restrict__ is_leaf, const int* __restrict__ nbegin,
@@ -448,8 +455,7 @@ static bool mv_bulk() {
 
 template <int D>
 static void launch_far_near(const h2_handle* h, double p2, const double* zh, double* yh, const double* xt, double* yt,
-                            int which) {
-  cudaStream_t s = h->stream;
+                            int which, cudaStream_t s) {
   if (which == 0 && h->n_cp > 0 && h->cp_stored) {
     const int64_t blocks = (h->n_cp + 7) / 8;
     const unsigned g = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
@@ -499,11 +505,11 @@ static void launch_far_near(const h2_handle* h, double p2, const double* zh, dou
 }
 
 static void far_near(const h2_handle* h, double p2, const double* zh, double* yh, const double* xt, double* yt,
-                     int which) {
+                     int which, cudaStream_t s) {
   switch (h->d) {
 #define H2_MV_CASE(DD) \
   case DD:             \
-    launch_far_near<DD>(h, p2, zh, yh, xt, yt, which); break;
+    launch_far_near<DD>(h, p2, zh, yh, xt, yt, which, s); break;
     H2_MV_CASE(1) H2_MV_CASE(2) H2_MV_CASE(3) H2_MV_CASE(4)
     H2_MV_CASE(5) H2_MV_CASE(6) H2_MV_CASE(7) H2_MV_CASE(8)
 #undef H2_MV_CASE
@@ -514,17 +520,33 @@ static void far_near(const h2_handle* h, double p2, const double* zh, double* yh
 // >= cut are summed over the ranks (each node is non-zero on its owner only), and the levels
 // above the cut are then computed by every rank; coupling and nearfield apply the rank's own
 // (row-owned) blocks in both directions, so y^ and y are partial sums completed by allreduces.
+// The nearfield pass (xt -> yt, by far the most bytes) depends only on the permuted input, so it
+// runs on a second stream concurrently with the farfield chain (up -> coupling -> down, xt -> yf);
+// the two outputs are added in the final permutation.
 void matvec(const h2_handle* h, const double* x, double* y) {
   cudaStream_t s = h->stream;
   const int64_t n = h->n;
   const int nn = h->nnodes, r = h->r;
   const bool sharded = h->nranks > 1;
-  Scratch xt(sizeof(double) * n, s), yt(sizeof(double) * n, s), zh(sizeof(double) * (size_t)nn * r, s),
-      yh(sizeof(double) * (size_t)nn * r, s);
+  Scratch xt(sizeof(double) * n, s), yt(sizeof(double) * n, s), yf(sizeof(double) * n, s),
+      zh(sizeof(double) * (size_t)nn * r, s), yh(sizeof(double) * (size_t)nn * r, s);
   H2_CUDA_TRY(cudaMemsetAsync(yt.p, 0, sizeof(double) * n, s));
+  H2_CUDA_TRY(cudaMemsetAsync(yf.p, 0, sizeof(double) * n, s));
   H2_CUDA_TRY(cudaMemsetAsync(yh.p, 0, sizeof(double) * (size_t)nn * r, s));
   H2_CUDA_TRY(cudaMemsetAsync(zh.p, 0, sizeof(double) * (size_t)nn * r, s));
   permute_in_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, h->perm, n, xt.as<double>());
+  const double p2 = kernel_p2(h->kid, h->kp);
+  // nearfield on the build's lowest-priority stream, forked after permute_in: its short CTAs yield
+  // SM slots to the farfield chain's level kernels on `s` as they retire
+  cudaStream_t ns = h->low ? h->low : s;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  if (ns != s) {
+    for (auto& e : ev) H2_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    H2_CUDA_TRY(cudaEventRecord(ev[0], s));
+    H2_CUDA_TRY(cudaStreamWaitEvent(ns, ev[0], 0));
+  }
+  far_near(h, p2, zh.as<double>(), yh.as<double>(), xt.as<double>(), yt.as<double>(), 1, ns);
+  if (ns != s) H2_CUDA_TRY(cudaEventRecord(ev[1], ns));
   auto up = [&](int l) {
     const LevelRange lr = level_range(h, l);
     if (lr.end > lr.begin)
@@ -536,21 +558,26 @@ void matvec(const h2_handle* h, const double* x, double* y) {
   for (int l = h->depth; l >= cut; l--) up(l);
   if (sharded) comm_allreduce_sum(h->comm, zh.as<double>(), zh.as<double>(), (int64_t)nn * r, s);
   for (int l = cut - 1; l >= 1; l--) up(l);
-  const double p2 = kernel_p2(h->kid, h->kp);
-  far_near(h, p2, zh.as<double>(), yh.as<double>(), xt.as<double>(), yt.as<double>(), 0);
+  far_near(h, p2, zh.as<double>(), yh.as<double>(), xt.as<double>(), yt.as<double>(), 0, s);
   if (sharded) comm_allreduce_sum(h->comm, yh.as<double>(), yh.as<double>(), (int64_t)nn * r, s);
   for (int l = 1; l <= h->depth; l++) {
     const LevelRange lr = level_range(h, l);
     if (lr.end > lr.begin)
       down_kernel<<<lr.end - lr.begin, kMvThreads, 0, s>>>(lr.begin, r, h->is_leaf, h->nbegin, h->parent, h->k,
                                                            h->xbar_n, h->child_off, h->u_off, h->U, h->p_lo, h->p_hi,
-                                                           yh.as<double>(), yt.as<double>());
+                                                           yh.as<double>(), yf.as<double>());
   }
-  far_near(h, p2, zh.as<double>(), yh.as<double>(), xt.as<double>(), yt.as<double>(), 1);
-  if (sharded) comm_allreduce_sum(h->comm, yt.as<double>(), yt.as<double>(), n, s);
-  permute_out_kernel<<<grid_for(n, 256), 256, 0, s>>>(yt.as<double>(), h->perm, n, y);
+  if (ns != s) H2_CUDA_TRY(cudaStreamWaitEvent(s, ev[1], 0));
+  if (sharded) {
+    add_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, yf.as<double>(), yt.as<double>());
+    H2_CUDA_TRY(cudaMemsetAsync(yf.p, 0, sizeof(double) * n, s));
+    comm_allreduce_sum(h->comm, yt.as<double>(), yt.as<double>(), n, s);
+  }
+  permute_out_kernel<<<grid_for(n, 256), 256, 0, s>>>(yt.as<double>(), yf.as<double>(), h->perm, n, y);
   H2_CHECK_LAUNCH();
   H2_CUDA_TRY(cudaStreamSynchronize(s));
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
 }
 
 }  // namespace h2
