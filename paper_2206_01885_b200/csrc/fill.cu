@@ -19,6 +19,13 @@
 namespace h2 {
 
 constexpr int kFillThreads = 256;
+#ifndef H2_NF_THREADS
+#define H2_NF_THREADS 128
+#endif
+// threads of a nearfield-fill CTA; the per-SM register budget is kept (MINB scaled): smaller CTAs
+// let a concurrent main-stream CTA displace less of an SM's fill work
+constexpr int kNfThreads = H2_NF_THREADS;
+constexpr int kNfScale = 256 / kNfThreads;
 
 // ---- symmetric-once pair lists, entry-parallel over the CSR ---------------------------------
 __device__ __forceinline__ int row_of(const int64_t* __restrict__ off, int nnodes, int64_t e) {
@@ -143,7 +150,7 @@ __device__ __forceinline__ void nf_unit_rows(const double* __restrict__ xr, int6
 }
 
 template <int D, int KID, int CW, int CL, int MINB>
-__global__ void __launch_bounds__(kFillThreads, MINB) nf_fill_kernel(int64_t nunits, const int* __restrict__ umap,
+__global__ void __launch_bounds__(kNfThreads, MINB * kNfScale) nf_fill_kernel(int64_t nunits, const int* __restrict__ umap,
                                                                      const int64_t* __restrict__ uoff,
                                                                      const int2* __restrict__ pairs,
                                                                      const int64_t* __restrict__ voff,
@@ -155,7 +162,7 @@ __global__ void __launch_bounds__(kFillThreads, MINB) nf_fill_kernel(int64_t nun
   static_assert(CW >= 1 && CW <= 8, "1..8 column slots");
   constexpr int WC = 32 * CW;
   __shared__ double tab[256];
-  tab[threadIdx.x] = kExp2Tab256[threadIdx.x];
+  for (int e = threadIdx.x; e < 256; e += kNfThreads) tab[e] = kExp2Tab256[e];
   __syncthreads();
   const int lane = threadIdx.x & 31;
   // Work is taken by warps in chunks of upc consecutive units from a global counter (ctl[0]).
@@ -310,7 +317,7 @@ template <class K, class... A>
 static void launch_nf(K kernel, unsigned g, cudaStream_t s, A... args) {
   const int sm = nf_smem_reserve();
   if (sm > 48 * 1024) H2_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-  kernel<<<g, kFillThreads, sm, s>>>(args...);
+  kernel<<<g, kNfThreads, sm, s>>>(args...);
 }
 
 template <int KID>
@@ -320,7 +327,8 @@ static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_
   if (mode == 1) {
     const bool clamp = fill_needs_clamp(h->kid, h->d, h->W, cs);
     const int upw = nf_units_per_warp();
-    const int64_t blocks = (nwork + 8 * upw - 1) / (8 * upw);  // one chunk per warp, 8 warps per CTA
+    constexpr int wpc = kNfThreads / 32;
+    const int64_t blocks = (nwork + wpc * upw - 1) / (wpc * upw);  // one chunk per warp
     unsigned g = (unsigned)(blocks < ((int64_t)1 << 30) ? blocks : ((int64_t)1 << 30));
 #define H2_NF_ARGS nwork, umap, uoff, pairs, voff, h->nbegin, h->nend, Xs, h->n, out, upw, ctl
     switch (h->d) {
