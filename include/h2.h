@@ -46,7 +46,9 @@ enum {
   H2_KERNEL_GAUSSIAN = 2, /* exp(-|x-y|^2 / h^2).          kernel_params[0] = h > 0          */
   H2_KERNEL_MATERN32 = 3, /* (1 + sqrt3 r/l) exp(-sqrt3 r/l), r=|x-y|.    kernel_params[0] = l > 0          */
   H2_KERNEL_LAPLACE = 4,  /* exp(-r/l) (P:91 at l = 1).                     kernel_params[0] = l > 0          */
-  H2_KERNEL_BUMP = 5      /* exp(-1/(1 - 0.1 r^2)) for 0.1 r^2 < 1, else 0 (Table 1 kappa_4).
+  H2_KERNEL_BUMP = 5,     /* exp(-1/(1 - 0.1 r^2)) for 0.1 r^2 < 1, else 0 (Table 1 kappa_4).
+                             kernel_params: none (may be NULL)                                            */
+  H2_KERNEL_COSDOT = 6    /* cos(x . y) (Table 1 kappa_3): symmetric, not a function of |x-y|.
                              kernel_params: none (may be NULL)                                            */
 };
 

@@ -85,7 +85,7 @@ static int64_t ipow_sat(int64_t m, int d) {
 /* kernel functions  (Table 1; Matern-3/2 from BASELINE.json configs[3])    */
 /* ------------------------------------------------------------------------------------------ */
 
-enum { ORC_COULOMB = 1, ORC_GAUSSIAN = 2, ORC_MATERN32 = 3, ORC_LAPLACE = 4, ORC_BUMP = 5 };
+enum { ORC_COULOMB = 1, ORC_GAUSSIAN = 2, ORC_MATERN32 = 3, ORC_LAPLACE = 4, ORC_BUMP = 5, ORC_COSDOT = 6 };
 
 static double sqdist(const double* x, const double* y, int d) {
   double s = 0.0;
@@ -120,6 +120,11 @@ static double kernel_of_s(int kid, double p, double s) {
 }
 
 double orc_kernel(int kid, double p, const double* x, const double* y, int d) {
+  if (kid == ORC_COSDOT) { /* kappa_3 of Table 1: cos(x . y), the dot summed in k order */
+    double t = 0.0;
+    for (int k = 0; k < d; k++) t = t + x[k] * y[k];
+    return cos(t);
+  }
   return kernel_of_s(kid, p, sqdist(x, y, d));
 }
 

@@ -156,12 +156,12 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
     set_error(H2_ERR_INVALID_ARG, "invalid argument (n, d, leaf_size, admissibility, id_tol or options)");
     return nullptr;
   }
-  if (kernel_id < H2_KERNEL_COULOMB || kernel_id > H2_KERNEL_BUMP) {
+  if (kernel_id < H2_KERNEL_COULOMB || kernel_id > H2_KERNEL_COSDOT) {
     set_error(H2_ERR_UNKNOWN_KERNEL, "unknown kernel_id");
     return nullptr;
   }
   double kp = 0.0;
-  if (kernel_id != H2_KERNEL_COULOMB && kernel_id != H2_KERNEL_BUMP) {
+  if (kernel_id != H2_KERNEL_COULOMB && kernel_id != H2_KERNEL_BUMP && kernel_id != H2_KERNEL_COSDOT) {
     if (!kernel_params || !(kernel_params[0] > 0.0) || !std::isfinite(kernel_params[0])) {
       set_error(H2_ERR_INVALID_ARG, "kernel parameter (h or l) must be finite and > 0");
       return nullptr;

@@ -37,6 +37,22 @@ __device__ __forceinline__ unsigned long long splitmix_at(unsigned long long see
   return z ^ (z >> 31);
 }
 
+// kappa(x, y) for two point-major points of a trial
+template <int D>
+__device__ __forceinline__ double calib_kernel(int kid, double p2, const double* x, const double* y) {
+  if (kid == H2_KERNEL_COSDOT) {
+    double t = 0.0;
+    for (int c = 0; c < D; c++) t = fma(x[c], y[c], t);
+    return kernel_cosdot(t);
+  }
+  double s = 0.0;
+  for (int c = 0; c < D; c++) {
+    const double df = x[c] - y[c];
+    s = fma(df, df, s);
+  }
+  return kernel_s(kid, p2, s);
+}
+
 struct PtAcc {
   const double* Z;
   int d;
@@ -83,12 +99,7 @@ __global__ void __launch_bounds__(kCalThreads) calib_prep_kernel(int kid, double
   // M = K(Z1, Z2*)^T : ns x N column-major (columns = Z1 candidates)
   for (int e = tid; e < ns * N; e += kCalThreads) {
     int a = e % ns, b = e / ns;
-    double s = 0.0;
-    for (int c = 0; c < D; c++) {
-      double df = W.Z1[b * D + c] - W.Z2[W.sel[a] * D + c];
-      s = fma(df, df, s);
-    }
-    W.M[e] = kernel_s(kid, p2, s);
+    W.M[e] = calib_kernel<D>(kid, p2, W.Z1 + b * D, W.Z2 + W.sel[a] * D);
   }
 }
 
@@ -108,12 +119,7 @@ __global__ void __launch_bounds__(kCalThreads) calib_ks_kernel(int kid, double p
   const int k = W.k;
   for (int x = threadIdx.x; x < k * N; x += kCalThreads) {
     const int t = x / N, e = x % N;
-    double s = 0.0;
-    for (int c = 0; c < D; c++) {
-      const double df = W.Z1[W.piv[t] * D + c] - W.Z2[e * D + c];
-      s = fma(df, df, s);
-    }
-    W.Ks[x] = kernel_s(kid, p2, s);
+    W.Ks[x] = calib_kernel<D>(kid, p2, W.Z1 + W.piv[t] * D, W.Z2 + e * D);
   }
 }
 
@@ -139,12 +145,7 @@ __global__ void __launch_bounds__(kCalThreads) calib_err_kernel(int kid, double 
 #pragma unroll
     for (int u = 0; u < EPL; u++) {
       const int e = lane + 32 * u;
-      double s = 0.0;
-      for (int c = 0; c < D; c++) {
-        const double df = W.Z1[row * D + c] - W.Z2[e * D + c];
-        s = fma(df, df, s);
-      }
-      kv[j][u] = kernel_s(kid, p2, s);
+      kv[j][u] = calib_kernel<D>(kid, p2, W.Z1 + row * D, W.Z2 + e * D);
       den += kv[j][u] * kv[j][u];
     }
   }

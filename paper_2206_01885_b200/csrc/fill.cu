@@ -133,13 +133,20 @@ __device__ __forceinline__ void nf_unit_rows(const double* __restrict__ xr, int6
     double v[NS];
 #pragma unroll
     for (int s = 0; s < NS; s++) {
-      double sq = kFillBias;
+      if constexpr (KID == H2_KERNEL_COSDOT) {  // cos(x . y) on unscaled coordinates (cs = 1)
+        double dt = 0.0;
 #pragma unroll
-      for (int c = 0; c < D; c++) {
-        const double df = xa[c] - xb[s][c];
-        sq = fma(df, df, sq);
+        for (int c = 0; c < D; c++) dt = fma(xa[c], xb[s][c], dt);
+        v[s] = kernel_cosdot(dt);
+      } else {
+        double sq = kFillBias;
+#pragma unroll
+        for (int c = 0; c < D; c++) {
+          const double df = xa[c] - xb[s][c];
+          sq = fma(df, df, sq);
+        }
+        v[s] = kernel_fill<KID, CL>(sq, tab);
       }
-      v[s] = kernel_fill<KID, CL>(sq, tab);
     }
 #pragma unroll
     for (int s = 0; s < NS; s++)  // slots before the last are full (see nslot)
@@ -272,13 +279,20 @@ __global__ void __launch_bounds__(kFillThreads) cp_fill_kernel(int64_t np, const
       if (e >= total) continue;
       const int loc = e - pre_q, row = loc / kj_q, col = loc - row * kj_q;
       const int a = sk[(int64_t)i_q * r + row], b = sk[(int64_t)j_q * r + col];
-      double sq = kFillBias;
+      if constexpr (KID == H2_KERNEL_COSDOT) {
+        double dt = 0.0;
 #pragma unroll
-      for (int c = 0; c < D; c++) {
-        const double df = X[c * n + a] * cs - X[c * n + b] * cs;
-        sq = fma(df, df, sq);
+        for (int c = 0; c < D; c++) dt = fma(X[c * n + a], X[c * n + b], dt);
+        __stcs(o + e, kernel_cosdot(dt));
+      } else {
+        double sq = kFillBias;
+#pragma unroll
+        for (int c = 0; c < D; c++) {
+          const double df = X[c * n + a] * cs - X[c * n + b] * cs;
+          sq = fma(df, df, sq);
+        }
+        __stcs(o + e, kernel_fill<KID, true>(sq, tab));
       }
-      __stcs(o + e, kernel_fill<KID, true>(sq, tab));
     }
   }
 }
@@ -386,8 +400,11 @@ static void launch_fill(const h2_handle* h, cudaStream_t s, int mode, int64_t nw
     case H2_KERNEL_LAPLACE:
       launch_fill_kid<H2_KERNEL_LAPLACE>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out, ctl);
       break;
-    default:
+    case H2_KERNEL_BUMP:
       launch_fill_kid<H2_KERNEL_BUMP>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out, ctl);
+      break;
+    default:
+      launch_fill_kid<H2_KERNEL_COSDOT>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out, ctl);
       break;
   }
 }

@@ -224,13 +224,14 @@ __global__ void __launch_bounds__(NT) id_kernel_smem(
 #pragma unroll
       for (int c = 0; c < D; c++) xr[c] = coord_x(c, b);
       for (int a = 0; a < ny; a++) {
-        double sq = 0.0;
+        double sq = 0.0, dt = 0.0;
 #pragma unroll
         for (int c = 0; c < D; c++) {
-          const double df = xr[c] - coord_y(c, a);
+          const double yc = coord_y(c, a), df = xr[c] - yc;
           sq = fma(df, df, sq);
+          dt = fma(xr[c], yc, dt);
         }
-        M[a * nx + b] = kernel_s(kid, p2, sq, tab);
+        M[a * nx + b] = kid == H2_KERNEL_COSDOT ? kernel_cosdot(dt) : kernel_s(kid, p2, sq, tab);
       }
     }
     __syncthreads();
@@ -240,13 +241,14 @@ __global__ void __launch_bounds__(NT) id_kernel_smem(
     // warp-per-column CPQR of cpqr.cuh on shared memory
     for (int e = tid; e < ny * nx; e += NT) {
       const int a = e % ny, b = e / ny;
-      double sq = 0.0;
+      double sq = 0.0, dt = 0.0;
 #pragma unroll
       for (int c = 0; c < D; c++) {
-        const double df = coord_x(c, b) - coord_y(c, a);
+        const double xc = coord_x(c, b), yc = coord_y(c, a), df = xc - yc;
         sq = fma(df, df, sq);
+        dt = fma(xc, yc, dt);
       }
-      M[e] = kernel_s(kid, p2, sq, tab);
+      M[e] = kid == H2_KERNEL_COSDOT ? kernel_cosdot(dt) : kernel_s(kid, p2, sq, tab);
     }
     __syncthreads();
     k = cta_cpqr<NT>(M, ny, nx, tol, piv, nrm2, v, csm_cm);

@@ -25,6 +25,7 @@ KERNEL_GAUSSIAN = 2
 KERNEL_MATERN32 = 3
 KERNEL_LAPLACE = 4
 KERNEL_BUMP = 5
+KERNEL_COSDOT = 6  # Table 1 kappa_3 = cos(x . y)
 
 # (n, d, kernel_id, kernel_params, leaf_size, id_tol, tau, name)
 CONFIGS = {

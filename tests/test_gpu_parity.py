@@ -149,10 +149,11 @@ def test_stored_blocks_sampled_against_kernel(cfg, n):
 
 
 @pytest.mark.parametrize("kid,kp,cfg,n", [(4, [0.3], 1, 8192), (4, [0.05], 4, 40000), (5, [], 1, 8192),
-                                         (5, [], 3, 20000)])
+                                         (5, [], 3, 20000), (6, [], 1, 8192), (6, [], 3, 20000)])
 def test_parity_laplace_and_bump(kid, kp, cfg, n):
-    """The Laplace kernel e^{-r/l} and Table 1's kappa_4 bump through the whole path:
-    bit-exact structure and r, matvec error within 2x of the oracle's, stored entries = kernel."""
+    """The Laplace kernel e^{-r/l} and Table 1's kappa_4 bump and kappa_3 = cos(x . y)
+     through the whole path: bit-exact structure and r, matvec error within 2x of the
+    oracle's, stored entries = kernel."""
     c = synth.CONFIGS[cfg]
     pts = synth.points(cfg, n)
     o, r = oracle_build(pts, kid, kp, 1e-6, c["q"], c["tau"])

@@ -25,6 +25,7 @@ INDEX_SETS = ["PERM", "NODES", "IL_OFF", "IL_IDX", "NF_OFF", "NF_IDX", "XS_OFF",
     (1, 8192, 2, [0.5], 1e-6),      # Coulomb geometry -> Gaussian
     (4, 60000, 2, [0.05], 1e-6),    # Matern geometry -> Gaussian
     (3, 30000, 3, [0.3], 1e-5),     # Gaussian geometry -> Matern, another tolerance
+    (3, 30000, 6, [], 1e-6),        # Gaussian geometry -> Table 1 kappa_3 = cos(x . y)
 ])
 def test_rebuild_equals_fresh_build_at_base_r(cfg, n, new_kid, new_kp, new_tol):
     c = synth.CONFIGS[cfg]
@@ -48,9 +49,9 @@ def test_rebuild_equals_fresh_build_at_base_r(cfg, n, new_kid, new_kp, new_tol):
     assert torch.isfinite(yb0).all()
     # oracle at the same r: the paper's "HiDR once for all" accuracy
     o = oracle.OracleH2(pts, c["q"], c["tau"])
-    o.build(new_kid, new_kp[0], new_tol, r)
+    o.build(new_kid, new_kp[0] if new_kp else 0.0, new_tol, r)
     rows = synth.sample_rows(cfg, n)
-    yd = oracle.dense_rows(pts, new_kid, new_kp[0], synth.matvec_vector(cfg, n), rows)
+    yd = oracle.dense_rows(pts, new_kid, new_kp[0] if new_kp else 0.0, synth.matvec_vector(cfg, n), rows)
     yo = o.matvec(synth.matvec_vector(cfg, n), None if n <= 16384 else rows)
     yo = yo[rows] if n <= 16384 else yo
     yg = ya.cpu().numpy()[rows]

@@ -181,7 +181,23 @@ def test_kernel_closed_forms_laplace_and_bump(orc):
     assert 0.0 < orc.kernel(Bu, 0.0, [0.0], [np.sqrt(10.0) * 0.999]) < 1e-80
 
 
-@pytest.mark.parametrize("kid,param,tol", [(synth.KERNEL_LAPLACE, 0.3, 1e-6), (synth.KERNEL_BUMP, 0.0, 1e-6)])
+def test_kernel_closed_forms_cosdot(orc):
+    """Table 1 kappa_3 = cos(x . y): orthogonal points give 1, x . y = pi/3 gives 1/2,
+    x . y = pi gives -1; symmetric, and not a function of |x - y| (two pairs at the same distance
+    with different dot products)."""
+    K3 = synth.KERNEL_COSDOT
+    assert orc.kernel(K3, 0.0, [1.0, 0.0, 0.0], [0.0, 1.0, 0.0]) == 1.0
+    assert orc.kernel(K3, 0.0, [1.0, 0.0], [np.pi / 3, 5.0]) == pytest.approx(0.5, rel=1e-15)
+    assert orc.kernel(K3, 0.0, [2.0, 1.0], [np.pi / 2, 0.0]) == pytest.approx(-1.0, rel=1e-15)
+    x, y = [0.3, -0.7, 0.2], [1.1, 0.4, -0.5]
+    assert orc.kernel(K3, 0.0, x, y) == orc.kernel(K3, 0.0, y, x)
+    a = orc.kernel(K3, 0.0, [0.0, 0.0], [1.0, 0.0])   # |x - y| = 1, x . y = 0
+    b = orc.kernel(K3, 0.0, [1.0, 0.0], [2.0, 0.0])   # |x - y| = 1, x . y = 2
+    assert a == 1.0 and b == pytest.approx(np.cos(2.0), rel=1e-15)
+
+
+@pytest.mark.parametrize("kid,param,tol", [(synth.KERNEL_LAPLACE, 0.3, 1e-6), (synth.KERNEL_BUMP, 0.0, 1e-6),
+                                           (synth.KERNEL_COSDOT, 0.0, 1e-6)])
 def test_new_kernels_full_pipeline_small(orc, kid, param, tol):
     """The pipeline on the two added kernels: the error falls with id_tol (BASELINE north_star pin)."""
     pts = synth.points(1, 3000)
