@@ -6,6 +6,10 @@
 //   CPQR ID of A^T (cpqr.cuh) -> k_i, X^_i = Xbar_i[piv[0:k]], U_i = P [I; T^T] (|Xbar| x k);
 //   for a parent, the rows of U_i belonging to child c are the transfer matrix R_c.
 // Symmetric kernels: V = U, W = R (reading F6).
+#include <cooperative_groups.h>
+
+#include <cstdlib>
+
 #include "cpqr.cuh"
 
 namespace h2 {
@@ -58,12 +62,22 @@ __host__ __device__ __forceinline__ int id_smem_class(int ny, int nx, int d) {
   return id_smem_bytes_lean(ny, nx) <= kIdLeanMax ? kIdLean : -1;
 }
 
+// The largest blocks (>= kIdClusterMin entries) take the cluster path (id_kernel_cluster): on one
+// SM the global-memory CPQR of such a block is bound by that SM's L2 / HBM bandwidth (tens of ms for
+// the biggest blocks of configs[4]), so a thread-block cluster of CS CTAs spreads its columns over CS
+// SMs.  cs = the cluster size the device runs (16, else 8; 0 disables the path); cl_min = the
+// block-entry threshold.
+constexpr int kIdClThreads = 512;
+__host__ __device__ __forceinline__ bool id_big(int ny, int nx, int d, int cs, int64_t cl_min) {
+  return cs >= 2 && nx >= 4 * cs && (int64_t)ny * nx >= cl_min && id_smem_class(ny, nx, d) < 0;
+}
+
 // per node of one level: |Xbar| (and child offsets), workspace and U sizes
 __global__ void id_sizes_kernel(int base, int count, int d, const int* __restrict__ is_leaf, const int* __restrict__ nbegin,
                                 const int* __restrict__ nend, const int* __restrict__ first_child,
                                 const int* __restrict__ nchild, const int* __restrict__ ys_cnt,
                                 const int* __restrict__ k, int* xbar_n, int* child_off, int64_t* wsz, int64_t* usz,
-                                int* smax) {
+                                int* smax, int cs, int64_t cl_min, int* cl_cnt, int* cl_list) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t > count) return;
   if (t == count) {
@@ -88,7 +102,14 @@ __global__ void id_sizes_kernel(int base, int count, int d, const int* __restric
   int mn = nx < ny ? nx : ny;
   // workspace: M (ny*nx doubles) + nrm2 (nx) + v (ny) + piv/xbar (2*nx ints, as doubles)
   const int cls = id_smem_class(ny, nx, d);
-  wsz[t] = nx > 0 && cls < 0 ? (int64_t)ny * nx + nx + ny + nx + 2 : 0;
+  const bool big = nx > 0 && id_big(ny, nx, d, cs, cl_min);
+  if (big) {
+    cl_list[atomicAdd(cl_cnt, 1)] = t;
+    atomicMax(smax + kIdClasses + 1, nx);  // the cluster kernel's shared memory is sized by it
+  }
+  // cluster path: M (column slices) + the staged candidate columns (2 parities x CS x ny)
+  wsz[t] = big ? (int64_t)ny * (((nx + cs - 1) / cs) * cs) + 2LL * cs * ny
+         : nx > 0 && cls < 0 ? (int64_t)ny * nx + nx + ny + nx + 2 : 0;
   usz[t] = (int64_t)nx * mn;
   if (nx > 0 && cls >= 0)
     atomicMax(smax + cls, (int)(cls == kIdLean ? id_smem_bytes_lean(ny, nx) : id_smem_bytes(ny, nx, d)));
@@ -100,7 +121,8 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
     const int* __restrict__ is_leaf, const int* __restrict__ nbegin, const int* __restrict__ first_child,
     const int* __restrict__ nchild, const int* __restrict__ ys_cnt, const int* __restrict__ ys,
     const int* __restrict__ xbar_n, const int64_t* __restrict__ woff, double* work, const int64_t* __restrict__ uoff,
-    double* U, int* kout, int* sk, unsigned long long* evals, int64_t min_block, int64_t max_block) {
+    double* U, int* kout, int* sk, unsigned long long* evals, int64_t min_block, int64_t max_block, int cs,
+    int64_t cl_min) {
   __shared__ CpqrSmem<kIdThreads> csm;
   // the Householder vector in shared memory for the big-block variant (ny <= r <= 4096, the budget
   // cap); the 256-thread variant keeps it in its global workspace (more CTAs per SM)
@@ -114,7 +136,7 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
     if (tid == 0) kout[i] = 0;
     return;
   }
-  if (id_smem_class(ny, nx, d) >= 0) return;  // handled by id_kernel_smem
+  if (id_smem_class(ny, nx, d) >= 0 || id_big(ny, nx, d, cs, cl_min)) return;  // id_kernel_smem / _cluster
   const int64_t blk = 8LL * nx * ny;
   if (blk < min_block || blk >= max_block) return;  // the other thread-count variant
   double* M = work + woff[t];
@@ -156,6 +178,272 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
     kout[i] = k;
     atomicAdd(evals, (unsigned long long)nx * ny);
   }
+}
+
+// Cluster path (id_big): a thread-block cluster of CS CTAs per node; CTA q owns the columns
+// [q w, q w + w), w = ceil(nx / CS), of A^T in the node's global workspace (column-major, ld = ny).
+// Columns never move: the pivot order lives in a position map replicated in every CTA (col_at) and
+// in each CTA's `pos` of its own columns.  One cluster barrier per pivot step: after it every CTA
+// reads the CTAs' candidates (largest residual norm, ties to the lowest position; DSMEM) and picks
+// the same pivot p; it reads column p from the owner's staged copy (global, double-buffered by step
+// parity, written before the barrier: L2 serves the CS readers), builds the Householder vector and
+// v^T v itself (the same arithmetic in every CTA), applies it to its own live columns, recomputes
+// their residual norms and stages its next candidate.  The pivot column is not written in that
+// phase (others read its staged copy); its diagonal alpha is stored after the next barrier, its rows
+// below the diagonal are never read again.  The algorithm and tie rule of cta_cpqr.
+struct IdClCand {
+  double x;  // sqrt of the residual norm^2 (-1: no live column)
+  int pos;   // position in the pivot order
+  int j;     // column index in Xbar
+};
+
+__global__ void __launch_bounds__(kIdClThreads) id_kernel_cluster(
+    int base, const int* __restrict__ list, int kid, double p2, double tol, const double* __restrict__ X, int64_t n,
+    int d, int r, const int* __restrict__ is_leaf, const int* __restrict__ nbegin,
+    const int* __restrict__ first_child, const int* __restrict__ nchild, const int* __restrict__ ys_cnt,
+    const int* __restrict__ ys, const int* __restrict__ xbar_n, const int64_t* __restrict__ woff, double* work,
+    const int64_t* __restrict__ uoff, double* U, int* kout, int* sk, unsigned long long* evals) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  constexpr int NT = kIdClThreads, NW = NT / 32;
+  const int CS = (int)cl.num_blocks(), q = (int)cl.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t = list[blockIdx.x / CS];
+  const int i = base + t;
+  const int nx = xbar_n[i], ny = ys_cnt[i];
+  const int w = (nx + CS - 1) / CS, j0 = q * w;
+  const int wl = nx - j0 < 0 ? 0 : (nx - j0 < w ? nx - j0 : w);  // live width of this CTA's slice
+  extern __shared__ double sh[];
+  double* v = sh;                       // Householder vector (ny)
+  double* nrm2 = v + ny;                // residual norms^2 of the own columns (w)
+  double* tab = nrm2 + w;               // exp table (64)
+  int* col_at = reinterpret_cast<int*>(tab + 64);  // position -> column (nx)
+  int* xb = col_at + nx;                // Xbar (nx)
+  int* pos = xb + nx;                   // own column -> position (w)
+  __shared__ IdClCand cand[2];          // this CTA's candidate by step parity (read by every CTA)
+  __shared__ IdClCand best_s;
+  __shared__ CpqrSmem<NT> csm;
+  double* const Mall = work + woff[t];
+  double* const Mq = Mall + (int64_t)q * w * ny;
+  double* const stage = Mall + (int64_t)CS * w * ny;  // [parity][CTA][ny]
+  auto staged = [&](int parity, int cta) { return stage + ((int64_t)parity * CS + cta) * ny; };
+  if (tid < 64) tab[tid] = kExp2Tab64[tid];
+  if (is_leaf[i]) {
+    for (int b = tid; b < nx; b += NT) xb[b] = nbegin[i] + b;
+  } else {
+    int o = 0;
+    for (int c = 0; c < nchild[i]; c++) {
+      const int ch = first_child[i] + c;
+      const int kc = kout[ch];
+      for (int a = tid; a < kc; a += NT) xb[o + a] = sk[(int64_t)ch * r + a];
+      o += kc;
+    }
+  }
+  for (int b = tid; b < nx; b += NT) col_at[b] = b;
+  for (int b = tid; b < w; b += NT) pos[b] = j0 + b;
+  __syncthreads();
+  // own columns of A^T: Mq[a + ny*jl] = K(Xbar[j0 + jl], Y^*[a])
+  const int* yv = ys + (int64_t)i * r;
+  for (int64_t e = tid; e < (int64_t)wl * ny; e += NT) {
+    const int a = (int)(e % ny), jl = (int)(e / ny);
+    Mq[e] = kernel_pts_d(kid, p2, X, n, d, xb[j0 + jl], yv[a]);
+  }
+  __syncthreads();
+  for (int jl = warp; jl < wl; jl += NW) {
+    const double* col = Mq + (int64_t)ny * jl;
+    double s = 0.0;
+    for (int a = lane; a < ny; a += 32) s += col[a] * col[a];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) nrm2[jl] = s;
+  }
+  __syncthreads();
+  // the candidate among the own live columns (position >= tt), published in shared memory, its
+  // column (rows tt..) staged in global memory
+  auto publish = [&](int tt) {
+    if (warp == 0) {
+      double bx = -1.0;
+      int bp = INT_MAX, bj = -1;
+      for (int jl = lane; jl < wl; jl += 32) {
+        const int ps = pos[jl];
+        if (ps < tt) continue;
+        const double x = sqrt(nrm2[jl]);
+        if (x > bx || (x == bx && ps < bp)) {
+          bx = x;
+          bp = ps;
+          bj = j0 + jl;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double x2 = __shfl_xor_sync(0xffffffffu, bx, o);
+        const int p2_ = __shfl_xor_sync(0xffffffffu, bp, o);
+        const int j2 = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (x2 > bx || (x2 == bx && p2_ < bp)) {
+          bx = x2;
+          bp = p2_;
+          bj = j2;
+        }
+      }
+      if (lane == 0) best_s = cand[tt & 1] = IdClCand{bx, bp, bj};
+    }
+    __syncthreads();
+    const int bj = best_s.j;
+    if (bj >= 0) {
+      const double* col = Mq + (int64_t)ny * (bj - j0);
+      double* dst = staged(tt & 1, q);
+      for (int a = tt + tid; a < ny; a += NT) dst[a] = col[a];
+    }
+  };
+  publish(0);
+  const int kmax = ny < nx ? ny : nx;
+  double r11 = 0.0;
+  int k = 0;
+  int pend_jl = -1, pend_row = 0;  // own pivot column whose diagonal is written after the barrier
+  double pend_alpha = 0.0;
+  for (int tt = 0; tt < kmax; tt++) {
+    cl.sync();
+    if (pend_jl >= 0 && tid == 0) Mq[(int64_t)ny * pend_jl + pend_row] = pend_alpha;
+    pend_jl = -1;
+    if (warp == 0) {  // the pivot: the best of the CTAs' candidates
+      IdClCand c{-1.0, INT_MAX, -1};
+      if (lane < CS) c = *cl.map_shared_rank(&cand[tt & 1], lane);
+      for (int o = 16; o > 0; o >>= 1) {
+        const double x2 = __shfl_xor_sync(0xffffffffu, c.x, o);
+        const int p2_ = __shfl_xor_sync(0xffffffffu, c.pos, o);
+        const int j2 = __shfl_xor_sync(0xffffffffu, c.j, o);
+        if (x2 > c.x || (x2 == c.x && p2_ < c.pos)) c = IdClCand{x2, p2_, j2};
+      }
+      if (lane == 0) best_s = c;
+    }
+    __syncthreads();
+    const IdClCand b = best_s;
+    const double nrm = b.x;
+    if (tt == 0) {
+      r11 = nrm;
+      if (r11 == 0.0) break;
+    }
+    if (nrm < tol * r11) break;
+    const int p = b.j, owner = p / w;
+    // the Householder vector of column p (rows tt..) from the owner's staged copy
+    const double* src = staged(tt & 1, owner);
+    const double x0 = src[tt];
+    const double alpha = x0 >= 0.0 ? -nrm : nrm;
+    double part = 0.0;
+    for (int a = tt + tid; a < ny; a += NT) {
+      const double vi = a == tt ? x0 - alpha : src[a];
+      v[a] = vi;
+      part += vi * vi;
+    }
+    const double vtv = cta_sum<NT>(part, csm);  // its barriers publish v
+    if (q == owner) {
+      pend_jl = p - j0;
+      pend_row = tt;
+      pend_alpha = alpha;
+    }
+    if (tid == 0) {  // position map: the column at position tt moves to the pivot's position
+      const int jt = col_at[tt];
+      col_at[b.pos] = jt;
+      col_at[tt] = p;
+      if (jt >= j0 && jt < j0 + wl) pos[jt - j0] = b.pos;
+      if (p >= j0 && p < j0 + wl) pos[p - j0] = tt;
+    }
+    __syncthreads();
+    // own live columns (positions > tt): reflector, residual norm over rows > tt
+    for (int jl = warp; jl < wl; jl += NW) {
+      if (pos[jl] <= tt) continue;
+      double* col = Mq + (int64_t)ny * jl;
+      if (vtv > 0.0) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int a = tt + lane;
+        for (; a + 96 < ny; a += 128) {
+          const double c0 = col[a], c1 = col[a + 32], c2 = col[a + 64], c3 = col[a + 96];
+          s0 += v[a] * c0;
+          s1 += v[a + 32] * c1;
+          s2 += v[a + 64] * c2;
+          s3 += v[a + 96] * c3;
+        }
+        for (; a < ny; a += 32) s0 += v[a] * col[a];
+        double s = (s0 + s1) + (s2 + s3);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const double f = 2.0 * s / vtv;
+        double n0 = 0.0, n1 = 0.0, n2 = 0.0, n3 = 0.0;
+        a = tt + lane;
+        for (; a + 96 < ny; a += 128) {
+          const double a0 = col[a] - f * v[a], a1 = col[a + 32] - f * v[a + 32];
+          const double a2 = col[a + 64] - f * v[a + 64], a3 = col[a + 96] - f * v[a + 96];
+          col[a] = a0;
+          col[a + 32] = a1;
+          col[a + 64] = a2;
+          col[a + 96] = a3;
+          if (a > tt) n0 += a0 * a0;
+          n1 += a1 * a1;
+          n2 += a2 * a2;
+          n3 += a3 * a3;
+        }
+        for (; a < ny; a += 32) {
+          const double x = col[a] - f * v[a];
+          col[a] = x;
+          if (a > tt) n0 += x * x;
+        }
+        double nn = (n0 + n1) + (n2 + n3);
+        for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+        if (lane == 0) nrm2[jl] = nn;
+      } else {
+        double nn = 0.0;
+        for (int a = tt + 1 + lane; a < ny; a += 32) nn += col[a] * col[a];
+        for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+        if (lane == 0) nrm2[jl] = nn;
+      }
+    }
+    k = tt + 1;
+    __syncthreads();
+    publish(tt + 1);
+  }
+  if (pend_jl >= 0 && tid == 0) Mq[(int64_t)ny * pend_jl + pend_row] = pend_alpha;
+  cl.sync();  // every R column final and visible (global memory, cluster scope)
+  // T = R11^{-1} R12 on the own live columns (positions >= k), R11 read from its owners' slices
+  // through a pointer table (in v's space: k <= ny); four partial sums per row
+  const double** rcol = reinterpret_cast<const double**>(v);
+  for (int l = tid; l < k; l += NT) {
+    const int jj = col_at[l];
+    rcol[l] = Mall + (int64_t)ny * jj;  // slice q' starts at q' w ny: column jj is at jj * ny
+  }
+  __syncthreads();
+  for (int jl = tid; jl < wl; jl += NT) {
+    if (pos[jl] < k) continue;
+    double* col = Mq + (int64_t)ny * jl;
+    for (int a = k - 1; a >= 0; a--) {
+      double s0 = col[a], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int l = a + 1;
+      for (; l + 3 < k; l += 4) {
+        s0 -= rcol[l][a] * col[l];
+        s1 -= rcol[l + 1][a] * col[l + 1];
+        s2 -= rcol[l + 2][a] * col[l + 2];
+        s3 -= rcol[l + 3][a] * col[l + 3];
+      }
+      for (; l < k; l++) s0 -= rcol[l][a] * col[l];
+      col[a] = ((s0 + s1) + (s2 + s3)) / rcol[a][a];
+    }
+  }
+  __syncthreads();
+  // outputs: skeleton (pivot order), U (nx x k column-major): identity rows of the skeleton, T for
+  // the others
+  double* Ui = U + uoff[t];
+  if (q == 0) {
+    for (int a = tid; a < k; a += NT) sk[(int64_t)i * r + a] = xb[col_at[a]];
+    for (int e = tid; e < k * k; e += NT) {
+      const int a = e % k, tt = e / k;
+      Ui[col_at[a] + (int64_t)nx * tt] = a == tt ? 1.0 : 0.0;
+    }
+  }
+  for (int e = tid; e < wl * k; e += NT) {
+    const int jl = e % wl, tt = e / wl;
+    if (pos[jl] >= k) Ui[j0 + jl + (int64_t)nx * tt] = Mq[(int64_t)ny * jl + tt];
+  }
+  if (q == 0 && tid == 0) {
+    kout[i] = k;
+    atomicAdd(evals, (unsigned long long)nx * ny);
+  }
+  cl.sync();  // no CTA leaves while another may still read its shared memory
 }
 
 // shared-memory path: the whole block and the CPQR live in shared memory (cpqr.cuh, row-major).
@@ -277,8 +565,54 @@ __global__ void kmax_kernel(int nnodes, const int* __restrict__ k, int* out) {
   if (i < nnodes) atomicMax(out, k[i]);
 }
 
+// dynamic shared memory of the cluster kernel: v (ny <= r) + nrm2 (w) + exp table doubles; col_at,
+// Xbar (nx) + pos (w) ints -- sized for the level's largest |Xbar|
+static size_t id_cl_smem(int r, int nx_max) {
+  return sizeof(double) * ((size_t)r + (size_t)nx_max + 64) + sizeof(int) * (3 * (size_t)nx_max) + 64;
+}
+
+// the largest cluster size the device schedules for the cluster kernel (16 needs the non-portable
+// opt-in), queried once; H2_ID_CLUSTER=0 disables the path (diagnostics)
+static int id_cluster_max() {
+  static int cs = -1;
+  if (cs >= 0) return cs;
+  const char* env = getenv("H2_ID_CLUSTER");
+  if (env && atoi(env) == 0) return cs = 0;
+  int best = 0;
+  for (int c : {16, 8}) {
+    if (c == 16 && cudaFuncSetAttribute(id_kernel_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                       cudaSuccess)
+      continue;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(c);
+    cfg.blockDim = dim3(kIdClThreads);
+    cfg.dynamicSmemBytes = 96 * 1024;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, id_kernel_cluster, &cfg) == cudaSuccess && nc > 0) {
+      best = c;
+      break;
+    }
+  }
+  cudaGetLastError();
+  return cs = best;
+}
+
 void id_sweep(h2_handle* h) {
   cudaStream_t s = h->stream;
+  H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  const int cs = id_cluster_max();
+  static const int64_t cl_min = [] {  // H2_ID_CLMIN (tuning knob): cluster-path threshold, block entries
+    const char* e = getenv("H2_ID_CLMIN");
+    return e ? (int64_t)atoll(e) : (int64_t)256 * 1024;
+  }();
   const int nn = h->nnodes;
   h->k = halloc<int>(h, nn);
   h->sk = halloc<int>(h, (size_t)nn * h->r);
@@ -304,22 +638,29 @@ void id_sweep(h2_handle* h) {
     const LevelRange lr = level_range(h, l);
     int base = lr.begin, count = lr.end - lr.begin;
     if (count == 0) continue;
-    Scratch sz(sizeof(int64_t) * 2 * (count + 1) + 4 * (kIdClasses + 1), s), off(sizeof(int64_t) * 2 * (count + 1), s);
-    int* smax = reinterpret_cast<int*>(sz.as<int64_t>() + 2 * (count + 1));  // one max per class (+ lean)
-    H2_CUDA_TRY(cudaMemsetAsync(smax, 0, (kIdClasses + 1) * sizeof(int), s));
+    Scratch sz(sizeof(int64_t) * 2 * (count + 1) + 4 * (kIdClasses + 2), s), off(sizeof(int64_t) * 2 * (count + 1), s);
+    // one max per class (+ lean), then the largest |Xbar| of the cluster-path nodes
+    int* smax = reinterpret_cast<int*>(sz.as<int64_t>() + 2 * (count + 1));
+    H2_CUDA_TRY(cudaMemsetAsync(smax, 0, (kIdClasses + 2) * sizeof(int), s));
     int64_t *wsz = sz.as<int64_t>(), *usz = wsz + count + 1;
     int64_t *woff = off.as<int64_t>(), *uo = woff + count + 1;
+    Scratch clw(sizeof(int) * (1 + (size_t)count), s);  // cluster-path node count + list
+    int* cl_cnt = clw.as<int>();
+    int* cl_list = cl_cnt + 1;
+    H2_CUDA_TRY(cudaMemsetAsync(cl_cnt, 0, sizeof(int), s));
     id_sizes_kernel<<<(count + 1 + 255) / 256, 256, 0, s>>>(base, count, h->d, h->is_leaf, h->nbegin, h->nend,
                                                             h->first_child, h->nchild, h->ys_cnt, h->k, h->xbar_n,
-                                                            h->child_off, wsz, usz, smax);
+                                                            h->child_off, wsz, usz, smax, cs, cl_min, cl_cnt, cl_list);
     scan_excl_i64(wsz, woff, count + 1, s);
     scan_excl_i64(usz, uo, count + 1, s);
     H2_CHECK_LAUNCH();
     int64_t tot[2];
-    int smem_bytes[kIdClasses + 1] = {0};
+    int smem_bytes[kIdClasses + 2] = {0};
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[0], woff + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[1], uo + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    H2_CUDA_TRY(cudaMemcpyAsync(smem_bytes, smax, (kIdClasses + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+    H2_CUDA_TRY(cudaMemcpyAsync(smem_bytes, smax, (kIdClasses + 2) * sizeof(int), cudaMemcpyDeviceToHost, s));
+    int ncl = 0;
+    H2_CUDA_TRY(cudaMemcpyAsync(&ncl, cl_cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaStreamSynchronize(s));
     if (uused + tot[1] > ucap) {
       int64_t nc = uused + tot[1];
@@ -332,6 +673,38 @@ void id_sweep(h2_handle* h) {
     }
     uoff_scatter_kernel<<<(count + 255) / 256, 256, 0, s>>>(base, count, uo, uused, h->u_off);
     Scratch work(sizeof(double) * (tot[0] > 0 ? tot[0] : 1), s);
+    cudaEvent_t cl_done = nullptr;
+    if (ncl > 0) {  // the largest blocks: one thread-block cluster per node, on its own stream
+      cudaStream_t cst = h->aux[2] ? h->aux[2] : s;
+      cudaEvent_t fork = nullptr;
+      if (cst != s) {
+        H2_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        H2_CUDA_TRY(cudaEventCreateWithFlags(&cl_done, cudaEventDisableTiming));
+        H2_CUDA_TRY(cudaEventRecord(fork, s));
+        H2_CUDA_TRY(cudaStreamWaitEvent(cst, fork, 0));
+        cudaEventDestroy(fork);
+      }
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3((unsigned)(ncl * cs));
+      cfg.blockDim = dim3(kIdClThreads);
+      cfg.dynamicSmemBytes = id_cl_smem(h->r, smem_bytes[kIdClasses + 1]);
+      cfg.stream = cst;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)cs;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      H2_CUDA_TRY(cudaLaunchKernelEx(&cfg, id_kernel_cluster, base, (const int*)cl_list, h->kid, p2, h->id_tol,
+                                     (const double*)h->X, h->n, h->d, h->r, (const int*)h->is_leaf,
+                                     (const int*)h->nbegin, (const int*)h->first_child, (const int*)h->nchild,
+                                     (const int*)h->ys_cnt, (const int*)h->ys, (const int*)h->xbar_n,
+                                     (const int64_t*)woff, work.as<double>(), (const int64_t*)(h->u_off + base), U,
+                                     h->k, h->sk, ev.as<unsigned long long>()));
+      if (cl_done) H2_CUDA_TRY(cudaEventRecord(cl_done, cst));
+      h->gpu_launches += 1;
+    }
     if (tot[0] > 0) {  // some node's block exceeds the shared-memory path: global-memory CPQR
       // the two thread-count variants run concurrently on auxiliary streams (disjoint nodes)
       cudaStream_t sa = h->aux[0] ? h->aux[0] : s, sb = h->aux[1] ? h->aux[1] : s;
@@ -343,11 +716,11 @@ void id_sweep(h2_handle* h) {
       id_kernel<256><<<count, 256, 0, sa>>>(base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf,
                                            h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
                                            work.as<double>(), h->u_off + base, U, h->k, h->sk,
-                                           ev.as<unsigned long long>(), 0, kIdBigBlock);
+                                           ev.as<unsigned long long>(), 0, kIdBigBlock, cs, cl_min);
       id_kernel<1024><<<count, 1024, 0, sb>>>(base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf,
                                              h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
                                              work.as<double>(), h->u_off + base, U, h->k, h->sk,
-                                             ev.as<unsigned long long>(), kIdBigBlock, INT64_MAX);
+                                             ev.as<unsigned long long>(), kIdBigBlock, INT64_MAX, cs, cl_min);
       H2_CHECK_LAUNCH();
       H2_CUDA_TRY(cudaEventRecord(gev[1], sa));
       H2_CUDA_TRY(cudaEventRecord(gev[2], sb));
@@ -425,6 +798,10 @@ void id_sweep(h2_handle* h) {
         H2_CUDA_TRY(cudaStreamWaitEvent(s, lev_ev[a], 0));
       }
       for (auto& e : lev_ev) cudaEventDestroy(e);
+    }
+    if (cl_done) {
+      H2_CUDA_TRY(cudaStreamWaitEvent(s, cl_done, 0));
+      cudaEventDestroy(cl_done);
     }
     h->gpu_launches += 2;
     uused += tot[1];  // u_off[] holds global offsets into the arena

@@ -333,3 +333,44 @@ def test_pruned_down_lattice_ties(d):
     g = gpu_build(pts, 2, [0.3], 1e-5, 8)
     assert g.info()["r"] == r
     assert_structure_equal(g, o)
+
+
+_ID_DUMP = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2206_01885_b200 as P, synth
+cfg, n, out = int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+c = synth.CONFIGS[cfg]
+X = torch.from_numpy(synth.points(cfg, n)).cuda()
+g = P.H2Matrix(X, c["kernel"], list(c["params"]), c["id_tol"], c["q"], c["tau"], storage=P.H2_STORE_ON_THE_FLY,
+               timing=True)
+x = torch.from_numpy(synth.matvec_vector(cfg, n)).cuda()
+np.savez(out, K=g.export("K"), SK_OFF=g.export("SK_OFF"), SK_IDX=g.export("SK_IDX"), U=g.export("U"),
+         y=g.matvec(x).cpu().numpy(), id_ms=g.info()["stage_ms"]["id_sweep"])
+"""
+
+
+@pytest.mark.parametrize("cfg,n", [(5, 262144), (3, 262144)])
+def test_id_cluster_path_equals_single_cta_path(cfg, n, tmp_path):
+    """a8, the largest blocks: the thread-block-cluster CPQR (columns spread over the CTAs of a
+    cluster, position map instead of column swaps) against the single-CTA global-memory CPQR
+    (H2_ID_CLUSTER=0) on the same build: same ranks and skeletons (same pivot rule; only the order
+    of a few fp64 sums differs), U and the matvec to rounding."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mode in ("1", "0"):
+        out = str(tmp_path / f"id{mode}.npz")
+        env = dict(os.environ, H2_ID_CLUSTER=mode)
+        subprocess.run([sys.executable, "-c", _ID_DUMP, root, str(cfg), str(n), out], env=env, check=True,
+                       timeout=600)
+        outs[mode] = np.load(out)
+    a, b = outs["1"], outs["0"]
+    print(f"cfg{cfg}: id_sweep ms cluster {float(a['id_ms']):.2f} single-CTA {float(b['id_ms']):.2f}")
+    same_k = np.mean(a["K"] == b["K"])
+    assert same_k >= 0.999, same_k
+    if np.array_equal(a["K"], b["K"]) and np.array_equal(a["SK_IDX"], b["SK_IDX"]):
+        np.testing.assert_allclose(a["U"], b["U"], rtol=0, atol=1e-9 * max(1.0, np.abs(b["U"]).max()))
+    ya, yb = a["y"], b["y"]
+    assert np.linalg.norm(ya - yb) <= 1e-9 * np.linalg.norm(yb)
