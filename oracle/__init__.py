@@ -61,6 +61,8 @@ def lib():
         L.orc_fill.restype = i64
         L.orc_fill.argtypes = [vp, vp, i64, vp]
         L.orc_vol.argtypes = [vp, i32, vp, i32, i32, vp]
+        L.orc_fps.argtypes = [vp, i32, vp, i32, i32, vp]
+        L.orc_set_reduct.argtypes = [vp, i32]
         L.orc_cpqr.argtypes = [vp, i32, i32, f64, vp]
         L.orc_id.argtypes = [vp, i32, i32, f64, vp, vp]
         L.orc_admissible.argtypes = [vp, i32, vp, i32, i32, f64]
@@ -94,6 +96,15 @@ def vol(X: np.ndarray, S, k: int) -> np.ndarray:
     S = np.ascontiguousarray(S, np.int32)
     out = np.empty(max(1, min(len(S), k)), np.int32)
     c = lib().orc_vol(_p(X), X.shape[1], _p(S), len(S), int(k), _p(out))
+    return out[:c].copy()
+
+
+def fps(X: np.ndarray, S, k: int) -> np.ndarray:
+    """C'. farthest point sampling FPS(S, k) (reading C6) over point-major coordinates X."""
+    X = np.ascontiguousarray(X, np.float64)
+    S = np.ascontiguousarray(S, np.int32)
+    out = np.empty(max(1, min(len(S), k)), np.int32)
+    c = lib().orc_fps(_p(X), X.shape[1], _p(S), len(S), int(k), _p(out))
     return out[:c].copy()
 
 
@@ -151,12 +162,14 @@ def dense_rows(pts: np.ndarray, kid: int, param: float, x: np.ndarray, rows) -> 
 class OracleH2:
     """A (partition) + B (lists) on construction; then calibrate / hidr / id_sweep / matvec."""
 
-    def __init__(self, pts: np.ndarray, q: int, tau: float = 0.5):
+    def __init__(self, pts: np.ndarray, q: int, tau: float = 0.5, reduct: int = 0):
+        """reduct: the DataReduct of HiDR, 0 volume-based (reading C1), 1 farthest point sampling (C6)."""
         self.pts = np.ascontiguousarray(pts, np.float64)
         self.n, self.d = self.pts.shape
         self._h = lib().orc_new(_p(self.pts), self.n, self.d, int(q), float(tau))
         if not self._h:
             raise ValueError("orc_new rejected the arguments")
+        lib().orc_set_reduct(self._h, int(reduct))
         self.q, self.tau = q, tau
         self.kid, self.param = None, 0.0
 

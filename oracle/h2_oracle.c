@@ -182,6 +182,45 @@ int orc_vol(const double* X, int d, const int* S, int ns, int k, int* out) {
   return sort_unique(out, cnt);
 }
 
+/* Farthest point sampling, PAPER §3.3: "S is initialized with one point only. Then FPS
+ * searches for a point in X\S that is farthest from S and adds the point to S ... until S reaches
+ * size k" (reading C6: the first point is the point nearest the centre of the tight bounding box --
+ * Vol(S, 1), the m = 1 case of C2-C4 -- distances as in C4, ties of the farthest point -> lowest
+ * index).  Returns |out| = min(k, |S|), sorted ascending (C5).                                  */
+int orc_fps(const double* X, int d, const int* S, int ns, int k, int* out) {
+  if (ns <= 0) return 0;
+  if (ns <= k) {
+    memcpy(out, S, sizeof(int) * (size_t)ns);
+    return sort_unique(out, ns);
+  }
+  int seed;
+  if (orc_vol(X, d, S, ns, 1, &seed) != 1) return -1;
+  double* mind = (double*)malloc(sizeof(double) * (size_t)ns);
+  int cnt = 0;
+  out[cnt++] = seed;
+  for (int s = 0; s < ns; s++) mind[s] = S[s] == seed ? -1.0 : sqdist(X + (int64_t)S[s] * d, X + (int64_t)seed * d, d);
+  while (cnt < k) {
+    double best = -1.0;
+    int bs = -1;
+    for (int s = 0; s < ns; s++)
+      if (mind[s] > best || (mind[s] == best && mind[s] >= 0.0 && S[s] < S[bs])) {
+        best = mind[s];
+        bs = s;
+      }
+    if (bs < 0 || best < 0.0) break; /* every point selected */
+    const int z = S[bs];
+    out[cnt++] = z;
+    mind[bs] = -1.0;
+    for (int s = 0; s < ns; s++)
+      if (mind[s] >= 0.0) {
+        const double dz = sqdist(X + (int64_t)S[s] * d, X + (int64_t)z * d, d);
+        if (dz < mind[s]) mind[s] = dz;
+      }
+  }
+  free(mind);
+  return sort_unique(out, cnt);
+}
+
 /* ------------------------------------------------------------------------------------------ */
 /* F. getBasis: column-pivoted Householder QR interpolative decomposition (Eqs.(4.1)-(4.4))    */
 /* ------------------------------------------------------------------------------------------ */
@@ -304,6 +343,7 @@ typedef struct orc_h2 {
   int *il_idx, *nf_idx;
   /* D */
   int r;
+  int reduct; /* DataReduct: 0 volume-based (reading C1), 1 farthest point sampling (reading C6) */
   int **xs, **ys;
   int *xs_n, *ys_n;
   int64_t max_S, max_T;
@@ -562,6 +602,13 @@ static void free_lists2(int** a, int n) {
   free(a);
 }
 
+/* the DataReduct of HiDR (readings C1, C6) */
+static int orc_reduct(const orc_h2* h, const int* S, int ns, int k, int* out) {
+  return h->reduct == 1 ? orc_fps(h->X, h->d, S, ns, k, out) : orc_vol(h->X, h->d, S, ns, k, out);
+}
+
+void orc_set_reduct(orc_h2* h, int reduct) { h->reduct = reduct; }
+
 int orc_hidr(orc_h2* h, int r) {
   if (r < 1) return -1;
   double t0 = wall();
@@ -597,7 +644,7 @@ int orc_hidr(orc_h2* h, int r) {
       }
       if (ns > maxS) maxS = ns;
       int* out = (int*)malloc(sizeof(int) * (size_t)(ns < r ? (ns > 0 ? ns : 1) : r));
-      h->xs_n[i] = orc_vol(h->X, h->d, S, ns, r, out);
+      h->xs_n[i] = orc_reduct(h, S, ns, r, out);
       h->xs[i] = out;
       free(S);
     }
@@ -624,7 +671,7 @@ int orc_hidr(orc_h2* h, int r) {
       int nu = sort_unique(T, o); /* set union */
       if (nu > maxT) maxT = nu;
       int* out = (int*)malloc(sizeof(int) * (size_t)(nu < r ? (nu > 0 ? nu : 1) : r));
-      h->ys_n[i] = orc_vol(h->X, h->d, T, nu, r, out);
+      h->ys_n[i] = orc_reduct(h, T, nu, r, out);
       h->ys[i] = out;
       free(T);
     }
