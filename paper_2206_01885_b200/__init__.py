@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libh2b200.so")
 H2_KERNEL_COULOMB, H2_KERNEL_GAUSSIAN, H2_KERNEL_MATERN32, H2_KERNEL_LAPLACE, H2_KERNEL_BUMP, H2_KERNEL_COSDOT = \
     1, 2, 3, 4, 5, 6
 H2_STORE_AUTO, H2_STORE_ALL, H2_STORE_ON_THE_FLY = 0, 1, 2
+H2_REDUCT_VOLUME, H2_REDUCT_FPS = 0, 1  # HiDR DataReduct (h2_options.reduct)
 
 EXPORT = dict(PERM=1, NODES=2, IL_OFF=4, IL_IDX=5, NF_OFF=6, NF_IDX=7, XS_OFF=8, XS_IDX=9, YS_OFF=10,
               YS_IDX=11, K=12, SK_OFF=13, SK_IDX=14, U_OFF=15, U=16, XBAR_N=17, TREE_X=18, SHARD=19)
@@ -35,7 +36,8 @@ EXPORTED_SYMBOLS = ["h2_build", "h2_build_ex", "h2_rebuild_ex", "h2_options_defa
 class h2_options(C.Structure):
     _fields_ = [("r_override", C.c_int32), ("storage", C.c_int32), ("mem_budget_bytes", C.c_int64),
                 ("stream", C.c_void_p), ("points_on_host", C.c_int32), ("timing", C.c_int32),
-                ("hidr_brute", C.c_int32), ("comm", C.c_void_p), ("serial_fill", C.c_int32)]
+                ("hidr_brute", C.c_int32), ("comm", C.c_void_p), ("serial_fill", C.c_int32),
+                ("reduct", C.c_int32)]
 
 
 class h2_info_t(C.Structure):
@@ -258,9 +260,10 @@ class H2Matrix:
     def __init__(self, points, kernel_id: int, kernel_params=(), id_tol: float = 1e-6, leaf_size: int = 64,
                  admissibility: float = 0.5, r: int = 0, storage: int = H2_STORE_AUTO, stream=None,
                  timing: bool = False, mem_budget_bytes: int = 0, hidr_brute: bool = False,
-                 comm: H2Comm | None = None):
+                 comm: H2Comm | None = None, reduct: int = H2_REDUCT_VOLUME):
         import torch
         o = h2_options_default()
+        o.reduct = int(reduct)
         if comm is not None:
             o.comm = C.c_void_p(comm.ptr)
             self._comm = comm

@@ -152,7 +152,7 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
   if (opt) o = *opt;
   if ((!points && !base) || n < 1 || n >= (1LL << 31) - 1 || d < 1 || d > kMaxD || leaf_size < 1 || !(admissibility > 0.0) ||
       !(admissibility <= 0.7) || !(id_tol > 0.0) || !(id_tol < 1.0) || o.r_override < 0 || o.r_override > 4096 ||
-      o.storage < 0 || o.storage > 2) {
+      o.storage < 0 || o.storage > 2 || o.reduct < H2_REDUCT_VOLUME || o.reduct > H2_REDUCT_FPS) {
     set_error(H2_ERR_INVALID_ARG, "invalid argument (n, d, leaf_size, admissibility, id_tol or options)");
     return nullptr;
   }
@@ -179,6 +179,7 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
   h->stream = static_cast<cudaStream_t>(o.stream);
   h->timing = o.timing;
   h->hidr_prune = o.hidr_brute ? 0 : 1;
+  h->reduct = o.reduct;
   h->comm = o.comm;
   h->nranks = h2_comm_size(o.comm);
   h->rank = h2_comm_rank(o.comm);

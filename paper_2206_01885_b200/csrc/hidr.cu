@@ -107,6 +107,192 @@ __global__ void __launch_bounds__(kHidrThreads) hidr_vol_kernel(const double* __
   if (threadIdx.x == 0) out_cnt[i] = c;
 }
 
+// Farthest point sampling (reading C6), one CTA per node over the gathered list:
+// the first point is the one nearest the centre of the tight bounding box (the m = 1 case of Vol,
+// the same arithmetic), then, r - 1 times, the point of largest C4 distance to the selected set
+// (ties to the lowest index).  mind[] (global scratch, one double per candidate) holds each
+// candidate's distance to the selected set, -1 once selected; every round fuses the update by the
+// last pick with the next argmax.  O(r |S|) distances per node.
+template <int D>
+__device__ __forceinline__ double fps_dist(const double* __restrict__ X, int64_t n, int a, const double* z) {
+  double df = __dsub_rn(X[a], z[0]);
+  double s = __dmul_rn(df, df);
+#pragma unroll
+  for (int c = 1; c < D; c++) {
+    df = __dsub_rn(X[(int64_t)c * n + a], z[c]);
+    s = __dadd_rn(s, __dmul_rn(df, df));
+  }
+  return s;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kHidrThreads) hidr_fps_kernel(const double* __restrict__ X, int64_t n, int base,
+                                                                 const int64_t* __restrict__ off,
+                                                                 const int* __restrict__ list, int r, int* out_cnt,
+                                                                 int* out_slots, double* mind_all,
+                                                                 unsigned long long* evals) {
+  constexpr int NT = kHidrThreads, NW = NT / 32;
+  __shared__ int sel[kVolSelCap];
+  __shared__ BlockScanSmem<NT> scan;
+  __shared__ double wv[NW], s_lo[D], s_hi[D], z[D];
+  __shared__ double wlo[D][NW], whi[D][NW];
+  __shared__ int wi[NW], wp[NW];
+  __shared__ int s_pick, s_pos;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t = blockIdx.x, i = base + t;
+  const int* L = list + off[t];
+  const int ns = (int)(off[t + 1] - off[t]);
+  double* mind = mind_all + off[t];
+  int* out = out_slots + (int64_t)i * r;
+  if (ns <= 0) {
+    if (tid == 0) out_cnt[i] = 0;
+    return;
+  }
+  if (ns <= r) {  // pass-through (reading C5)
+    for (int a = tid; a < ns; a += NT) sel[a] = L[a];
+    __syncthreads();
+    const int c = cta_sort_unique_write<NT>(scan, sel, ns, out);
+    if (tid == 0) out_cnt[i] = c;
+    return;
+  }
+  // tight bounding box (exact min / max) and its centre, as Vol with m = 1
+  {
+    double lo[D], hi[D];
+#pragma unroll
+    for (int c = 0; c < D; c++) {
+      lo[c] = DBL_MAX;
+      hi[c] = -DBL_MAX;
+    }
+    for (int a = tid; a < ns; a += NT)
+#pragma unroll
+      for (int c = 0; c < D; c++) {
+        const double v = X[(int64_t)c * n + L[a]];
+        lo[c] = fmin(lo[c], v);
+        hi[c] = fmax(hi[c], v);
+      }
+#pragma unroll
+    for (int c = 0; c < D; c++)
+      for (int o = 16; o > 0; o >>= 1) {
+        lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+        hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+      }
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < D; c++) {
+        wlo[c][warp] = lo[c];
+        whi[c][warp] = hi[c];
+      }
+    __syncthreads();
+    if (tid < D) {
+      double a = DBL_MAX, b = -DBL_MAX;
+      for (int w = 0; w < NW; w++) {
+        a = fmin(a, wlo[tid][w]);
+        b = fmax(b, whi[tid][w]);
+      }
+      s_lo[tid] = a;
+      s_hi[tid] = b;
+      z[tid] = __dadd_rn(a, __dmul_rn(0.5, __ddiv_rn(__dsub_rn(b, a), 1.0)));
+    }
+    __syncthreads();
+  }
+  // block arg-extremum of (value, index) over the candidates: sign = +1 max, -1 min; ties -> lowest
+  // index; returns through s_pick / s_pos
+  auto block_pick = [&](double v, int ix, int ps, double sign) {
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, ix, o), p2 = __shfl_xor_sync(0xffffffffu, ps, o);
+      if (sign * v2 > sign * v || (v2 == v && i2 < ix)) {
+        v = v2;
+        ix = i2;
+        ps = p2;
+      }
+    }
+    if (lane == 0) {
+      wv[warp] = v;
+      wi[warp] = ix;
+      wp[warp] = ps;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double bv = wv[0];
+      int bi = wi[0], bp = wp[0];
+      for (int w = 1; w < NW; w++)
+        if (sign * wv[w] > sign * bv || (wv[w] == bv && wi[w] < bi)) {
+          bv = wv[w];
+          bi = wi[w];
+          bp = wp[w];
+        }
+      s_pick = bi;
+      s_pos = bp;
+      wv[0] = bv;
+    }
+    __syncthreads();
+  };
+  // the seed: nearest to the box centre
+  {
+    double bv = INFINITY;
+    int bix = INT_MAX, bps = -1;
+    for (int a = tid; a < ns; a += NT) {
+      const double dv = fps_dist<D>(X, n, L[a], z);
+      if (dv < bv || (dv == bv && L[a] < bix)) {
+        bv = dv;
+        bix = L[a];
+        bps = a;
+      }
+    }
+    block_pick(bv, bix, bps, -1.0);
+  }
+  int cnt = 0;
+  for (;;) {
+    const int pick = s_pick, ppos = s_pos;
+    if (tid == 0) {
+      sel[cnt] = pick;
+      mind[ppos] = -1.0;
+    }
+    if (tid < D) z[tid] = X[(int64_t)tid * n + pick];
+    cnt++;
+    __syncthreads();
+    if (cnt >= r) break;
+    // update by the last pick, then the farthest remaining candidate
+    double bv = -1.0;
+    int bix = INT_MAX, bps = -1;
+    for (int a = tid; a < ns; a += NT) {
+      double m = cnt == 1 ? (a == ppos ? -1.0 : INFINITY) : mind[a];
+      if (m >= 0.0) {
+        const double dv = fps_dist<D>(X, n, L[a], z);
+        if (dv < m) m = dv;
+        mind[a] = m;
+        if (m > bv || (m == bv && L[a] < bix)) {
+          bv = m;
+          bix = L[a];
+          bps = a;
+        }
+      } else if (cnt == 1) {
+        mind[a] = -1.0;
+      }
+    }
+    block_pick(bv, bix, bps, 1.0);
+    if (wv[0] < 0.0) break;  // every candidate selected
+  }
+  if (evals && tid == 0) atomicAdd(evals, (unsigned long long)cnt * (unsigned long long)ns);
+  __syncthreads();
+  const int c = cta_sort_unique_write<NT>(scan, sel, cnt, out);
+  if (tid == 0) out_cnt[i] = c;
+}
+
+static void launch_fps(int d, unsigned grid, cudaStream_t s, const double* X, int64_t n, int base,
+                       const int64_t* off, const int* list, int r, int* cnt, int* slots, double* mind,
+                       unsigned long long* ev) {
+  switch (d) {
+#define H2_FPS_CASE(DD) \
+  case DD:              \
+    hidr_fps_kernel<DD><<<grid, kHidrThreads, 0, s>>>(X, n, base, off, list, r, cnt, slots, mind, ev); break;
+    H2_FPS_CASE(1) H2_FPS_CASE(2) H2_FPS_CASE(3) H2_FPS_CASE(4)
+    H2_FPS_CASE(5) H2_FPS_CASE(6) H2_FPS_CASE(7) H2_FPS_CASE(8)
+#undef H2_FPS_CASE
+  }
+}
+
 static void launch_vol(int d, unsigned grid, cudaStream_t s, const double* X, int64_t n, int base,
                        const int64_t* off, const int* list, int r, int* cnt, int* slots, unsigned long long* ev) {
   switch (d) {
@@ -180,8 +366,14 @@ static void hidr_level(h2_handle* h, int mode, int l, unsigned long long* ev) {
                                                     h->first_child, h->nchild, h->parent, h->il_off, h->il_idx,
                                                     h->xs_cnt, h->xs, h->ys_cnt, h->ys, h->r, list.as<int>());
   H2_CHECK_LAUNCH();
-  launch_vol(h->d, count, s, h->X, h->n, base, off.as<int64_t>(), list.as<int>(), h->r,
-             mode == 0 ? h->xs_cnt : h->ys_cnt, mode == 0 ? h->xs : h->ys, ev);
+  if (h->reduct == H2_REDUCT_FPS) {
+    Scratch mind(sizeof(double) * (total > 0 ? total : 1), s);
+    launch_fps(h->d, count, s, h->X, h->n, base, off.as<int64_t>(), list.as<int>(), h->r,
+               mode == 0 ? h->xs_cnt : h->ys_cnt, mode == 0 ? h->xs : h->ys, mind.as<double>(), ev);
+  } else {
+    launch_vol(h->d, count, s, h->X, h->n, base, off.as<int64_t>(), list.as<int>(), h->r,
+               mode == 0 ? h->xs_cnt : h->ys_cnt, mode == 0 ? h->xs : h->ys, ev);
+  }
   H2_CHECK_LAUNCH();
   h->gpu_launches += 3;
   if (mode == 0) launch_sel_box(h, base, count, h->xs_cnt, h->xs, h->xbox, h->xboxf, h->xs_xyz);
@@ -228,7 +420,8 @@ void hidr_down(h2_handle* h) {
     const LevelRange lr = level_range(h, l);
     const int base = lr.begin, count = lr.end - lr.begin;
     if (count == 0) continue;
-    if (h->hidr_prune && hidr_down_level_pruned(h, l, ev.as<unsigned long long>(), evd.as<unsigned long long>()))
+    if (h->hidr_prune && h->reduct == H2_REDUCT_VOLUME &&
+        hidr_down_level_pruned(h, l, ev.as<unsigned long long>(), evd.as<unsigned long long>()))
       launch_sel_box(h, base, count, h->ys_cnt, h->ys, h->ybox, h->yboxf, h->ys_xyz);
     else
       hidr_level(h, 1, l, ev.as<unsigned long long>());
