@@ -22,7 +22,7 @@ import paper_2206_01885_b200 as P  # noqa: E402
 _key = itertools.count(1000)
 
 
-def build_sharded(pts, R, kid, kp, id_tol, q, tau=0.5, storage=P.H2_STORE_ALL):
+def build_sharded(pts, R, kid, kp, id_tol, q, tau=0.5, storage=P.H2_STORE_ALL, reduct=P.H2_REDUCT_VOLUME):
     key = next(_key)
     X = torch.from_numpy(np.ascontiguousarray(pts)).cuda()
     out, errs = [None] * R, []
@@ -32,7 +32,8 @@ def build_sharded(pts, R, kid, kp, id_tol, q, tau=0.5, storage=P.H2_STORE_ALL):
             torch.cuda.set_device(0)
             comm = P.H2Comm.local(R, rank, key)
             st = torch.cuda.Stream()
-            out[rank] = P.H2Matrix(X, kid, kp, id_tol, q, tau, storage=storage, stream=st, timing=True, comm=comm)
+            out[rank] = P.H2Matrix(X, kid, kp, id_tol, q, tau, storage=storage, stream=st, timing=True, comm=comm,
+                                   reduct=reduct)
         except Exception as e:  # pragma: no cover - reported below
             errs.append(e)
 
@@ -175,4 +176,28 @@ def test_sharded_rebuild_equals_single_gpu_rebuild():
     x = torch.from_numpy(synth.matvec_vector(1, 8192)).cuda()
     y_ref = ref.matvec(x).cpu().numpy()
     for y in collective_matvec(out, x):
+        assert np.linalg.norm(y - y_ref) <= 1e-12 * np.linalg.norm(y_ref)
+
+
+def test_sharded_fps_equals_single_gpu_fps():
+    """Farthest point sampling (reading C6) on a sharded build: every rank's X^* / Y^* and skeletons
+    equal the single-GPU FPS build, and the collective matvec equals its matvec."""
+    c = synth.CONFIGS[4]
+    pts = synth.points(4, 30000)
+    X = torch.from_numpy(pts).cuda()
+    kp = list(c["params"])
+    ref = P.H2Matrix(X, c["kernel"], kp, c["id_tol"], c["q"], c["tau"], storage=P.H2_STORE_ALL,
+                     reduct=P.H2_REDUCT_FPS)
+    hs = build_sharded(pts, 3, c["kernel"], kp, c["id_tol"], c["q"], c["tau"], reduct=P.H2_REDUCT_FPS)
+    depth = ref.info()["depth"]
+    xs_ref, ys_ref, sk_ref = slots(ref, "XS"), slots(ref, "YS"), slots(ref, "SK")
+    for g in hs:  # exchanged: X^* and skeletons of every node; Y^* of the nodes the rank computed
+        assert all(np.array_equal(a, b) for a, b in zip(slots(g, "XS"), xs_ref))
+        assert all(np.array_equal(a, b) for a, b in zip(slots(g, "SK"), sk_ref))
+        ys, rng = slots(g, "YS"), g.export("SHARD")[5:].reshape(depth + 1, 2)
+        for lo, hi in rng:
+            assert all(np.array_equal(ys[i], ys_ref[i]) for i in range(lo, hi))
+    x = torch.from_numpy(synth.matvec_vector(4, 30000)).cuda()
+    y_ref = ref.matvec(x).cpu().numpy()
+    for y in collective_matvec(hs, x):
         assert np.linalg.norm(y - y_ref) <= 1e-12 * np.linalg.norm(y_ref)
