@@ -106,15 +106,17 @@ typedef struct h2_options {
   int32_t serial_fill;     /* 1: run the nearfield fill (a10) after a9 on the main stream instead of */
                            /*    concurrently with a5-a9 on a low-priority side stream (default 0;  */
                            /*    same result; for measuring the fill kernel in isolation)           */
-  int32_t reduct;          /* HiDR's DataReduct (PAPER §3.3, P:423-433): H2_REDUCT_VOLUME (default, */
-                           /*    the one of all the paper's runs) or H2_REDUCT_FPS (farthest */
-                           /*    point sampling; O(r |S|) per node)                      */
+  int32_t reduct;          /* HiDR's DataReduct (PAPER §3.3, P:423-440): H2_REDUCT_VOLUME (default, */
+                           /*    the one of all the paper's runs), H2_REDUCT_FPS (farthest   */
+                           /*    point sampling) or H2_REDUCT_SURFACE; the last two O(r |S|)/node   */
 } h2_options;
 
 /* ---- DataReduct of HiDR (h2_options.reduct) ---------------------------------------------------- */
 enum {
   H2_REDUCT_VOLUME = 0, /* nearest point to every node of an m^d grid over the tight bounding box (C1-C5) */
-  H2_REDUCT_FPS = 1     /* farthest point sampling from the point nearest the box centre (reading C6)   */
+  H2_REDUCT_FPS = 1,    /* farthest point sampling from the point nearest the box centre (reading C6)   */
+  H2_REDUCT_SURFACE = 2 /* nearest point to reference points on three ellipsoids, gamma 0.3/0.6/1.2
+                           (reading C7); d = 2 or 3 only (H2_ERR_INVALID_ARG otherwise)     */
 };
 
 /* h2_options with the defaults listed above (r calibrated, AUTO, whole-device budget, timing off) */

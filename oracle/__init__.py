@@ -63,6 +63,7 @@ def lib():
         L.orc_vol.argtypes = [vp, i32, vp, i32, i32, vp]
         L.orc_fps.argtypes = [vp, i32, vp, i32, i32, vp]
         L.orc_set_reduct.argtypes = [vp, i32]
+        L.orc_surface.argtypes = [vp, i32, vp, i32, i32, vp]
         L.orc_cpqr.argtypes = [vp, i32, i32, f64, vp]
         L.orc_id.argtypes = [vp, i32, i32, f64, vp, vp]
         L.orc_admissible.argtypes = [vp, i32, vp, i32, i32, f64]
@@ -105,6 +106,17 @@ def fps(X: np.ndarray, S, k: int) -> np.ndarray:
     S = np.ascontiguousarray(S, np.int32)
     out = np.empty(max(1, min(len(S), k)), np.int32)
     c = lib().orc_fps(_p(X), X.shape[1], _p(S), len(S), int(k), _p(out))
+    return out[:c].copy()
+
+
+def surface(X: np.ndarray, S, k: int) -> np.ndarray:
+    """C''. surface-based DataReduct (reading C7; d = 2 or 3)."""
+    X = np.ascontiguousarray(X, np.float64)
+    S = np.ascontiguousarray(S, np.int32)
+    out = np.empty(max(1, min(len(S), k)), np.int32)
+    c = lib().orc_surface(_p(X), X.shape[1], _p(S), len(S), int(k), _p(out))
+    if c < 0:
+        raise ValueError("surface DataReduct needs d = 2 or 3")
     return out[:c].copy()
 
 
@@ -163,7 +175,8 @@ class OracleH2:
     """A (partition) + B (lists) on construction; then calibrate / hidr / id_sweep / matvec."""
 
     def __init__(self, pts: np.ndarray, q: int, tau: float = 0.5, reduct: int = 0):
-        """reduct: the DataReduct of HiDR, 0 volume-based (reading C1), 1 farthest point sampling (C6)."""
+        """reduct: the DataReduct of HiDR, 0 volume-based (reading C1), 1 farthest point sampling (C6),
+        2 surface-based (C7)."""
         self.pts = np.ascontiguousarray(pts, np.float64)
         self.n, self.d = self.pts.shape
         self._h = lib().orc_new(_p(self.pts), self.n, self.d, int(q), float(tau))

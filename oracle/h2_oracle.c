@@ -343,7 +343,7 @@ typedef struct orc_h2 {
   int *il_idx, *nf_idx;
   /* D */
   int r;
-  int reduct; /* DataReduct: 0 volume-based (reading C1), 1 farthest point sampling (reading C6) */
+  int reduct; /* DataReduct: 0 volume-based (C1), 1 farthest point sampling (C6), 2 surface-based (C7) */
   int **xs, **ys;
   int *xs_n, *ys_n;
   int64_t max_S, max_T;
@@ -602,9 +602,90 @@ static void free_lists2(int** a, int n) {
   free(a);
 }
 
+/* Surface-based DataReduct, PAPER §3.3: reference points on three ellipsoids centred
+ * at the centre of the tight bounding box, principal semi-axes gamma times the box width in each
+ * dimension, gamma = 0.3, 0.6, 1.2 (the values of the paper's runs); for every reference point the
+ * nearest point of S (C4 distances, ties -> lowest index); sorted and de-duplicated (C5).
+ * Reading C7: d = 2 or 3 only.  The k reference points are dealt round-robin to the ellipsoids
+ * (ellipsoid e gets floor(k/3) + [e < k mod 3]); on an ellipsoid with M points, point j has the
+ * unit direction (cos t, sin t), t = 2 pi j / M in 2-D, and the Fibonacci-sphere direction
+ * (rho cos f, rho sin f, z), z = 1 - (2j+1)/M, rho = sqrt(1 - z^2), f = j pi (3 - sqrt 5) in 3-D;
+ * the reference point is c_c + (gamma w_c) u_c with c the box centre lo + 0.5 (hi - lo), w = hi - lo.
+ * Returns |out| <= k, or -1 for d outside {2, 3}.                                               */
+static const double kSurfGamma[3] = {0.3, 0.6, 1.2};
+
+int orc_surface_dirs(int d, int k, double* u) { /* u[(e*k + j)*d + c]; returns the count */
+  if (d != 2 && d != 3) return -1;
+  int cnt = 0;
+  for (int e = 0; e < 3; e++) {
+    const int M = k / 3 + (e < k % 3 ? 1 : 0);
+    for (int j = 0; j < M; j++) {
+      double* v = u + (int64_t)cnt * (d + 1);
+      if (d == 2) {
+        const double t = 2.0 * M_PI * (double)j / (double)M;
+        v[0] = cos(t);
+        v[1] = sin(t);
+      } else {
+        const double z = 1.0 - (2.0 * (double)j + 1.0) / (double)M;
+        const double rho = sqrt(1.0 - z * z);
+        const double f = (double)j * (M_PI * (3.0 - sqrt(5.0)));
+        v[0] = rho * cos(f);
+        v[1] = rho * sin(f);
+        v[2] = z;
+      }
+      v[d] = kSurfGamma[e];
+      cnt++;
+    }
+  }
+  return cnt;
+}
+
+int orc_surface(const double* X, int d, const int* S, int ns, int k, int* out) {
+  if (d != 2 && d != 3) return -1;
+  if (ns <= 0) return 0;
+  if (ns <= k) {
+    memcpy(out, S, sizeof(int) * (size_t)ns);
+    return sort_unique(out, ns);
+  }
+  double lo[ORC_MAXD], hi[ORC_MAXD], cen[ORC_MAXD], w[ORC_MAXD];
+  for (int c = 0; c < d; c++) lo[c] = hi[c] = X[(int64_t)S[0] * d + c];
+  for (int s = 1; s < ns; s++)
+    for (int c = 0; c < d; c++) {
+      double v = X[(int64_t)S[s] * d + c];
+      if (v < lo[c]) lo[c] = v;
+      if (v > hi[c]) hi[c] = v;
+    }
+  for (int c = 0; c < d; c++) {
+    w[c] = hi[c] - lo[c];
+    cen[c] = lo[c] + 0.5 * (w[c] / 1.0);
+  }
+  double* u = (double*)malloc(sizeof(double) * (size_t)k * (d + 1));
+  const int nq = orc_surface_dirs(d, k, u);
+  int cnt = 0;
+  for (int g = 0; g < nq; g++) {
+    const double* v = u + (int64_t)g * (d + 1);
+    double q[ORC_MAXD];
+    for (int c = 0; c < d; c++) q[c] = cen[c] + (v[d] * w[c]) * v[c];
+    double best = INFINITY;
+    int bi = INT_MAX;
+    for (int s = 0; s < ns; s++) {
+      double dist = sqdist(X + (int64_t)S[s] * d, q, d);
+      if (dist < best || (dist == best && S[s] < bi)) {
+        best = dist;
+        bi = S[s];
+      }
+    }
+    out[cnt++] = bi;
+  }
+  free(u);
+  return sort_unique(out, cnt);
+}
+
 /* the DataReduct of HiDR (readings C1, C6) */
 static int orc_reduct(const orc_h2* h, const int* S, int ns, int k, int* out) {
-  return h->reduct == 1 ? orc_fps(h->X, h->d, S, ns, k, out) : orc_vol(h->X, h->d, S, ns, k, out);
+  if (h->reduct == 1) return orc_fps(h->X, h->d, S, ns, k, out);
+  if (h->reduct == 2) return orc_surface(h->X, h->d, S, ns, k, out);
+  return orc_vol(h->X, h->d, S, ns, k, out);
 }
 
 void orc_set_reduct(orc_h2* h, int reduct) { h->reduct = reduct; }

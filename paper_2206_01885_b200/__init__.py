@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libh2b200.so")
 H2_KERNEL_COULOMB, H2_KERNEL_GAUSSIAN, H2_KERNEL_MATERN32, H2_KERNEL_LAPLACE, H2_KERNEL_BUMP, H2_KERNEL_COSDOT = \
     1, 2, 3, 4, 5, 6
 H2_STORE_AUTO, H2_STORE_ALL, H2_STORE_ON_THE_FLY = 0, 1, 2
-H2_REDUCT_VOLUME, H2_REDUCT_FPS = 0, 1  # HiDR DataReduct (h2_options.reduct)
+H2_REDUCT_VOLUME, H2_REDUCT_FPS, H2_REDUCT_SURFACE = 0, 1, 2  # HiDR DataReduct (h2_options.reduct)
 
 EXPORT = dict(PERM=1, NODES=2, IL_OFF=4, IL_IDX=5, NF_OFF=6, NF_IDX=7, XS_OFF=8, XS_IDX=9, YS_OFF=10,
               YS_IDX=11, K=12, SK_OFF=13, SK_IDX=14, U_OFF=15, U=16, XBAR_N=17, TREE_X=18, SHARD=19)

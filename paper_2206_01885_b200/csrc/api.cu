@@ -152,7 +152,8 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
   if (opt) o = *opt;
   if ((!points && !base) || n < 1 || n >= (1LL << 31) - 1 || d < 1 || d > kMaxD || leaf_size < 1 || !(admissibility > 0.0) ||
       !(admissibility <= 0.7) || !(id_tol > 0.0) || !(id_tol < 1.0) || o.r_override < 0 || o.r_override > 4096 ||
-      o.storage < 0 || o.storage > 2 || o.reduct < H2_REDUCT_VOLUME || o.reduct > H2_REDUCT_FPS) {
+      o.storage < 0 || o.storage > 2 || o.reduct < H2_REDUCT_VOLUME || o.reduct > H2_REDUCT_SURFACE ||
+      (o.reduct == H2_REDUCT_SURFACE && d != 2 && d != 3)) {
     set_error(H2_ERR_INVALID_ARG, "invalid argument (n, d, leaf_size, admissibility, id_tol or options)");
     return nullptr;
   }

@@ -6,6 +6,9 @@
 // Level-synchronous: per level, (1) a size kernel, (2) an exclusive scan, (3) a gather kernel
 // writing every node's S_i / T_i index list contiguously (the union is disjoint by the tiling of
 // the block partition, so it is a concatenation), (4) one CTA per node runs Vol.
+#include <cmath>
+#include <vector>
+
 #include "hidr_down.cuh"
 
 namespace h2 {
@@ -280,6 +283,107 @@ __global__ void __launch_bounds__(kHidrThreads) hidr_fps_kernel(const double* __
   if (tid == 0) out_cnt[i] = c;
 }
 
+// Surface-based DataReduct (reading C7, d = 2 or 3): reference points
+// c + (gamma w) u on three ellipsoids about the centre c of the tight bounding box (w = its widths),
+// the unit directions u and gammas from h->surf_dirs (computed once on the host with the C math
+// library, as the oracle does); for every reference point the nearest candidate (C4, ties -> lowest
+// index).  One CTA per node, a thread per reference point over all candidates (warp-uniform
+// candidate loads).  O(r |S|) distances per node.
+template <int D>
+__global__ void __launch_bounds__(kHidrThreads) hidr_surface_kernel(const double* __restrict__ X, int64_t n,
+                                                                     int base, const int64_t* __restrict__ off,
+                                                                     const int* __restrict__ list, int r,
+                                                                     const double* __restrict__ dirs, int nq,
+                                                                     int* out_cnt, int* out_slots,
+                                                                     unsigned long long* evals) {
+  constexpr int NT = kHidrThreads, NW = NT / 32;
+  __shared__ int sel[kVolSelCap];
+  __shared__ BlockScanSmem<NT> scan;
+  __shared__ double wlo[D][NW], whi[D][NW], s_cen[D], s_w[D];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t = blockIdx.x, i = base + t;
+  const int* L = list + off[t];
+  const int ns = (int)(off[t + 1] - off[t]);
+  int* out = out_slots + (int64_t)i * r;
+  if (ns <= 0) {
+    if (tid == 0) out_cnt[i] = 0;
+    return;
+  }
+  if (ns <= r) {  // pass-through (reading C5)
+    for (int a = tid; a < ns; a += NT) sel[a] = L[a];
+    __syncthreads();
+    const int c = cta_sort_unique_write<NT>(scan, sel, ns, out);
+    if (tid == 0) out_cnt[i] = c;
+    return;
+  }
+  {
+    double lo[D], hi[D];
+#pragma unroll
+    for (int c = 0; c < D; c++) {
+      lo[c] = DBL_MAX;
+      hi[c] = -DBL_MAX;
+    }
+    for (int a = tid; a < ns; a += NT)
+#pragma unroll
+      for (int c = 0; c < D; c++) {
+        const double v = X[(int64_t)c * n + L[a]];
+        lo[c] = fmin(lo[c], v);
+        hi[c] = fmax(hi[c], v);
+      }
+#pragma unroll
+    for (int c = 0; c < D; c++)
+      for (int o = 16; o > 0; o >>= 1) {
+        lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+        hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+      }
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < D; c++) {
+        wlo[c][warp] = lo[c];
+        whi[c][warp] = hi[c];
+      }
+    __syncthreads();
+    if (tid < D) {
+      double a = DBL_MAX, b = -DBL_MAX;
+      for (int w = 0; w < NW; w++) {
+        a = fmin(a, wlo[tid][w]);
+        b = fmax(b, whi[tid][w]);
+      }
+      const double w = __dsub_rn(b, a);
+      s_w[tid] = w;
+      s_cen[tid] = __dadd_rn(a, __dmul_rn(0.5, __ddiv_rn(w, 1.0)));
+    }
+    __syncthreads();
+  }
+  for (int g = tid; g < nq; g += NT) {
+    const double* u = dirs + (int64_t)g * (D + 1);
+    double q[D];
+#pragma unroll
+    for (int c = 0; c < D; c++) q[c] = __dadd_rn(s_cen[c], __dmul_rn(__dmul_rn(u[D], s_w[c]), u[c]));
+    double best = INFINITY;
+    int bi = INT_MAX;
+    for (int a = 0; a < ns; a++) {
+      const int idx = L[a];
+      double df = __dsub_rn(X[idx], q[0]);
+      double sd = __dmul_rn(df, df);
+#pragma unroll
+      for (int c = 1; c < D; c++) {
+        df = __dsub_rn(X[(int64_t)c * n + idx], q[c]);
+        sd = __dadd_rn(sd, __dmul_rn(df, df));
+      }
+      if (sd < best || (sd == best && idx < bi)) {
+        best = sd;
+        bi = idx;
+      }
+    }
+    sel[g] = bi;
+  }
+  if (evals && tid == 0) atomicAdd(evals, (unsigned long long)nq * (unsigned long long)ns);
+  __syncthreads();
+  const int c = cta_sort_unique_write<NT>(scan, sel, nq, out);
+  if (tid == 0) out_cnt[i] = c;
+}
+
 static void launch_fps(int d, unsigned grid, cudaStream_t s, const double* X, int64_t n, int base,
                        const int64_t* off, const int* list, int r, int* cnt, int* slots, double* mind,
                        unsigned long long* ev) {
@@ -366,7 +470,17 @@ static void hidr_level(h2_handle* h, int mode, int l, unsigned long long* ev) {
                                                     h->first_child, h->nchild, h->parent, h->il_off, h->il_idx,
                                                     h->xs_cnt, h->xs, h->ys_cnt, h->ys, h->r, list.as<int>());
   H2_CHECK_LAUNCH();
-  if (h->reduct == H2_REDUCT_FPS) {
+  if (h->reduct == H2_REDUCT_SURFACE) {
+    const int nq = (int)(h->surf_dirs_n);
+    if (h->d == 2)
+      hidr_surface_kernel<2><<<count, kHidrThreads, 0, s>>>(h->X, h->n, base, off.as<int64_t>(), list.as<int>(),
+                                                            h->r, h->surf_dirs, nq, mode == 0 ? h->xs_cnt : h->ys_cnt,
+                                                            mode == 0 ? h->xs : h->ys, ev);
+    else
+      hidr_surface_kernel<3><<<count, kHidrThreads, 0, s>>>(h->X, h->n, base, off.as<int64_t>(), list.as<int>(),
+                                                            h->r, h->surf_dirs, nq, mode == 0 ? h->xs_cnt : h->ys_cnt,
+                                                            mode == 0 ? h->xs : h->ys, ev);
+  } else if (h->reduct == H2_REDUCT_FPS) {
     Scratch mind(sizeof(double) * (total > 0 ? total : 1), s);
     launch_fps(h->d, count, s, h->X, h->n, base, off.as<int64_t>(), list.as<int>(), h->r,
                mode == 0 ? h->xs_cnt : h->ys_cnt, mode == 0 ? h->xs : h->ys, mind.as<double>(), ev);
@@ -380,8 +494,41 @@ static void hidr_level(h2_handle* h, int mode, int l, unsigned long long* ev) {
   else launch_sel_box(h, base, count, h->ys_cnt, h->ys, h->ybox, h->yboxf, h->ys_xyz);
 }
 
+// reading C7: the surface reference directions (unit vector + gamma per point, k = r points dealt
+// round-robin to the three ellipsoids), computed with the host C math library
+static void make_surface_dirs(h2_handle* h) {
+  const int d = h->d, k = h->r;
+  const double gam[3] = {0.3, 0.6, 1.2};
+  std::vector<double> u;
+  for (int e = 0; e < 3; e++) {
+    const int M = k / 3 + (e < k % 3 ? 1 : 0);
+    for (int j = 0; j < M; j++) {
+      if (d == 2) {
+        const double t = 2.0 * M_PI * (double)j / (double)M;
+        u.push_back(cos(t));
+        u.push_back(sin(t));
+      } else {
+        const double z = 1.0 - (2.0 * (double)j + 1.0) / (double)M;
+        const double rho = sqrt(1.0 - z * z);
+        const double f = (double)j * (M_PI * (3.0 - sqrt(5.0)));
+        u.push_back(rho * cos(f));
+        u.push_back(rho * sin(f));
+        u.push_back(z);
+      }
+      u.push_back(gam[e]);
+    }
+  }
+  h->surf_dirs_n = (int64_t)(u.size() / (size_t)(d + 1));
+  h->surf_dirs = halloc<double>(h, u.size() > 0 ? u.size() : 1);
+  if (!u.empty())
+    H2_CUDA_TRY(cudaMemcpyAsync(h->surf_dirs, u.data(), sizeof(double) * u.size(), cudaMemcpyHostToDevice,
+                                h->stream));
+  H2_CUDA_TRY(cudaStreamSynchronize(h->stream));  // u is a host temporary
+}
+
 void hidr_up(h2_handle* h) {
   if (h->r > kVolSelCap) throw Error{H2_ERR_INVALID_ARG, "r exceeds the supported budget 4096"};
+  if (h->reduct == H2_REDUCT_SURFACE) make_surface_dirs(h);
   h->xs_cnt = halloc<int>(h, h->nnodes);
   h->xs = halloc<int>(h, (size_t)h->nnodes * h->r);
   h->ys_cnt = halloc<int>(h, h->nnodes);

@@ -376,24 +376,33 @@ def test_id_cluster_path_equals_single_cta_path(cfg, n, tmp_path):
     assert np.linalg.norm(ya - yb) <= 1e-9 * np.linalg.norm(yb)
 
 
+@pytest.mark.parametrize("reduct", [1, 2])
 @pytest.mark.parametrize("cfg,n,q", [(1, 8192, None), (4, 30000, None), (3, 20000, None), (2, 20000, 64)])
-def test_parity_fps(cfg, n, q):
+def test_parity_fps(cfg, n, q, reduct):
     """HiDR with farthest point sampling (reading C6; h2_options.reduct =
-    H2_REDUCT_FPS): X_i^*, Y_i^* bit-exact with the oracle's FPS, the rest of the path as usual."""
+    H2_REDUCT_FPS) and with the surface-based reduction (reading C7; H2_REDUCT_SURFACE):
+    X_i^*, Y_i^* bit-exact with the oracle's, the rest of the path as usual."""
     c = synth.CONFIGS[cfg]
     pts = synth.points(cfg, n)
     kp = list(c["params"])
-    o = oracle.OracleH2(pts, q or c["q"], c["tau"], reduct=1)
+    o = oracle.OracleH2(pts, q or c["q"], c["tau"], reduct=reduct)
     r = o.build(c["kernel"], kp[0] if kp else 0.0, c["id_tol"])
     X = torch.from_numpy(np.ascontiguousarray(pts)).cuda()
     g = P.H2Matrix(X, c["kernel"], kp, c["id_tol"], q or c["q"], c["tau"], storage=P.H2_STORE_ALL, timing=True,
-                   reduct=P.H2_REDUCT_FPS)
+                   reduct=reduct)
     assert g.info()["r"] == r
     assert_structure_equal(g, o)
     assert skeleton_agreement(g, o) >= 0.9
     eg, eo, agree = matvec_check(g, o, pts, c["kernel"], kp, c["id_tol"], cfg)
-    print(f"FPS cfg{cfg} n={n}: r={r} err_gpu={eg:.3e} err_oracle={eo:.3e} gpu-vs-oracle={agree:.3e} "
+    print(f"reduct {reduct} cfg{cfg} n={n}: r={r} err_gpu={eg:.3e} err_oracle={eo:.3e} gpu-vs-oracle={agree:.3e} "
           f"hidr ms up {g.info()['stage_ms']['hidr_up']:.2f} down {g.info()['stage_ms']['hidr_down']:.2f}")
     assert eg <= 2.0 * eo + 1e-15
     assert agree <= 10 * c["id_tol"]
     g.close()
+
+
+def test_surface_reduct_needs_d_2_or_3():
+    pts = synth.points(5, 3000)
+    with pytest.raises(Exception):
+        P.H2Matrix(torch.from_numpy(pts).cuda(), 2, [1.0], 1e-4, 64, reduct=P.H2_REDUCT_SURFACE)
+    assert P.last_error()[0] == -1  # H2_ERR_INVALID_ARG

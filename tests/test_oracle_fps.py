@@ -97,3 +97,53 @@ def test_hidr_with_fps_pipeline():
         errs.append(np.linalg.norm(y - yd) / np.linalg.norm(yd))
         o.close()
     assert errs[0] > errs[1] > errs[2], errs
+
+
+# ---- surface-based DataReduct (reading C7) -------------------------------------------
+def _surface_brute(X, S, k):
+    """Plain numpy version of reading C7, written from the paper's description."""
+    S = list(S)
+    if len(S) <= k:
+        return sorted(set(S))
+    d = X.shape[1]
+    lo, hi = X[S].min(0), X[S].max(0)
+    w = hi - lo
+    cen = lo + 0.5 * (w / 1.0)
+    out = []
+    for e, gam in enumerate((0.3, 0.6, 1.2)):
+        M = k // 3 + (1 if e < k % 3 else 0)
+        for j in range(M):
+            if d == 2:
+                t = 2.0 * np.pi * j / M
+                u = np.array([np.cos(t), np.sin(t)])
+            else:
+                z = 1.0 - (2.0 * j + 1.0) / M
+                rho = np.sqrt(1.0 - z * z)
+                f = j * (np.pi * (3.0 - np.sqrt(5.0)))
+                u = np.array([rho * np.cos(f), rho * np.sin(f), z])
+            q = cen + (gam * w) * u
+            out.append(min(S, key=lambda s: (_c4(X[s], q), s)))
+    return sorted(set(out))
+
+
+def test_surface_k3_axis_points():
+    # k = 3 in 2-D: one reference point per ellipsoid, at angle 0: (c + gamma w, c_y) on the x axis
+    xs = np.linspace(0.0, 1.0, 11)
+    X = np.stack([np.concatenate([xs, xs]), np.concatenate([np.full(11, 0.4), np.full(11, 0.6)])], 1)
+    # box [0,1] x [0.4,0.6]: centre (0.5, 0.5); gamma 0.3 -> x = 0.8, 0.6 -> x = 1.1, 1.2 -> x = 1.7
+    out = oracle.surface(X, np.arange(22), 3)
+    assert list(out) == [8, 10]  # (0.8, 0.4) (lower index of the tie with row 0.6) and (1.0, 0.4)
+
+
+@pytest.mark.parametrize("seed,n,d,k", [(1, 80, 2, 9), (2, 120, 3, 12), (3, 60, 2, 5), (4, 200, 3, 27)])
+def test_surface_against_brute_force(seed, n, d, k):
+    X = np.random.default_rng(seed).random((n, d))
+    S = np.random.default_rng(seed + 10).permutation(n)[: n - 5]
+    out = oracle.surface(X, S, k)
+    assert list(out) == _surface_brute(X, S, k)
+    assert len(out) <= k and set(out) <= set(S)
+
+
+def test_surface_rejects_other_dimensions():
+    with pytest.raises(ValueError):
+        oracle.surface(np.random.default_rng(0).random((30, 4)), np.arange(30), 6)
