@@ -116,11 +116,6 @@ __device__ __forceinline__ float warp_min_f(float v) {
   return __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(v)));
 }
 
-__device__ __forceinline__ double warp_min_d(double v) {
-  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
 // An upper bound of the warp minimum of v >= 0 (distances) in ONE instruction: high words of
 // non-negative doubles order like the doubles, so the least high word with an all-ones low word
 // bounds the minimum from above (at most 2^-20 relative above it).  The pruning only needs
