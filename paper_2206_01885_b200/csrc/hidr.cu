@@ -96,17 +96,50 @@ struct ListAcc {
   __device__ __forceinline__ int index(int pos) const { return list[pos]; }
 };
 
+// `split` CTAs per node (levels with few nodes): each computes a share of the grid nodes; the
+// selection is then sorted and de-duplicated by vol_finalize_kernel (one CTA per node).
 template <int D>
 __global__ void __launch_bounds__(kHidrThreads) hidr_vol_kernel(const double* __restrict__ X, int64_t n, int base,
                                                                  const int64_t* __restrict__ off,
                                                                  const int* __restrict__ list, int r, int* out_cnt,
-                                                                 int* out_slots, unsigned long long* evals) {
+                                                                 int* out_slots, unsigned long long* evals,
+                                                                 int split) {
   __shared__ VolSmem<D, kHidrThreads> sm;
-  const int t = blockIdx.x;
+  const int t = blockIdx.x / split, part = blockIdx.x % split;
   const int i = base + t;
   ListAcc acc{X, n, list + off[t]};
   int ns = (int)(off[t + 1] - off[t]);
-  int c = cta_vol<D, kHidrThreads>(acc, ns, r, out_slots + (int64_t)i * r, sm, evals);
+  if (ns <= r || split == 1) {  // pass-through or a single CTA: the whole selection here
+    if (part != 0) return;
+    const int c = cta_vol<D, kHidrThreads>(acc, ns, r, out_slots + (int64_t)i * r, sm, evals);
+    if (threadIdx.x == 0) out_cnt[i] = c;
+    return;
+  }
+  cta_vol<D, kHidrThreads>(acc, ns, r, out_slots + (int64_t)i * r, sm, evals, part, split);
+}
+
+// sort and de-duplicate the grid nodes' nearest points parked in the output slots (split levels)
+template <int D>
+__global__ void __launch_bounds__(kHidrThreads) vol_finalize_kernel(int base, const int64_t* __restrict__ off,
+                                                                    int r, int* out_cnt, int* out_slots) {
+  __shared__ int sel[kVolSelCap];
+  __shared__ BlockScanSmem<kHidrThreads> scan;
+  const int t = blockIdx.x, i = base + t;
+  const int ns = (int)(off[t + 1] - off[t]);
+  if (ns <= r) return;  // done by the pass-through
+  int m = 1;
+  for (;;) {
+    long long p = 1;
+    for (int c = 0; c < D; c++) p *= (m + 1);
+    if (p > r) break;
+    m++;
+  }
+  int G = 1;
+  for (int c = 0; c < D; c++) G *= m;
+  int* out = out_slots + (int64_t)i * r;
+  for (int g = threadIdx.x; g < G; g += kHidrThreads) sel[g] = out[g];
+  __syncthreads();
+  const int c = cta_sort_unique_write<kHidrThreads>(scan, sel, G, out);
   if (threadIdx.x == 0) out_cnt[i] = c;
 }
 
@@ -397,12 +430,31 @@ static void launch_fps(int d, unsigned grid, cudaStream_t s, const double* X, in
   }
 }
 
-static void launch_vol(int d, unsigned grid, cudaStream_t s, const double* X, int64_t n, int base,
+static void launch_vol(int d, unsigned count, cudaStream_t s, const double* X, int64_t n, int base,
                        const int64_t* off, const int* list, int r, int* cnt, int* slots, unsigned long long* ev) {
+  // few nodes: several CTAs per node (at least 64 grid nodes each) so a level fills the machine
+  long long G = 1;
+  {
+    int m = 1;
+    for (;;) {
+      long long p = 1;
+      for (int c = 0; c < d; c++) p *= (m + 1);
+      if (p > r) break;
+      m++;
+    }
+    for (int c = 0; c < d; c++) G *= m;
+  }
+  int split = (int)((4LL * 148 + count - 1) / count);
+  const int smax = (int)(G / 64);
+  if (split > smax) split = smax;
+  if (split < 1) split = 1;
+  const unsigned grid = count * (unsigned)split;
   switch (d) {
-#define H2_VOL_CASE(DD) \
-  case DD:              \
-    hidr_vol_kernel<DD><<<grid, kHidrThreads, 0, s>>>(X, n, base, off, list, r, cnt, slots, ev); break;
+#define H2_VOL_CASE(DD)                                                                                   \
+  case DD:                                                                                                \
+    hidr_vol_kernel<DD><<<grid, kHidrThreads, 0, s>>>(X, n, base, off, list, r, cnt, slots, ev, split);      \
+    if (split > 1) vol_finalize_kernel<DD><<<count, kHidrThreads, 0, s>>>(base, off, r, cnt, slots);     \
+    break;
     H2_VOL_CASE(1) H2_VOL_CASE(2) H2_VOL_CASE(3) H2_VOL_CASE(4)
     H2_VOL_CASE(5) H2_VOL_CASE(6) H2_VOL_CASE(7) H2_VOL_CASE(8)
 #undef H2_VOL_CASE

@@ -123,9 +123,11 @@ __device__ int cta_sort_unique_write(BlockScanSmem<NT>& scan, int* sel, int cnt,
 }
 
 // Acc: __device__ double coord(int pos, int c) const; __device__ int index(int pos) const
+// part / split > 1 (ns > k): this CTA handles only the grid nodes [part G / split, (part+1) G / split),
+// parks their nearest points in out[g] and returns -1; vol_finalize then sorts and de-duplicates.
 template <int D, int NT, class Acc>
 __device__ int cta_vol(const Acc& acc, int ns, int k, int* out, VolSmem<D, NT>& sm,
-                       unsigned long long* evals = nullptr) {
+                       unsigned long long* evals = nullptr, int part = 0, int split = 1) {
   constexpr int TILE = vol_tile(D);
   constexpr int GPT = kVolGPT;
   const int tid = threadIdx.x;
@@ -196,7 +198,8 @@ __device__ int cta_vol(const Acc& acc, int ns, int k, int* out, VolSmem<D, NT>& 
   // compared against GPT grid nodes.  Exact rule (C4): s < best, or s == best and a lower index,
   // written as a rare branch on s <= best.  s = d0^2 + d1^2 + ... with every operation rounded
   // separately (0 + d0^2 == d0^2 exactly, so the sum starts from the first square).
-  const int ngroups = (G + GPT - 1) / GPT;
+  const int g_lo = (int)((int64_t)G * part / split), g_hi = (int)((int64_t)G * (part + 1) / split);
+  const int ngroups = (g_hi - g_lo + GPT - 1) / GPT;
   const int nslice = ngroups >= NT ? 1 : NT / ngroups;
   const int gstride = ngroups >= NT ? NT : ngroups;
   const int slice = ngroups >= NT ? 0 : tid / ngroups;
@@ -217,7 +220,7 @@ __device__ int cta_vol(const Acc& acc, int ns, int k, int* out, VolSmem<D, NT>& 
     int bi[GPT];
 #pragma unroll
     for (int kk = 0; kk < GPT; kk++) {
-      int rem = grp * GPT + kk;
+      int rem = g_lo + grp * GPT + kk;
 #pragma unroll
       for (int c = 0; c < D; c++) {
         const int j = rem % m;
@@ -274,8 +277,8 @@ __device__ int cta_vol(const Acc& acc, int ns, int k, int* out, VolSmem<D, NT>& 
     if (gact && slice == 0) {
 #pragma unroll
       for (int kk = 0; kk < GPT; kk++) {
-        const int g = grp * GPT + kk;
-        if (g >= G) break;
+        const int g = g_lo + grp * GPT + kk;
+        if (g >= g_hi) break;
         double b = best[kk];
         int ib = bi[kk];
         for (int sl = 1; sl < nslice; sl++) {
@@ -292,7 +295,8 @@ __device__ int cta_vol(const Acc& acc, int ns, int k, int* out, VolSmem<D, NT>& 
     }
     __syncthreads();
   }
-  if (evals && tid == 0) atomicAdd(evals, (unsigned long long)G * (unsigned long long)ns);
+  if (evals && tid == 0) atomicAdd(evals, (unsigned long long)(g_hi - g_lo) * (unsigned long long)ns);
+  if (split > 1) return -1;
   int* sel = sm.u.out.sel;
   for (int g = tid; g < G; g += NT) sel[g] = out[g];
   __syncthreads();
