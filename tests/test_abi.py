@@ -66,3 +66,15 @@ def test_null_safe_calls(P):
     assert L.h2_matvec(None, None, None) == -1
     assert L.h2_info(None, None) == -1
     assert L.h2_export(None, 1, None, 0, None) == -1
+
+
+@pytest.mark.parametrize("reduct,d", [(3, 3), (-1, 3), (2, 5), (2, 1)])
+def test_invalid_reduct_rejected(P, reduct, d):
+    """h2_options.reduct outside H2_REDUCT_*, or the surface reduction with d not in {2, 3}."""
+    L = P.lib()
+    o = P.h2_options_default()
+    o.reduct = reduct
+    dummy = (C.c_double * 8)()
+    h = L.h2_build_ex(C.cast(dummy, C.c_void_p), 100, d, 1, None, 1e-6, 16, 0.5, C.byref(o))
+    assert not h
+    assert L.h2_last_error() == -1

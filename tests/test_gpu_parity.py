@@ -406,3 +406,34 @@ def test_surface_reduct_needs_d_2_or_3():
     with pytest.raises(Exception):
         P.H2Matrix(torch.from_numpy(pts).cuda(), 2, [1.0], 1e-4, 64, reduct=P.H2_REDUCT_SURFACE)
     assert P.last_error()[0] == -1  # H2_ERR_INVALID_ARG
+
+
+@pytest.mark.parametrize("d,n,q", [(4, 6000, 32), (6, 5000, 64), (8, 4000, 64)])
+def test_parity_high_dimensions(d, n, q):
+    """d = 4, 6, 8 (the ABI's maximum): structure and r bit-exact, matvec within 2x of the oracle."""
+    pts = synth.uniform_cube(n, d, seed=10 + d)
+    o, r = oracle_build(pts, 2, [1.0], 1e-4, q)
+    g = gpu_build(pts, 2, [1.0], 1e-4, q)
+    assert g.info()["r"] == r
+    assert_structure_equal(g, o)
+    x = np.random.default_rng(d).standard_normal(n)
+    rows = np.arange(0, n, max(1, n // 500))
+    yg = g.matvec(torch.from_numpy(x).cuda()).cpu().numpy()[rows]
+    yo = o.matvec(x, rows)
+    yd = oracle.dense_rows(pts, 2, 1.0, x, rows)
+    eg = np.linalg.norm(yg - yd) / np.linalg.norm(yd)
+    eo = np.linalg.norm(yo - yd) / np.linalg.norm(yd)
+    assert eg <= 2.0 * eo + 1e-15
+    g.close()
+
+
+def test_parity_degenerate_collinear_points():
+    """Points on a line in 3-D (two box widths zero): the Vol grid collapses along those axes; the
+    structure and r stay bit-exact with the oracle."""
+    t = np.random.default_rng(5).random(8000)
+    pts = np.stack([t, 0.5 * t + 0.25, np.full_like(t, 0.3)], 1)
+    o, r = oracle_build(pts, 3, [0.2], 1e-6, 32)
+    g = gpu_build(pts, 3, [0.2], 1e-6, 32)
+    assert g.info()["r"] == r
+    assert_structure_equal(g, o)
+    g.close()
