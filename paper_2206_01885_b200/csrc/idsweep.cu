@@ -68,8 +68,9 @@ __host__ __device__ __forceinline__ int id_smem_class(int ny, int nx, int d) {
 // SMs.  cs = the cluster size the device runs (16, else 8; 0 disables the path); cl_min = the
 // block-entry threshold.
 constexpr int kIdClThreads = 512;
+constexpr int kIdClMaxNx = 8192;  // the cluster kernel's shared memory (~20 nx + 8 r bytes) stays < 200 KB
 __host__ __device__ __forceinline__ bool id_big(int ny, int nx, int d, int cs, int64_t cl_min) {
-  return cs >= 2 && nx >= 4 * cs && (int64_t)ny * nx >= cl_min && id_smem_class(ny, nx, d) < 0;
+  return cs >= 2 && nx >= 4 * cs && nx <= kIdClMaxNx && (int64_t)ny * nx >= cl_min && id_smem_class(ny, nx, d) < 0;
 }
 
 // per node of one level: |Xbar| (and child offsets), workspace and U sizes
@@ -606,7 +607,7 @@ static int id_cluster_max() {
 
 void id_sweep(h2_handle* h) {
   cudaStream_t s = h->stream;
-  H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   const int cs = id_cluster_max();
   static const int64_t cl_min = [] {  // H2_ID_CLMIN (tuning knob): cluster-path threshold, block entries
