@@ -574,11 +574,9 @@ static size_t id_cl_smem(int r, int nx_max) {
 
 // the largest cluster size the device schedules for the cluster kernel (16 needs the non-portable
 // opt-in), queried once; H2_ID_CLUSTER=0 disables the path (diagnostics)
-static int id_cluster_max() {
-  static int cs = -1;
-  if (cs >= 0) return cs;
+static int id_cluster_probe() {
   const char* env = getenv("H2_ID_CLUSTER");
-  if (env && atoi(env) == 0) return cs = 0;
+  if (env && atoi(env) == 0) return 0;
   int best = 0;
   for (int c : {16, 8}) {
     if (c == 16 && cudaFuncSetAttribute(id_kernel_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
@@ -602,7 +600,11 @@ static int id_cluster_max() {
     }
   }
   cudaGetLastError();
-  return cs = best;
+  return best;
+}
+static int id_cluster_max() {
+  static const int cs = id_cluster_probe();  // thread-safe one-time initialisation
+  return cs;
 }
 
 void id_sweep(h2_handle* h) {
