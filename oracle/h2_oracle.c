@@ -18,6 +18,8 @@
  *   B  admissibility Eq.(2.1) + interaction/nearfield lists
  *       via dual traversal                             orc_new
  *   C  volume-based DataReduct (used in all runs P:839)       orc_vol
+ *   C' farthest point sampling (reading C6)                    orc_fps
+ *   C'' surface-based DataReduct (reading C7)                  orc_surface
  *   D  HiDR, Algorithm 1                                     orc_hidr
  *   E  r calibration, Algorithm 2 line 2 + P:628-630                     orc_calibrate
  *   F  getBasis = pivoted-QR ID, Eqs.(4.1)-(4.4), bottom-up
