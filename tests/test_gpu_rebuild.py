@@ -77,3 +77,24 @@ def test_rebuild_rejects_a_foreign_comm_and_null_base():
     assert not P.lib().h2_rebuild_ex(None, 2, kp, 1e-6, None)
     comm.close()
     g.close()
+
+
+@pytest.mark.parametrize("reduct", [1, 2])
+def test_rebuild_keeps_the_reduction_of_the_base(reduct):
+    """HiDR once for all from a base built with FPS / the surface reduction: the rebuild reuses those
+    representor sets -- equal to a fresh build of the new kernel with the same reduction and r."""
+    c = synth.CONFIGS[4]
+    pts = synth.points(4, 40000)
+    X = torch.from_numpy(pts).cuda()
+    base = P.H2Matrix(X, c["kernel"], list(c["params"]), c["id_tol"], c["q"], c["tau"], storage=P.H2_STORE_ALL,
+                      reduct=reduct)
+    r = base.info()["r"]
+    rb = base.rebuild(2, [0.05], 1e-6, storage=P.H2_STORE_ALL)
+    fresh = P.H2Matrix(X, 2, [0.05], 1e-6, c["q"], c["tau"], r=r, storage=P.H2_STORE_ALL, reduct=reduct)
+    for name in ("XS_OFF", "XS_IDX", "YS_OFF", "YS_IDX", "K", "SK_IDX"):
+        assert np.array_equal(rb.export(name), fresh.export(name)), name
+    x = torch.from_numpy(synth.matvec_vector(4, 40000)).cuda()
+    ya, yb = rb.matvec(x), fresh.matvec(x)
+    assert torch.linalg.norm(ya - yb) <= 1e-12 * torch.linalg.norm(yb)
+    for g in (rb, fresh, base):
+        g.close()

@@ -179,16 +179,17 @@ def test_sharded_rebuild_equals_single_gpu_rebuild():
         assert np.linalg.norm(y - y_ref) <= 1e-12 * np.linalg.norm(y_ref)
 
 
-def test_sharded_fps_equals_single_gpu_fps():
-    """Farthest point sampling (reading C6) on a sharded build: every rank's X^* / Y^* and skeletons
-    equal the single-GPU FPS build, and the collective matvec equals its matvec."""
+@pytest.mark.parametrize("reduct", [1, 2])
+def test_sharded_fps_equals_single_gpu_fps(reduct):
+    """Farthest point sampling (reading C6) and the surface reduction (C7) on a sharded build: every
+    rank's X^* / Y^* and skeletons equal the single-GPU build, and the collective matvec equals its
+    matvec."""
     c = synth.CONFIGS[4]
     pts = synth.points(4, 30000)
     X = torch.from_numpy(pts).cuda()
     kp = list(c["params"])
-    ref = P.H2Matrix(X, c["kernel"], kp, c["id_tol"], c["q"], c["tau"], storage=P.H2_STORE_ALL,
-                     reduct=P.H2_REDUCT_FPS)
-    hs = build_sharded(pts, 3, c["kernel"], kp, c["id_tol"], c["q"], c["tau"], reduct=P.H2_REDUCT_FPS)
+    ref = P.H2Matrix(X, c["kernel"], kp, c["id_tol"], c["q"], c["tau"], storage=P.H2_STORE_ALL, reduct=reduct)
+    hs = build_sharded(pts, 3, c["kernel"], kp, c["id_tol"], c["q"], c["tau"], reduct=reduct)
     depth = ref.info()["depth"]
     xs_ref, ys_ref, sk_ref = slots(ref, "XS"), slots(ref, "YS"), slots(ref, "SK")
     for g in hs:  # exchanged: X^* and skeletons of every node; Y^* of the nodes the rank computed
