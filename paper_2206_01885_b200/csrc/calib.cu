@@ -67,11 +67,15 @@ template <int D>
 __global__ void __launch_bounds__(kCalThreads) calib_prep_kernel(int kid, double p2, double tau,
                                                                  const double* __restrict__ wl,
                                                                  const int* __restrict__ lv, const int* __restrict__ mv,
-                                                                 CalWork* work) {
+                                                                 const int* __restrict__ skip_level, CalWork* work) {
   __shared__ VolSmem<D, kCalThreads> vsm;
   __shared__ int s_ns;
   const int tid = threadIdx.x;
   CalWork& W = work[blockIdx.x];
+  if (skip_level && skip_level[lv[blockIdx.x]]) {  // the level already passed at a smaller m
+    if (tid == 0) W.ns = -1;
+    return;
+  }
   const double w = wl[blockIdx.x];
   const int level = lv[blockIdx.x], m = mv[blockIdx.x];
   const unsigned long long seed = kCalibSeed + (unsigned long long)level;
@@ -108,6 +112,7 @@ __global__ void __launch_bounds__(kCalCpqrThreads) calib_cpqr_kernel(double eps,
   __shared__ CpqrSmem<kCalCpqrThreads> csm;
   __shared__ double sv[N];
   CalWork& W = work[blockIdx.x];
+  if (W.ns < 0) return;  // skipped trial
   const int k = cta_cpqr<kCalCpqrThreads>(W.M, W.ns, N, 1e-3 * eps, W.piv, W.nrm2, sv, csm);
   if (threadIdx.x == 0) W.k = k;
 }
@@ -116,6 +121,7 @@ __global__ void __launch_bounds__(kCalCpqrThreads) calib_cpqr_kernel(double eps,
 template <int D>
 __global__ void __launch_bounds__(kCalThreads) calib_ks_kernel(int kid, double p2, CalWork* work) {
   CalWork& W = work[blockIdx.x];
+  if (W.ns < 0) return;
   const int k = W.k;
   for (int x = threadIdx.x; x < k * N; x += kCalThreads) {
     const int t = x / N, e = x % N;
@@ -133,6 +139,7 @@ __global__ void __launch_bounds__(kCalThreads) calib_err_kernel(int kid, double 
   __shared__ CpqrSmem<kCalThreads> csm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   CalWork& W = work[blockIdx.x / kErrSlices];
+  if (W.ns < 0) return;
   const int q = blockIdx.x % kErrSlices;
   const int ns = W.ns, k = W.k;
   constexpr int CPW = 4, EPL = N / 32;  // columns per warp, points per lane
@@ -187,6 +194,11 @@ __global__ void calib_final_kernel(double eps, const int* __restrict__ mv, int d
                                    int* pass) {
   const int t = blockIdx.x;  // one thread per trial
   CalWork& W = work[t];
+  if (W.ns < 0) {  // skipped: never chosen
+    err[t] = -1.0;
+    pass[t] = 0;
+    return;
+  }
   double num = 0.0, den = 0.0;
   for (int q = 0; q < kErrSlices; q++) {
     num += W.pnum[q];
@@ -225,7 +237,8 @@ static char* pinned_slot(int slot, size_t bytes) {
 // One batch of (level, m) trials on stream s; the per-trial pass flags land in job.pass_h
 // (page-locked) once the stream has reached the end of the batch.
 static void launch_trials(h2_handle* h, cudaStream_t s, int slot, const std::vector<double>& wl,
-                          const std::vector<int>& lv, const std::vector<int>& mv, CalibJob& job) {
+                          const std::vector<int>& lv, const std::vector<int>& mv, const int* skip_level,
+                          CalibSet& job) {
   const int T = (int)wl.size();
   job.T = T;
   if (T == 0) return;
@@ -252,7 +265,7 @@ static void launch_trials(h2_handle* h, cudaStream_t s, int slot, const std::vec
 #define H2_CAL_CASE(DD)                                                                                   \
   case DD:                                                                                                \
     calib_prep_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, h->tau, dw + b0, dl + b0, dm + b0,         \
-                                                     job.work.as<CalWork>());                              \
+                                                     skip_level, job.work.as<CalWork>());                  \
     calib_cpqr_kernel<<<nb, kCalCpqrThreads, 0, s>>>(h->id_tol, job.work.as<CalWork>());                  \
     calib_ks_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, job.work.as<CalWork>());                    \
     calib_err_kernel<DD><<<nb * kErrSlices, kCalThreads, 0, s>>>(h->kid, p2, job.work.as<CalWork>());        \
@@ -271,34 +284,53 @@ static void launch_trials(h2_handle* h, cudaStream_t s, int slot, const std::vec
   job.mv = mv;
 }
 
+// passed[lv[t]] = 1 for every passing trial t of phase 0 (benign same-value races).
+__global__ void level_passed_kernel(int T, const int* __restrict__ lv, const int* __restrict__ pass, int* passed) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < T && pass[t]) passed[lv[t]] = 1;
+}
+
 static long long grid_size(int d, int m) {
   long long G = 1;
   for (int c = 0; c < d; c++) G *= m;
   return G;
 }
 
-// Phase 0, issued right after the tree (a1-a3) on the stream `s`: the trials with m^d <= 64 for
-// EVERY level 1..depth.  A trial depends only on the level's box width W 2^-l, not on the lists,
-// so it overlaps a4; calibrate_end keeps the levels that hold an admissible pair.
+// Issued right after the tree (a1-a3) on the stream `s`, overlapping a4 -- a trial depends only on
+// the level's box width W 2^-l, not on the lists.  Phase 0: the trials with m^d <= 64 for EVERY level
+// 1..depth.  Phase 1 (speculative): the trials with m^d > 64 for every level, each exiting at once
+// when a phase-0 trial of its level passed.  calibrate_end keeps the levels that hold an admissible
+// pair; levels without one cost trials but never decide r.
 void calibrate_begin(h2_handle* h, cudaStream_t s, CalibJob& job) {
   job.stream = s;
-  std::vector<double> wl;
-  std::vector<int> lv, mv;
+  std::vector<double> wl, wl1;
+  std::vector<int> lv, mv, lv1, mv1;
   for (int l = 1; l <= h->depth; l++)
     for (int m = 1;; m++) {
       const long long G = grid_size(h->d, m);
-      if (G > 64 && m > 1) break;
-      wl.push_back(ldexp(h->W, -l));
-      lv.push_back(l);
-      mv.push_back(m);
+      const bool p0 = G <= 64 || m == 1;
+      (p0 ? wl : wl1).push_back(ldexp(h->W, -l));
+      (p0 ? lv : lv1).push_back(l);
+      (p0 ? mv : mv1).push_back(m);
       if (G >= N) break;
     }
-  launch_trials(h, s, 0, wl, lv, mv, job);
+  job.passed = Scratch(sizeof(int) * 64, s);
+  H2_CUDA_TRY(cudaMemsetAsync(job.passed.p, 0, sizeof(int) * 64, s));
+  launch_trials(h, s, 0, wl, lv, mv, nullptr, job.p0);
+  if (!wl1.empty()) {
+    if (job.p0.T > 0) {
+      const int* dl = reinterpret_cast<const int*>(job.p0.params.as<double>() + job.p0.T);
+      const int* dpass = reinterpret_cast<const int*>(job.p0.outs.as<double>() + job.p0.T);
+      level_passed_kernel<<<(job.p0.T + 127) / 128, 128, 0, s>>>(job.p0.T, dl, dpass, job.passed.as<int>());
+      H2_CHECK_LAUNCH();
+      h->gpu_launches += 1;
+    }
+    launch_trials(h, s, 1, wl1, lv1, mv1, job.passed.as<int>(), job.p1);
+  }
   job.active = true;
 }
 
-// r = max over the levels holding an admissible pair of the first passing m^d (phase 0 results,
-// then phase 1 -- m^d > 64 -- on h->stream for the levels still open).
+// r = max over the levels holding an admissible pair of the first passing m^d (phase 0, then phase 1).
 int calibrate_end(h2_handle* h, CalibJob& job) {
   cudaStream_t s = h->stream;
   Scratch hasd(sizeof(int) * 64, s);
@@ -311,35 +343,19 @@ int calibrate_end(h2_handle* h, CalibJob& job) {
   H2_CUDA_TRY(cudaStreamSynchronize(s));
   if (job.active) H2_CUDA_TRY(cudaStreamSynchronize(job.stream));
   std::vector<int> chosen(h->depth + 1, 0);
-  for (int t = 0; t < job.T; t++)  // trials of a level are in increasing m: keep the first pass
-    if (job.pass_h[t] && !chosen[job.lv[t]]) chosen[job.lv[t]] = job.mv[t];
-  // release phase 0's buffers on h->stream (ordered after the synchronisation above)
-  job.work.s = job.params.s = job.outs.s = s;
-  job.work = Scratch();
-  job.params = Scratch();
-  job.outs = Scratch();
+  for (CalibSet* set : {&job.p0, &job.p1})  // trials of a level are in increasing m: keep the first pass
+    for (int t = 0; t < set->T; t++)
+      if (set->pass_h[t] && !chosen[set->lv[t]]) chosen[set->lv[t]] = set->mv[t];
+  // release the buffers on h->stream (ordered after the synchronisation above)
+  for (CalibSet* set : {&job.p0, &job.p1}) {
+    set->work.s = set->params.s = set->outs.s = s;
+    set->work = Scratch();
+    set->params = Scratch();
+    set->outs = Scratch();
+  }
+  job.passed.s = s;
+  job.passed = Scratch();
   job.active = false;
-  std::vector<double> wl;
-  std::vector<int> lv, mv;
-  for (int l = 1; l <= h->depth; l++) {
-    if (!has[l] || chosen[l]) continue;
-    for (int m = 1;; m++) {
-      const long long G = grid_size(h->d, m);
-      if (G > 64) {
-        wl.push_back(ldexp(h->W, -l));
-        lv.push_back(l);
-        mv.push_back(m);
-      }
-      if (G >= N) break;
-    }
-  }
-  if (!wl.empty()) {
-    CalibJob p1;
-    launch_trials(h, s, 1, wl, lv, mv, p1);
-    H2_CUDA_TRY(cudaStreamSynchronize(s));
-    for (int t = 0; t < p1.T; t++)
-      if (p1.pass_h[t] && !chosen[p1.lv[t]]) chosen[p1.lv[t]] = p1.mv[t];
-  }
   int r = 1;
   for (int l = 1; l <= h->depth; l++)
     if (has[l] && chosen[l]) r = (int)std::max<long long>(r, grid_size(h->d, chosen[l]));
