@@ -198,12 +198,21 @@ __global__ void __launch_bounds__(256, 2) nf_matvec_kernel(int64_t nitems, const
                                                            const int64_t* __restrict__ voff,
                                                            const int* __restrict__ nbegin, const int* __restrict__ nend,
                                                            const double* __restrict__ Dv, const double* __restrict__ xt,
-                                                           double* yt) {
+                                                           double* yt, int kMvPfRows,
+                                                           unsigned long long* ctr) {
   constexpr int WC = 32 * CW * SPLIT, G = 16, PF = CW >= 3 ? 4 : 8;
   static_assert(G % PF == 0, "the prefetch ring must wrap with the row groups");
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < nitems * SPLIT; v += nw) {
+  // items in grid-stride order, or (ctr != nullptr) taken dynamically by whole warps
+  auto next = [&](int64_t cur) -> int64_t {
+    if (!ctr) return cur + nw;
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(ctr, 1ULL);
+    return (int64_t)__shfl_sync(0xffffffffu, t, 0);
+  };
+  const int64_t v0 = ctr ? next(0) : (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  for (int64_t v = v0; v < nitems * SPLIT; v = next(v)) {
     const int64_t it = v / SPLIT;
     const int half = (int)(v - it * SPLIT);
     const int p = imap[it];
@@ -222,7 +231,32 @@ __global__ void __launch_bounds__(256, 2) nf_matvec_kernel(int64_t nitems, const
       xj[s] = ok[s] ? xt[bj + col] : 0.0;
       acc[s] = 0.0;
     }
-    const double* Dp = Dv + voff[p] + c0 + lane;
+    const double* Db = Dv + voff[p] + c0;
+    const double* Dp = Db + lane;
+    // L2 prefetch of rows [a, a + G) of the slice, kMvPfRows rows ahead of their use: the register
+    // ring holds only PF rows, so HBM would see too few bytes in flight per warp; prefetches hold no
+    // registers.  A slice spanning whole rows is one contiguous range (128-byte lines over the
+    // lanes); otherwise lane l takes row a + (l & 15) and every second line from l >> 4.
+    const bool contig = c0 == 0 && nj <= 32 * CW;
+    const int wbytes = 8 * (nj - c0 < 32 * CW ? nj - c0 : 32 * CW);
+    auto prefetch_rows = [&](int a, int a_end) {
+      if (a_end > ni) a_end = ni;
+      if (a >= a_end) return;
+      if (contig) {
+        const uintptr_t b = reinterpret_cast<uintptr_t>(Db + (int64_t)a * nj) & ~(uintptr_t)127;
+        const uintptr_t e = reinterpret_cast<uintptr_t>(Db + (int64_t)a_end * nj);
+        for (uintptr_t q = b + 128 * lane; q < e; q += 32 * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+      } else {
+        const int row = a + (lane & 15);
+        if (row < a_end) {
+          const uintptr_t b = reinterpret_cast<uintptr_t>(Db + (int64_t)row * nj);
+          for (int o = 128 * (lane >> 4); o < wbytes + 128; o += 256)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"((b & ~(uintptr_t)127) + o));
+        }
+      }
+    };
+    if (kMvPfRows > 0) prefetch_rows(0, kMvPfRows + G);
     auto load_row = [&](int a, double (&b)[CW], double& xa) {
       if (a < ni) {  // warp-uniform
         const double* row = Dp + (int64_t)a * nj;
@@ -240,6 +274,7 @@ __global__ void __launch_bounds__(256, 2) nf_matvec_kernel(int64_t nitems, const
 #pragma unroll
     for (int q = 0; q < PF; q++) load_row(q, buf[q], xbuf[q]);
     for (int a0 = 0; a0 < ni; a0 += G) {
+      if (kMvPfRows > 0) prefetch_rows(a0 + kMvPfRows + G, a0 + kMvPfRows + 2 * G);
       double part[G];
 #pragma unroll
       for (int q = 0; q < G; q++) {
@@ -453,6 +488,24 @@ static bool mv_bulk() {
   return v;
 }
 
+// H2_MV_PF (A/B knob, read once): the nearfield matvec's L2 prefetch distance in rows beyond the
+// current 16-row group (0 = no prefetch)
+static int mv_pf_rows() {
+  static const int v = [] {
+    const char* e = getenv("H2_MV_PF");
+    return e ? atoi(e) : 16;
+  }();
+  return v;
+}
+
+static bool mv_dyn() {
+  static const bool v = [] {
+    const char* e = getenv("H2_MV_DYN");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 template <int D>
 static void launch_far_near(const h2_handle* h, double p2, const double* zh, double* yh, const double* xt, double* yt,
                             int which, cudaStream_t s) {
@@ -468,7 +521,7 @@ static void launch_far_near(const h2_handle* h, double p2, const double* zh, dou
   if (which == 1 && h->n_np > 0 && h->np_stored && h->nf_nunits > 0) {
     const int cw = h->nf_wc / 32;
     const int64_t blocks = (2 * h->nf_nitems + 7) / 8;  // (split items: up to two warps per item)
-    const unsigned g = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
+    unsigned g = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
     if (mv_bulk()) {
       const int smem = (int)(sizeof(double) * (2 * kMvBulkBuf + kMvBulkWarps * 32 * cw));
       const unsigned gb = (unsigned)(h->nf_nunits < 148 * 2 ? h->nf_nunits : 148 * 2);
@@ -486,11 +539,20 @@ static void launch_far_near(const h2_handle* h, double p2, const double* zh, dou
       }
       return;
     }
+    // H2_MV_DYN (default 1): one resident wave (2 CTAs per SM) taking items from a counter
+    Scratch ctr_s;
+    unsigned long long* ctr = nullptr;
+    if (mv_dyn()) {
+      ctr_s = Scratch(sizeof(unsigned long long), s);
+      ctr = ctr_s.as<unsigned long long>();
+      H2_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s));
+      if (g > 148 * 2) g = 148 * 2;
+    }
     switch (cw) {
 #define H2_NFMV_CASE(C, CWW, SP)                                                                              \
   case C:                                                                                                    \
     nf_matvec_kernel<CWW, SP><<<g, 256, 0, s>>>(h->nf_nitems, h->nf_imap, h->nf_ioff, h->np_pairs, h->np_off,     \
-                                                h->nbegin, h->nend, h->np_val, xt, yt);                      \
+                                                h->nbegin, h->nend, h->np_val, xt, yt, mv_pf_rows(), ctr);    \
     break;
       H2_NFMV_CASE(2, 2, 1) H2_NFMV_CASE(3, 3, 1) H2_NFMV_CASE(4, 4, 1) H2_NFMV_CASE(5, 5, 1)
       H2_NFMV_CASE(6, 3, 2) H2_NFMV_CASE(8, 4, 2)
