@@ -88,36 +88,72 @@ __global__ void coupling_kernel(int64_t np, const int2* __restrict__ pairs, cons
   }
 }
 
-// stored coupling blocks (k_i x k_j, small): warp per pair, lanes over columns; each row adds one
-// warp-reduced dot to y^_i (one atomic per row) and its column contributions to registers (one
-// atomic per column per pair): every entry read once, coalesced along the row
+// stored coupling blocks (k_i x k_j, small): warp per pair, lanes over columns, rows in chunks of
+// 8 (eight independent loads in flight); the row dots of a chunk are warp-reduced by a transposing
+// butterfly (lane l ends with row l & 7: one atomic per row) and the column contributions kept in
+// registers (one atomic per column per pair): every entry read once, coalesced along the row
 __global__ void __launch_bounds__(256) coupling_mv_kernel(int64_t np, const int2* __restrict__ pairs,
                                                           const int64_t* __restrict__ voff, const double* __restrict__ B,
                                                           const int* __restrict__ k, int r,
                                                           const double* __restrict__ zh, double* yh) {
+  constexpr int RC = 8;
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < np; p += nw) {
-    const int2 pr = pairs[p];
-    const int i = pr.x, j = pr.y, ki = k[i], kj = k[j];
-    const double* Bp = B + voff[p];
-    const double* zi = zh + (int64_t)i * r;
-    const double* zj = zh + (int64_t)j * r;
-    double* yi = yh + (int64_t)i * r;
-    double* yj = yh + (int64_t)j * r;
-    for (int c0 = 0; c0 < kj; c0 += 32) {
-      const int col = c0 + lane;
-      const bool ok = col < kj;
-      const double zc = ok ? zj[col] : 0.0;
-      double acc = 0.0;
-      for (int a = 0; a < ki; a++) {
-        const double v = ok ? Bp[(int64_t)a * kj + col] : 0.0;
-        double part = v * zc;
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        if (lane == 0) atomicAdd(yi + a, part);
-        acc = fma(v, zi[a], acc);
+  // the warp takes 32 consecutive pairs at a time; their metadata is loaded in one round (lane t
+  // holds pair p0 + t) and broadcast by shuffles, so no pair waits on its own dependent loads
+  for (int64_t p0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 32; p0 < np; p0 += nw * 32) {
+    const int64_t pl = p0 + lane;
+    int mi = 0, mj = 0, mki = 0, mkj = 0;
+    long long mvo = 0;
+    if (pl < np) {
+      const int2 pr = pairs[pl];
+      mi = pr.x;
+      mj = pr.y;
+      mvo = voff[pl];
+      mki = k[mi];
+      mkj = k[mj];
+    }
+    const int cnt = np - p0 < 32 ? (int)(np - p0) : 32;
+    for (int t = 0; t < cnt; t++) {
+      const int i = __shfl_sync(0xffffffffu, mi, t), j = __shfl_sync(0xffffffffu, mj, t);
+      const int ki = __shfl_sync(0xffffffffu, mki, t), kj = __shfl_sync(0xffffffffu, mkj, t);
+      const double* Bp = B + __shfl_sync(0xffffffffu, mvo, t);
+      const double* zi = zh + (int64_t)i * r;
+      const double* zj = zh + (int64_t)j * r;
+      double* yi = yh + (int64_t)i * r;
+      double* yj = yh + (int64_t)j * r;
+      for (int c0 = 0; c0 < kj; c0 += 32) {
+        const int col = c0 + lane;
+        const bool ok = col < kj;
+        const double zc = ok ? zj[col] : 0.0;
+        double acc = 0.0;
+        for (int a0 = 0; a0 < ki; a0 += RC) {
+          double v[RC], part[RC];
+#pragma unroll
+          for (int u = 0; u < RC; u++) v[u] = ok && a0 + u < ki ? Bp[(int64_t)(a0 + u) * kj + col] : 0.0;
+#pragma unroll
+          for (int u = 0; u < RC; u++) {
+            part[u] = v[u] * zc;
+            acc = fma(v[u], a0 + u < ki ? zi[a0 + u] : 0.0, acc);
+          }
+#pragma unroll
+          for (int u = 0; u < RC; u++) {
+            part[u] += __shfl_xor_sync(0xffffffffu, part[u], 16);
+            part[u] += __shfl_xor_sync(0xffffffffu, part[u], 8);
+          }
+#pragma unroll
+          for (int o = 4, w = 4; o > 0; o >>= 1, w >>= 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int q = 0; q < w; q++) {
+              const double lo = part[q], hi = part[q + w];
+              part[q] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, o);
+            }
+          }
+          if (lane < RC && a0 + lane < ki) atomicAdd(yi + a0 + lane, part[0]);
+        }
+        if (ok) atomicAdd(yj + col, acc);
       }
-      if (ok) atomicAdd(yj + col, acc);
     }
   }
 }
@@ -498,6 +534,14 @@ static int mv_pf_rows() {
   return v;
 }
 
+static int mv_order() {
+  static const int v = [] {
+    const char* e = getenv("H2_MV_ORDER");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 static bool mv_dyn() {
   static const bool v = [] {
     const char* e = getenv("H2_MV_DYN");
@@ -510,7 +554,7 @@ template <int D>
 static void launch_far_near(const h2_handle* h, double p2, const double* zh, double* yh, const double* xt, double* yt,
                             int which, cudaStream_t s) {
   if (which == 0 && h->n_cp > 0 && h->cp_stored) {
-    const int64_t blocks = (h->n_cp + 7) / 8;
+    const int64_t blocks = (h->n_cp + 255) / 256;  // 8 warps x 32 pairs
     const unsigned g = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
     coupling_mv_kernel<<<g, 256, 0, s>>>(h->n_cp, h->cp_pairs, h->cp_off, h->cp_val, h->k, h->r, zh, yh);
   } else if (which == 0 && h->n_cp > 0) {
@@ -600,14 +644,16 @@ void matvec(const h2_handle* h, const double* x, double* y) {
   const double p2 = kernel_p2(h->kid, h->kp);
   // nearfield on the build's lowest-priority stream, forked after permute_in: its short CTAs yield
   // SM slots to the farfield chain's level kernels on `s` as they retire
-  cudaStream_t ns = h->low ? h->low : s;
+  // H2_MV_ORDER=1 (A/B knob): the farfield chain first, then the nearfield pass, on one stream
+  const bool far_first = mv_order() == 1;
+  cudaStream_t ns = h->low && !far_first ? h->low : s;
   cudaEvent_t ev[2] = {nullptr, nullptr};
   if (ns != s) {
     for (auto& e : ev) H2_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     H2_CUDA_TRY(cudaEventRecord(ev[0], s));
     H2_CUDA_TRY(cudaStreamWaitEvent(ns, ev[0], 0));
   }
-  far_near(h, p2, zh.as<double>(), yh.as<double>(), xt.as<double>(), yt.as<double>(), 1, ns);
+  if (!far_first) far_near(h, p2, zh.as<double>(), yh.as<double>(), xt.as<double>(), yt.as<double>(), 1, ns);
   if (ns != s) H2_CUDA_TRY(cudaEventRecord(ev[1], ns));
   auto up = [&](int l) {
     const LevelRange lr = level_range(h, l);
@@ -629,6 +675,7 @@ void matvec(const h2_handle* h, const double* x, double* y) {
                                                            h->xbar_n, h->child_off, h->u_off, h->U, h->p_lo, h->p_hi,
                                                            yh.as<double>(), yf.as<double>());
   }
+  if (far_first) far_near(h, p2, zh.as<double>(), yh.as<double>(), xt.as<double>(), yt.as<double>(), 1, s);
   if (ns != s) H2_CUDA_TRY(cudaStreamWaitEvent(s, ev[1], 0));
   if (sharded) {
     add_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, yf.as<double>(), yt.as<double>());
