@@ -168,8 +168,8 @@ __global__ void __launch_bounds__(kNfThreads, MINB * kNfScale) nf_fill_kernel(in
                                                                      unsigned long long* ctl) {
   static_assert(CW >= 1 && CW <= 8, "1..8 column slots");
   constexpr int WC = 32 * CW;
-  __shared__ double tab[256];
-  for (int e = threadIdx.x; e < 256; e += kNfThreads) tab[e] = kExp2Tab256[e];
+  __shared__ double tab[kFillTab];
+  for (int e = threadIdx.x; e < kFillTab; e += kNfThreads) tab[e] = kExp2Tab2048[e];
   __syncthreads();
   const int lane = threadIdx.x & 31;
   // Work is taken by warps in chunks of upc consecutive units from a global counter (ctl[0]).
@@ -238,8 +238,8 @@ __global__ void __launch_bounds__(kFillThreads) cp_fill_kernel(int64_t np, const
                                                                const int* __restrict__ k, const int* __restrict__ sk,
                                                                int r, const double* __restrict__ X, int64_t n,
                                                                double cs, double* __restrict__ out) {
-  __shared__ double tab[256];
-  tab[threadIdx.x] = kExp2Tab256[threadIdx.x];
+  __shared__ double tab[kFillTab];
+  for (int e = threadIdx.x; e < kFillTab; e += blockDim.x) tab[e] = kExp2Tab2048[e];
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t nunits = (np + 31) >> 5;
