@@ -72,7 +72,11 @@ __global__ void __launch_bounds__(kCalThreads) calib_prep_kernel(int kid, double
   __shared__ int s_ns;
   const int tid = threadIdx.x;
   CalWork& W = work[blockIdx.x];
-  if (skip_level && skip_level[lv[blockIdx.x]]) {  // the level already passed at a smaller m
+  long long Gm = 1;
+  for (int c = 0; c < D; c++) Gm *= mv[blockIdx.x];
+  // skipped: the level already passed at a smaller m, or m^d >= N (passes by definition, so its
+  // error is never needed)
+  if ((skip_level && skip_level[lv[blockIdx.x]]) || Gm >= N) {
     if (tid == 0) W.ns = -1;
     return;
   }
@@ -194,9 +198,11 @@ __global__ void calib_final_kernel(double eps, const int* __restrict__ mv, int d
                                    int* pass) {
   const int t = blockIdx.x;  // one thread per trial
   CalWork& W = work[t];
-  if (W.ns < 0) {  // skipped: never chosen
-    err[t] = -1.0;
-    pass[t] = 0;
+  long long G = 1;
+  for (int c = 0; c < d; c++) G *= mv[t];
+  if (W.ns < 0) {  // skipped: a pass-through trial (m^d >= N) passes, a skipped level's never counts
+    err[t] = G >= N ? 0.0 : -1.0;
+    pass[t] = G >= N;
     return;
   }
   double num = 0.0, den = 0.0;
@@ -204,8 +210,6 @@ __global__ void calib_final_kernel(double eps, const int* __restrict__ mv, int d
     num += W.pnum[q];
     den += W.pden[q];
   }
-  long long G = 1;
-  for (int c = 0; c < d; c++) G *= mv[t];
   const double e = den > 0.0 ? sqrt(num) / sqrt(den) : 0.0;
   err[t] = e;
   pass[t] = (e < 1e-2 * eps) || G >= N;
