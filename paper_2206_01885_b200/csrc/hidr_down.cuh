@@ -126,7 +126,7 @@ __device__ __forceinline__ double warp_min_ub(double v) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(kDownThreads, 4) hidr_down_kernel(
+__global__ void __launch_bounds__(kDownThreads, D <= 2 ? 5 : 4) hidr_down_kernel(
     const double* __restrict__ X, int64_t n, int base, int r, const int* __restrict__ parent,
     const int64_t* __restrict__ il_off, const int* __restrict__ il_idx,
     const int* __restrict__ xs, const double* __restrict__ xbox, const double* __restrict__ ybox,
