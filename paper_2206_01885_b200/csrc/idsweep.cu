@@ -46,6 +46,11 @@ constexpr int kIdLean = kIdClasses;      // its class number
 __host__ __device__ __forceinline__ int64_t id_smem_bytes_lean(int ny, int nx) {
   return 8LL * ((int64_t)ny * nx + nx + ny) + 8LL * nx + 512;
 }
+// what a lean node asks for: its footprint plus staged coordinates when both fit the class
+__host__ __device__ __forceinline__ int64_t id_lean_request(int ny, int nx, int d) {
+  const int64_t b = id_smem_bytes_lean(ny, nx), bs = b + 8LL * d * (nx + ny);
+  return bs <= kIdLeanMax ? bs : b;
+}
 // Layout of a shared-memory block: row-major with a thread per column (cta_cpqr_rm) unless the
 // block is tall enough that a warp per column (cta_cpqr, column-major) takes fewer serial steps:
 // per pivot step ~ceil(nx / NT) * ny smem accesses per thread against ceil(nx / (NT/32)) *
@@ -113,7 +118,7 @@ __global__ void id_sizes_kernel(int base, int count, int d, const int* __restric
          : nx > 0 && cls < 0 ? (int64_t)ny * nx + nx + ny + nx + 2 : 0;
   usz[t] = (int64_t)nx * mn;
   if (nx > 0 && cls >= 0)
-    atomicMax(smax + cls, (int)(cls == kIdLean ? id_smem_bytes_lean(ny, nx) : id_smem_bytes(ny, nx, d)));
+    atomicMax(smax + cls, (int)(cls == kIdLean ? id_lean_request(ny, nx, d) : id_smem_bytes(ny, nx, d)));
 }
 
 template <int kIdThreads>
@@ -473,11 +478,19 @@ __global__ void __launch_bounds__(NT) id_kernel_smem(
   double* M = sh;
   double* nrm2 = M + (int64_t)ny * nx;
   double* v = nrm2 + nx;
-  double* cx = v + ny;                      // Xbar coordinates, [c * nx + b] (staged classes)
-  double* cy = cx + D * nx;                 // Y^* coordinates, [c * ny + a]
-  double* tab = kLean ? v + ny : cy + D * ny;  // exp table
+  double* tab = kLean ? v + ny : v + ny + D * (nx + ny);  // exp table
   int* piv = reinterpret_cast<int*>(tab + 64);
   int* xb = piv + nx;
+  // staged coordinates: Xbar [c * nx + b], Y^* [c * ny + a]; before the table in the staged classes,
+  // behind xb in the lean one, whose CTAs all get the level's largest request (id_lean_request): a
+  // node whose block leaves room stages them too (its block generation then reads no global memory)
+  double* cx = kLean ? reinterpret_cast<double*>(xb + nx) : v + ny;
+  double* cy = cx + D * nx;
+  const bool staged = !kLean || [&] {
+    unsigned dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    return id_smem_bytes_lean(ny, nx) + 8LL * D * (nx + ny) <= (int64_t)dyn;
+  }();
   if (tid < 64) tab[tid] = kExp2Tab64[tid];
   if (is_leaf[i]) {
     for (int b = tid; b < nx; b += NT) xb[b] = nbegin[i] + b;
@@ -491,7 +504,7 @@ __global__ void __launch_bounds__(NT) id_kernel_smem(
     }
   }
   const int* yv = ys + (int64_t)i * r;
-  if (!kLean) {
+  if (staged) {
     for (int a = tid; a < ny; a += NT)
 #pragma unroll
       for (int c = 0; c < D; c++) cy[c * ny + a] = X[c * n + yv[a]];
@@ -502,8 +515,8 @@ __global__ void __launch_bounds__(NT) id_kernel_smem(
   }
   __syncthreads();
   const bool tall = id_tall(ny, nx, NT);
-  auto coord_x = [&](int c, int b) { return kLean ? X[c * n + xb[b]] : cx[c * nx + b]; };
-  auto coord_y = [&](int c, int a) { return kLean ? X[c * n + yv[a]] : cy[c * ny + a]; };
+  auto coord_x = [&](int c, int b) { return staged ? cx[c * nx + b] : X[c * n + xb[b]]; };
+  auto coord_y = [&](int c, int a) { return staged ? cy[c * ny + a] : X[c * n + yv[a]]; };
   int k;
   if (!tall) {
     // A^T row-major: M[a*nx + b] = K(Xbar[b], Y^*[a]), Y^* ascending; thread per column b, the
