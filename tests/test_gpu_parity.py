@@ -437,3 +437,33 @@ def test_parity_degenerate_collinear_points():
     assert g.info()["r"] == r
     assert_structure_equal(g, o)
     g.close()
+
+
+_MV_DUMP = """
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2206_01885_b200 as P, synth
+cfg, n, out = int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+c = synth.CONFIGS[cfg]
+X = torch.from_numpy(synth.points(cfg, n)).cuda()
+g = P.H2Matrix(X, c["kernel"], list(c["params"]), c["id_tol"], c["q"], c["tau"], storage=P.H2_STORE_ALL)
+x = torch.from_numpy(synth.matvec_vector(cfg, n)).cuda()
+np.save(out, g.matvec(x).cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("knobs", [{"H2_MV_DYN": "0"}, {"H2_MV_PF": "0"}, {"H2_MV_ORDER": "1"}, {"H2_MV_BULK": "1"}])
+def test_matvec_variants_equal_default(knobs, tmp_path):
+    """The stored-block matvec's scheduling variants (grid-stride instead of the resident wave, no L2
+    prefetch, farfield chain first, the bulk-copy nearfield kernel) against the default on the same
+    stored build: the same products, summed by atomics in another order (relative 1e-12)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    ys = []
+    for env_extra in ({}, knobs):
+        out = str(tmp_path / f"y{len(ys)}.npy")
+        env = dict(os.environ, **env_extra)
+        subprocess.run([sys.executable, "-c", _MV_DUMP, root, "4", "200000", out], env=env, check=True, timeout=600)
+        ys.append(np.load(out))
+    assert np.linalg.norm(ys[1] - ys[0]) <= 1e-12 * np.linalg.norm(ys[0])
