@@ -52,6 +52,10 @@ def lib():
         L.orc_calib_level.argtypes = [i32, i32, f64, f64, f64, f64, i32]
         L.orc_calib_trial.restype = f64
         L.orc_calib_trial.argtypes = [i32, i32, f64, f64, f64, f64, i32, i32, vp]
+        L.orc_calib_trial_ex.restype = f64
+        L.orc_calib_trial_ex.argtypes = [i32, i32, f64, f64, f64, f64, i32, i32, vp, vp, vp, vp, vp]
+        L.orc_calib_points.argtypes = [i32, f64, f64, i32, vp, vp]
+        L.orc_calib_levels.argtypes = [vp, vp]
         L.orc_id_sweep.argtypes = [vp, i32, f64, f64]
         L.orc_export.restype = i64
         L.orc_export.argtypes = [vp, i32, vp, i64]
@@ -156,6 +160,26 @@ def calib_trial(d, kid, param, eps, tau, w, level, m):
     return float(e), int(G[0])
 
 
+def calib_points(d, tau, w, level):
+    """E4/E6: the calibration point sets (Z1, Z2) of one level, each 256 x d."""
+    Z1 = np.empty((256, d), np.float64)
+    Z2 = np.empty((256, d), np.float64)
+    lib().orc_calib_points(d, float(tau), float(w), int(level), _p(Z1), _p(Z2))
+    return Z1, Z2
+
+
+def calib_trial_ex(d, kid, param, eps, tau, w, level, m) -> dict:
+    """One calibration trial with its internals: e, G = m^d, the ID rank k, the skeleton rows
+    (indices into Z1) and the columns Z2* (indices into Z2)."""
+    G = np.zeros(1, np.int64)
+    k = np.zeros(1, np.int32)
+    ns = np.zeros(1, np.int32)
+    skel = np.zeros(256, np.int32)
+    sel = np.zeros(256, np.int32)
+    e = lib().orc_calib_trial_ex(d, kid, param, eps, tau, w, level, m, _p(G), _p(k), _p(skel), _p(sel), _p(ns))
+    return dict(e=float(e), G=int(G[0]), k=int(k[0]), skel=skel[:k[0]].copy(), sel=sel[:ns[0]].copy())
+
+
 def dense_rows(pts: np.ndarray, kid: int, param: float, x: np.ndarray, rows) -> np.ndarray:
     """I. exact (K x)[rows] over all n points (original order)."""
     pts = np.ascontiguousarray(pts, np.float64)
@@ -249,6 +273,12 @@ class OracleH2:
     # --- stages ---
     def calibrate(self, kid: int, param: float, eps: float) -> int:
         return int(lib().orc_calibrate(self._h, kid, float(param), float(eps)))
+
+    def calib_levels(self) -> np.ndarray:
+        """E4: the per-level r of the last calibrate() (0 where a level has no admissible pair)."""
+        out = np.zeros(64, np.int32)
+        c = lib().orc_calib_levels(self._h, _p(out))
+        return out[:c].copy()
 
     def hidr(self, r: int):
         if lib().orc_hidr(self._h, int(r)) != 0:

@@ -28,8 +28,9 @@
  *   H  H^2 matvec, four passes                                   orc_matvec_rows
  *   I  dense rows of K x                                     orc_dense_rows
  *
- * Parity pins: see tests/test_oracle_*.py.  Every function here is pinned except the calibration
- * (E) beyond its special cases -- "parity unpinned" for E's general case.
+ * Parity pins: see tests/test_oracle_*.py.  Every function here is pinned; the calibration (E) and
+ * the top-down composition of D by tests/test_oracle_calib_topdown_pins.py (Eckart-Young and
+ * least-squares identities, the pass-through bound, an independent SplitMix64, a hand golden).
  */
 #include <limits.h>
 #include <math.h>
@@ -357,6 +358,7 @@ typedef struct orc_h2 {
   int* xbar_n;    /* |Xbar_i| */
   double** U;     /* |Xbar_i| x k_i, column-major */
   int* child_off; /* offset of node's skeleton rows inside its parent's Xbar */
+  int calib_r[64]; /* E: per-level r of the last orc_calibrate (0 = level without an admissible pair) */
   double t_stage[8];
 } orc_h2;
 
@@ -780,17 +782,27 @@ static uint64_t splitmix64(uint64_t* state) {
 #define ORC_CAL_NPTS 256
 #define ORC_CAL_SEED 2206018850ULL
 
-/* calibration trial at box width w and grid m: returns the relative Frobenius error e (E5) of
- * the ID built from K(Z1, Z2*) applied to the full K(Z1, Z2); *G_out = m^d.                  */
-double orc_calib_trial(int d, int kid, double p, double eps, double tau, double w, int level,
-                       int m, int64_t* G_out) {
+/* The random well-separated point sets of one calibration level (E4, E6): Z1 = 256 points in
+ * [0,w]^d, then Z2 = 256 points in [0,w]^d shifted by w/tau in every coordinate, drawn with
+ * SplitMix64 from seed 2206018850 + level, point-major, coordinate = ((x >> 11) 2^-53) w (+ w/tau). */
+void orc_calib_points(int d, double tau, double w, int level, double* Z1, double* Z2) {
   const int N = ORC_CAL_NPTS;
-  double* Z1 = (double*)malloc(sizeof(double) * (size_t)N * (size_t)d);
-  double* Z2 = (double*)malloc(sizeof(double) * (size_t)N * (size_t)d);
   uint64_t st = ORC_CAL_SEED + (uint64_t)level;
   for (int i = 0; i < N * d; i++) Z1[i] = (double)(splitmix64(&st) >> 11) * 0x1.0p-53 * w;
   double shift = w / tau;
   for (int i = 0; i < N * d; i++) Z2[i] = (double)(splitmix64(&st) >> 11) * 0x1.0p-53 * w + shift;
+}
+
+/* calibration trial at box width w and grid m: returns the relative Frobenius error e (E5) of
+ * the ID built from K(Z1, Z2*) applied to the full K(Z1, Z2); *G_out = m^d.  The optional
+ * outputs expose the trial for its pins: *k_out the ID rank, skel_out[0:k] the skeleton rows
+ * (indices into Z1, pivot order), sel_out[0:*ns_out] the columns Z2* (indices into Z2).       */
+double orc_calib_trial_ex(int d, int kid, double p, double eps, double tau, double w, int level,
+                          int m, int64_t* G_out, int* k_out, int* skel_out, int* sel_out, int* ns_out) {
+  const int N = ORC_CAL_NPTS;
+  double* Z1 = (double*)malloc(sizeof(double) * (size_t)N * (size_t)d);
+  double* Z2 = (double*)malloc(sizeof(double) * (size_t)N * (size_t)d);
+  orc_calib_points(d, tau, w, level, Z1, Z2);
   int64_t G = ipow_sat(m, d);
   *G_out = G;
   int idx[ORC_CAL_NPTS], sel[ORC_CAL_NPTS];
@@ -822,11 +834,20 @@ double orc_calib_trial(int d, int kid, double p, double eps, double tau, double 
       num = num + df * df;
       den = den + kv * kv;
     }
+  if (k_out) *k_out = k;
+  if (skel_out) memcpy(skel_out, skel, sizeof(int) * (size_t)k);
+  if (sel_out) memcpy(sel_out, sel, sizeof(int) * (size_t)ns);
+  if (ns_out) *ns_out = ns;
   free(Z1);
   free(Z2);
   free(A);
   free(U);
   return den > 0.0 ? sqrt(num) / sqrt(den) : 0.0;
+}
+
+double orc_calib_trial(int d, int kid, double p, double eps, double tau, double w, int level,
+                       int m, int64_t* G_out) {
+  return orc_calib_trial_ex(d, kid, p, eps, tau, w, level, m, G_out, NULL, NULL, NULL, NULL);
 }
 
 /* r for one level: first m = 1, 2, ... with e < 1e-2 eps, or m^d >= 256 (E2) */
@@ -851,6 +872,7 @@ int orc_calibrate(orc_h2* h, int kid, double p, double eps) {
     if (has[l]) rl[l] = orc_calib_level(h->d, kid, p, eps, h->tau, ldexp(h->W, -l), l);
   for (int l = 0; l <= h->depth; l++)
     if (has[l] && rl[l] > r) r = rl[l];
+  for (int l = 0; l < 64; l++) h->calib_r[l] = l <= h->depth && has[l] ? rl[l] : 0;
   free(has);
   h->t_stage[2] = wall() - t0;
   return r;
@@ -1283,6 +1305,12 @@ void orc_info(const orc_h2* h, int64_t* out, double* W, double* t_stage) {
   out[10] = h->max_T;
   if (W) *W = h->W;
   if (t_stage) memcpy(t_stage, h->t_stage, sizeof(h->t_stage));
+}
+
+/* per-level r of the last orc_calibrate (E4): out[l] for l = 0..depth (0 = no admissible pair) */
+int orc_calib_levels(const orc_h2* h, int* out) {
+  for (int l = 0; l <= h->depth; l++) out[l] = h->calib_r[l];
+  return h->depth + 1;
 }
 
 void orc_free(orc_h2* h) {

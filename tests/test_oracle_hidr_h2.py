@@ -2,8 +2,8 @@
 
 D: containment in X_i and in the brute-force farfield, size bounds (Fig. 6/7
    captions P:307/Theorem 3.1's |S_i| <= 2^d r, |T_i| <= c_sp r + r).
-E: Gaussian with tiny bandwidth -> r = 1; r non-decreasing as eps falls.
-   Beyond these special cases E is "parity unpinned".
+E: Gaussian with tiny bandwidth -> r = 1; r non-decreasing as eps falls (the
+   general case of E is pinned in tests/test_oracle_calib_topdown_pins.py).
 F: skeleton containment / size chain of Eq.(4.4); nested-basis identity.
 G/H/I: single leaf = dense exact (S:356/S:375); closed-form dense rows (harmonic numbers);
    linearity; error falls as id_tol falls (BASELINE north_star); rows-mode = full mode.
