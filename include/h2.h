@@ -150,7 +150,13 @@ h2_handle* h2_rebuild_ex(const h2_handle* base, int32_t kernel_id, const double*
  */
 int h2_matvec(const h2_handle* h, const double* x, double* y);
 
-/* frees every device buffer of the handle; NULL-safe. */
+/* h2_matvec with the caller's vector length: n must equal the handle's point count, else
+ * H2_ERR_DIM_MISMATCH and nothing is read or written.  Otherwise as h2_matvec. */
+int h2_matvec_ex(const h2_handle* h, const double* x, double* y, int64_t n);
+
+/* frees every device buffer of the handle (the H^2 of Algorithm 2's output: bases,
+ * transfer matrices, coupling and nearfield blocks, tree and lists); NULL-safe.  Waits for the
+ * handle's outstanding device work first.  Never fails. */
 void h2_free(h2_handle* h);
 
 /* thread-local status / message of the last failing call on this thread (H2_OK if none). */
@@ -235,7 +241,10 @@ enum {
   H2_EXPORT_TREE_X = 18,  /* double[n*d] tree-order coordinates, point-major                     */
   H2_EXPORT_SHARD = 19,   /* int64[5 + 2*(depth+1)]: nranks, rank, cut level, p_lo, p_hi, then per */
                           /* level l the node range [lo_l, hi_l) this rank computed               */
-  H2_EXPORT_BLOCK_SAMPLE = 20 /* see h2_sample_blocks                                            */
+  H2_EXPORT_BLOCK_SAMPLE = 20, /* see h2_sample_blocks                                           */
+  H2_EXPORT_ID_PATH = 21  /* int32[nnodes]: the a8 code path of each node's ID: 0..6 staged       */
+                          /* shared-memory size classes, 7 lean shared-memory class, 8 / 9 global */
+                          /* memory (256 / 1024 threads), 10 thread-block cluster, -1 no basis    */
 };
 
 /* Copies array `what` into host_buf when cap_bytes suffices; *needed_bytes receives its size.

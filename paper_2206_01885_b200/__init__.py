@@ -21,13 +21,13 @@ H2_STORE_AUTO, H2_STORE_ALL, H2_STORE_ON_THE_FLY = 0, 1, 2
 H2_REDUCT_VOLUME, H2_REDUCT_FPS, H2_REDUCT_SURFACE = 0, 1, 2  # HiDR DataReduct (h2_options.reduct)
 
 EXPORT = dict(PERM=1, NODES=2, IL_OFF=4, IL_IDX=5, NF_OFF=6, NF_IDX=7, XS_OFF=8, XS_IDX=9, YS_OFF=10,
-              YS_IDX=11, K=12, SK_OFF=13, SK_IDX=14, U_OFF=15, U=16, XBAR_N=17, TREE_X=18, SHARD=19)
+              YS_IDX=11, K=12, SK_OFF=13, SK_IDX=14, U_OFF=15, U=16, XBAR_N=17, TREE_X=18, SHARD=19, ID_PATH=21)
 _EXPORT_DTYPE = dict(PERM=np.int32, NODES=np.int32, IL_OFF=np.int64, IL_IDX=np.int32, NF_OFF=np.int64,
                      NF_IDX=np.int32, XS_OFF=np.int64, XS_IDX=np.int32, YS_OFF=np.int64, YS_IDX=np.int32,
                      K=np.int32, SK_OFF=np.int64, SK_IDX=np.int32, U_OFF=np.int64, U=np.float64,
-                     XBAR_N=np.int32, TREE_X=np.float64, SHARD=np.int64)
+                     XBAR_N=np.int32, TREE_X=np.float64, SHARD=np.int64, ID_PATH=np.int32)
 
-EXPORTED_SYMBOLS = ["h2_build", "h2_build_ex", "h2_rebuild_ex", "h2_options_default", "h2_matvec", "h2_free", "h2_last_error",
+EXPORTED_SYMBOLS = ["h2_build", "h2_build_ex", "h2_rebuild_ex", "h2_options_default", "h2_matvec", "h2_matvec_ex", "h2_free", "h2_last_error",
                     "h2_last_error_message", "h2_info", "h2_export", "h2_sample_blocks", "h2_comm_nccl_unique_id",
                     "h2_comm_init_nccl", "h2_comm_init_local", "h2_comm_free", "h2_comm_size", "h2_comm_rank",
                     "h2_shard_cut_level", "h2_shard_split"]
@@ -78,6 +78,8 @@ def lib():
         L.h2_rebuild_ex.argtypes = [vp, i32, vp, f64, C.POINTER(h2_options)]
         L.h2_matvec.restype = C.c_int
         L.h2_matvec.argtypes = [vp, vp, vp]
+        L.h2_matvec_ex.restype = C.c_int
+        L.h2_matvec_ex.argtypes = [vp, vp, vp, i64]
         L.h2_free.argtypes = [vp]
         L.h2_last_error.restype = C.c_int
         L.h2_last_error_message.restype = C.c_char_p
@@ -134,8 +136,13 @@ def h2_build(points_ptr: int, n: int, d: int, kernel_id: int, kernel_params, id_
     return h
 
 
-def h2_matvec(h: int, x_ptr: int, y_ptr: int) -> None:
-    if lib().h2_matvec(C.c_void_p(h), C.c_void_p(x_ptr), C.c_void_p(y_ptr)) != 0:
+def h2_matvec(h: int, x_ptr: int, y_ptr: int, n: int | None = None) -> None:
+    """h2_matvec (or h2_matvec_ex when the caller's length n is given: H2_ERR_DIM_MISMATCH on a
+    mismatch)."""
+    L = lib()
+    rc = (L.h2_matvec(C.c_void_p(h), C.c_void_p(x_ptr), C.c_void_p(y_ptr)) if n is None else
+          L.h2_matvec_ex(C.c_void_p(h), C.c_void_p(x_ptr), C.c_void_p(y_ptr), int(n)))
+    if rc != 0:
         _raise()
 
 
@@ -311,9 +318,13 @@ class H2Matrix:
         return out
 
     def matvec(self, x):
+        """y = K~ x for a CUDA float64 contiguous vector of length n (original point order)."""
         import torch
+        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float64 and x.is_contiguous()
+                and x.dim() == 1):
+            raise H2Error("matvec: x must be a contiguous 1-D float64 CUDA tensor")
         y = torch.empty_like(x)
-        h2_matvec(self.h, x.data_ptr(), y.data_ptr())
+        h2_matvec(self.h, x.data_ptr(), y.data_ptr(), x.numel())
         return y
 
     def info(self) -> dict:

@@ -337,8 +337,23 @@ int h2_matvec(const h2_handle* h, const double* x, double* y) {
     comm_abort(h->comm);
     cudaGetLastError();
     return e.code;
+  } catch (const std::exception& e) {
+    set_error(H2_ERR_INTERNAL, e.what());
+    comm_abort(h->comm);
+    cudaGetLastError();
+    return H2_ERR_INTERNAL;
   }
   return H2_OK;
+}
+
+int h2_matvec_ex(const h2_handle* h, const double* x, double* y, int64_t n) {
+  clear_error();
+  if (h && n != h->n) {
+    set_error(H2_ERR_DIM_MISMATCH, "h2_matvec_ex: vector length " + std::to_string(n) + " != n = " +
+                                       std::to_string(h->n));
+    return H2_ERR_DIM_MISMATCH;
+  }
+  return h2_matvec(h, x, y);
 }
 
 void h2_free(h2_handle* h) { free_handle(h); }
@@ -450,6 +465,11 @@ static std::vector<char> export_bytes(const h2_handle* h, int what) {
         if (off[i + 1] > off[i]) std::memcpy(&out[off[i]], &U[uo[i]], 8 * (off[i + 1] - off[i]));
       return bytes(out.data(), 8 * out.size());
     }
+    case H2_EXPORT_ID_PATH: {
+      if (!h->id_path) break;
+      auto v = d2h(h->id_path, nn, s);
+      return bytes(v.data(), 4 * v.size());
+    }
     case H2_EXPORT_SHARD: {
       std::vector<int64_t> v = {h->nranks, h->rank, h->cut, h->p_lo, h->p_hi};
       for (int l = 0; l <= h->depth; l++) {
@@ -489,6 +509,9 @@ int h2_export(const h2_handle* h, int what, void* host_buf, size_t cap_bytes, si
   } catch (const Error& e) {
     set_error(e.code, e.msg);
     return e.code;
+  } catch (const std::exception& e) {
+    set_error(H2_ERR_INTERNAL, e.what());
+    return H2_ERR_INTERNAL;
   }
   return H2_OK;
 }
@@ -506,6 +529,9 @@ int h2_sample_blocks(const h2_handle* h, int64_t count, const int32_t* kind, con
   } catch (const Error& e) {
     set_error(e.code, e.msg);
     return e.code;
+  } catch (const std::exception& e) {
+    set_error(H2_ERR_INTERNAL, e.what());
+    return H2_ERR_INTERNAL;
   }
   return H2_OK;
 }

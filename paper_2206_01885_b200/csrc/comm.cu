@@ -19,6 +19,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <thread>
 
 #include "h2_internal.cuh"
 
@@ -37,6 +38,8 @@ struct NcclApi {
   ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -57,6 +60,9 @@ static NcclApi& nccl() {
     api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(api.so, "ncclAllGather"));
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(api.so, "ncclAllReduce"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.so, "ncclCommDestroy"));
+    api.CommAbort = reinterpret_cast<decltype(api.CommAbort)>(dlsym(api.so, "ncclCommAbort"));
+    api.CommGetAsyncError =
+        reinterpret_cast<decltype(api.CommGetAsyncError)>(dlsym(api.so, "ncclCommGetAsyncError"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.so, "ncclGetErrorString"));
   });
   if (!api.so || !api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.AllReduce || !api.CommDestroy)
@@ -95,6 +101,7 @@ struct h2_comm {
   int kind = 0;  // 1 NCCL, 2 LOCAL
   int nranks = 1, rank = 0;
   ncclComm_t nc = nullptr;
+  bool aborted = false;  // NCCL: aborted after a failure on this rank; every later call fails
   std::shared_ptr<h2::LocalGroup> group;
   long long key = 0;
 };
@@ -123,11 +130,62 @@ static void local_barrier(LocalGroup& g) {
   }
 }
 
+// A rank that fails between collectives would leave its peers blocked inside NCCL kernels: abort
+// the communicator (ncclCommAbort makes the peers' pending and later collectives return errors)
+// and mark the comm unusable.  LOCAL: release the other threads' barriers.
 void comm_abort(h2_comm* c) {
-  if (!c || c->kind != 2) return;
+  if (!c) return;
+  if (c->kind == 1) {
+    if (c->aborted) return;
+    c->aborted = true;
+    if (c->nc) {
+      try {
+        NcclApi& api = nccl();
+        if (api.CommAbort) api.CommAbort(c->nc);
+      } catch (...) {
+      }
+      c->nc = nullptr;
+    }
+    return;
+  }
+  if (c->kind != 2) return;
   std::lock_guard<std::mutex> lk(c->group->mu);
   c->group->aborted = true;
   c->group->cv.notify_all();
+}
+
+static void nccl_usable(const h2_comm* c) {
+  if (c->aborted || !c->nc) throw Error{H2_ERR_NCCL, "NCCL comm was aborted after an earlier failure"};
+}
+
+// Waits for stream s after NCCL collectives were enqueued on it: polls the stream and the
+// communicator's asynchronous error, and gives up after $H2_NCCL_TIMEOUT_S seconds (default 300),
+// instead of a bare cudaStreamSynchronize that would hang forever when a peer has died.
+void comm_sync(h2_comm* c, cudaStream_t s) {
+  if (!c || c->kind != 1) {
+    H2_CUDA_TRY(cudaStreamSynchronize(s));
+    return;
+  }
+  static const double limit = [] {
+    const char* e = getenv("H2_NCCL_TIMEOUT_S");
+    return e ? atof(e) : 300.0;
+  }();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return;
+    if (q != cudaErrorNotReady) H2_CUDA_TRY(q);
+    NcclApi& api = nccl();
+    if (api.CommGetAsyncError && c->nc) {
+      ncclResult_t ae = 0;
+      if (api.CommGetAsyncError(c->nc, &ae) == 0 && ae != 0 && ae != 7 /* ncclInProgress */)
+        throw Error{H2_ERR_NCCL, std::string("NCCL asynchronous error: ") +
+                                     (api.GetErrorString ? api.GetErrorString(ae) : "error")};
+    }
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit)
+      throw Error{H2_ERR_NCCL, "NCCL collective did not complete within H2_NCCL_TIMEOUT_S"};
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
 }
 
 __global__ void sum_ranks_kernel(int nranks, int64_t count, const double* __restrict__ all, double* __restrict__ out) {
@@ -141,6 +199,7 @@ __global__ void sum_ranks_kernel(int nranks, int64_t count, const double* __rest
 // recv[q * bytes ... (q+1) * bytes) = rank q's send buffer, for every rank q (DEVICE buffers)
 void comm_allgather(h2_comm* c, const void* send, void* recv, size_t bytes, cudaStream_t s) {
   if (c->kind == 1) {
+    nccl_usable(c);
     H2_NCCL_TRY(nccl().AllGather(send, recv, bytes, kNcclUint8, c->nc, s));
     return;
   }
@@ -162,6 +221,7 @@ void comm_allgather(h2_comm* c, const void* send, void* recv, size_t bytes, cuda
 // out[t] = sum over ranks of in[t] (DEVICE, fp64); the LOCAL transport sums in rank order
 void comm_allreduce_sum(h2_comm* c, const double* in, double* out, int64_t count, cudaStream_t s) {
   if (c->kind == 1) {
+    nccl_usable(c);
     H2_NCCL_TRY(nccl().AllReduce(in, out, (size_t)count, kNcclFloat64, kNcclSum, c->nc, s));
     return;
   }
@@ -246,7 +306,7 @@ h2_comm* h2_comm_init_local(int32_t nranks, int32_t rank, int64_t group_key) {
 
 void h2_comm_free(h2_comm* c) {
   if (!c) return;
-  if (c->kind == 1 && c->nc) {
+  if (c->kind == 1 && c->nc && !c->aborted) {
     try {
       nccl().CommDestroy(c->nc);
     } catch (...) {

@@ -83,7 +83,7 @@ __global__ void id_sizes_kernel(int base, int count, int d, const int* __restric
                                 const int* __restrict__ nend, const int* __restrict__ first_child,
                                 const int* __restrict__ nchild, const int* __restrict__ ys_cnt,
                                 const int* __restrict__ k, int* xbar_n, int* child_off, int64_t* wsz, int64_t* usz,
-                                int* smax, int cs, int64_t cl_min, int* cl_cnt, int* cl_list) {
+                                int* smax, int cs, int64_t cl_min, int* cl_cnt, int* cl_list, int* id_path) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t > count) return;
   if (t == count) {
@@ -117,6 +117,9 @@ __global__ void id_sizes_kernel(int base, int count, int d, const int* __restric
   wsz[t] = big ? (int64_t)ny * (((nx + cs - 1) / cs) * cs) + 2LL * cs * ny
          : nx > 0 && cls < 0 ? (int64_t)ny * nx + nx + ny + nx + 2 : 0;
   usz[t] = (int64_t)nx * mn;
+  // the code path (H2_EXPORT_ID_PATH): 0..6 staged shared-memory classes, 7 lean class, 8 global
+  // memory (256 threads), 9 global memory (1024 threads), 10 thread-block cluster, -1 none
+  id_path[i] = nx == 0 ? -1 : big ? 10 : cls >= 0 ? cls : (8LL * nx * ny < kIdBigBlock ? 8 : 9);
   if (nx > 0 && cls >= 0)
     atomicMax(smax + cls, (int)(cls == kIdLean ? id_lean_request(ny, nx, d) : id_smem_bytes(ny, nx, d)));
 }
@@ -635,6 +638,8 @@ void id_sweep(h2_handle* h) {
   h->xbar_n = halloc<int>(h, nn);
   h->child_off = halloc<int>(h, nn);
   h->u_off = halloc<int64_t>(h, nn + 1);
+  h->id_path = halloc<int>(h, nn);
+  H2_CUDA_TRY(cudaMemsetAsync(h->id_path, 0xff, sizeof(int) * nn, s));
   H2_CUDA_TRY(cudaMemsetAsync(h->k, 0, sizeof(int) * nn, s));
   H2_CUDA_TRY(cudaMemsetAsync(h->xbar_n, 0, sizeof(int) * nn, s));
   H2_CUDA_TRY(cudaMemsetAsync(h->child_off, 0, sizeof(int) * nn, s));
@@ -666,7 +671,8 @@ void id_sweep(h2_handle* h) {
     H2_CUDA_TRY(cudaMemsetAsync(cl_cnt, 0, sizeof(int), s));
     id_sizes_kernel<<<(count + 1 + 255) / 256, 256, 0, s>>>(base, count, h->d, h->is_leaf, h->nbegin, h->nend,
                                                             h->first_child, h->nchild, h->ys_cnt, h->k, h->xbar_n,
-                                                            h->child_off, wsz, usz, smax, cs, cl_min, cl_cnt, cl_list);
+                                                            h->child_off, wsz, usz, smax, cs, cl_min, cl_cnt, cl_list,
+                                                            h->id_path);
     scan_excl_i64(wsz, woff, count + 1, s);
     scan_excl_i64(usz, uo, count + 1, s);
     H2_CHECK_LAUNCH();

@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(256, 2) nf_matvec_kernel(int64_t nitems, const
   }
 }
 
-// ---- stored nearfield blocks, bulk-staged (the default) --------------------------------------
+// ---- stored nearfield blocks, bulk-staged (opt-in variant, H2_MV_BULK=1) ----------------------
 // A CTA walks its nearfield units with a two-deep ring of shared-memory buffers: one elected
 // thread arms an mbarrier with the unit's byte count and issues cp.async.bulk copies (the TMA
 // bulk engine: a unit of a block with nj <= 32 CW columns is ONE contiguous range; wider blocks
@@ -356,7 +356,9 @@ __global__ void __launch_bounds__(256, 2) nf_matvec_kernel(int64_t nitems, const
 // r0 + w, r0 + w + 8, ...; lanes over columns; row sums by warp shuffles (one atomic per row),
 // the D^T x_i column partials reduced across the 8 warps in shared memory (one atomic per column
 // per unit).  Diagonal blocks multiply forward only.
-constexpr int kMvBulkThreads = 256, kMvBulkWarps = kMvBulkThreads / 32, kMvBulkBuf = 4160;
+// Buffer: a contiguous unit takes <= kWarpUnitEntries + 2 doubles; a row-wise unit R = 4096 / WC rows
+// of stride mv_row_stride(nc) <= WC + 2, at most 64 x 66 = 4224 doubles (CW = 2).
+constexpr int kMvBulkThreads = 256, kMvBulkWarps = kMvBulkThreads / 32, kMvBulkBuf = 4224;
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
@@ -416,12 +418,16 @@ __device__ __forceinline__ MvUnit mv_unit(int64_t u, const int* __restrict__ uma
   return m;
 }
 
+// row stride of a row-wise staged unit: even (every row copy lands 16-byte aligned) and >= nc + 2
+// (a copy starts at the even global index below the row and spans at most nc + 2 doubles)
+__device__ __forceinline__ int mv_row_stride(int nc) { return ((nc + 1) & ~1) + 2; }
+
 // shared-memory position of (row a - r0, column b - c0) of a staged unit; copies start at an
 // even global index (16-byte alignment), hence the +1 when the range starts odd
 __device__ __forceinline__ int mv_pos(const MvUnit& m, int ra, int cb) {
   if (m.contig) return (int)(m.base & 1) + ra * m.nj + cb;
   const int64_t rs = m.base + (int64_t)ra * m.nj;
-  return ra * (m.nc + 4) + (int)(rs & 1) + cb;
+  return ra * mv_row_stride(m.nc) + (int)(rs & 1) + cb;
 }
 
 template <int WC>
@@ -441,7 +447,7 @@ __device__ __forceinline__ void mv_issue(const MvUnit& m, const double* __restri
     for (int ra = 0; ra < m.r1 - m.r0; ra++) {
       const int64_t rs = m.base + (int64_t)ra * m.nj;
       const unsigned bytes = (unsigned)((((rs + m.nc) - (rs & ~1LL) + 1) & ~1LL) * 8);
-      bulk_g2s(buf + ra * (m.nc + 4), Dv + (rs & ~1LL), bytes, bar);
+      bulk_g2s(buf + ra * mv_row_stride(m.nc), Dv + (rs & ~1LL), bytes, bar);
     }
   }
 }
@@ -684,7 +690,8 @@ void matvec(const h2_handle* h, const double* x, double* y) {
   }
   permute_out_kernel<<<grid_for(n, 256), 256, 0, s>>>(yt.as<double>(), yf.as<double>(), h->perm, n, y);
   H2_CHECK_LAUNCH();
-  H2_CUDA_TRY(cudaStreamSynchronize(s));
+  if (sharded) comm_sync(h->comm, s);
+  else H2_CUDA_TRY(cudaStreamSynchronize(s));
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);
 }

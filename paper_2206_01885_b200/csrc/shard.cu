@@ -148,8 +148,9 @@ void exchange_slots(h2_handle* h, int* cnt, int* slots) {
   comm_allgather(h->comm, send.p, recv.p, sizeof(int) * sw, s);
   if (segs.size() > npack) seg_copy_kernel<<<(unsigned)(segs.size() - npack), 256, 0, s>>>(table.as<Seg>() + npack);
   H2_CHECK_LAUNCH();
-  // the table is host-sourced: keep it alive until the copies ran
-  H2_CUDA_TRY(cudaStreamSynchronize(s));
+  // the table is host-sourced: keep it alive until the copies ran (bounded wait: a dead peer
+  // raises H2_ERR_NCCL instead of hanging)
+  comm_sync(h->comm, s);
   h->gpu_launches += 2;
 }
 

@@ -95,7 +95,7 @@ def test_parity_config_shapes(name, cfg, n, q):
     agree_sk = skeleton_agreement(g, o)
     eg, eo, agree = matvec_check(g, o, pts, c["kernel"], kp, c["id_tol"], cfg)
     print(f"{name}: r={r} skel-agree={agree_sk:.4f} err_gpu={eg:.3e} err_oracle={eo:.3e} gpu-vs-oracle={agree:.3e}")
-    assert agree_sk >= 0.9
+    assert agree_sk >= 0.99
     assert eg <= 2.0 * eo + 1e-15
     assert agree <= 10 * c["id_tol"]
     g.close()
@@ -160,7 +160,7 @@ def test_parity_laplace_and_bump(kid, kp, cfg, n):
     g = gpu_build(pts, kid, kp, 1e-6, c["q"], c["tau"])
     assert g.info()["r"] == r
     assert_structure_equal(g, o)
-    assert skeleton_agreement(g, o) >= 0.9
+    assert skeleton_agreement(g, o) >= 0.99
     eg, eo, agree = matvec_check(g, o, pts, kid, kp, 1e-6, cfg)
     print(f"kernel {kid}{kp} cfg{cfg}: r={r} err_gpu={eg:.3e} err_oracle={eo:.3e} gpu-vs-oracle={agree:.3e}")
     assert eg <= 2.0 * eo + 1e-15
@@ -251,10 +251,10 @@ def test_parity_bench_config_full_size():
     g = gpu_build(pts, c["kernel"], kp, c["id_tol"], c["q"])
     assert g.info()["r"] == r
     assert_structure_equal(g, o)
-    assert skeleton_agreement(g, o) >= 0.9
+    assert skeleton_agreement(g, o) >= 0.99
     n = len(pts)
     x = synth.matvec_vector(4, n)
-    rows = synth.sample_rows(4, n)[:256]
+    rows = synth.sample_rows(4, n)
     yg = g.matvec(torch.from_numpy(x).cuda()).cpu().numpy()[rows]
     yo = o.matvec(x, rows)
     yd = oracle.dense_rows(pts, c["kernel"], kp[0], x, rows)
@@ -283,10 +283,10 @@ def test_parity_full_size_other_configs(cfg):
     assert g.info()["r"] == r
     assert_structure_equal(g, o)
     agree_sk = skeleton_agreement(g, o)
-    assert agree_sk >= 0.9
+    assert agree_sk >= 0.99
     n = len(pts)
     x = synth.matvec_vector(cfg, n)
-    rows = synth.sample_rows(cfg, n)[:256]
+    rows = synth.sample_rows(cfg, n)
     yg = g.matvec(torch.from_numpy(x).cuda()).cpu().numpy()[rows]
     yo = o.matvec(x, rows)
     yd = oracle.dense_rows(pts, c["kernel"], kp[0] if kp else 0.0, x, rows)
@@ -392,7 +392,7 @@ def test_parity_fps(cfg, n, q, reduct):
                    reduct=reduct)
     assert g.info()["r"] == r
     assert_structure_equal(g, o)
-    assert skeleton_agreement(g, o) >= 0.9
+    assert skeleton_agreement(g, o) >= 0.99
     eg, eo, agree = matvec_check(g, o, pts, c["kernel"], kp, c["id_tol"], cfg)
     print(f"reduct {reduct} cfg{cfg} n={n}: r={r} err_gpu={eg:.3e} err_oracle={eo:.3e} gpu-vs-oracle={agree:.3e} "
           f"hidr ms up {g.info()['stage_ms']['hidr_up']:.2f} down {g.info()['stage_ms']['hidr_down']:.2f}")
@@ -452,11 +452,15 @@ np.save(out, g.matvec(x).cpu().numpy())
 """
 
 
-@pytest.mark.parametrize("knobs", [{"H2_MV_DYN": "0"}, {"H2_MV_PF": "0"}, {"H2_MV_ORDER": "1"}, {"H2_MV_BULK": "1"}])
-def test_matvec_variants_equal_default(knobs, tmp_path):
+@pytest.mark.parametrize("knobs,cfg,n", [({"H2_MV_DYN": "0"}, 4, 200000), ({"H2_MV_PF": "0"}, 4, 200000),
+                                         ({"H2_MV_ORDER": "1"}, 4, 200000), ({"H2_MV_BULK": "1"}, 4, 200000),
+                                         ({"H2_MV_BULK": "1"}, 5, 40000), ({"H2_MV_BULK": "1"}, 2, 120000)])
+def test_matvec_variants_equal_default(knobs, cfg, n, tmp_path):
     """The stored-block matvec's scheduling variants (grid-stride instead of the resident wave, no L2
     prefetch, farfield chain first, the bulk-copy nearfield kernel) against the default on the same
-    stored build: the same products, summed by atomics in another order (relative 1e-12)."""
+    stored build: the same products, summed by atomics in another order (relative 1e-12).  The bulk
+    variant also on configs[4] / configs[1] shapes (d = 5 / 3: units wider than one column chunk,
+    odd block widths -> row-wise copies)."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -464,6 +468,7 @@ def test_matvec_variants_equal_default(knobs, tmp_path):
     for env_extra in ({}, knobs):
         out = str(tmp_path / f"y{len(ys)}.npy")
         env = dict(os.environ, **env_extra)
-        subprocess.run([sys.executable, "-c", _MV_DUMP, root, "4", "200000", out], env=env, check=True, timeout=600)
+        subprocess.run([sys.executable, "-c", _MV_DUMP, root, str(cfg), str(n), out], env=env, check=True,
+                       timeout=600)
         ys.append(np.load(out))
     assert np.linalg.norm(ys[1] - ys[0]) <= 1e-12 * np.linalg.norm(ys[0])
