@@ -52,6 +52,63 @@ def workload_desc(cfg: int) -> str:
             f"id_tol={c['id_tol']} tau={c['tau']}; full build a1-a10, all blocks stored symmetric-once")
 
 
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r02_fp64_peak.json")
+# FP64 instructions per kernel evaluation (fill / ID block generation) and per
+# squared distance + compare (HiDR, 3d - 1 DADD/DMUL + a compare)
+KERNEL_FP64_INSTR = {1: 18, 2: 23, 3: 17, 4: 22, 5: 26, 6: 30}
+
+
+def fp64_peak() -> dict:
+    """Measured FP64 instruction rate (tools/micro/fp64_peak.cu, profiles/r02_fp64_peak.json), else
+    the 148 SMs x 64 FP64 lanes x 1.965 GHz datasheet figure, saying which."""
+    if os.path.exists(FP64_PEAK_FILE):
+        try:
+            j = json.load(open(FP64_PEAK_FILE))
+            return {"instr_per_s": float(j["dfma_per_s"]), "tflops": float(j["fp64_tflops"]),
+                    "source": "measured: tools/micro/fp64_peak.cu (profiles/r02_fp64_peak.json)"}
+        except Exception:
+            pass
+    r = 148 * FP64_LANES_PER_SM * 1.965e9
+    return {"instr_per_s": r, "tflops": 2 * r / 1e12, "source": "datasheet 148 SMs x 64 lanes x 1.965 GHz"}
+
+
+def host_cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def build_roofline(c, info, k, xbar, ys_cnt, t_ms, hbm_gbs, fp64):
+    """SURVEY §8(d) whole-build roofline: T_roof = sum over steps of max(B_s / BW_HBM, I_s / P_FP64)
+    with the algorithmic bytes B_s and FP64 instructions I_s of each step (the top-down HiDR counted
+    at the distances the exact pruned search evaluates), against the measured build time."""
+    n, d = info["n"], c["d"]
+    ck = KERNEL_FP64_INSTR.get(c["kernel"], 20) + (3 * d - 1)
+    bw, P = hbm_gbs * 1e9, fp64["instr_per_s"]
+    down = info["hidr_dist_done"] or max(0, info["hidr_dist_evals"] - info["hidr_up_evals"])
+    cpqr = float(np.sum(2.0 * ys_cnt.astype(np.float64) * xbar.astype(np.float64) * k.astype(np.float64)))
+    steps = {  # name: (bytes, fp64 instructions)
+        "a1-a3 tree": (8.0 * n * d * 2 + 8 * 24.0 * n, 0.0),
+        "a4 lists": (12.0 * (info["n_il"] + info["n_nf"]), 0.0),
+        "a6 HiDR up": (0.0, 3.0 * d * info["hidr_up_evals"]),
+        "a7 HiDR down": (0.0, 3.0 * d * down),
+        "a8 ID": (8.0 * float(np.sum(xbar.astype(np.float64) * k)), ck * info["id_kernel_evals"] + cpqr),
+        "a9 coupling": (8.0 * info["coupling_entries"], ck * info["coupling_entries"]),
+        "a10 nearfield": (8.0 * info["nearfield_entries"], ck * info["nearfield_entries"]),
+    }
+    per = {nm: round(1e3 * max(b / bw, i / P), 4) for nm, (b, i) in steps.items()}
+    t_roof = sum(per.values())
+    return {"t_roof_ms": round(t_roof, 3), "t_measured_ms": round(t_ms, 3), "frac": round(t_roof / t_ms, 4),
+            "per_step_floor_ms": per, "hbm_gbs": hbm_gbs, "fp64_instr_per_s": P,
+            "note": "algorithmic bytes / FP64 instructions per step (kernel eval %d instr incl. distance, CPQR "
+                    "2 DFMA per entry per pivot, HiDR 3d per distance; down = distances evaluated by the exact "
+                    "pruned search); floors of concurrent steps are summed" % ck}
+
+
 # ------------------------------------------------------------------------------------------ clocks
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -142,14 +199,43 @@ def oracle_sample_run(cfg: int, n_sample: int):
     return dt, entries
 
 
-def cpu_baseline(cfg: int, n_sample: int) -> dict:
+def cpu_baseline(cfg: int, n_sample: int, y_gpu_rows=None) -> tuple[dict, dict | None]:
+    """The oracle timed on the host cores (a1-a8 + evaluate-only a9/a10 on n_sample points), and,
+    outside that timing, the accuracy of the timed GPU build: the relative matvec error of the GPU
+    H^2 on the 1024 seeded rows against the exact dense K x, next to the oracle's own error on the
+    same rows (when the oracle ran on the whole workload)."""
     import oracle
-    dt, entries = oracle_sample_run(cfg, n_sample)
-    what = ("the whole workload" if n_sample == synth.CONFIGS[cfg]["n"]
-            else "points of the same distribution as the workload")
-    return {"value": round(n_sample / dt / 1e6, 6), "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+    c = synth.CONFIGS[cfg]
+    pts = synth.points(cfg, n_sample)
+    kp = c["params"][0] if c["params"] else 0.0
+    t0 = time.perf_counter()
+    h = oracle.OracleH2(pts, c["q"], c["tau"])
+    r = h.build(c["kernel"], kp, c["id_tol"])
+    entries, _ = h.fill(store=False)
+    dt = time.perf_counter() - t0
+    whole = n_sample == c["n"]
+    what = "the whole workload" if whole else "points of the same distribution as the workload"
+    base = {"value": round(n_sample / dt / 1e6, 6), "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "cpu_model": host_cpu_model(),
             "sample": f"oracle a1-a8 + evaluate-only a9/a10 ({entries} block entries) on n={n_sample} ({what}); "
                       f"wall {dt:.2f} s"}
+    acc = None
+    if y_gpu_rows is not None:
+        n = c["n"]
+        x = synth.matvec_vector(cfg, n)
+        rows = synth.sample_rows(cfg, n)
+        yd = oracle.dense_rows(synth.points(cfg), c["kernel"], kp, x, rows)
+        eg = float(np.linalg.norm(y_gpu_rows - yd) / np.linalg.norm(yd))
+        acc = {"matvec_rel_err": eg, "rows": int(len(rows)), "id_tol": c["id_tol"],
+               "definition": "||K~x - Kx|| / ||Kx|| on the seeded sampled rows (all rows if n <= 16384), "
+                             "x = synth.matvec_vector, dense K x by the oracle"}
+        if whole:
+            yo = h.matvec(x, rows)
+            eo = float(np.linalg.norm(yo - yd) / np.linalg.norm(yd))
+            acc.update({"oracle_matvec_rel_err": eo, "oracle_r": r, "ratio_to_oracle": round(eg / eo, 4),
+                        "gpu_vs_oracle": float(np.linalg.norm(y_gpu_rows - yo) / np.linalg.norm(yo))})
+    h.close()
+    return base, acc
 
 
 def run_reference(args):
@@ -223,6 +309,17 @@ def run_ours(args):
         ptr = src if src is not None else pts.data_ptr()
         return P.h2_build(ptr, n, c["d"], c["kernel"], kp, c["id_tol"], c["q"], c["tau"], opts(host, serial))
 
+    # the first build of the process, timed (cold: lazy module loading of every kernel, first
+    # driver allocations of the block store and the caching allocator's pool); not a bench value
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tc0 = time.perf_counter()
+    c0.record(stream)
+    h = one()
+    c1.record(stream)
+    c1.synchronize()
+    cold = {"device_ms": round(c0.elapsed_time(c1), 3), "wall_ms": round(1e3 * (time.perf_counter() - tc0), 3)}
+    P.h2_free(h)
     for _ in range(args.warmup):
         h = one()
         P.h2_free(h)
@@ -283,9 +380,13 @@ def run_ours(args):
     # H^2 matvec on one stored build: y = K~ x, every pass on the GPU; the
     # stored blocks are read once (the nearfield pass dominates: 8 B per stored entry)
     stored = args.storage == "all"
-    h = one() if stored else None
-    xv = torch.randn(n, dtype=torch.float64, device="cuda")
+    h = one()
+    # accuracy of the benched configuration (outside every timed region): y = K~ x for the seeded x
+    xv = torch.from_numpy(synth.matvec_vector(cfg, n)).cuda()
     yv = torch.empty_like(xv)
+    P.h2_matvec(h, xv.data_ptr(), yv.data_ptr(), n)
+    y_rows = yv.cpu().numpy()[synth.sample_rows(cfg, n)]
+    ex = {nm: P.h2_export(h, nm) for nm in ("K", "XBAR_N", "YS_OFF")}
     torch.cuda.synchronize()
     for _ in range(2 if stored else 0):
         P.h2_matvec(h, xv.data_ptr(), yv.data_ptr())
@@ -301,9 +402,9 @@ def run_ours(args):
         mv_ms.append(m0.elapsed_time(m1))
     if stored:
         mv_info = P.h2_info(h)
-        P.h2_free(h)
         mv_t = float(np.median(mv_ms))
         mv_bytes = 8 * (mv_info["nearfield_entries"] + mv_info["coupling_entries"])
+    P.h2_free(h)
 
     # the same build with the nearfield fill run alone (serial_fill): the kernel's own roofline
     iso_ms = []
@@ -328,15 +429,15 @@ def run_ours(args):
                 traffic = tr.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    sm_mhz = clocks.get("sm_mhz") or 1965.0
-    fp64_peak = 148 * FP64_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    fp64 = fp64_peak()
+    whole = build_roofline(c, info, ex["K"], ex["XBAR_N"], np.diff(ex["YS_OFF"]), t_step, hbm, fp64)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic,
                 "kernel": "nf_fill_kernel<D=2,MATERN32> (a10, nearfield fill)", "kernel_ms": round(nf_ms, 3),
                 "step_share": round(nf_ms / t_step, 4),
                 "note": "live: the kernel runs concurrently with a5-a9 (side stream), sharing the SMs",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650 GB/s",
-                "fp64_peak_tflops_at_sm_clock": round(fp64_peak, 2)}
+                "fp64_peak_tflops": round(fp64["tflops"], 2), "fp64_peak_source": fp64["source"]}
     iso = float(np.mean(iso_ms)) if stored else 1.0
     roofline_isolated = {"bound": "hbm", "achieved": round(nf_bytes / (iso * 1e-3) / 1e9, 1), "peak": hbm,
                          "unit": "GB/s", "frac": round(nf_bytes / (iso * 1e-3) / 1e9 / hbm, 4),
@@ -357,6 +458,7 @@ def run_ours(args):
                            "l2": "flushed (512 MiB write) before every timed step",
                            "wall_s_timed_region": round(t_wall, 3)},
                 "stages_ms": mean_stages, "clocks": clocks, "e2e": e2e, "gpu_launches": launches,
+                "cold_first_build": cold, "roofline_whole_build": whole,
                 "roofline": roofline if stored else None,
                 "roofline_isolated": roofline_isolated if stored else None,
                 "matvec": {"ms": round(mv_t, 3), "stored_bytes_read": mv_bytes,
@@ -368,7 +470,7 @@ def run_ours(args):
         if not stored:
             line["config"]["storage"] = "blocks not stored (skeleton build a1-a8; a9/a10 evaluated in the matvec)"
         if ws == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample)
+            line["cpu_baseline"], line["accuracy"] = cpu_baseline(cfg, args.cpu_sample, y_rows)
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
@@ -401,6 +503,16 @@ def main():
         args.cpu_sample = default_sample
     if args.ref_sample is None:
         args.ref_sample = default_sample
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # --gpus N without a launcher: start the N ranks ourselves (one process per GPU, the same
+        # torch.distributed.run launch the driver uses), so n_gpus is never silently 1
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -216,6 +216,7 @@ typedef struct h2_info_t {
    * [7] nearfield fill a10, [8] whole build                                                     */
   float stage_ms[9];
   int64_t hidr_dist_done;                    /* distances the pruned top-down Vol evaluated        */
+  int64_t hidr_up_evals;                     /* the bottom-up sweep's share of hidr_dist_evals     */
 } h2_info_t;
 
 int h2_info(const h2_handle* h, h2_info_t* out);

@@ -46,7 +46,8 @@ class h2_info_t(C.Structure):
                 ("n_nf", C.c_int64), ("coupling_entries", C.c_int64), ("nearfield_entries", C.c_int64),
                 ("stored_bytes", C.c_int64), ("coupling_stored", C.c_int32), ("nearfield_stored", C.c_int32),
                 ("hidr_dist_evals", C.c_int64), ("id_kernel_evals", C.c_int64), ("kmax", C.c_int32),
-                ("gpu_launches", C.c_int32), ("stage_ms", C.c_float * 9), ("hidr_dist_done", C.c_int64)]
+                ("gpu_launches", C.c_int32), ("stage_ms", C.c_float * 9), ("hidr_dist_done", C.c_int64),
+                ("hidr_up_evals", C.c_int64)]
 
 
 STAGES = ["tree", "lists", "calibrate", "hidr_up", "hidr_down", "id_sweep", "coupling_fill", "nearfield_fill",

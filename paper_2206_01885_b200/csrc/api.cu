@@ -116,6 +116,7 @@ static void clone_geometry(h2_handle* h, const h2_handle* b) {
   h->ys = dup(b->ys, nn * r);
   h->hidr_dist_evals = 0;  // nothing of HiDR ran for this handle
   h->hidr_dist_done = 0;
+  h->hidr_up_evals = 0;
   h->nranks = b->nranks;
   h->rank = b->rank;
   h->cut = b->cut;
@@ -381,6 +382,7 @@ int h2_info(const h2_handle* h, h2_info_t* out) {
   out->nearfield_stored = h->np_stored;
   out->hidr_dist_evals = h->hidr_dist_evals;
   out->hidr_dist_done = h->hidr_dist_done;
+  out->hidr_up_evals = h->hidr_up_evals;
   out->id_kernel_evals = h->id_kernel_evals;
   out->kmax = h->kmax;
   out->gpu_launches = h->gpu_launches;

@@ -606,6 +606,7 @@ void hidr_up(h2_handle* h) {
     }
   }
   h->hidr_dist_evals = (int64_t)read1(ev.as<unsigned long long>(), h->stream);
+  h->hidr_up_evals = h->hidr_dist_evals;
 }
 
 void hidr_down(h2_handle* h) {

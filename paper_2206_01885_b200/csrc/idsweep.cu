@@ -11,6 +11,7 @@
 #include <cstdlib>
 
 #include "cpqr.cuh"
+#include "cpqr_panel.cuh"
 
 namespace h2 {
 
@@ -33,18 +34,25 @@ __host__ __device__ __forceinline__ int id_class(int64_t bytes) {
   return c;
 }
 
-// shared-memory footprint of one node's ID: M (ny x nx) + nrm2 (nx) + v (ny) + piv, Xbar (2 nx ints)
-// (+ staged coordinates of Xbar and Y^*: 8 (nx + ny) d bytes, + the exp table)
+constexpr int kIdPanelNb = 8;  // panel width of the blocked CPQR (cpqr_panel.cuh)
+// rows the panel CPQR's leading dimension adds for a node of nx columns on NT threads (panel_ld)
+__host__ __device__ __forceinline__ int id_pad_rows(int nx, int nt) {
+  const int G = panel_group(nx, nt);
+  return G <= 8 ? 2 * G - 1 : 0;
+}
+// shared-memory footprint of one node's ID: M (ny + pad rows x nx) + F (NB x nx) + nrm2 (nx) + v (ny)
+// + piv, Xbar (2 nx ints) (+ staged coordinates of Xbar and Y^*: 8 (nx + ny) d bytes, + the exp table)
 __host__ __device__ __forceinline__ int64_t id_smem_bytes(int ny, int nx, int d) {
-  return 8LL * ((int64_t)ny * nx + nx + ny) + 8LL * nx + 8LL * d * (nx + ny) + 512;
+  return 8LL * ((int64_t)(ny + id_pad_rows(nx, 128)) * nx + kIdPanelNb * nx + nx + ny) + 8LL * nx +
+         8LL * d * (nx + ny) + 512;
 }
 // the lean layout of the one-CTA-per-SM class: no staged coordinates (the block generation reads
 // them from global memory / L1)
 constexpr int kIdLeanThreads = 512;
-constexpr int kIdLeanMax = 226 * 1024;  // dynamic shared memory of that class (+ the small static part)
+constexpr int kIdLeanMax = 224 * 1024;  // dynamic shared memory of that class (+ the small static part)
 constexpr int kIdLean = kIdClasses;      // its class number
 __host__ __device__ __forceinline__ int64_t id_smem_bytes_lean(int ny, int nx) {
-  return 8LL * ((int64_t)ny * nx + nx + ny) + 8LL * nx + 512;
+  return 8LL * ((int64_t)(ny + id_pad_rows(nx, 512)) * nx + kIdPanelNb * nx + nx + ny) + 8LL * nx + 512;
 }
 // what a lean node asks for: its footprint plus staged coordinates when both fit the class
 __host__ __device__ __forceinline__ int64_t id_lean_request(int ny, int nx, int d) {
@@ -115,7 +123,7 @@ __global__ void id_sizes_kernel(int base, int count, int d, const int* __restric
   }
   // cluster path: M (column slices) + the staged candidate columns (2 parities x CS x ny)
   wsz[t] = big ? (int64_t)ny * (((nx + cs - 1) / cs) * cs) + 2LL * cs * ny
-         : nx > 0 && cls < 0 ? (int64_t)ny * nx + nx + ny + nx + 2 : 0;
+         : nx > 0 && cls < 0 ? (int64_t)ny * nx + kIdPanelNb * nx + nx + ny + nx + 2 : 0;
   usz[t] = (int64_t)nx * mn;
   // the code path (H2_EXPORT_ID_PATH): 0..6 staged shared-memory classes, 7 lean class, 8 global
   // memory (256 threads), 9 global memory (1024 threads), 10 thread-block cluster, -1 none
@@ -131,8 +139,10 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
     const int* __restrict__ nchild, const int* __restrict__ ys_cnt, const int* __restrict__ ys,
     const int* __restrict__ xbar_n, const int64_t* __restrict__ woff, double* work, const int64_t* __restrict__ uoff,
     double* U, int* kout, int* sk, unsigned long long* evals, int64_t min_block, int64_t max_block, int cs,
-    int64_t cl_min) {
+    int64_t cl_min, int use_panel) {
   __shared__ CpqrSmem<kIdThreads> csm;
+  constexpr int kNbG = kIdThreads >= 1024 ? 4 : kIdPanelNb;  // (64 registers per thread at 1024)
+  __shared__ PanelSmem<kIdThreads, kNbG> psm;
   // the Householder vector in shared memory for the big-block variant (ny <= r <= 4096, the budget
   // cap); the 256-thread variant keeps it in its global workspace (more CTAs per SM)
   __shared__ double sv[kIdThreads >= 1024 ? 4096 : 1];
@@ -148,8 +158,15 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
   if (id_smem_class(ny, nx, d) >= 0 || id_big(ny, nx, d, cs, cl_min)) return;  // id_kernel_smem / _cluster
   const int64_t blk = 8LL * nx * ny;
   if (blk < min_block || blk >= max_block) return;  // the other thread-count variant
+  // the panel-blocked CPQR with at least 4 threads per column (32-byte sectors of L2), when the
+  // columns fit RMAX rounds of thread groups; else the warp-per-column one
+  constexpr int kRmaxG = 4;
+  const int Gp = panel_group(nx, kIdThreads);
+  const int G = Gp < 4 ? 4 : Gp;
+  const bool panel = use_panel && (int64_t)nx * G <= (int64_t)kIdThreads * kRmaxG;
   double* M = work + woff[t];
-  double* nrm2 = M + (int64_t)ny * nx;
+  double* Fs = M + (int64_t)ny * nx;
+  double* nrm2 = Fs + kIdPanelNb * nx;
   double* v = nrm2 + nx;
   int* piv = reinterpret_cast<int*>(v + ny);
   int* xb = piv + nx;
@@ -174,13 +191,14 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
     M[e] = kernel_pts_d(kid, p2, X, n, d, xb[b], yv[a]);
   }
   __syncthreads();
-  const int k = cta_cpqr<kIdThreads>(M, ny, nx, tol, piv, nrm2, kIdThreads >= 1024 ? sv : v, csm);
+  const int k = panel ? cta_cpqr_panel<kIdThreads, kNbG, kRmaxG>(M, ny, ny, nx, tol, G, piv, Fs, psm)
+                      : cta_cpqr<kIdThreads>(M, ny, nx, tol, piv, nrm2, kIdThreads >= 1024 ? sv : v, csm);
   // outputs: k, skeleton (pivot order), U (nx x k column-major)
   double* Ui = U + uoff[t];
   for (int a = tid; a < k; a += kIdThreads) sk[(int64_t)i * r + a] = xb[piv[a]];
   for (int64_t e = tid; e < (int64_t)nx * k; e += kIdThreads) {
     int c = (int)(e % nx), tt = (int)(e / nx);
-    double val = c < k ? (c == tt ? 1.0 : 0.0) : M[tt + (int64_t)ny * c];
+    double val = c < k ? (c == tt ? 1.0 : 0.0) : M[tt + (int64_t)ny * (panel ? piv[c] : c)];
     Ui[piv[c] + (int64_t)nx * tt] = val;
   }
   if (tid == 0) {
@@ -459,15 +477,16 @@ __global__ void __launch_bounds__(kIdClThreads) id_kernel_cluster(
 // NT = kIdSmemThreads for the staged classes (several CTAs per SM), kIdLeanThreads for the lean
 // one-CTA-per-SM class (coordinates read from global memory, no staging).
 template <int D, int NT>
-__global__ void __launch_bounds__(NT) id_kernel_smem(
+__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 6) id_kernel_smem(
     int base, int kid, double p2, double tol, const double* __restrict__ X, int64_t n, int d_unused, int r,
     const int* __restrict__ is_leaf, const int* __restrict__ nbegin, const int* __restrict__ first_child,
     const int* __restrict__ nchild, const int* __restrict__ ys_cnt, const int* __restrict__ ys,
     const int* __restrict__ xbar_n, const int64_t* __restrict__ uoff, double* U, int* kout, int* sk,
-    unsigned long long* evals, int cls) {
+    unsigned long long* evals, int cls, int use_panel) {
   extern __shared__ double sh[];
-  __shared__ CpqrRmSmem<NT> csm;
+  __shared__ PanelSmem<NT, kIdPanelNb> psm;
   __shared__ CpqrSmem<NT> csm_cm;
+  __shared__ CpqrRmSmem<NT> csm;
   constexpr bool kLean = NT == kIdLeanThreads;
   const int i = base + blockIdx.x;
   const int nx = xbar_n[i];
@@ -478,8 +497,15 @@ __global__ void __launch_bounds__(NT) id_kernel_smem(
     const int nc = id_smem_class(ny, nx, D);
     if (kLean ? nc != kIdLean : (nc < 0 || nc == kIdLean || (cls >= 0 && nc != cls))) return;
   }
+  // the panel-blocked CPQR (cpqr_panel.cuh) when the node's columns fit the thread groups, else
+  // the warp-per-column one (cpqr.cuh); both on A^T column-major, leading dimension ld <= ny + 15
+  constexpr int kRmax = NT >= 512 ? 4 : 2;
+  const int G = panel_group(nx, NT);
+  const bool panel = use_panel && nx * G <= NT * kRmax;
+  const int ld = panel ? panel_ld(ny, G) : ny;
   double* M = sh;
-  double* nrm2 = M + (int64_t)ny * nx;
+  double* Fs = M + (int64_t)(ny + id_pad_rows(nx, NT)) * nx;
+  double* nrm2 = Fs + kIdPanelNb * nx;
   double* v = nrm2 + nx;
   double* tab = kLean ? v + ny : v + ny + D * (nx + ny);  // exp table
   int* piv = reinterpret_cast<int*>(tab + 64);
@@ -517,13 +543,15 @@ __global__ void __launch_bounds__(NT) id_kernel_smem(
       for (int c = 0; c < D; c++) cx[c * nx + b] = X[c * n + xb[b]];
   }
   __syncthreads();
-  const bool tall = id_tall(ny, nx, NT);
   auto coord_x = [&](int c, int b) { return staged ? cx[c * nx + b] : X[c * n + xb[b]]; };
   auto coord_y = [&](int c, int a) { return staged ? cy[c * ny + a] : X[c * n + yv[a]]; };
+  // unblocked fallback: wide blocks row-major with a thread per column (cta_cpqr_rm), tall ones
+  // column-major with a warp per column (cta_cpqr); the panel CPQR is column-major (ld)
+  const bool rm = !panel && !id_tall(ny, nx, NT);
   int k;
-  if (!tall) {
-    // A^T row-major: M[a*nx + b] = K(Xbar[b], Y^*[a]), Y^* ascending; thread per column b, the
-    // column's point in registers, rows' points broadcast from shared memory (or L1)
+  if (rm) {
+    // A^T row-major: M[a*nx + b] = K(Xbar[b], Y^*[a]); thread per column b, the column's point in
+    // registers, rows' points broadcast from shared memory (or L1)
     for (int b = tid; b < nx; b += NT) {
       double xr[D];
 #pragma unroll
@@ -542,8 +570,7 @@ __global__ void __launch_bounds__(NT) id_kernel_smem(
     __syncthreads();
     k = cta_cpqr_rm<NT>(M, ny, nx, nx, tol, piv, nrm2, v, csm);
   } else {
-    // tall block (few candidates, many farfield rows): A^T column-major, M[a + ny*b], and the
-    // warp-per-column CPQR of cpqr.cuh on shared memory
+    // A^T column-major: M[a + ld*b] = K(Xbar[b], Y^*[a]), Y^* ascending
     for (int e = tid; e < ny * nx; e += NT) {
       const int a = e % ny, b = e / ny;
       double sq = 0.0, dt = 0.0;
@@ -553,16 +580,19 @@ __global__ void __launch_bounds__(NT) id_kernel_smem(
         sq = fma(df, df, sq);
         dt = fma(xc, yc, dt);
       }
-      M[e] = kid == H2_KERNEL_COSDOT ? kernel_cosdot(dt) : kernel_s(kid, p2, sq, tab);
+      M[a + ld * b] = kid == H2_KERNEL_COSDOT ? kernel_cosdot(dt) : kernel_s(kid, p2, sq, tab);
     }
     __syncthreads();
-    k = cta_cpqr<NT>(M, ny, nx, tol, piv, nrm2, v, csm_cm);
+    k = panel ? cta_cpqr_panel<NT, kIdPanelNb, kRmax>(M, ld, ny, nx, tol, G, piv, Fs, psm)
+              : cta_cpqr<NT>(M, ny, nx, tol, piv, nrm2, v, csm_cm);
   }
   double* Ui = U + uoff[blockIdx.x];
   for (int a = tid; a < k; a += NT) sk[(int64_t)i * r + a] = xb[piv[a]];
+  // T of position c: in physical column piv[c] (panel: columns never move) or c (swapped columns)
   for (int e = tid; e < nx * k; e += NT) {
     const int c = e % nx, tt = e / nx;
-    const double val = c < k ? (c == tt ? 1.0 : 0.0) : (tall ? M[tt + ny * c] : M[tt * nx + c]);
+    const double val = c < k ? (c == tt ? 1.0 : 0.0)
+                             : rm ? M[tt * nx + c] : M[tt + (int64_t)ld * (panel ? piv[c] : c)];
     Ui[piv[c] + (int64_t)nx * tt] = val;
   }
   if (tid == 0) {
@@ -628,6 +658,10 @@ void id_sweep(h2_handle* h) {
   H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   const int cs = id_cluster_max();
+  static const int use_panel = [] {  // H2_ID_PANEL=0 (A/B knob): the unblocked CPQR on every path
+    const char* e = getenv("H2_ID_PANEL");
+    return e ? atoi(e) : 1;
+  }();
   static const int64_t cl_min = [] {  // H2_ID_CLMIN (tuning knob): cluster-path threshold, block entries
     const char* e = getenv("H2_ID_CLMIN");
     return e ? (int64_t)atoll(e) : (int64_t)256 * 1024;
@@ -738,11 +772,12 @@ void id_sweep(h2_handle* h) {
       id_kernel<256><<<count, 256, 0, sa>>>(base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf,
                                            h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
                                            work.as<double>(), h->u_off + base, U, h->k, h->sk,
-                                           ev.as<unsigned long long>(), 0, kIdBigBlock, cs, cl_min);
+                                           ev.as<unsigned long long>(), 0, kIdBigBlock, cs, cl_min, use_panel);
       id_kernel<1024><<<count, 1024, 0, sb>>>(base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf,
                                              h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
                                              work.as<double>(), h->u_off + base, U, h->k, h->sk,
-                                             ev.as<unsigned long long>(), kIdBigBlock, INT64_MAX, cs, cl_min);
+                                             ev.as<unsigned long long>(), kIdBigBlock, INT64_MAX, cs, cl_min,
+                                             use_panel);
       H2_CHECK_LAUNCH();
       H2_CUDA_TRY(cudaEventRecord(gev[1], sa));
       H2_CUDA_TRY(cudaEventRecord(gev[2], sb));
@@ -797,14 +832,14 @@ void id_sweep(h2_handle* h) {
       id_kernel_smem<DD, kIdLeanThreads><<<count, kIdLeanThreads, smem, cs>>>(                                  \
           base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child,           \
           h->nchild, h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>(), \
-          cls);                                                                                                 \
+          cls, use_panel);                                                                                      \
     } else {                                                                                                    \
       H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_smem<DD, kIdSmemThreads>,                                      \
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kIdSmemMax));               \
       id_kernel_smem<DD, kIdSmemThreads><<<count, kIdSmemThreads, smem, cs>>>(                                  \
           base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child,           \
           h->nchild, h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>(), \
-          cls);                                                                                                 \
+          cls, use_panel);                                                                                      \
     }                                                                                                           \
     break;
         H2_ID_CASE(1) H2_ID_CASE(2) H2_ID_CASE(3) H2_ID_CASE(4)
