@@ -21,11 +21,15 @@ CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "
 PERM, NODES, CELLS, IL_OFF, IL_IDX, NF_OFF, NF_IDX = 1, 2, 3, 4, 5, 6, 7
 XS_OFF, XS_IDX, YS_OFF, YS_IDX, K, SK_OFF, SK_IDX, U_OFF, U, XBAR_N, TREE_X, CHILD_OFF = (
     8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19)
+# the non-symmetric path's column bases (Algorithm 2 line 11, second getBasis)
+K_COL, SKC_OFF, SKC_IDX, V_OFF, V, XBARC_N = 20, 21, 22, 23, 24, 25
+KERNEL_MQSHIFT = 7  # sqrt(1 + c |x - y + a|^2), non-symmetric
 
 _DTYPES = {PERM: np.int32, NODES: np.int32, CELLS: np.int64, IL_OFF: np.int64, IL_IDX: np.int32,
            NF_OFF: np.int64, NF_IDX: np.int32, XS_OFF: np.int64, XS_IDX: np.int32, YS_OFF: np.int64,
            YS_IDX: np.int32, K: np.int32, SK_OFF: np.int64, SK_IDX: np.int32, U_OFF: np.int64,
-           U: np.float64, XBAR_N: np.int32, TREE_X: np.float64, CHILD_OFF: np.int32}
+           U: np.float64, XBAR_N: np.int32, TREE_X: np.float64, CHILD_OFF: np.int32, K_COL: np.int32,
+           SKC_OFF: np.int64, SKC_IDX: np.int32, V_OFF: np.int64, V: np.float64, XBARC_N: np.int32}
 
 
 def build(force: bool = False) -> str:
@@ -67,6 +71,9 @@ def lib():
         L.orc_vol.argtypes = [vp, i32, vp, i32, i32, vp]
         L.orc_fps.argtypes = [vp, i32, vp, i32, i32, vp]
         L.orc_set_reduct.argtypes = [vp, i32]
+        L.orc_set_nonsym.argtypes = [vp, i32]
+        L.orc_set_kernel_shift.argtypes = [vp, i32]
+        L.orc_calib_level_tr.argtypes = [i32, i32, f64, f64, f64, f64, i32, i32]
         L.orc_surface.argtypes = [vp, i32, vp, i32, i32, vp]
         L.orc_cpqr.argtypes = [vp, i32, i32, f64, vp]
         L.orc_id.argtypes = [vp, i32, i32, f64, vp, vp]
@@ -150,8 +157,15 @@ def admissible(ci, li: int, cj, lj: int, tau: float) -> bool:
     return bool(lib().orc_admissible(_p(ci), li, _p(cj), lj, ci.size, float(tau)))
 
 
-def calib_level(d, kid, param, eps, tau, w, level) -> int:
-    return int(lib().orc_calib_level(d, kid, param, eps, tau, w, level))
+def calib_level(d, kid, param, eps, tau, w, level, tr: int = 0) -> int:
+    """r of one level (tr = 1: the transposed kernel kappa(y, x), the column-basis orientation)."""
+    return int(lib().orc_calib_level_tr(d, kid, param, eps, tau, w, level, int(tr)))
+
+
+def set_kernel_shift(a) -> None:
+    """The shift a of kernel 7 (sqrt(1 + c |x - y + a|^2)); global to the oracle library."""
+    a = np.ascontiguousarray(a, np.float64)
+    lib().orc_set_kernel_shift(_p(a), a.size)
 
 
 def calib_trial(d, kid, param, eps, tau, w, level, m):
@@ -198,15 +212,18 @@ def dense_rows(pts: np.ndarray, kid: int, param: float, x: np.ndarray, rows) -> 
 class OracleH2:
     """A (partition) + B (lists) on construction; then calibrate / hidr / id_sweep / matvec."""
 
-    def __init__(self, pts: np.ndarray, q: int, tau: float = 0.5, reduct: int = 0):
+    def __init__(self, pts: np.ndarray, q: int, tau: float = 0.5, reduct: int = 0, nonsym: bool = False):
         """reduct: the DataReduct of HiDR, 0 volume-based (reading C1), 1 farthest point sampling (C6),
-        2 surface-based (C7)."""
+        2 surface-based (C7).  nonsym: build row AND column bases and every ordered block (Algorithm 2
+        with X^(row) != X^(col); required for kernel 7, allowed for symmetric kernels)."""
         self.pts = np.ascontiguousarray(pts, np.float64)
         self.n, self.d = self.pts.shape
         self._h = lib().orc_new(_p(self.pts), self.n, self.d, int(q), float(tau))
         if not self._h:
             raise ValueError("orc_new rejected the arguments")
         lib().orc_set_reduct(self._h, int(reduct))
+        lib().orc_set_nonsym(self._h, int(bool(nonsym)))
+        self.nonsym = bool(nonsym)
         self.q, self.tau = q, tau
         self.kid, self.param = None, 0.0
 
@@ -266,6 +283,9 @@ class OracleH2:
 
     def skeletons(self):
         return self.csr(SK_OFF, SK_IDX)
+
+    def skeletons_col(self):
+        return self.csr(SKC_OFF, SKC_IDX)
 
     def tree_points(self):
         return self.export(TREE_X).reshape(-1, self.d)

@@ -88,7 +88,15 @@ static int64_t ipow_sat(int64_t m, int d) {
 /* kernel functions  (Table 1; Matern-3/2 from BASELINE.json configs[3])    */
 /* ------------------------------------------------------------------------------------------ */
 
-enum { ORC_COULOMB = 1, ORC_GAUSSIAN = 2, ORC_MATERN32 = 3, ORC_LAPLACE = 4, ORC_BUMP = 5, ORC_COSDOT = 6 };
+enum { ORC_COULOMB = 1, ORC_GAUSSIAN = 2, ORC_MATERN32 = 3, ORC_LAPLACE = 4, ORC_BUMP = 5, ORC_COSDOT = 6,
+       ORC_MQSHIFT = 7 };
+
+/* the shift a of the non-symmetric shifted multiquadric (kernel 7); set by orc_set_kernel_shift */
+static double g_shift[ORC_MAXD];
+
+void orc_set_kernel_shift(const double* a, int d) {
+  for (int k = 0; k < ORC_MAXD; k++) g_shift[k] = k < d ? a[k] : 0.0;
+}
 
 static double sqdist(const double* x, const double* y, int d) {
   double s = 0.0;
@@ -123,6 +131,15 @@ static double kernel_of_s(int kid, double p, double s) {
 }
 
 double orc_kernel(int kid, double p, const double* x, const double* y, int d) {
+  if (kid == ORC_MQSHIFT) { /* sqrt(1 + c |x - y + a|^2), PAPER §4 P:711-716 (c = 100, a = [0, 20]^T
+                               there): smooth and NOT symmetric, kappa(x,y) != kappa(y,x) */
+    double t = 0.0;
+    for (int k = 0; k < d; k++) {
+      double df = x[k] - y[k] + g_shift[k];
+      t = t + df * df;
+    }
+    return sqrt(1.0 + p * t);
+  }
   if (kid == ORC_COSDOT) { /* kappa_3 of Table 1: cos(x . y), the dot summed in k order */
     double t = 0.0;
     for (int k = 0; k < d; k++) t = t + x[k] * y[k];
@@ -359,6 +376,11 @@ typedef struct orc_h2 {
   double** U;     /* |Xbar_i| x k_i, column-major */
   int* child_off; /* offset of node's skeleton rows inside its parent's Xbar */
   int calib_r[64]; /* E: per-level r of the last orc_calibrate (0 = level without an admissible pair) */
+  /* non-symmetric path (Algorithm 2 lines 4-12 with separate row / column sets): the
+   * column bases V_i (W = stacked V of the children), skeletons X^_i^(col), ranks */
+  int nonsym;
+  int *k_col, **sk_col, *xbar_col_n, *child_off_col;
+  double** V;
   double t_stage[8];
 } orc_h2;
 
@@ -693,6 +715,9 @@ static int orc_reduct(const orc_h2* h, const int* S, int ns, int k, int* out) {
 }
 
 void orc_set_reduct(orc_h2* h, int reduct) { h->reduct = reduct; }
+/* 1: build row AND column bases (Algorithm 2 line 11, both getBasis calls), blocks for all ordered
+ * pairs; required for a non-symmetric kernel, allowed for a symmetric one (then V = U exactly) */
+void orc_set_nonsym(orc_h2* h, int nonsym) { h->nonsym = nonsym; }
 
 int orc_hidr(orc_h2* h, int r) {
   if (r < 1) return -1;
@@ -797,8 +822,14 @@ void orc_calib_points(int d, double tau, double w, int level, double* Z1, double
  * the ID built from K(Z1, Z2*) applied to the full K(Z1, Z2); *G_out = m^d.  The optional
  * outputs expose the trial for its pins: *k_out the ID rank, skel_out[0:k] the skeleton rows
  * (indices into Z1, pivot order), sel_out[0:*ns_out] the columns Z2* (indices into Z2).       */
-double orc_calib_trial_ex(int d, int kid, double p, double eps, double tau, double w, int level,
-                          int m, int64_t* G_out, int* k_out, int* skel_out, int* sel_out, int* ns_out) {
+/* kappa(x, y), or kappa^T(x, y) = kappa(y, x) when tr (the column-basis orientation of a
+ * non-symmetric kernel, Algorithm 2 line 11: getBasis(K_{Y X}^T)) */
+static double kern_tr(int kid, double p, const double* x, const double* y, int d, int tr) {
+  return tr ? orc_kernel(kid, p, y, x, d) : orc_kernel(kid, p, x, y, d);
+}
+
+static double calib_trial_impl(int d, int kid, double p, double eps, double tau, double w, int level, int m,
+                               int tr, int64_t* G_out, int* k_out, int* skel_out, int* sel_out, int* ns_out) {
   const int N = ORC_CAL_NPTS;
   double* Z1 = (double*)malloc(sizeof(double) * (size_t)N * (size_t)d);
   double* Z2 = (double*)malloc(sizeof(double) * (size_t)N * (size_t)d);
@@ -818,7 +849,7 @@ double orc_calib_trial_ex(int d, int kid, double p, double eps, double tau, doub
   double* A = (double*)malloc(sizeof(double) * (size_t)N * (size_t)ns);
   for (int b = 0; b < N; b++)
     for (int a = 0; a < ns; a++)
-      A[(int64_t)b * ns + a] = orc_kernel(kid, p, Z1 + (int64_t)b * d, Z2 + (int64_t)sel[a] * d, d);
+      A[(int64_t)b * ns + a] = kern_tr(kid, p, Z1 + (int64_t)b * d, Z2 + (int64_t)sel[a] * d, d, tr);
   int skel[ORC_CAL_NPTS];
   double* U = (double*)malloc(sizeof(double) * (size_t)N * (size_t)(ns > 0 ? ns : 1));
   int k = orc_id(A, N, ns, 1e-3 * eps, skel, U);
@@ -826,10 +857,10 @@ double orc_calib_trial_ex(int d, int kid, double p, double eps, double tau, doub
   double num = 0.0, den = 0.0;
   for (int b = 0; b < N; b++)
     for (int c = 0; c < N; c++) {
-      double kv = orc_kernel(kid, p, Z1 + (int64_t)b * d, Z2 + (int64_t)c * d, d);
+      double kv = kern_tr(kid, p, Z1 + (int64_t)b * d, Z2 + (int64_t)c * d, d, tr);
       double ap = 0.0;
       for (int t = 0; t < k; t++)
-        ap = ap + U[b + (int64_t)N * t] * orc_kernel(kid, p, Z1 + (int64_t)skel[t] * d, Z2 + (int64_t)c * d, d);
+        ap = ap + U[b + (int64_t)N * t] * kern_tr(kid, p, Z1 + (int64_t)skel[t] * d, Z2 + (int64_t)c * d, d, tr);
       double df = kv - ap;
       num = num + df * df;
       den = den + kv * kv;
@@ -845,18 +876,27 @@ double orc_calib_trial_ex(int d, int kid, double p, double eps, double tau, doub
   return den > 0.0 ? sqrt(num) / sqrt(den) : 0.0;
 }
 
-double orc_calib_trial(int d, int kid, double p, double eps, double tau, double w, int level,
-                       int m, int64_t* G_out) {
-  return orc_calib_trial_ex(d, kid, p, eps, tau, w, level, m, G_out, NULL, NULL, NULL, NULL);
+double orc_calib_trial_ex(int d, int kid, double p, double eps, double tau, double w, int level,
+                          int m, int64_t* G_out, int* k_out, int* skel_out, int* sel_out, int* ns_out) {
+  return calib_trial_impl(d, kid, p, eps, tau, w, level, m, 0, G_out, k_out, skel_out, sel_out, ns_out);
 }
 
-/* r for one level: first m = 1, 2, ... with e < 1e-2 eps, or m^d >= 256 (E2) */
-int orc_calib_level(int d, int kid, double p, double eps, double tau, double w, int level) {
+double orc_calib_trial(int d, int kid, double p, double eps, double tau, double w, int level,
+                       int m, int64_t* G_out) {
+  return calib_trial_impl(d, kid, p, eps, tau, w, level, m, 0, G_out, NULL, NULL, NULL, NULL);
+}
+
+/* r for one level and orientation: first m = 1, 2, ... with e < 1e-2 eps, or m^d >= 256 (E2) */
+int orc_calib_level_tr(int d, int kid, double p, double eps, double tau, double w, int level, int tr) {
   for (int m = 1;; m++) {
     int64_t G;
-    double e = orc_calib_trial(d, kid, p, eps, tau, w, level, m, &G);
+    double e = calib_trial_impl(d, kid, p, eps, tau, w, level, m, tr, &G, NULL, NULL, NULL, NULL);
     if (e < 1e-2 * eps || G >= ORC_CAL_NPTS) return (int)G;
   }
+}
+
+int orc_calib_level(int d, int kid, double p, double eps, double tau, double w, int level) {
+  return orc_calib_level_tr(d, kid, p, eps, tau, w, level, 0);
 }
 
 /* r = max over levels holding an admissible pair of that level's r (E4); 1 if none */
@@ -869,7 +909,13 @@ int orc_calibrate(orc_h2* h, int kid, double p, double eps) {
   int rl[64] = {0};
 #pragma omp parallel for schedule(dynamic, 1)
   for (int l = 0; l <= h->depth; l++)
-    if (has[l]) rl[l] = orc_calib_level(h->d, kid, p, eps, h->tau, ldexp(h->W, -l), l);
+    if (has[l]) {
+      rl[l] = orc_calib_level(h->d, kid, p, eps, h->tau, ldexp(h->W, -l), l);
+      if (h->nonsym) { /* reading E7: the column bases need the same accuracy: max of both orientations */
+        int rt = orc_calib_level_tr(h->d, kid, p, eps, h->tau, ldexp(h->W, -l), l, 1);
+        if (rt > rl[l]) rl[l] = rt;
+      }
+    }
   for (int l = 0; l <= h->depth; l++)
     if (has[l] && rl[l] > r) r = rl[l];
   for (int l = 0; l < 64; l++) h->calib_r[l] = l <= h->depth && has[l] ? rl[l] : 0;
@@ -882,26 +928,13 @@ int orc_calibrate(orc_h2* h, int kid, double p, double eps) {
 /* F. bottom-up ID sweep (Algorithm 2 lines 10-13; readings F1-F6)                  */
 /* ------------------------------------------------------------------------------------------ */
 
-int orc_id_sweep(orc_h2* h, int kid, double p, double id_tol) {
-  if (!h->ys_n) return -1;
-  double t0 = wall();
-  int nn = h->nnodes, d = h->d;
-  h->kid = kid;
-  h->kparam = p;
-  h->id_tol = id_tol;
-  free_lists2(h->sk, nn);
-  if (h->U) {
-    for (int i = 0; i < nn; i++) free(h->U[i]);
-    free(h->U);
-  }
-  free(h->k);
-  free(h->xbar_n);
-  free(h->child_off);
-  h->k = (int*)calloc((size_t)nn, sizeof(int));
-  h->xbar_n = (int*)calloc((size_t)nn, sizeof(int));
-  h->child_off = (int*)calloc((size_t)nn, sizeof(int));
-  h->sk = (int**)calloc((size_t)nn, sizeof(int*));
-  h->U = (double**)calloc((size_t)nn, sizeof(double*));
+/* One bottom-up getBasis sweep (Algorithm 2 lines 10-12): for every non-root node with
+ * Y_i^* != {}, Xbar_i = X_i at a leaf or the children's skeletons (child order); A = kappa(Xbar_i,
+ * Y_i^*) (tr = 0: the row bases U_i, getBasis(K_{Xbar Y*})) or kappa(Y_i^*, Xbar_i)^T (tr = 1: the
+ * column bases V_i, getBasis(K_{Y* Xbar}^T)); ID -> k, skeleton, U (|Xbar| x k). */
+static void id_sweep_one(orc_h2* h, int kid, double p, double id_tol, int tr, int* K, int** SK, double** UU,
+                         int* XBN, int* CHO) {
+  int d = h->d;
   for (int l = h->depth; l >= 1; l--) {
 #pragma omp parallel for schedule(dynamic, 1)
     for (int i = h->lvl_start[l]; i < h->lvl_start[l + 1]; i++) {
@@ -910,8 +943,8 @@ int orc_id_sweep(orc_h2* h, int kid, double p, double id_tol) {
       int nx = 0;
       if (h->is_leaf[i]) nx = h->end[i] - h->begin[i];
       else
-        for (int c = 0; c < h->nchild[i]; c++) nx += h->k[h->first_child[i] + c];
-      h->xbar_n[i] = nx;
+        for (int c = 0; c < h->nchild[i]; c++) nx += K[h->first_child[i] + c];
+      XBN[i] = nx;
       if (nx == 0) continue;
       int* Xb = (int*)malloc(sizeof(int) * (size_t)nx);
       if (h->is_leaf[i]) {
@@ -920,29 +953,70 @@ int orc_id_sweep(orc_h2* h, int kid, double p, double id_tol) {
         int o = 0;
         for (int c = 0; c < h->nchild[i]; c++) {
           int ch = h->first_child[i] + c;
-          h->child_off[ch] = o;
-          if (h->k[ch] > 0) memcpy(Xb + o, h->sk[ch], sizeof(int) * (size_t)h->k[ch]);
-          o += h->k[ch];
+          CHO[ch] = o;
+          if (K[ch] > 0) memcpy(Xb + o, SK[ch], sizeof(int) * (size_t)K[ch]);
+          o += K[ch];
         }
       }
       int ny = h->ys_n[i];
-      /* A = K(Xbar_i, Y_i^*), columns in ascending Y^* order (F3) */
+      /* A = K(Xbar_i, Y_i^*) (or its transposed-kernel version), columns in ascending Y^* order (F3) */
       double* A = (double*)malloc(sizeof(double) * (size_t)nx * (size_t)ny);
       for (int b = 0; b < nx; b++)
         for (int a = 0; a < ny; a++)
-          A[(int64_t)b * ny + a] = orc_kernel(kid, p, h->X + (int64_t)Xb[b] * d, h->X + (int64_t)h->ys[i][a] * d, d);
+          A[(int64_t)b * ny + a] = kern_tr(kid, p, h->X + (int64_t)Xb[b] * d, h->X + (int64_t)h->ys[i][a] * d, d, tr);
       int* skel = (int*)malloc(sizeof(int) * (size_t)(nx < ny ? nx : ny));
       double* U = (double*)malloc(sizeof(double) * (size_t)nx * (size_t)(nx < ny ? nx : ny));
       int k = orc_id(A, nx, ny, id_tol, skel, U);
       int* sk = (int*)malloc(sizeof(int) * (size_t)(k > 0 ? k : 1));
       for (int t = 0; t < k; t++) sk[t] = Xb[skel[t]];
-      h->k[i] = k;
-      h->sk[i] = sk;
-      h->U[i] = U;
+      K[i] = k;
+      SK[i] = sk;
+      UU[i] = U;
       free(skel);
       free(A);
       free(Xb);
     }
+  }
+}
+
+static void free_basis(int nn, int** k, int*** sk, double*** U, int** xbn, int** cho) {
+  if (*sk) free_lists2(*sk, nn);
+  if (*U) {
+    for (int i = 0; i < nn; i++) free((*U)[i]);
+    free(*U);
+  }
+  free(*k);
+  free(*xbn);
+  free(*cho);
+  *k = NULL;
+  *sk = NULL;
+  *U = NULL;
+  *xbn = NULL;
+  *cho = NULL;
+}
+
+int orc_id_sweep(orc_h2* h, int kid, double p, double id_tol) {
+  if (!h->ys_n) return -1;
+  double t0 = wall();
+  int nn = h->nnodes;
+  h->kid = kid;
+  h->kparam = p;
+  h->id_tol = id_tol;
+  free_basis(nn, &h->k, &h->sk, &h->U, &h->xbar_n, &h->child_off);
+  free_basis(nn, &h->k_col, &h->sk_col, &h->V, &h->xbar_col_n, &h->child_off_col);
+  h->k = (int*)calloc((size_t)nn, sizeof(int));
+  h->xbar_n = (int*)calloc((size_t)nn, sizeof(int));
+  h->child_off = (int*)calloc((size_t)nn, sizeof(int));
+  h->sk = (int**)calloc((size_t)nn, sizeof(int*));
+  h->U = (double**)calloc((size_t)nn, sizeof(double*));
+  id_sweep_one(h, kid, p, id_tol, 0, h->k, h->sk, h->U, h->xbar_n, h->child_off);
+  if (h->nonsym) { /* the column bases: second getBasis of Algorithm 2 line 11 */
+    h->k_col = (int*)calloc((size_t)nn, sizeof(int));
+    h->xbar_col_n = (int*)calloc((size_t)nn, sizeof(int));
+    h->child_off_col = (int*)calloc((size_t)nn, sizeof(int));
+    h->sk_col = (int**)calloc((size_t)nn, sizeof(int*));
+    h->V = (double**)calloc((size_t)nn, sizeof(double*));
+    id_sweep_one(h, kid, p, id_tol, 1, h->k_col, h->sk_col, h->V, h->xbar_col_n, h->child_off_col);
   }
   h->t_stage[4] = wall() - t0;
   return 0;
@@ -954,20 +1028,24 @@ int orc_id_sweep(orc_h2* h, int kid, double p, double id_tol) {
 
 /* Evaluates every coupling block B_ij = K(X^_i, X^_j) (i<j in IL) and nearfield block
  * D_ij = K(X_i, X_j) (i<=j in NF) into `buf` (when non-NULL and large enough, consecutively,
- * row-major) and returns the entry count; `checksum` receives the sum of all entries.        */
+ * row-major) and returns the entry count; `checksum` receives the sum of all entries.
+ * Non-symmetric path: every ordered pair, B_ij = K(X^_i^(row), X^_j^(col)).        */
 int64_t orc_fill(const orc_h2* h, double* buf, int64_t cap, double* checksum) {
   int d = h->d;
   int nn = h->nnodes;
+  const int ns = h->nonsym;
+  const int* kc = ns ? h->k_col : h->k;
+  int* const* skc = ns ? h->sk_col : h->sk;
   int64_t* off = (int64_t*)calloc((size_t)nn + 1, sizeof(int64_t));
   for (int i = 0; i < nn; i++) {
     int64_t s = 0;
     for (int64_t e = h->il_off[i]; e < h->il_off[i + 1]; e++) {
       int j = h->il_idx[e];
-      if (j > i) s += (int64_t)h->k[i] * h->k[j];
+      if (ns || j > i) s += (int64_t)h->k[i] * kc[j];
     }
     for (int64_t e = h->nf_off[i]; e < h->nf_off[i + 1]; e++) {
       int j = h->nf_idx[e];
-      if (j >= i) s += (int64_t)(h->end[i] - h->begin[i]) * (h->end[j] - h->begin[j]);
+      if (ns || j >= i) s += (int64_t)(h->end[i] - h->begin[i]) * (h->end[j] - h->begin[j]);
     }
     off[i + 1] = off[i] + s;
   }
@@ -979,10 +1057,10 @@ int64_t orc_fill(const orc_h2* h, double* buf, int64_t cap, double* checksum) {
     int64_t o = off[i];
     for (int64_t e = h->il_off[i]; e < h->il_off[i + 1]; e++) {
       int j = h->il_idx[e];
-      if (j <= i) continue;
+      if (!ns && j <= i) continue;
       for (int a = 0; a < h->k[i]; a++)
-        for (int b = 0; b < h->k[j]; b++) {
-          double v = orc_kernel(h->kid, h->kparam, h->X + (int64_t)h->sk[i][a] * d, h->X + (int64_t)h->sk[j][b] * d, d);
+        for (int b = 0; b < kc[j]; b++) {
+          double v = orc_kernel(h->kid, h->kparam, h->X + (int64_t)h->sk[i][a] * d, h->X + (int64_t)skc[j][b] * d, d);
           if (store) buf[o] = v;
           o++;
           cs += v;
@@ -990,7 +1068,7 @@ int64_t orc_fill(const orc_h2* h, double* buf, int64_t cap, double* checksum) {
     }
     for (int64_t e = h->nf_off[i]; e < h->nf_off[i + 1]; e++) {
       int j = h->nf_idx[e];
-      if (j < i) continue;
+      if (!ns && j < i) continue;
       for (int a = h->begin[i]; a < h->end[i]; a++)
         for (int b = h->begin[j]; b < h->end[j]; b++) {
           double v = orc_kernel(h->kid, h->kparam, h->X + (int64_t)a * d, h->X + (int64_t)b * d, d);
@@ -1040,17 +1118,25 @@ int orc_matvec_rows(const orc_h2* h, const double* x, const int64_t* rows, int64
   double** zh = (double**)calloc((size_t)nn, sizeof(double*));
   double** yh = (double**)calloc((size_t)nn, sizeof(double*));
   for (int i = 0; i < nn; i++) {
-    zh[i] = (double*)calloc((size_t)(h->k[i] > 0 ? h->k[i] : 1), sizeof(double));
+    int kz = h->nonsym ? h->k_col[i] : h->k[i];
+    zh[i] = (double*)calloc((size_t)(kz > 0 ? kz : 1), sizeof(double));
     yh[i] = (double*)calloc((size_t)(h->k[i] > 0 ? h->k[i] : 1), sizeof(double));
   }
-  /* upward pass */
+  /* upward pass with the column bases: z^_i = V_i^T x_i (leaf), z^_p = sum_c W_c^T z^_c (V = U, W = R
+   * for a symmetric build, reading F6) */
+  const int ns = h->nonsym;
+  const int* kc = ns ? h->k_col : h->k;
+  int* const* skc = ns ? h->sk_col : h->sk;
+  double* const* VV = ns ? h->V : h->U;
+  const int* xbc = ns ? h->xbar_col_n : h->xbar_n;
+  const int* choc = ns ? h->child_off_col : h->child_off;
   for (int l = h->depth; l >= 1; l--) {
 #pragma omp parallel for schedule(dynamic, 4)
     for (int i = h->lvl_start[l]; i < h->lvl_start[l + 1]; i++) {
-      int k = h->k[i];
+      int k = kc[i];
       if (k == 0) continue;
-      int nx = h->xbar_n[i];
-      const double* U = h->U[i];
+      int nx = xbc[i];
+      const double* U = VV[i];
       for (int c = 0; c < k; c++) {
         double s = 0.0;
         if (h->is_leaf[i]) {
@@ -1058,7 +1144,7 @@ int orc_matvec_rows(const orc_h2* h, const double* x, const int64_t* rows, int64
         } else {
           for (int cc = 0; cc < h->nchild[i]; cc++) {
             int ch = h->first_child[i] + cc;
-            for (int a = 0; a < h->k[ch]; a++) s = s + U[h->child_off[ch] + a + (int64_t)nx * c] * zh[ch][a];
+            for (int a = 0; a < kc[ch]; a++) s = s + U[choc[ch] + a + (int64_t)nx * c] * zh[ch][a];
           }
         }
         zh[i][c] = s;
@@ -1073,8 +1159,8 @@ int orc_matvec_rows(const orc_h2* h, const double* x, const int64_t* rows, int64
       int j = h->il_idx[e];
       for (int a = 0; a < h->k[i]; a++) {
         double s = 0.0;
-        for (int b = 0; b < h->k[j]; b++)
-          s = s + orc_kernel(h->kid, h->kparam, h->X + (int64_t)h->sk[i][a] * d, h->X + (int64_t)h->sk[j][b] * d, d) * zh[j][b];
+        for (int b = 0; b < kc[j]; b++)
+          s = s + orc_kernel(h->kid, h->kparam, h->X + (int64_t)h->sk[i][a] * d, h->X + (int64_t)skc[j][b] * d, d) * zh[j][b];
         yh[i][a] = yh[i][a] + s;
       }
     }
@@ -1165,7 +1251,8 @@ enum {
   ORC_PERM = 1, ORC_NODES = 2, ORC_CELLS = 3, ORC_IL_OFF = 4, ORC_IL_IDX = 5, ORC_NF_OFF = 6,
   ORC_NF_IDX = 7, ORC_XS_OFF = 8, ORC_XS_IDX = 9, ORC_YS_OFF = 10, ORC_YS_IDX = 11, ORC_K = 12,
   ORC_SK_OFF = 13, ORC_SK_IDX = 14, ORC_U_OFF = 15, ORC_U = 16, ORC_XBAR_N = 17, ORC_TREE_X = 18,
-  ORC_CHILD_OFF = 19
+  ORC_CHILD_OFF = 19, ORC_K_COL = 20, ORC_SKC_OFF = 21, ORC_SKC_IDX = 22, ORC_V_OFF = 23, ORC_V = 24,
+  ORC_XBARC_N = 25
 };
 
 static int64_t pack_lists(int** a, const int* cnt, int nn, int64_t* off, int* idx) {
@@ -1285,6 +1372,45 @@ int64_t orc_export(const orc_h2* h, int what, void* buf, int64_t cap) {
       }
       return s;
     }
+    case ORC_K_COL:
+    case ORC_XBARC_N:
+      if (!h->k_col) return -1;
+      need = nn;
+      if (buf && cap >= need) memcpy(buf, what == ORC_K_COL ? h->k_col : h->xbar_col_n, sizeof(int) * (size_t)nn);
+      return need;
+    case ORC_SKC_OFF:
+    case ORC_SKC_IDX:
+      if (!h->k_col) return -1;
+      if (what == ORC_SKC_OFF) {
+        need = nn + 1;
+        if (buf && cap >= need) pack_lists(h->sk_col, h->k_col, nn, (int64_t*)buf, NULL);
+        return need;
+      }
+      need = pack_lists(h->sk_col, h->k_col, nn, NULL, NULL);
+      if (buf && cap >= need) pack_lists(h->sk_col, h->k_col, nn, NULL, (int*)buf);
+      return need;
+    case ORC_V_OFF:
+    case ORC_V: {
+      if (!h->k_col) return -1;
+      int64_t s = 0;
+      for (int i = 0; i < nn; i++) {
+        if (what == ORC_V_OFF && buf && cap >= nn + 1) ((int64_t*)buf)[i] = s;
+        s += (int64_t)h->xbar_col_n[i] * h->k_col[i];
+      }
+      if (what == ORC_V_OFF) {
+        if (buf && cap >= nn + 1) ((int64_t*)buf)[nn] = s;
+        return nn + 1;
+      }
+      if (buf && cap >= s) {
+        int64_t o = 0;
+        for (int i = 0; i < nn; i++) {
+          int64_t sz = (int64_t)h->xbar_col_n[i] * h->k_col[i];
+          if (sz > 0) memcpy((double*)buf + o, h->V[i], sizeof(double) * (size_t)sz);
+          o += sz;
+        }
+      }
+      return s;
+    }
     default:
       return -1;
   }
@@ -1344,6 +1470,7 @@ void orc_free(orc_h2* h) {
   free(h->k);
   free(h->xbar_n);
   free(h->child_off);
+  free_basis(nn, &h->k_col, &h->sk_col, &h->V, &h->xbar_col_n, &h->child_off_col);
   free(h);
 }
 

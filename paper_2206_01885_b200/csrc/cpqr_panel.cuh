@@ -38,7 +38,6 @@ namespace h2 {
 template <int NT, int NB>
 struct PanelSmem {
   double wval[NT / 32];   // per-warp candidate: residual norm^2 (-1: none)
-  double part[NT / 32][NB + 1];
   double tot[NB + 1];
   int wpos[NT / 32], wcol[NT / 32];
   double xt;  // x_t of the pivot column (row t)
@@ -83,9 +82,17 @@ __device__ int cta_cpqr_panel(double* __restrict__ M, const int ld, const int ny
   for (int r = 0; r < RMAX; r++) {
     const int c = grp + r * ngrp;
     const bool act = c < nx;
-    double s = 0.0;
-    if (act)
-      for (int i = g; i < ny; i += G) s += M[i + (int64_t)ld * c] * M[i + (int64_t)ld * c];
+    double s = 0.0, s1 = 0.0;
+    if (act) {
+      const double* col = M + (int64_t)ld * c;
+      int i = g;
+      for (; i + G < ny; i += 2 * G) {
+        s += col[i] * col[i];
+        s1 += col[i + G] * col[i + G];
+      }
+      for (; i < ny; i += G) s += col[i] * col[i];
+    }
+    s += s1;
     for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
     nrm[r] = act ? s : -1.0;
     ref[r] = s;
@@ -138,16 +145,37 @@ __device__ int cta_cpqr_panel(double* __restrict__ M, const int ld, const int ny
         if (act) {
           double* col = M + (int64_t)ld * c;
           double fc[NB];
+          int vc[NB];
 #pragma unroll
-          for (int l = 0; l < NB; l++) fc[l] = l < j ? Fs[l * nx + c] : 0.0;
-          for (int i = t + g; i < ny; i += G) {
+          for (int l = 0; l < NB; l++) {
+            fc[l] = l < j ? Fs[l * nx + c] : 0.0;
+            vc[l] = l < j ? vcol[l] : 0;
+          }
+          double s1 = 0.0;
+          int i = t + g;
+          for (; i + G < ny; i += 2 * G) {
+            double a = col[i], b = col[i + G];
+#pragma unroll
+            for (int l = 0; l < NB; l++)
+              if (l < j) {
+                const double* vl = M + (int64_t)ld * vc[l];
+                a -= vl[i] * fc[l];
+                b -= vl[i + G] * fc[l];
+              }
+            col[i] = a;
+            col[i + G] = b;
+            s += a * a;
+            s1 += b * b;
+          }
+          for (; i < ny; i += G) {
             double a = col[i];
 #pragma unroll
             for (int l = 0; l < NB; l++)
-              if (l < j) a -= M[i + (int64_t)ld * vcol[l]] * fc[l];
+              if (l < j) a -= M[i + (int64_t)ld * vc[l]] * fc[l];
             col[i] = a;
             s += a * a;
           }
+          s += s1;
         }
         for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
         if (act) {
@@ -182,42 +210,35 @@ __device__ int cta_cpqr_panel(double* __restrict__ M, const int ld, const int ny
     const int p = bc, posp = bp;
     const int ct = col_at[t];  // the column at position t moves to the pivot's position
     const double* fpp = Fs + p;  // F[p, l] at fpp[l * nx]
-    // ---- the pivot column brought up to date: x = a0_p - V F_p^T (rows >= t); partial sums of
-    // |x|^2 and of V^T x -----------------------------------------------------------------------------
-    double px2 = 0.0, pw[NB];
-#pragma unroll
-    for (int l = 0; l < NB; l++) pw[l] = 0.0;
+    // ---- the pivot column brought up to date: x = a0_p - V F_p^T (rows >= t), then (one warp per
+    // quantity, in parallel) |x|^2 and the dots (V^T x)_l ------------------------------------------
     double* colp = M + (int64_t)ld * p;
     for (int i = t + tid; i < ny; i += NT) {
-      double x = colp[i];
+      double x0 = colp[i], x1 = 0.0;
 #pragma unroll
-      for (int l = 0; l < NB; l++)
-        if (l < j) x -= M[i + (int64_t)ld * vcol[l]] * fpp[l * nx];
+      for (int l = 0; l < NB; l += 2) {
+        if (l < j) x0 -= M[i + (int64_t)ld * vcol[l]] * fpp[l * nx];
+        if (l + 1 < j) x1 -= M[i + (int64_t)ld * vcol[l + 1]] * fpp[(l + 1) * nx];
+      }
+      const double x = x0 + x1;
       colp[i] = x;
       if (i == t) sm.xt = x;
-      px2 += x * x;
-#pragma unroll
-      for (int l = 0; l < NB; l++)
-        if (l < j) pw[l] += M[i + (int64_t)ld * vcol[l]] * x;
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      px2 += __shfl_xor_sync(kFull, px2, o);
-#pragma unroll
-      for (int l = 0; l < NB; l++)
-        if (l < j) pw[l] += __shfl_xor_sync(kFull, pw[l], o);
-    }
-    if (lane == 0) {
-      sm.part[warp][NB] = px2;
-#pragma unroll
-      for (int l = 0; l < NB; l++)
-        if (l < j) sm.part[warp][l] = pw[l];
     }
     __syncthreads();
-    for (int qq = warp; qq <= j; qq += NW) {  // quantity q < j: (V^T x)_q; q = j: |x|^2
-      const int q = qq == j ? NB : qq;
-      double s = lane < NW ? sm.part[lane][q] : 0.0;
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-      if (lane == 0) sm.tot[q] = s;
+    for (int qq = warp; qq <= j; qq += NW) {  // quantity q < j: (V^T x)_q over rows >= t; q = j: |x|^2
+      const double* a = qq == j ? colp : M + (int64_t)ld * vcol[qq];
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int i = t + lane;
+      for (; i + 96 < ny; i += 128) {
+        s0 += a[i] * colp[i];
+        s1 += a[i + 32] * colp[i + 32];
+        s2 += a[i + 64] * colp[i + 64];
+        s3 += a[i + 96] * colp[i + 96];
+      }
+      for (; i < ny; i += 32) s0 += a[i] * colp[i];
+      double sq = (s0 + s1) + (s2 + s3);
+      for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(kFull, sq, o);
+      if (lane == 0) sm.tot[qq == j ? NB : qq] = sq;
     }
     __syncthreads();
     // ---- the reflector H = I - tau v v^T, v = x - alpha e_t ---------------------------------------
@@ -244,8 +265,17 @@ __device__ int cta_cpqr_panel(double* __restrict__ M, const int ld, const int ny
       if (act) {
         const double* col = M + (int64_t)ld * c;
         at = col[t];
-        if (g == 0) s = vhead * at;
-        for (int i = t + 1 + g; i < ny; i += G) s += colp[i] * col[i];
+        double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        s = g == 0 ? vhead * at : 0.0;
+        int i = t + 1 + g;
+        for (; i + 3 * G < ny; i += 4 * G) {
+          s += colp[i] * col[i];
+          s1 += colp[i + G] * col[i + G];
+          s2 += colp[i + 2 * G] * col[i + 2 * G];
+          s3 += colp[i + 3 * G] * col[i + 3 * G];
+        }
+        for (; i < ny; i += G) s += colp[i] * col[i];
+        s = (s + s1) + (s2 + s3);
       }
       for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
       if (act) {

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
   if (blk < min_block || blk >= max_block) return;  // the other thread-count variant
   // the panel-blocked CPQR with at least 4 threads per column (32-byte sectors of L2), when the
   // columns fit RMAX rounds of thread groups; else the warp-per-column one
-  constexpr int kRmaxG = 4;
+  constexpr int kRmaxG = kIdThreads >= 1024 ? 2 : 4;
   const int Gp = panel_group(nx, kIdThreads);
   const int G = Gp < 4 ? 4 : Gp;
   const bool panel = use_panel && (int64_t)nx * G <= (int64_t)kIdThreads * kRmaxG;
@@ -570,17 +570,22 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 6) id_kernel_smem(
     __syncthreads();
     k = cta_cpqr_rm<NT>(M, ny, nx, nx, tol, piv, nrm2, v, csm);
   } else {
-    // A^T column-major: M[a + ld*b] = K(Xbar[b], Y^*[a]), Y^* ascending
-    for (int e = tid; e < ny * nx; e += NT) {
-      const int a = e % ny, b = e / ny;
-      double sq = 0.0, dt = 0.0;
+    // A^T column-major: M[a + ld*b] = K(Xbar[b], Y^*[a]), Y^* ascending; a warp per column b (its
+    // point broadcast), lanes over the rows a
+    for (int b = tid >> 5; b < nx; b += NT / 32) {
+      double xb_[D];
 #pragma unroll
-      for (int c = 0; c < D; c++) {
-        const double xc = coord_x(c, b), yc = coord_y(c, a), df = xc - yc;
-        sq = fma(df, df, sq);
-        dt = fma(xc, yc, dt);
+      for (int c = 0; c < D; c++) xb_[c] = coord_x(c, b);
+      for (int a = tid & 31; a < ny; a += 32) {
+        double sq = 0.0, dt = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; c++) {
+          const double yc = coord_y(c, a), df = xb_[c] - yc;
+          sq = fma(df, df, sq);
+          dt = fma(xb_[c], yc, dt);
+        }
+        M[a + ld * b] = kid == H2_KERNEL_COSDOT ? kernel_cosdot(dt) : kernel_s(kid, p2, sq, tab);
       }
-      M[a + ld * b] = kid == H2_KERNEL_COSDOT ? kernel_cosdot(dt) : kernel_s(kid, p2, sq, tab);
     }
     __syncthreads();
     k = panel ? cta_cpqr_panel<NT, kIdPanelNb, kRmax>(M, ld, ny, nx, tol, G, piv, Fs, psm)
