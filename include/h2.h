@@ -27,8 +27,11 @@
  *     h2_free.
  *   - On failure a call returns NULL (builders) or a negative H2_ERR_* code, and the thread-local
  *     h2_last_error()/h2_last_error_message() describe it.  No call aborts the process.
- *   - Symmetric kernels only (all three below): row and column bases coincide (V = U, W = R,
- *     reading F6) and symmetric blocks are stored once (i < j coupling, i <= j nearfield).
+ *   - Symmetric kernels (1-6): row and column bases coincide (V = U, W = R, reading F6) and
+ *     symmetric blocks are stored once (i < j coupling, i <= j nearfield).  Non-symmetric kernels
+ *     (7), or h2_options.nonsymmetric = 1: Algorithm 2 with separate row and column sets (both
+ *     getBasis calls of line 11): row bases U/R, column bases V/W, and every ordered block
+ *     B_ij = K(X^_i^(row), X^_j^(col)), K(X_i, X_j) stored.
  */
 #ifndef H2_B200_H
 #define H2_B200_H
@@ -48,8 +51,12 @@ enum {
   H2_KERNEL_LAPLACE = 4,  /* exp(-r/l) (P:91 at l = 1).                     kernel_params[0] = l > 0          */
   H2_KERNEL_BUMP = 5,     /* exp(-1/(1 - 0.1 r^2)) for 0.1 r^2 < 1, else 0 (Table 1 kappa_4).
                              kernel_params: none (may be NULL)                                            */
-  H2_KERNEL_COSDOT = 6    /* cos(x . y) (Table 1 kappa_3): symmetric, not a function of |x-y|.
+  H2_KERNEL_COSDOT = 6,   /* cos(x . y) (Table 1 kappa_3): symmetric, not a function of |x-y|.
                              kernel_params: none (may be NULL)                                            */
+  H2_KERNEL_MQSHIFT = 7   /* sqrt(1 + c |x - y + a|^2), the shifted multiquadric of PAPER §4 (P:711-716,
+                             c = 100, a = [0, 20] there): smooth, NOT symmetric (kappa(x,y) != kappa(y,x)).
+                             kernel_params: d + 1 values {c > 0, a_0, ..., a_{d-1}}, all finite.
+                             Always built on the non-symmetric path.                                      */
 };
 
 /* ---- status codes ------------------------------------------------------------------------------ */
@@ -109,6 +116,9 @@ typedef struct h2_options {
   int32_t reduct;          /* HiDR's DataReduct (PAPER §3.3): H2_REDUCT_VOLUME (default, */
                            /*    the one of all the paper's runs), H2_REDUCT_FPS (farthest   */
                            /*    point sampling) or H2_REDUCT_SURFACE; the last two O(r |S|)/node   */
+  int32_t nonsymmetric;    /* 1: the non-symmetric path (row AND column bases, every ordered block)  */
+                           /*    for any kernel -- for a symmetric one it reproduces V = U,          */
+                           /*    X^(col) = X^(row) bit for bit; H2_KERNEL_MQSHIFT implies it         */
 } h2_options;
 
 /* ---- DataReduct of HiDR (h2_options.reduct) ---------------------------------------------------- */
@@ -217,6 +227,8 @@ typedef struct h2_info_t {
   float stage_ms[9];
   int64_t hidr_dist_done;                    /* distances the pruned top-down Vol evaluated        */
   int64_t hidr_up_evals;                     /* the bottom-up sweep's share of hidr_dist_evals     */
+  int32_t nonsymmetric;                      /* 1: separate column bases, every ordered block      */
+  int32_t kmax_col;                          /* max column skeleton size (non-symmetric path)      */
 } h2_info_t;
 
 int h2_info(const h2_handle* h, h2_info_t* out);
@@ -243,9 +255,12 @@ enum {
   H2_EXPORT_SHARD = 19,   /* int64[5 + 2*(depth+1)]: nranks, rank, cut level, p_lo, p_hi, then per */
                           /* level l the node range [lo_l, hi_l) this rank computed               */
   H2_EXPORT_BLOCK_SAMPLE = 20, /* see h2_sample_blocks                                           */
-  H2_EXPORT_ID_PATH = 21  /* int32[nnodes]: the a8 code path of each node's ID: 0..6 staged       */
+  H2_EXPORT_ID_PATH = 21, /* int32[nnodes]: the a8 code path of each node's ID: 0..6 staged       */
                           /* shared-memory size classes, 7 lean shared-memory class, 8 / 9 global */
                           /* memory (256 / 1024 threads), 10 thread-block cluster, -1 no basis    */
+  /* the column bases of the non-symmetric path (as K, SK_*, U_*, XBAR_N for the row bases)       */
+  H2_EXPORT_K_COL = 22, H2_EXPORT_SKC_OFF = 23, H2_EXPORT_SKC_IDX = 24, H2_EXPORT_V_OFF = 25,
+  H2_EXPORT_V = 26, H2_EXPORT_XBARC_N = 27
 };
 
 /* Copies array `what` into host_buf when cap_bytes suffices; *needed_bytes receives its size.
@@ -253,8 +268,9 @@ enum {
 int h2_export(const h2_handle* h, int what, void* host_buf, size_t cap_bytes, size_t* needed_bytes);
 
 /* Reads stored block entries for parity sampling.  For each s < count: kind[s] = 0 coupling /
- * 1 nearfield, pair[s] = index into the symmetric-once pair list of that kind (ordered as the
- * CSR with i < j resp. i <= j), entry[s] = row-major entry index inside that block.  Writes
+ * 1 nearfield, pair[s] = index into the stored pair list of that kind (ordered as the CSR with
+ * i < j resp. i <= j; every ordered pair on the non-symmetric path), entry[s] = row-major entry
+ * index inside that block (rows: X^_i^(row) resp. X_i; columns: X^_j^(col) resp. X_j).  Writes
  * value[s] (HOST), and row_pt[s], col_pt[s] = the tree-order point indices of that entry
  * (HOST int32).  Returns H2_OK, H2_ERR_INVALID_ARG if a class is not stored or out of range. */
 int h2_sample_blocks(const h2_handle* h, int64_t count, const int32_t* kind, const int64_t* pair,

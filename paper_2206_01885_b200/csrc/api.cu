@@ -127,6 +127,34 @@ static void clone_geometry(h2_handle* h, const h2_handle* b) {
   h->gpu_launches += 0;  // copies only
 }
 
+// out[k n + t] = X[k n + t] + sign a_k (tree-order SoA coordinates shifted by +-a)
+struct ShiftVec {
+  double a[kMaxD];
+};
+__global__ void shift_coords_kernel(int64_t n, int d, const double* __restrict__ X, ShiftVec a, double sign,
+                                    double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * d; e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = X[e] + sign * a.a[e / n];
+}
+
+// kappa's first-argument coordinates (h2_internal.cuh: Xf = X + a, Xfn = X - a for the shifted
+// multiquadric; X itself for the other kernels)
+static void make_first_arg_coords(h2_handle* h) {
+  if (h->kid != H2_KERNEL_MQSHIFT) {
+    h->Xf = h->Xfn = h->X;
+    return;
+  }
+  ShiftVec a{};
+  for (int c = 0; c < h->d; c++) a.a[c] = h->kpa[c];
+  const int64_t m = (int64_t)h->n * h->d;
+  h->Xf = halloc<double>(h, m);
+  h->Xfn = halloc<double>(h, m);
+  shift_coords_kernel<<<grid_for(m, 256), 256, 0, h->stream>>>(h->n, h->d, h->X, a, 1.0, h->Xf);
+  shift_coords_kernel<<<grid_for(m, 256), 256, 0, h->stream>>>(h->n, h->d, h->X, a, -1.0, h->Xfn);
+  H2_CHECK_LAUNCH();
+  h->gpu_launches += 2;
+}
+
 }  // namespace h2
 
 using namespace h2;
@@ -158,12 +186,23 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
     set_error(H2_ERR_INVALID_ARG, "invalid argument (n, d, leaf_size, admissibility, id_tol or options)");
     return nullptr;
   }
-  if (kernel_id < H2_KERNEL_COULOMB || kernel_id > H2_KERNEL_COSDOT) {
+  if (kernel_id < H2_KERNEL_COULOMB || kernel_id > H2_KERNEL_MQSHIFT) {
     set_error(H2_ERR_UNKNOWN_KERNEL, "unknown kernel_id");
     return nullptr;
   }
-  double kp = 0.0;
-  if (kernel_id != H2_KERNEL_COULOMB && kernel_id != H2_KERNEL_BUMP && kernel_id != H2_KERNEL_COSDOT) {
+  double kp = 0.0, kpa[kMaxD] = {0};
+  if (kernel_id == H2_KERNEL_MQSHIFT) {  // {c, a_0, ..., a_{d-1}}
+    bool ok = kernel_params && kernel_params[0] > 0.0 && std::isfinite(kernel_params[0]);
+    for (int c = 0; ok && c < d; c++) {
+      ok = std::isfinite(kernel_params[1 + c]);
+      kpa[c] = kernel_params[1 + c];
+    }
+    if (!ok) {
+      set_error(H2_ERR_INVALID_ARG, "H2_KERNEL_MQSHIFT needs d + 1 finite parameters {c > 0, a_0..a_{d-1}}");
+      return nullptr;
+    }
+    kp = kernel_params[0];
+  } else if (kernel_id != H2_KERNEL_COULOMB && kernel_id != H2_KERNEL_BUMP && kernel_id != H2_KERNEL_COSDOT) {
     if (!kernel_params || !(kernel_params[0] > 0.0) || !std::isfinite(kernel_params[0])) {
       set_error(H2_ERR_INVALID_ARG, "kernel parameter (h or l) must be finite and > 0");
       return nullptr;
@@ -175,6 +214,8 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
   h->d = d;
   h->kid = kernel_id;
   h->kp = kp;
+  std::memcpy(h->kpa, kpa, sizeof(kpa));
+  h->nonsym = o.nonsymmetric || kernel_id == H2_KERNEL_MQSHIFT;
   h->id_tol = id_tol;
   h->q = leaf_size;
   h->tau = admissibility;
@@ -222,9 +263,11 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
     const bool calibrated = o.r_override <= 0 && !base;
     if (base) {
       clone_geometry(h, base);  // a1-a4, a6-a7 (and the shard plan) of the base handle
+      make_first_arg_coords(h);
       mark(1);
     } else {
       build_tree(h, pts);  // a1-a3
+      make_first_arg_coords(h);
       mark(1);
       if (calibrated) {  // a5 phase 0 overlaps a4 (calib.cu)
         H2_CUDA_TRY(cudaEventRecord(fork_ev, h->stream));
@@ -383,6 +426,8 @@ int h2_info(const h2_handle* h, h2_info_t* out) {
   out->hidr_dist_evals = h->hidr_dist_evals;
   out->hidr_dist_done = h->hidr_dist_done;
   out->hidr_up_evals = h->hidr_up_evals;
+  out->nonsymmetric = h->nonsym;
+  out->kmax_col = h->kmax_col;
   out->id_kernel_evals = h->id_kernel_evals;
   out->kmax = h->kmax;
   out->gpu_launches = h->gpu_launches;
@@ -452,16 +497,29 @@ static std::vector<char> export_bytes(const h2_handle* h, int what) {
       auto v = d2h(what == H2_EXPORT_K ? h->k : h->xbar_n, nn, s);
       return bytes(v.data(), 4 * v.size());
     }
+    case H2_EXPORT_K_COL:
+    case H2_EXPORT_XBARC_N: {
+      if (!h->k_col) break;
+      auto v = d2h(what == H2_EXPORT_K_COL ? h->k_col : h->xbar_col_n, nn, s);
+      return bytes(v.data(), 4 * v.size());
+    }
+    case H2_EXPORT_SKC_OFF:
+    case H2_EXPORT_SKC_IDX:
+      if (!h->k_col) break;
+      return pack_slots(h->k_col, h->sk_col, what == H2_EXPORT_SKC_OFF);
     case H2_EXPORT_U_OFF:
-    case H2_EXPORT_U: {
-      if (!h->k) break;
-      auto k = d2h(h->k, nn, s);
-      auto xb = d2h(h->xbar_n, nn, s);
+    case H2_EXPORT_U:
+    case H2_EXPORT_V_OFF:
+    case H2_EXPORT_V: {
+      const bool col = what == H2_EXPORT_V_OFF || what == H2_EXPORT_V;
+      if (!h->k || (col && !h->k_col)) break;
+      auto k = d2h(col ? h->k_col : h->k, nn, s);
+      auto xb = d2h(col ? h->xbar_col_n : h->xbar_n, nn, s);
       std::vector<int64_t> off(nn + 1, 0);
       for (int i = 0; i < nn; i++) off[i + 1] = off[i] + (int64_t)k[i] * xb[i];
-      if (what == H2_EXPORT_U_OFF) return bytes(off.data(), 8 * off.size());
-      auto uo = d2h(h->u_off, nn + 1, s);
-      auto U = d2h(h->U, h->u_total, s);
+      if (what == H2_EXPORT_U_OFF || what == H2_EXPORT_V_OFF) return bytes(off.data(), 8 * off.size());
+      auto uo = d2h(col ? h->u_off_col : h->u_off, nn + 1, s);
+      auto U = d2h(col ? h->V : h->U, col ? h->v_total : h->u_total, s);
       std::vector<double> out(off[nn]);
       for (int i = 0; i < nn; i++)
         if (off[i + 1] > off[i]) std::memcpy(&out[off[i]], &U[uo[i]], 8 * (off[i + 1] - off[i]));

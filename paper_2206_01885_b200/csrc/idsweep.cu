@@ -40,19 +40,31 @@ __host__ __device__ __forceinline__ int id_pad_rows(int nx, int nt) {
   const int G = panel_group(nx, nt);
   return G <= 8 ? 2 * G - 1 : 0;
 }
-// shared-memory footprint of one node's ID: M (ny + pad rows x nx) + F (NB x nx) + nrm2 (nx) + v (ny)
-// + piv, Xbar (2 nx ints) (+ staged coordinates of Xbar and Y^*: 8 (nx + ny) d bytes, + the exp table)
+__host__ __device__ __forceinline__ bool id_tall(int ny, int nx, int nt);
+// the panel-blocked CPQR runs a node of a shared-memory class on NT threads when the block is tall
+// (the column-major layout; wide blocks keep the row-major thread-per-column CPQR) and its columns
+// fit the thread groups (cpqr_panel.cuh: at most RMAX columns per group)
+__host__ __device__ __forceinline__ int id_panel_rmax(int nt) { return nt >= 512 ? 4 : 2; }
+__host__ __device__ __forceinline__ bool id_panel(int ny, int nx, int nt) {
+  return id_tall(ny, nx, nt) && (int64_t)nx * panel_group(nx, nt) <= (int64_t)nt * id_panel_rmax(nt);
+}
+// doubles a node's block and CPQR scratch take: M (+ the panel's padding rows and F) + nrm2 + v
+__host__ __device__ __forceinline__ int64_t id_block_doubles(int ny, int nx, int nt) {
+  return id_panel(ny, nx, nt) ? (int64_t)(ny + id_pad_rows(nx, nt)) * nx + kIdPanelNb * nx + nx + ny
+                              : (int64_t)ny * nx + nx + ny;
+}
+// shared-memory footprint of one node's ID: block + scratch + piv, Xbar (2 nx ints) (+ staged
+// coordinates of Xbar and Y^*: 8 (nx + ny) d bytes, + the exp table)
 __host__ __device__ __forceinline__ int64_t id_smem_bytes(int ny, int nx, int d) {
-  return 8LL * ((int64_t)(ny + id_pad_rows(nx, 128)) * nx + kIdPanelNb * nx + nx + ny) + 8LL * nx +
-         8LL * d * (nx + ny) + 512;
+  return 8LL * id_block_doubles(ny, nx, 128) + 8LL * nx + 8LL * d * (nx + ny) + 512;
 }
 // the lean layout of the one-CTA-per-SM class: no staged coordinates (the block generation reads
 // them from global memory / L1)
 constexpr int kIdLeanThreads = 512;
-constexpr int kIdLeanMax = 224 * 1024;  // dynamic shared memory of that class (+ the small static part)
+constexpr int kIdLeanMax = 226 * 1024;  // dynamic shared memory of that class (+ the small static part)
 constexpr int kIdLean = kIdClasses;      // its class number
 __host__ __device__ __forceinline__ int64_t id_smem_bytes_lean(int ny, int nx) {
-  return 8LL * ((int64_t)(ny + id_pad_rows(nx, 512)) * nx + kIdPanelNb * nx + nx + ny) + 8LL * nx + 512;
+  return 8LL * id_block_doubles(ny, nx, 512) + 8LL * nx + 512;
 }
 // what a lean node asks for: its footprint plus staged coordinates when both fit the class
 __host__ __device__ __forceinline__ int64_t id_lean_request(int ny, int nx, int d) {
@@ -128,13 +140,17 @@ __global__ void id_sizes_kernel(int base, int count, int d, const int* __restric
   // the code path (H2_EXPORT_ID_PATH): 0..6 staged shared-memory classes, 7 lean class, 8 global
   // memory (256 threads), 9 global memory (1024 threads), 10 thread-block cluster, -1 none
   id_path[i] = nx == 0 ? -1 : big ? 10 : cls >= 0 ? cls : (8LL * nx * ny < kIdBigBlock ? 8 : 9);
-  if (nx > 0 && cls >= 0)
+  if (nx > 0 && cls >= 0) {
     atomicMax(smax + cls, (int)(cls == kIdLean ? id_lean_request(ny, nx, d) : id_smem_bytes(ny, nx, d)));
+    // which instantiations the class needs: bit 0 unblocked / row-major nodes, bit 1 panel nodes
+    atomicOr(smax + kIdClasses + 2 + cls, id_panel(ny, nx, cls == kIdLean ? kIdLeanThreads : kIdSmemThreads) ? 2 : 1);
+  }
 }
 
 template <int kIdThreads>
 __global__ void __launch_bounds__(kIdThreads) id_kernel(
-    int base, int kid, double p2, double tol, const double* __restrict__ X, int64_t n, int d, int r,
+    int base, int kid, double p2, double tol, const double* __restrict__ Xf, const double* __restrict__ X, int64_t n,
+    int d, int r,
     const int* __restrict__ is_leaf, const int* __restrict__ nbegin, const int* __restrict__ first_child,
     const int* __restrict__ nchild, const int* __restrict__ ys_cnt, const int* __restrict__ ys,
     const int* __restrict__ xbar_n, const int64_t* __restrict__ woff, double* work, const int64_t* __restrict__ uoff,
@@ -163,7 +179,7 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
   constexpr int kRmaxG = kIdThreads >= 1024 ? 2 : 4;
   const int Gp = panel_group(nx, kIdThreads);
   const int G = Gp < 4 ? 4 : Gp;
-  const bool panel = use_panel && (int64_t)nx * G <= (int64_t)kIdThreads * kRmaxG;
+  const bool panel = (use_panel & 4) && (int64_t)nx * G <= (int64_t)kIdThreads * kRmaxG;
   double* M = work + woff[t];
   double* Fs = M + (int64_t)ny * nx;
   double* nrm2 = Fs + kIdPanelNb * nx;
@@ -188,7 +204,7 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
   const int* yv = ys + (int64_t)i * r;
   for (int64_t e = tid; e < (int64_t)ny * nx; e += kIdThreads) {
     int a = (int)(e % ny), b = (int)(e / ny);
-    M[e] = kernel_pts_d(kid, p2, X, n, d, xb[b], yv[a]);
+    M[e] = kernel_pts_d(kid, p2, Xf, X, n, d, xb[b], yv[a]);
   }
   __syncthreads();
   const int k = panel ? cta_cpqr_panel<kIdThreads, kNbG, kRmaxG>(M, ny, ny, nx, tol, G, piv, Fs, psm)
@@ -225,7 +241,8 @@ struct IdClCand {
 };
 
 __global__ void __launch_bounds__(kIdClThreads) id_kernel_cluster(
-    int base, const int* __restrict__ list, int kid, double p2, double tol, const double* __restrict__ X, int64_t n,
+    int base, const int* __restrict__ list, int kid, double p2, double tol, const double* __restrict__ Xf,
+    const double* __restrict__ X, int64_t n,
     int d, int r, const int* __restrict__ is_leaf, const int* __restrict__ nbegin,
     const int* __restrict__ first_child, const int* __restrict__ nchild, const int* __restrict__ ys_cnt,
     const int* __restrict__ ys, const int* __restrict__ xbar_n, const int64_t* __restrict__ woff, double* work,
@@ -273,7 +290,7 @@ __global__ void __launch_bounds__(kIdClThreads) id_kernel_cluster(
   const int* yv = ys + (int64_t)i * r;
   for (int64_t e = tid; e < (int64_t)wl * ny; e += NT) {
     const int a = (int)(e % ny), jl = (int)(e / ny);
-    Mq[e] = kernel_pts_d(kid, p2, X, n, d, xb[j0 + jl], yv[a]);
+    Mq[e] = kernel_pts_d(kid, p2, Xf, X, n, d, xb[j0 + jl], yv[a]);
   }
   __syncthreads();
   for (int jl = warp; jl < wl; jl += NW) {
@@ -476,15 +493,18 @@ __global__ void __launch_bounds__(kIdClThreads) id_kernel_cluster(
 // shared-memory path: the whole block and the CPQR live in shared memory (cpqr.cuh, row-major).
 // NT = kIdSmemThreads for the staged classes (several CTAs per SM), kIdLeanThreads for the lean
 // one-CTA-per-SM class (coordinates read from global memory, no staging).
-template <int D, int NT>
-__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 6) id_kernel_smem(
-    int base, int kid, double p2, double tol, const double* __restrict__ X, int64_t n, int d_unused, int r,
+// PANEL: this instantiation runs the nodes whose blocks take the panel layout (id_panel); the other
+// one the rest (its registers stay at the unblocked CPQR's ~64, for occupancy)
+template <int D, int NT, bool PANEL>
+__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : (PANEL ? 6 : 8)) id_kernel_smem(
+    int base, int kid, double p2, double tol, const double* __restrict__ Xf, const double* __restrict__ X, int64_t n,
+    int d_unused, int r,
     const int* __restrict__ is_leaf, const int* __restrict__ nbegin, const int* __restrict__ first_child,
     const int* __restrict__ nchild, const int* __restrict__ ys_cnt, const int* __restrict__ ys,
     const int* __restrict__ xbar_n, const int64_t* __restrict__ uoff, double* U, int* kout, int* sk,
     unsigned long long* evals, int cls, int use_panel) {
   extern __shared__ double sh[];
-  __shared__ PanelSmem<NT, kIdPanelNb> psm;
+  __shared__ PanelSmem<NT, PANEL ? kIdPanelNb : 1> psm;
   __shared__ CpqrSmem<NT> csm_cm;
   __shared__ CpqrRmSmem<NT> csm;
   constexpr bool kLean = NT == kIdLeanThreads;
@@ -500,12 +520,15 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 6) id_kernel_smem(
   // the panel-blocked CPQR (cpqr_panel.cuh) when the node's columns fit the thread groups, else
   // the warp-per-column one (cpqr.cuh); both on A^T column-major, leading dimension ld <= ny + 15
   constexpr int kRmax = NT >= 512 ? 4 : 2;
+  static_assert(kRmax == (NT >= 512 ? 4 : 2), "id_panel_rmax");
   const int G = panel_group(nx, NT);
-  const bool panel = use_panel && nx * G <= NT * kRmax;
+  const bool fits_panel = id_panel(ny, nx, NT);  // the block's layout (id_block_doubles)
+  if (fits_panel != PANEL) return;  // the other instantiation's node
+  const bool panel = PANEL && (use_panel & (kLean ? 2 : 1));
   const int ld = panel ? panel_ld(ny, G) : ny;
   double* M = sh;
-  double* Fs = M + (int64_t)(ny + id_pad_rows(nx, NT)) * nx;
-  double* nrm2 = Fs + kIdPanelNb * nx;
+  double* Fs = M + (int64_t)(fits_panel ? ny + id_pad_rows(nx, NT) : ny) * nx;
+  double* nrm2 = Fs + (fits_panel ? kIdPanelNb * nx : 0);
   double* v = nrm2 + nx;
   double* tab = kLean ? v + ny : v + ny + D * (nx + ny);  // exp table
   int* piv = reinterpret_cast<int*>(tab + 64);
@@ -540,10 +563,11 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 6) id_kernel_smem(
     __syncthreads();
     for (int b = tid; b < nx; b += NT)
 #pragma unroll
-      for (int c = 0; c < D; c++) cx[c * nx + b] = X[c * n + xb[b]];
+      for (int c = 0; c < D; c++) cx[c * nx + b] = Xf[c * n + xb[b]];
   }
   __syncthreads();
-  auto coord_x = [&](int c, int b) { return staged ? cx[c * nx + b] : X[c * n + xb[b]]; };
+  // Xbar is kappa's first argument (coordinates from Xf), Y^* the second
+  auto coord_x = [&](int c, int b) { return staged ? cx[c * nx + b] : Xf[c * n + xb[b]]; };
   auto coord_y = [&](int c, int a) { return staged ? cy[c * ny + a] : X[c * n + yv[a]]; };
   // unblocked fallback: wide blocks row-major with a thread per column (cta_cpqr_rm), tall ones
   // column-major with a warp per column (cta_cpqr); the panel CPQR is column-major (ld)
@@ -588,8 +612,12 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 6) id_kernel_smem(
       }
     }
     __syncthreads();
-    k = panel ? cta_cpqr_panel<NT, kIdPanelNb, kRmax>(M, ld, ny, nx, tol, G, piv, Fs, psm)
-              : cta_cpqr<NT>(M, ny, nx, tol, piv, nrm2, v, csm_cm);
+    if constexpr (PANEL) {
+      k = panel ? cta_cpqr_panel<NT, kIdPanelNb, kRmax>(M, ld, ny, nx, tol, G, piv, Fs, psm)
+                : cta_cpqr<NT>(M, ny, nx, tol, piv, nrm2, v, csm_cm);
+    } else {
+      k = cta_cpqr<NT>(M, ny, nx, tol, piv, nrm2, v, csm_cm);
+    }
   }
   double* Ui = U + uoff[blockIdx.x];
   for (int a = tid; a < k; a += NT) sk[(int64_t)i * r + a] = xb[piv[a]];
@@ -658,14 +686,16 @@ static int id_cluster_max() {
   return cs;
 }
 
-void id_sweep(h2_handle* h) {
+// One getBasis sweep (Algorithm 2 lines 10-12) into the handle's row-basis fields, kappa's first
+// argument (Xbar) read from Xf.
+static void id_sweep_pass(h2_handle* h, const double* Xf) {
   cudaStream_t s = h->stream;
   H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   const int cs = id_cluster_max();
-  static const int use_panel = [] {  // H2_ID_PANEL=0 (A/B knob): the unblocked CPQR on every path
-    const char* e = getenv("H2_ID_PANEL");
-    return e ? atoi(e) : 1;
+  static const int use_panel = [] {  // H2_ID_PANEL (A/B knob): bit mask of the paths running the
+    const char* e = getenv("H2_ID_PANEL");  // panel CPQR: 1 staged, 2 lean, 4 global memory
+    return e ? atoi(e) : 3;
   }();
   static const int64_t cl_min = [] {  // H2_ID_CLMIN (tuning knob): cluster-path threshold, block entries
     const char* e = getenv("H2_ID_CLMIN");
@@ -698,10 +728,12 @@ void id_sweep(h2_handle* h) {
     const LevelRange lr = level_range(h, l);
     int base = lr.begin, count = lr.end - lr.begin;
     if (count == 0) continue;
-    Scratch sz(sizeof(int64_t) * 2 * (count + 1) + 4 * (kIdClasses + 2), s), off(sizeof(int64_t) * 2 * (count + 1), s);
-    // one max per class (+ lean), then the largest |Xbar| of the cluster-path nodes
+    constexpr int kSmaxN = 2 * kIdClasses + 3;
+    Scratch sz(sizeof(int64_t) * 2 * (count + 1) + 4 * kSmaxN, s), off(sizeof(int64_t) * 2 * (count + 1), s);
+    // one max per class (+ lean), the largest |Xbar| of the cluster-path nodes, then the kind
+    // flags per class (+ lean)
     int* smax = reinterpret_cast<int*>(sz.as<int64_t>() + 2 * (count + 1));
-    H2_CUDA_TRY(cudaMemsetAsync(smax, 0, (kIdClasses + 2) * sizeof(int), s));
+    H2_CUDA_TRY(cudaMemsetAsync(smax, 0, kSmaxN * sizeof(int), s));
     int64_t *wsz = sz.as<int64_t>(), *usz = wsz + count + 1;
     int64_t *woff = off.as<int64_t>(), *uo = woff + count + 1;
     Scratch clw(sizeof(int) * (1 + (size_t)count), s);  // cluster-path node count + list
@@ -716,10 +748,11 @@ void id_sweep(h2_handle* h) {
     scan_excl_i64(usz, uo, count + 1, s);
     H2_CHECK_LAUNCH();
     int64_t tot[2];
-    int smem_bytes[kIdClasses + 2] = {0};
+    int smem_bytes[kSmaxN] = {0};
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[0], woff + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[1], uo + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    H2_CUDA_TRY(cudaMemcpyAsync(smem_bytes, smax, (kIdClasses + 2) * sizeof(int), cudaMemcpyDeviceToHost, s));
+    H2_CUDA_TRY(cudaMemcpyAsync(smem_bytes, smax, kSmaxN * sizeof(int), cudaMemcpyDeviceToHost, s));
+    const int* kinds = smem_bytes + kIdClasses + 2;
     int ncl = 0;
     H2_CUDA_TRY(cudaMemcpyAsync(&ncl, cl_cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaStreamSynchronize(s));
@@ -758,7 +791,7 @@ void id_sweep(h2_handle* h) {
       cfg.attrs = at;
       cfg.numAttrs = 1;
       H2_CUDA_TRY(cudaLaunchKernelEx(&cfg, id_kernel_cluster, base, (const int*)cl_list, h->kid, p2, h->id_tol,
-                                     (const double*)h->X, h->n, h->d, h->r, (const int*)h->is_leaf,
+                                     Xf, (const double*)h->X, h->n, h->d, h->r, (const int*)h->is_leaf,
                                      (const int*)h->nbegin, (const int*)h->first_child, (const int*)h->nchild,
                                      (const int*)h->ys_cnt, (const int*)h->ys, (const int*)h->xbar_n,
                                      (const int64_t*)woff, work.as<double>(), (const int64_t*)(h->u_off + base), U,
@@ -774,11 +807,11 @@ void id_sweep(h2_handle* h) {
       H2_CUDA_TRY(cudaEventRecord(gev[0], s));
       H2_CUDA_TRY(cudaStreamWaitEvent(sa, gev[0], 0));
       H2_CUDA_TRY(cudaStreamWaitEvent(sb, gev[0], 0));
-      id_kernel<256><<<count, 256, 0, sa>>>(base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf,
+      id_kernel<256><<<count, 256, 0, sa>>>(base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf,
                                            h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
                                            work.as<double>(), h->u_off + base, U, h->k, h->sk,
                                            ev.as<unsigned long long>(), 0, kIdBigBlock, cs, cl_min, use_panel);
-      id_kernel<1024><<<count, 1024, 0, sb>>>(base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf,
+      id_kernel<1024><<<count, 1024, 0, sb>>>(base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf,
                                              h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
                                              work.as<double>(), h->u_off + base, U, h->k, h->sk,
                                              ev.as<unsigned long long>(), kIdBigBlock, INT64_MAX, cs, cl_min,
@@ -820,39 +853,49 @@ void id_sweep(h2_handle* h) {
       const int cls = launches[li];
       const int smem = cls < 0 ? smax_all : smem_bytes[cls];
       if (smem == 0) continue;
-      cudaStream_t cs = s;
-      if (fan) {
-        const int a = used % h2_handle::kAux;
-        cs = h->aux[a];
-        if (used < h2_handle::kAux) H2_CUDA_TRY(cudaStreamWaitEvent(cs, lev_ev[h2_handle::kAux], 0));
-        used++;
-      }
-      const bool lean = cls == kIdLean;
-      switch (h->d) {
+      int kind = 0;  // instantiations this launch needs
+      if (cls >= 0) kind = kinds[cls];
+      else
+        for (int c2 = 0; c2 < kIdClasses; c2++) kind |= kinds[c2];
+      for (int pv = 0; pv < 2; pv++) {
+        if (!(kind & (1 << pv))) continue;
+        cudaStream_t cs = s;
+        if (fan) {
+          const int a = used % h2_handle::kAux;
+          cs = h->aux[a];
+          if (used < h2_handle::kAux) H2_CUDA_TRY(cudaStreamWaitEvent(cs, lev_ev[h2_handle::kAux], 0));
+          used++;
+        }
+        const bool lean = cls == kIdLean;
+        switch (h->d) {
+#define H2_ID_LAUNCH(DD, NTT, PV, MAXS)                                                                          \
+  do {                                                                                                          \
+    H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_smem<DD, NTT, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                     MAXS));                                                                    \
+    id_kernel_smem<DD, NTT, PV><<<count, NTT, smem, cs>>>(                                                       \
+        base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child,          \
+        h->nchild,                                                                                              \
+        h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>(), cls,         \
+        use_panel);                                                                                             \
+  } while (0)
 #define H2_ID_CASE(DD)                                                                                          \
   case DD:                                                                                                      \
     if (lean) {                                                                                                 \
-      H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_smem<DD, kIdLeanThreads>,                                      \
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kIdLeanMax));               \
-      id_kernel_smem<DD, kIdLeanThreads><<<count, kIdLeanThreads, smem, cs>>>(                                  \
-          base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child,           \
-          h->nchild, h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>(), \
-          cls, use_panel);                                                                                      \
+      if (pv) H2_ID_LAUNCH(DD, kIdLeanThreads, true, kIdLeanMax);                                               \
+      else H2_ID_LAUNCH(DD, kIdLeanThreads, false, kIdLeanMax);                                                 \
     } else {                                                                                                    \
-      H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_smem<DD, kIdSmemThreads>,                                      \
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kIdSmemMax));               \
-      id_kernel_smem<DD, kIdSmemThreads><<<count, kIdSmemThreads, smem, cs>>>(                                  \
-          base, h->kid, p2, h->id_tol, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child,           \
-          h->nchild, h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>(), \
-          cls, use_panel);                                                                                      \
+      if (pv) H2_ID_LAUNCH(DD, kIdSmemThreads, true, kIdSmemMax);                                               \
+      else H2_ID_LAUNCH(DD, kIdSmemThreads, false, kIdSmemMax);                                                 \
     }                                                                                                           \
     break;
-        H2_ID_CASE(1) H2_ID_CASE(2) H2_ID_CASE(3) H2_ID_CASE(4)
-        H2_ID_CASE(5) H2_ID_CASE(6) H2_ID_CASE(7) H2_ID_CASE(8)
+          H2_ID_CASE(1) H2_ID_CASE(2) H2_ID_CASE(3) H2_ID_CASE(4)
+          H2_ID_CASE(5) H2_ID_CASE(6) H2_ID_CASE(7) H2_ID_CASE(8)
 #undef H2_ID_CASE
+#undef H2_ID_LAUNCH
+        }
+        H2_CHECK_LAUNCH();
+        h->gpu_launches += 1;
       }
-      H2_CHECK_LAUNCH();
-      h->gpu_launches += 1;
     }
     if (fan) {
       for (int a = 0; a < h2_handle::kAux && a < used; a++) {
@@ -879,6 +922,49 @@ void id_sweep(h2_handle* h) {
   H2_CHECK_LAUNCH();
   h->kmax = read1(km.as<int>(), s);
   h->id_kernel_evals = (int64_t)read1(ev.as<unsigned long long>(), s);
+}
+
+// a8: the row bases (getBasis(K_{Xbar Y*}), first argument X + a for the shifted multiquadric) and,
+// on the non-symmetric path, the column bases: getBasis(K_{Y* Xbar}^T) = the same sweep for the
+// transposed kernel kappa^T(x, y) = kappa(y, x) (Algorithm 2 line 11), whose first argument is
+// X - a; its results move to the *_col fields.  For a symmetric kernel the second sweep repeats the
+// first bit for bit (V = U).
+void id_sweep(h2_handle* h) {
+  id_sweep_pass(h, h->Xf);
+  if (!h->nonsym) {
+    h->k_col = h->k;
+    h->sk_col = h->sk;
+    h->xbar_col_n = h->xbar_n;
+    h->child_off_col = h->child_off;
+    h->u_off_col = h->u_off;
+    h->V = h->U;
+    h->v_total = h->u_total;
+    h->kmax_col = h->kmax;
+    return;
+  }
+  int *k = h->k, *sk = h->sk, *xb = h->xbar_n, *co = h->child_off, *path = h->id_path, kmax = h->kmax;
+  int64_t* uo = h->u_off;
+  double* U = h->U;
+  const int64_t ut = h->u_total, ev = h->id_kernel_evals;
+  id_sweep_pass(h, h->Xfn);
+  h->k_col = h->k;
+  h->sk_col = h->sk;
+  h->xbar_col_n = h->xbar_n;
+  h->child_off_col = h->child_off;
+  h->u_off_col = h->u_off;
+  h->V = h->U;
+  h->v_total = h->u_total;
+  h->kmax_col = h->kmax;
+  h->id_kernel_evals += ev;
+  h->k = k;
+  h->sk = sk;
+  h->xbar_n = xb;
+  h->child_off = co;
+  h->id_path = path;
+  h->kmax = kmax;
+  h->u_off = uo;
+  h->U = U;
+  h->u_total = ut;
 }
 
 }  // namespace h2
