@@ -17,15 +17,18 @@ LIB_PATH = os.path.join(_HERE, "lib", "libh2b200.so")
 
 H2_KERNEL_COULOMB, H2_KERNEL_GAUSSIAN, H2_KERNEL_MATERN32, H2_KERNEL_LAPLACE, H2_KERNEL_BUMP, H2_KERNEL_COSDOT = \
     1, 2, 3, 4, 5, 6
+H2_KERNEL_MQSHIFT = 7  # sqrt(1 + c |x - y + a|^2), non-symmetric; kernel_params = (c, a_0, ..., a_{d-1})
 H2_STORE_AUTO, H2_STORE_ALL, H2_STORE_ON_THE_FLY = 0, 1, 2
 H2_REDUCT_VOLUME, H2_REDUCT_FPS, H2_REDUCT_SURFACE = 0, 1, 2  # HiDR DataReduct (h2_options.reduct)
 
 EXPORT = dict(PERM=1, NODES=2, IL_OFF=4, IL_IDX=5, NF_OFF=6, NF_IDX=7, XS_OFF=8, XS_IDX=9, YS_OFF=10,
-              YS_IDX=11, K=12, SK_OFF=13, SK_IDX=14, U_OFF=15, U=16, XBAR_N=17, TREE_X=18, SHARD=19, ID_PATH=21)
+              YS_IDX=11, K=12, SK_OFF=13, SK_IDX=14, U_OFF=15, U=16, XBAR_N=17, TREE_X=18, SHARD=19, ID_PATH=21,
+              K_COL=22, SKC_OFF=23, SKC_IDX=24, V_OFF=25, V=26, XBARC_N=27)
 _EXPORT_DTYPE = dict(PERM=np.int32, NODES=np.int32, IL_OFF=np.int64, IL_IDX=np.int32, NF_OFF=np.int64,
                      NF_IDX=np.int32, XS_OFF=np.int64, XS_IDX=np.int32, YS_OFF=np.int64, YS_IDX=np.int32,
                      K=np.int32, SK_OFF=np.int64, SK_IDX=np.int32, U_OFF=np.int64, U=np.float64,
-                     XBAR_N=np.int32, TREE_X=np.float64, SHARD=np.int64, ID_PATH=np.int32)
+                     XBAR_N=np.int32, TREE_X=np.float64, SHARD=np.int64, ID_PATH=np.int32, K_COL=np.int32,
+                     SKC_OFF=np.int64, SKC_IDX=np.int32, V_OFF=np.int64, V=np.float64, XBARC_N=np.int32)
 
 EXPORTED_SYMBOLS = ["h2_build", "h2_build_ex", "h2_rebuild_ex", "h2_options_default", "h2_matvec", "h2_matvec_ex", "h2_free", "h2_last_error",
                     "h2_last_error_message", "h2_info", "h2_export", "h2_sample_blocks", "h2_comm_nccl_unique_id",
@@ -37,7 +40,7 @@ class h2_options(C.Structure):
     _fields_ = [("r_override", C.c_int32), ("storage", C.c_int32), ("mem_budget_bytes", C.c_int64),
                 ("stream", C.c_void_p), ("points_on_host", C.c_int32), ("timing", C.c_int32),
                 ("hidr_brute", C.c_int32), ("comm", C.c_void_p), ("serial_fill", C.c_int32),
-                ("reduct", C.c_int32)]
+                ("reduct", C.c_int32), ("nonsymmetric", C.c_int32)]
 
 
 class h2_info_t(C.Structure):
@@ -47,7 +50,7 @@ class h2_info_t(C.Structure):
                 ("stored_bytes", C.c_int64), ("coupling_stored", C.c_int32), ("nearfield_stored", C.c_int32),
                 ("hidr_dist_evals", C.c_int64), ("id_kernel_evals", C.c_int64), ("kmax", C.c_int32),
                 ("gpu_launches", C.c_int32), ("stage_ms", C.c_float * 9), ("hidr_dist_done", C.c_int64),
-                ("hidr_up_evals", C.c_int64)]
+                ("hidr_up_evals", C.c_int64), ("nonsymmetric", C.c_int32), ("kmax_col", C.c_int32)]
 
 
 STAGES = ["tree", "lists", "calibrate", "hidr_up", "hidr_down", "id_sweep", "coupling_fill", "nearfield_fill",
@@ -268,10 +271,11 @@ class H2Matrix:
     def __init__(self, points, kernel_id: int, kernel_params=(), id_tol: float = 1e-6, leaf_size: int = 64,
                  admissibility: float = 0.5, r: int = 0, storage: int = H2_STORE_AUTO, stream=None,
                  timing: bool = False, mem_budget_bytes: int = 0, hidr_brute: bool = False,
-                 comm: H2Comm | None = None, reduct: int = H2_REDUCT_VOLUME):
+                 comm: H2Comm | None = None, reduct: int = H2_REDUCT_VOLUME, nonsymmetric: bool = False):
         import torch
         o = h2_options_default()
         o.reduct = int(reduct)
+        o.nonsymmetric = int(bool(nonsymmetric))
         if comm is not None:
             o.comm = C.c_void_p(comm.ptr)
             self._comm = comm

@@ -63,11 +63,20 @@ struct PtAcc {
 // A trial runs as three launches over the batch: prep (Z1, Z2, Vol(Z2, m^d), the block M; 256
 // threads), the CPQR ID of M (1024 threads: the block lives in global memory / L2 and the steps are
 // latency-bound, so more columns in flight), and the error of the interpolation (256 threads).
+// the shift of H2_KERNEL_MQSHIFT (kappa's first argument is x + a, or x - a for the transposed
+// kernel of the column bases: reading E7)
+struct CalShift {
+  double a[kMaxD];
+};
+
+// A trial's level field is a VIRTUAL level: l for kappa, l + 32 for the transposed kernel kappa^T(x,
+// y) = kappa(y, x) of a non-symmetric build (its column bases); the points are those of level l.
 template <int D>
 __global__ void __launch_bounds__(kCalThreads) calib_prep_kernel(int kid, double p2, double tau,
                                                                  const double* __restrict__ wl,
                                                                  const int* __restrict__ lv, const int* __restrict__ mv,
-                                                                 const int* __restrict__ skip_level, CalWork* work) {
+                                                                 const int* __restrict__ skip_level, CalShift sh,
+                                                                 CalWork* work) {
   __shared__ VolSmem<D, kCalThreads> vsm;
   __shared__ int s_ns;
   const int tid = threadIdx.x;
@@ -81,13 +90,16 @@ __global__ void __launch_bounds__(kCalThreads) calib_prep_kernel(int kid, double
     return;
   }
   const double w = wl[blockIdx.x];
-  const int level = lv[blockIdx.x], m = mv[blockIdx.x];
+  const int level = lv[blockIdx.x] & 31, m = mv[blockIdx.x];
+  const double sgn = lv[blockIdx.x] >= 32 ? -1.0 : 1.0;
   const unsigned long long seed = kCalibSeed + (unsigned long long)level;
   const double shift = __ddiv_rn(w, tau);
   for (int e = tid; e < N * D; e += kCalThreads) {
     double u1 = (double)(splitmix_at(seed, e) >> 11) * 0x1.0p-53;
     double u2 = (double)(splitmix_at(seed, N * D + e) >> 11) * 0x1.0p-53;
-    W.Z1[e] = __dmul_rn(u1, w);
+    // Z1 is every kernel evaluation's first argument: for the shifted multiquadric it is stored
+    // shifted by +-a (the points themselves are only used through the kernel)
+    W.Z1[e] = __dmul_rn(u1, w) + (kid == H2_KERNEL_MQSHIFT ? sgn * sh.a[e % D] : 0.0);
     W.Z2[e] = __dadd_rn(__dmul_rn(u2, w), shift);
   }
   __syncthreads();
@@ -248,6 +260,8 @@ static void launch_trials(h2_handle* h, cudaStream_t s, int slot, const std::vec
   if (T == 0) return;
   const int d = h->d;
   const double p2 = kernel_p2(h->kid, h->kp);
+  CalShift sh{};
+  for (int c = 0; c < d; c++) sh.a[c] = h->kpa[c];
   const int batch = 256;
   job.work = Scratch(sizeof(CalWork) * (T < batch ? T : batch), s);
   job.params = Scratch(sizeof(double) * T + sizeof(int) * 2 * T, s);
@@ -269,7 +283,7 @@ static void launch_trials(h2_handle* h, cudaStream_t s, int slot, const std::vec
 #define H2_CAL_CASE(DD)                                                                                   \
   case DD:                                                                                                \
     calib_prep_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, h->tau, dw + b0, dl + b0, dm + b0,         \
-                                                     skip_level, job.work.as<CalWork>());                  \
+                                                     skip_level, sh, job.work.as<CalWork>());              \
     calib_cpqr_kernel<<<nb, kCalCpqrThreads, 0, s>>>(h->id_tol, job.work.as<CalWork>());                  \
     calib_ks_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, job.work.as<CalWork>());                    \
     calib_err_kernel<DD><<<nb * kErrSlices, kCalThreads, 0, s>>>(h->kid, p2, job.work.as<CalWork>());        \
@@ -309,15 +323,16 @@ void calibrate_begin(h2_handle* h, cudaStream_t s, CalibJob& job) {
   job.stream = s;
   std::vector<double> wl, wl1;
   std::vector<int> lv, mv, lv1, mv1;
-  for (int l = 1; l <= h->depth; l++)
-    for (int m = 1;; m++) {
-      const long long G = grid_size(h->d, m);
-      const bool p0 = G <= 64 || m == 1;
-      (p0 ? wl : wl1).push_back(ldexp(h->W, -l));
-      (p0 ? lv : lv1).push_back(l);
-      (p0 ? mv : mv1).push_back(m);
-      if (G >= N) break;
-    }
+  for (int o = 0; o < (h->nonsym ? 2 : 1); o++)  // o = 1: the transposed kernel (reading E7)
+    for (int l = 1; l <= h->depth; l++)
+      for (int m = 1;; m++) {
+        const long long G = grid_size(h->d, m);
+        const bool p0 = G <= 64 || m == 1;
+        (p0 ? wl : wl1).push_back(ldexp(h->W, -l));
+        (p0 ? lv : lv1).push_back(l + 32 * o);
+        (p0 ? mv : mv1).push_back(m);
+        if (G >= N) break;
+      }
   job.passed = Scratch(sizeof(int) * 64, s);
   H2_CUDA_TRY(cudaMemsetAsync(job.passed.p, 0, sizeof(int) * 64, s));
   launch_trials(h, s, 0, wl, lv, mv, nullptr, job.p0);
@@ -346,7 +361,7 @@ int calibrate_end(h2_handle* h, CalibJob& job) {
   H2_CUDA_TRY(cudaMemcpyAsync(has, hasd.p, sizeof(int) * 64, cudaMemcpyDeviceToHost, s));
   H2_CUDA_TRY(cudaStreamSynchronize(s));
   if (job.active) H2_CUDA_TRY(cudaStreamSynchronize(job.stream));
-  std::vector<int> chosen(h->depth + 1, 0);
+  std::vector<int> chosen(64, 0);  // per virtual level (l, l + 32)
   for (CalibSet* set : {&job.p0, &job.p1})  // trials of a level are in increasing m: keep the first pass
     for (int t = 0; t < set->T; t++)
       if (set->pass_h[t] && !chosen[set->lv[t]]) chosen[set->lv[t]] = set->mv[t];
@@ -362,7 +377,8 @@ int calibrate_end(h2_handle* h, CalibJob& job) {
   job.active = false;
   int r = 1;
   for (int l = 1; l <= h->depth; l++)
-    if (has[l] && chosen[l]) r = (int)std::max<long long>(r, grid_size(h->d, chosen[l]));
+    for (int vl : {l, l + 32})
+      if (has[l] && chosen[vl]) r = (int)std::max<long long>(r, grid_size(h->d, chosen[vl]));
   return r;
 }
 

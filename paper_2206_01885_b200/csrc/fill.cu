@@ -38,9 +38,11 @@ __device__ __forceinline__ int row_of(const int64_t* __restrict__ off, int nnode
   return lo;
 }
 
-// a pair is stored (and applied by the matvec) by the rank owning its row: nbegin[i] in [p_lo, p_hi)
-__global__ void pair_flag_kernel(int mode, int nnodes, int64_t m, const int64_t* __restrict__ off,
-                                 const int* __restrict__ idx, const int* __restrict__ k,
+// a pair is stored (and applied by the matvec) by the rank owning its row: nbegin[i] in [p_lo, p_hi).
+// Symmetric: i < j (coupling), i <= j (nearfield); non-symmetric: every ordered pair (the column
+// ranks kc of the coupling blocks are the column-basis ranks).
+__global__ void pair_flag_kernel(int mode, int nonsym, int nnodes, int64_t m, const int64_t* __restrict__ off,
+                                 const int* __restrict__ idx, const int* __restrict__ k, const int* __restrict__ kc,
                                  const int* __restrict__ nbegin, int p_lo, int p_hi, int64_t* flag) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= m; e += (int64_t)gridDim.x * blockDim.x) {
     if (e == m) {
@@ -49,12 +51,13 @@ __global__ void pair_flag_kernel(int mode, int nnodes, int64_t m, const int64_t*
     }
     int i = row_of(off, nnodes, e), j = idx[e];
     const bool own = nbegin[i] >= p_lo && nbegin[i] < p_hi;
-    flag[e] = own && (mode == 0 ? (j > i && k[i] > 0 && k[j] > 0) : (j >= i));
+    flag[e] = own && (mode == 0 ? ((nonsym || j > i) && k[i] > 0 && kc[j] > 0) : (nonsym || j >= i));
   }
 }
 
 __global__ void pair_emit_kernel(int mode, int nnodes, int64_t m, const int64_t* __restrict__ off,
-                                 const int* __restrict__ idx, const int* __restrict__ k, const int* __restrict__ nbegin,
+                                 const int* __restrict__ idx, const int* __restrict__ k, const int* __restrict__ kc,
+                                 const int* __restrict__ nbegin,
                                  const int* __restrict__ nend, const int64_t* __restrict__ pos, int2* pairs,
                                  int64_t* size) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
@@ -62,7 +65,7 @@ __global__ void pair_emit_kernel(int mode, int nnodes, int64_t m, const int64_t*
     int i = row_of(off, nnodes, e), j = idx[e];
     int64_t o = pos[e];
     pairs[o] = make_int2(i, j);
-    size[o] = mode == 0 ? (int64_t)k[i] * k[j] : (int64_t)(nend[i] - nbegin[i]) * (nend[j] - nbegin[j]);
+    size[o] = mode == 0 ? (int64_t)k[i] * kc[j] : (int64_t)(nend[i] - nbegin[i]) * (nend[j] - nbegin[j]);
   }
 }
 
@@ -163,7 +166,8 @@ __global__ void __launch_bounds__(kNfThreads, MINB * kNfScale) nf_fill_kernel(in
                                                                      const int64_t* __restrict__ voff,
                                                                      const int* __restrict__ nbegin,
                                                                      const int* __restrict__ nend,
-                                                                     const double* __restrict__ X, int64_t n,
+                                                                     const double* __restrict__ X,
+                                                                     const double* __restrict__ Xr, int64_t n,
                                                                      double* __restrict__ out, int upc,
                                                                      unsigned long long* ctl) {
   static_assert(CW >= 1 && CW <= 8, "1..8 column slots");
@@ -205,7 +209,7 @@ __global__ void __launch_bounds__(kNfThreads, MINB * kNfScale) nf_fill_kernel(in
       for (int c = 0; c < D; c++) xb[s][c] = ok ? X[c * n + bj + col] : 0.0;
     }
     double* o = out + voff[p] + (int64_t)r0 * nj + c0 + lane;
-    const double* xr = X + bi;
+    const double* xr = Xr + bi;  // rows: kappa's first argument (= X but for the shifted multiquadric)
     int nslot = (nj - c0 + 31) >> 5;  // warp-uniform: slots with at least one column
     if (nslot > CW) nslot = CW;
     const bool last_ok = c0 + lane + 32 * (nslot - 1) < nj;  // only the last slot can be partial
@@ -236,7 +240,10 @@ template <int D, int KID>
 __global__ void __launch_bounds__(kFillThreads) cp_fill_kernel(int64_t np, const int2* __restrict__ pairs,
                                                                const int64_t* __restrict__ voff,
                                                                const int* __restrict__ k, const int* __restrict__ sk,
-                                                               int r, const double* __restrict__ X, int64_t n,
+                                                               const int* __restrict__ kc,
+                                                               const int* __restrict__ skc, int r,
+                                                               const double* __restrict__ Xf,
+                                                               const double* __restrict__ X, int64_t n,
                                                                double cs, double* __restrict__ out) {
   __shared__ double tab[kFillTab];
   for (int e = threadIdx.x; e < kFillTab; e += blockDim.x) tab[e] = kExp2Tab2048[e];
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__(kFillThreads) cp_fill_kernel(int64_t np, const
       pi = pr.x;
       pj = pr.y;
       ki = k[pi];
-      kj = k[pj];
+      kj = kc[pj];
     }
     int sz = ki * kj, pre = sz;  // inclusive scan of the pairs' sizes
 #pragma unroll
@@ -278,17 +285,19 @@ __global__ void __launch_bounds__(kFillThreads) cp_fill_kernel(int64_t np, const
       const int kj_q = __shfl_sync(0xffffffffu, kj, q);
       if (e >= total) continue;
       const int loc = e - pre_q, row = loc / kj_q, col = loc - row * kj_q;
-      const int a = sk[(int64_t)i_q * r + row], b = sk[(int64_t)j_q * r + col];
+      // B_ij = K(X^_i^(row), X^_j^(col)): rows from the row skeletons (first argument, Xf), columns
+      // from the column skeletons (the same arrays on the symmetric path)
+      const int a = sk[(int64_t)i_q * r + row], b = skc[(int64_t)j_q * r + col];
       if constexpr (KID == H2_KERNEL_COSDOT) {
         double dt = 0.0;
 #pragma unroll
-        for (int c = 0; c < D; c++) dt = fma(X[c * n + a], X[c * n + b], dt);
+        for (int c = 0; c < D; c++) dt = fma(Xf[c * n + a], X[c * n + b], dt);
         __stcs(o + e, kernel_cosdot(dt));
       } else {
         double sq = kFillBias;
 #pragma unroll
         for (int c = 0; c < D; c++) {
-          const double df = X[c * n + a] * cs - X[c * n + b] * cs;
+          const double df = Xf[c * n + a] * cs - X[c * n + b] * cs;
           sq = fma(df, df, sq);
         }
         __stcs(o + e, kernel_fill<KID, true>(sq, tab));
@@ -336,15 +345,15 @@ static void launch_nf(K kernel, unsigned g, cudaStream_t s, A... args) {
 
 template <int KID>
 static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_t nwork, int64_t np, const int* umap,
-                            const int64_t* uoff, const int2* pairs, const int64_t* voff, const double* Xs, double cs,
-                            double* out, unsigned long long* ctl) {
+                            const int64_t* uoff, const int2* pairs, const int64_t* voff, const double* Xs,
+                            const double* Xrs, double cs, double* out, unsigned long long* ctl) {
   if (mode == 1) {
     const bool clamp = fill_needs_clamp(h->kid, h->d, h->W, cs);
     const int upw = nf_units_per_warp();
     constexpr int wpc = kNfThreads / 32;
     const int64_t blocks = (nwork + wpc * upw - 1) / (wpc * upw);  // one chunk per warp
     unsigned g = (unsigned)(blocks < ((int64_t)1 << 30) ? blocks : ((int64_t)1 << 30));
-#define H2_NF_ARGS nwork, umap, uoff, pairs, voff, h->nbegin, h->nend, Xs, h->n, out, upw, ctl
+#define H2_NF_ARGS nwork, umap, uoff, pairs, voff, h->nbegin, h->nend, Xs, Xrs, h->n, out, upw, ctl
     switch (h->d) {
       case 2:
         switch (nf_variant()) {  // tuning variants of the D = 2 kernel (CW, clamp, MINB)
@@ -373,7 +382,8 @@ static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_
     switch (h->d) {
 #define H2_CP_CASE(DD)                                                                                        \
   case DD:                                                                                                    \
-    cp_fill_kernel<DD, KID><<<g, kFillThreads, 0, s>>>(np, pairs, voff, h->k, h->sk, h->r, h->X, h->n, cs, out);   \
+    cp_fill_kernel<DD, KID><<<g, kFillThreads, 0, s>>>(np, pairs, voff, h->k, h->sk, h->k_col, h->sk_col, h->r,  \
+                                                       h->Xf, h->X, h->n, cs, out);                            \
     break;
       H2_CP_CASE(1) H2_CP_CASE(2) H2_CP_CASE(3) H2_CP_CASE(4)
       H2_CP_CASE(5) H2_CP_CASE(6) H2_CP_CASE(7) H2_CP_CASE(8)
@@ -383,30 +393,21 @@ static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_
 }
 
 static void launch_fill(const h2_handle* h, cudaStream_t s, int mode, int64_t nwork, int64_t np, const int* umap,
-                        const int64_t* uoff, const int2* pairs, const int64_t* voff, const double* Xs, double* out,
-                        unsigned long long* ctl = nullptr) {
+                        const int64_t* uoff, const int2* pairs, const int64_t* voff, const double* Xs,
+                        const double* Xrs, double* out, unsigned long long* ctl = nullptr) {
   if (nwork < 1) return;
   const double cs = kernel_cscale(h->kid, h->kp);
+#define H2_FILL_KID(K) launch_fill_kid<K>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, Xrs, cs, out, ctl)
   switch (h->kid) {
-    case H2_KERNEL_COULOMB:
-      launch_fill_kid<H2_KERNEL_COULOMB>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out, ctl);
-      break;
-    case H2_KERNEL_GAUSSIAN:
-      launch_fill_kid<H2_KERNEL_GAUSSIAN>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out, ctl);
-      break;
-    case H2_KERNEL_MATERN32:
-      launch_fill_kid<H2_KERNEL_MATERN32>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out, ctl);
-      break;
-    case H2_KERNEL_LAPLACE:
-      launch_fill_kid<H2_KERNEL_LAPLACE>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out, ctl);
-      break;
-    case H2_KERNEL_BUMP:
-      launch_fill_kid<H2_KERNEL_BUMP>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out, ctl);
-      break;
-    default:
-      launch_fill_kid<H2_KERNEL_COSDOT>(h, s, mode, nwork, np, umap, uoff, pairs, voff, Xs, cs, out, ctl);
-      break;
+    case H2_KERNEL_COULOMB: H2_FILL_KID(H2_KERNEL_COULOMB); break;
+    case H2_KERNEL_GAUSSIAN: H2_FILL_KID(H2_KERNEL_GAUSSIAN); break;
+    case H2_KERNEL_MATERN32: H2_FILL_KID(H2_KERNEL_MATERN32); break;
+    case H2_KERNEL_LAPLACE: H2_FILL_KID(H2_KERNEL_LAPLACE); break;
+    case H2_KERNEL_BUMP: H2_FILL_KID(H2_KERNEL_BUMP); break;
+    case H2_KERNEL_MQSHIFT: H2_FILL_KID(H2_KERNEL_MQSHIFT); break;
+    default: H2_FILL_KID(H2_KERNEL_COSDOT); break;
   }
+#undef H2_FILL_KID
 }
 
 // builds the symmetric-once pair list of one class (CSR order) with entry offsets, on stream s
@@ -417,8 +418,8 @@ static void make_pairs(h2_handle* h, cudaStream_t s, int mode, int64_t& np, int2
   const int* idx = mode == 0 ? h->il_idx : h->nf_idx;
   const int64_t m = mode == 0 ? h->n_il : h->n_nf;
   Scratch flag(sizeof(int64_t) * (m + 1), s), pos(sizeof(int64_t) * (m + 1), s);
-  pair_flag_kernel<<<grid_for(m + 1, 256), 256, 0, s>>>(mode, nn, m, off, idx, h->k, h->nbegin, h->p_lo, h->p_hi,
-                                                        flag.as<int64_t>());
+  pair_flag_kernel<<<grid_for(m + 1, 256), 256, 0, s>>>(mode, h->nonsym, nn, m, off, idx, h->k, h->k_col, h->nbegin,
+                                                        h->p_lo, h->p_hi, flag.as<int64_t>());
   scan_excl_i64(flag.as<int64_t>(), pos.as<int64_t>(), m + 1, s);
   H2_CHECK_LAUNCH();
   np = read1(pos.as<int64_t>() + m, s);
@@ -427,7 +428,7 @@ static void make_pairs(h2_handle* h, cudaStream_t s, int mode, int64_t& np, int2
   Scratch size(sizeof(int64_t) * (np + 1), s);
   H2_CUDA_TRY(cudaMemsetAsync(size.as<int64_t>() + np, 0, sizeof(int64_t), s));
   if (m > 0)
-    pair_emit_kernel<<<grid_for(m, 256), 256, 0, s>>>(mode, nn, m, off, idx, h->k, h->nbegin, h->nend,
+    pair_emit_kernel<<<grid_for(m, 256), 256, 0, s>>>(mode, nn, m, off, idx, h->k, h->k_col, h->nbegin, h->nend,
                                                       pos.as<int64_t>(), pairs, size.as<int64_t>());
   scan_excl_i64(size.as<int64_t>(), voff, np + 1, s);
   H2_CHECK_LAUNCH();
@@ -493,15 +494,19 @@ void fill_nearfield_begin(h2_handle* h, cudaStream_t side, int storage, int64_t 
   }
   if (h->timing) H2_CUDA_TRY(cudaEventRecord(job.t0, side));
   if (nunits > 0) {
-    job.xs = Scratch(sizeof(double) * (size_t)h->n * h->d, side);
-    scale_coords_kernel<<<grid_for((int64_t)h->n * h->d, 256), 256, 0, side>>>(
-        (int64_t)h->n * h->d, h->X, kernel_cscale(h->kid, h->kp), job.xs.as<double>());
+    const int64_t m = (int64_t)h->n * h->d;
+    const bool shifted = h->Xf != h->X;  // the rows' coordinates differ (shifted multiquadric)
+    job.xs = Scratch(sizeof(double) * (size_t)m * (shifted ? 2 : 1), side);
+    scale_coords_kernel<<<grid_for(m, 256), 256, 0, side>>>(m, h->X, kernel_cscale(h->kid, h->kp), job.xs.as<double>());
+    if (shifted)
+      scale_coords_kernel<<<grid_for(m, 256), 256, 0, side>>>(m, h->Xf, kernel_cscale(h->kid, h->kp),
+                                                              job.xs.as<double>() + m);
     // chunk counter + "main stream past a9" flag (set at once when the fill runs on the main stream)
     job.ctl = Scratch(2 * sizeof(unsigned long long), side);
     H2_CUDA_TRY(cudaMemsetAsync(job.ctl.p, 0, 2 * sizeof(unsigned long long), side));
     if (side == h->stream) H2_CUDA_TRY(cudaMemsetAsync(job.ctl.as<unsigned long long>() + 1, 1, 1, side));
     launch_fill(h, side, 1, nunits, h->n_np, h->nf_umap, h->nf_uoff, h->np_pairs, h->np_off, job.xs.as<double>(),
-                h->np_val, job.ctl.as<unsigned long long>());
+                job.xs.as<double>() + (shifted ? m : 0), h->np_val, job.ctl.as<unsigned long long>());
     h->gpu_launches += 1;
     H2_CHECK_LAUNCH();
     h->gpu_launches += 1;
@@ -527,7 +532,7 @@ void fill_coupling(h2_handle* h, int storage, int64_t budget, const NfJob& job) 
   }
   if (h->timing) H2_CUDA_TRY(cudaEventRecord(ev[0], s));
   if (store_cp && h->n_cp > 0) {
-    launch_fill(h, s, 0, h->n_cp, h->n_cp, nullptr, nullptr, h->cp_pairs, h->cp_off, h->X, h->cp_val);
+    launch_fill(h, s, 0, h->n_cp, h->n_cp, nullptr, nullptr, h->cp_pairs, h->cp_off, h->X, h->Xf, h->cp_val);
     H2_CHECK_LAUNCH();
     h->gpu_launches += 1;
   }
@@ -573,16 +578,17 @@ NfJob::~NfJob() {
 __global__ void sample_kernel(int64_t count, const int32_t* kind, const int64_t* pair, const int64_t* entry,
                               const int2* cpp, const int64_t* cpo, const double* cpv, const int2* npp,
                               const int64_t* npo, const double* npv, const int* nbegin, const int* nend,
-                              const int* k, const int* sk, int r, double* val, int32_t* rp, int32_t* cp) {
+                              const int* k, const int* sk, const int* kc, const int* skc, int r, double* val,
+                              int32_t* rp, int32_t* cp) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < count; s += (int64_t)gridDim.x * blockDim.x) {
     int md = kind[s];
     int64_t p = pair[s], e = entry[s];
     int2 pr = md == 0 ? cpp[p] : npp[p];
-    int nj = md == 0 ? k[pr.y] : nend[pr.y] - nbegin[pr.y];
+    int nj = md == 0 ? kc[pr.y] : nend[pr.y] - nbegin[pr.y];
     int row = (int)(e / nj), col = (int)(e % nj);
     val[s] = md == 0 ? cpv[cpo[p] + e] : npv[npo[p] + e];
     rp[s] = md == 0 ? sk[(int64_t)pr.x * r + row] : nbegin[pr.x] + row;
-    cp[s] = md == 0 ? sk[(int64_t)pr.y * r + col] : nbegin[pr.y] + col;
+    cp[s] = md == 0 ? skc[(int64_t)pr.y * r + col] : nbegin[pr.y] + col;
   }
 }
 
@@ -608,7 +614,7 @@ void sample_blocks(const h2_handle* h, int64_t count, const int32_t* kind, const
   H2_CUDA_TRY(cudaMemcpyAsync(de, entry, 8 * count, cudaMemcpyHostToDevice, s));
   sample_kernel<<<grid_for(count, 256), 256, 0, s>>>(count, dk, dp, de, h->cp_pairs, h->cp_off, h->cp_val,
                                                      h->np_pairs, h->np_off, h->np_val, h->nbegin, h->nend, h->k,
-                                                     h->sk, h->r, dv, dr, dc);
+                                                     h->sk, h->k_col, h->sk_col, h->r, dv, dr, dc);
   H2_CHECK_LAUNCH();
   H2_CUDA_TRY(cudaMemcpyAsync(value, dv, 8 * count, cudaMemcpyDeviceToHost, s));
   H2_CUDA_TRY(cudaMemcpyAsync(row_pt, dr, 4 * count, cudaMemcpyDeviceToHost, s));

@@ -58,33 +58,40 @@ __global__ void up_kernel(int base, int r, const int* __restrict__ is_leaf, cons
 }
 
 template <int D>
-__device__ __forceinline__ double kval(int kid, double p2, const double* __restrict__ X, int64_t n, int a, int b) {
-  return kernel_pts<D>(kid, p2, X, n, a, b);
+__device__ __forceinline__ double kval(int kid, double p2, const double* __restrict__ Xf,
+                                       const double* __restrict__ X, int64_t n, int a, int b) {
+  return kernel_pts<D>(kid, p2, Xf, X, n, a, b);
 }
 
+// B_ij = K(X^_i^(row), X^_j^(col)) (stored or evaluated): y^_i += B z^_j, and for a symmetric build
+// (sym: pairs stored once) also y^_j += B^T z^_i
 template <int D>
 __global__ void coupling_kernel(int64_t np, const int2* __restrict__ pairs, const int64_t* __restrict__ voff,
-                                const double* __restrict__ B, int kid, double p2, const double* __restrict__ X,
-                                int64_t n, const int* __restrict__ k, const int* __restrict__ sk, int r,
-                                const double* __restrict__ zh, double* yh) {
+                                const double* __restrict__ B, int kid, double p2, const double* __restrict__ Xf,
+                                const double* __restrict__ X, int64_t n, const int* __restrict__ k,
+                                const int* __restrict__ sk, const int* __restrict__ kc, const int* __restrict__ skc,
+                                int r, int sym, const double* __restrict__ zh, double* yh) {
   for (int64_t p = blockIdx.x; p < np; p += gridDim.x) {
     const int2 pr = pairs[p];
-    const int i = pr.x, j = pr.y, ki = k[i], kj = k[j];
+    const int i = pr.x, j = pr.y, ki = k[i], kj = kc[j];
     const double* Bp = B ? B + voff[p] : nullptr;
     const int* si = sk + (int64_t)i * r;
-    const int* sj = sk + (int64_t)j * r;
+    const int* sj = skc + (int64_t)j * r;
     const double* zi = zh + (int64_t)i * r;
     const double* zj = zh + (int64_t)j * r;
     for (int a = threadIdx.x; a < ki; a += blockDim.x) {  // y^_i += B z^_j
       double s = 0.0;
-      for (int b = 0; b < kj; b++) s += (Bp ? Bp[(int64_t)a * kj + b] : kval<D>(kid, p2, X, n, si[a], sj[b])) * zj[b];
+      for (int b = 0; b < kj; b++)
+        s += (Bp ? Bp[(int64_t)a * kj + b] : kval<D>(kid, p2, Xf, X, n, si[a], sj[b])) * zj[b];
       atomicAdd(yh + (int64_t)i * r + a, s);
     }
-    for (int b = threadIdx.x; b < kj; b += blockDim.x) {  // y^_j += B^T z^_i
-      double s = 0.0;
-      for (int a = 0; a < ki; a++) s += (Bp ? Bp[(int64_t)a * kj + b] : kval<D>(kid, p2, X, n, si[a], sj[b])) * zi[a];
-      atomicAdd(yh + (int64_t)j * r + b, s);
-    }
+    if (sym)
+      for (int b = threadIdx.x; b < kj; b += blockDim.x) {  // y^_j += B^T z^_i
+        double s = 0.0;
+        for (int a = 0; a < ki; a++)
+          s += (Bp ? Bp[(int64_t)a * kj + b] : kval<D>(kid, p2, Xf, X, n, si[a], sj[b])) * zi[a];
+        atomicAdd(yh + (int64_t)j * r + b, s);
+      }
   }
 }
 
@@ -94,8 +101,8 @@ __global__ void coupling_kernel(int64_t np, const int2* __restrict__ pairs, cons
 // registers (one atomic per column per pair): every entry read once, coalesced along the row
 __global__ void __launch_bounds__(256) coupling_mv_kernel(int64_t np, const int2* __restrict__ pairs,
                                                           const int64_t* __restrict__ voff, const double* __restrict__ B,
-                                                          const int* __restrict__ k, int r,
-                                                          const double* __restrict__ zh, double* yh) {
+                                                          const int* __restrict__ k, const int* __restrict__ kc, int r,
+                                                          int sym, const double* __restrict__ zh, double* yh) {
   constexpr int RC = 8;
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -111,7 +118,7 @@ __global__ void __launch_bounds__(256) coupling_mv_kernel(int64_t np, const int2
       mj = pr.y;
       mvo = voff[pl];
       mki = k[mi];
-      mkj = k[mj];
+      mkj = kc[mj];
     }
     const int cnt = np - p0 < 32 ? (int)(np - p0) : 32;
     for (int t = 0; t < cnt; t++) {
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(256) coupling_mv_kernel(int64_t np, const int2
           }
           if (lane < RC && a0 + lane < ki) atomicAdd(yi + a0 + lane, part[0]);
         }
-        if (ok) atomicAdd(yj + col, acc);
+        if (ok && sym) atomicAdd(yj + col, acc);  // y^_j += B^T z^_i (symmetric-once storage)
       }
     }
   }
@@ -192,9 +199,9 @@ __global__ void down_kernel(int base, int r, const int* __restrict__ is_leaf, co
 
 template <int D>
 __global__ void nearfield_kernel(int64_t np, const int2* __restrict__ pairs, const int64_t* __restrict__ voff,
-                                 const double* __restrict__ Dv, int kid, double p2, const double* __restrict__ X,
-                                 int64_t n, const int* __restrict__ nbegin, const int* __restrict__ nend,
-                                 const double* __restrict__ xt, double* yt) {
+                                 const double* __restrict__ Dv, int kid, double p2, const double* __restrict__ Xf,
+                                 const double* __restrict__ X, int64_t n, const int* __restrict__ nbegin,
+                                 const int* __restrict__ nend, int sym, const double* __restrict__ xt, double* yt) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int64_t p = blockIdx.x; p < np; p += gridDim.x) {
     const int2 pr = pairs[p];
@@ -204,15 +211,15 @@ __global__ void nearfield_kernel(int64_t np, const int2* __restrict__ pairs, con
     for (int a = warp; a < ni; a += nw) {  // y_i += D x_j (warp per row, coalesced)
       double s = 0.0;
       for (int b = lane; b < nj; b += 32)
-        s += (Dp ? Dp[(int64_t)a * nj + b] : kval<D>(kid, p2, X, n, bi + a, bj + b)) * xt[bj + b];
+        s += (Dp ? Dp[(int64_t)a * nj + b] : kval<D>(kid, p2, Xf, X, n, bi + a, bj + b)) * xt[bj + b];
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) atomicAdd(yt + bi + a, s);
     }
-    if (i != j)
+    if (sym && i != j)
       for (int b = threadIdx.x; b < nj; b += blockDim.x) {  // y_j += D^T x_i
         double s = 0.0;
         for (int a = 0; a < ni; a++)
-          s += (Dp ? Dp[(int64_t)a * nj + b] : kval<D>(kid, p2, X, n, bi + a, bj + b)) * xt[bi + a];
+          s += (Dp ? Dp[(int64_t)a * nj + b] : kval<D>(kid, p2, Xf, X, n, bi + a, bj + b)) * xt[bi + a];
         atomicAdd(yt + bj + b, s);
       }
   }
@@ -235,7 +242,7 @@ __global__ void __launch_bounds__(256, 2) nf_matvec_kernel(int64_t nitems, const
                                                            const int* __restrict__ nbegin, const int* __restrict__ nend,
                                                            const double* __restrict__ Dv, const double* __restrict__ xt,
                                                            double* yt, int kMvPfRows,
-                                                           unsigned long long* ctr) {
+                                                           unsigned long long* ctr, int sym) {
   constexpr int WC = 32 * CW * SPLIT, G = 16, PF = CW >= 3 ? 4 : 8;
   static_assert(G % PF == 0, "the prefetch ring must wrap with the row groups");
   const int lane = threadIdx.x & 31;
@@ -253,7 +260,7 @@ __global__ void __launch_bounds__(256, 2) nf_matvec_kernel(int64_t nitems, const
     const int half = (int)(v - it * SPLIT);
     const int p = imap[it];
     const int2 pr = pairs[p];
-    const bool diag = pr.x == pr.y;
+    const bool diag = !sym || pr.x == pr.y;  // forward only (non-symmetric: every block is stored)
     const int bi = nbegin[pr.x], bj = nbegin[pr.y];
     const int ni = nend[pr.x] - bi, nj = nend[pr.y] - bj;
     const int c0 = (int)(it - ioff[p]) * WC + half * 32 * CW;
@@ -456,7 +463,7 @@ template <int CW>
 __global__ void __launch_bounds__(kMvBulkThreads) nf_matvec_bulk_kernel(
     int64_t nunits, const int* __restrict__ umap, const int64_t* __restrict__ uoff, const int2* __restrict__ pairs,
     const int64_t* __restrict__ voff, const int* __restrict__ nbegin, const int* __restrict__ nend,
-    const double* __restrict__ Dv, const double* __restrict__ xt, double* yt) {
+    const double* __restrict__ Dv, const double* __restrict__ xt, double* yt, int sym) {
   constexpr int WC = 32 * CW;
   extern __shared__ double sm[];  // buf[2][kMvBulkBuf], red[kMvBulkWarps][WC]
   __shared__ __align__(8) uint64_t bar[2];
@@ -479,7 +486,7 @@ __global__ void __launch_bounds__(kMvBulkThreads) nf_matvec_bulk_kernel(
                    &bar[cur ^ 1]);
     }
     const MvUnit m = mv_unit<WC>(u, umap, uoff, pairs, voff, nbegin, nend);
-    const bool diag = m.pi == m.pj;
+    const bool diag = !sym || m.pi == m.pj;
     const double* buf = sm + cur * kMvBulkBuf;
     double xj[CW], acc[CW];
 #pragma unroll
@@ -562,11 +569,13 @@ static void launch_far_near(const h2_handle* h, double p2, const double* zh, dou
   if (which == 0 && h->n_cp > 0 && h->cp_stored) {
     const int64_t blocks = (h->n_cp + 255) / 256;  // 8 warps x 32 pairs
     const unsigned g = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
-    coupling_mv_kernel<<<g, 256, 0, s>>>(h->n_cp, h->cp_pairs, h->cp_off, h->cp_val, h->k, h->r, zh, yh);
+    coupling_mv_kernel<<<g, 256, 0, s>>>(h->n_cp, h->cp_pairs, h->cp_off, h->cp_val, h->k, h->k_col, h->r,
+                                         !h->nonsym, zh, yh);
   } else if (which == 0 && h->n_cp > 0) {
     unsigned g = (unsigned)(h->n_cp < 148 * 64 ? h->n_cp : 148 * 64);
     coupling_kernel<D><<<g, kMvThreads, 0, s>>>(h->n_cp, h->cp_pairs, h->cp_off, h->cp_stored ? h->cp_val : nullptr,
-                                                h->kid, p2, h->X, h->n, h->k, h->sk, h->r, zh, yh);
+                                                h->kid, p2, h->Xf, h->X, h->n, h->k, h->sk, h->k_col, h->sk_col, h->r,
+                                                !h->nonsym, zh, yh);
   }
   if (which == 1 && h->n_np > 0 && h->np_stored && h->nf_nunits > 0) {
     const int cw = h->nf_wc / 32;
@@ -581,7 +590,8 @@ static void launch_far_near(const h2_handle* h, double p2, const double* zh, dou
     H2_CUDA_TRY(cudaFuncSetAttribute(nf_matvec_bulk_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
                                      200 * 1024));                                                               \
     nf_matvec_bulk_kernel<C><<<gb, kMvBulkThreads, smem, s>>>(h->nf_nunits, h->nf_umap, h->nf_uoff, h->np_pairs,  \
-                                                              h->np_off, h->nbegin, h->nend, h->np_val, xt, yt); \
+                                                              h->np_off, h->nbegin, h->nend, h->np_val, xt, yt,  \
+                                                              !h->nonsym);                                       \
     break;
         H2_NFMVB_CASE(2) H2_NFMVB_CASE(3) H2_NFMVB_CASE(4) H2_NFMVB_CASE(5) H2_NFMVB_CASE(6) H2_NFMVB_CASE(8)
 #undef H2_NFMVB_CASE
@@ -602,7 +612,8 @@ static void launch_far_near(const h2_handle* h, double p2, const double* zh, dou
 #define H2_NFMV_CASE(C, CWW, SP)                                                                              \
   case C:                                                                                                    \
     nf_matvec_kernel<CWW, SP><<<g, 256, 0, s>>>(h->nf_nitems, h->nf_imap, h->nf_ioff, h->np_pairs, h->np_off,     \
-                                                h->nbegin, h->nend, h->np_val, xt, yt, mv_pf_rows(), ctr);    \
+                                                h->nbegin, h->nend, h->np_val, xt, yt, mv_pf_rows(), ctr,     \
+                                                !h->nonsym);                                                  \
     break;
       H2_NFMV_CASE(2, 2, 1) H2_NFMV_CASE(3, 3, 1) H2_NFMV_CASE(4, 4, 1) H2_NFMV_CASE(5, 5, 1)
       H2_NFMV_CASE(6, 3, 2) H2_NFMV_CASE(8, 4, 2)
@@ -612,7 +623,7 @@ static void launch_far_near(const h2_handle* h, double p2, const double* zh, dou
   } else if (which == 1 && h->n_np > 0) {
     unsigned g = (unsigned)(h->n_np < 148 * 64 ? h->n_np : 148 * 64);
     nearfield_kernel<D><<<g, kMvThreads, 0, s>>>(h->n_np, h->np_pairs, h->np_off, h->np_stored ? h->np_val : nullptr,
-                                                 h->kid, p2, h->X, h->n, h->nbegin, h->nend, xt, yt);
+                                                 h->kid, p2, h->Xf, h->X, h->n, h->nbegin, h->nend, !h->nonsym, xt, yt);
   }
 }
 
@@ -665,8 +676,8 @@ void matvec(const h2_handle* h, const double* x, double* y) {
     const LevelRange lr = level_range(h, l);
     if (lr.end > lr.begin)
       up_kernel<<<lr.end - lr.begin, kMvThreads, 0, s>>>(lr.begin, r, h->is_leaf, h->nbegin, h->first_child,
-                                                         h->nchild, h->k, h->xbar_n, h->child_off, h->u_off, h->U,
-                                                         xt.as<double>(), zh.as<double>());
+                                                         h->nchild, h->k_col, h->xbar_col_n, h->child_off_col,
+                                                         h->u_off_col, h->V, xt.as<double>(), zh.as<double>());
   };
   const int cut = sharded ? (h->cut > 1 ? h->cut : 1) : 1;
   for (int l = h->depth; l >= cut; l--) up(l);

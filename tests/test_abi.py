@@ -45,8 +45,8 @@ def test_options_default(P):
 
 @pytest.mark.parametrize("args,code", [
     (dict(n=0), -1), (dict(d=0), -1), (dict(d=9), -1), (dict(q=0), -1), (dict(tau=0.0), -1), (dict(tau=0.8), -1),
-    (dict(tol=0.0), -1), (dict(tol=1.0), -1), (dict(kid=7), -3), (dict(kid=2, kp=(-1.0,)), -1),
-    (dict(kid=3, kp=(0.0,)), -1)])
+    (dict(tol=0.0), -1), (dict(tol=1.0), -1), (dict(kid=8), -3), (dict(kid=0), -3), (dict(kid=2, kp=(-1.0,)), -1),
+    (dict(kid=3, kp=(0.0,)), -1), (dict(kid=7), -1), (dict(kid=7, kp=(-100.0,)), -1)])
 def test_invalid_arguments_rejected(P, args, code):
     a = dict(n=100, d=3, kid=1, kp=(), tol=1e-6, q=16, tau=0.5)
     a.update(args)
