@@ -274,8 +274,8 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
         H2_CUDA_TRY(cudaStreamWaitEvent(bs.calib, fork_ev, 0));
         calibrate_begin(h, bs.calib, cal);
       }
-      build_lists(h);                    // a4
       if (h->nranks > 1) shard_plan(h);  // cut level, owned subtrees and block rows (shard.cu)
+      build_lists(h);                    // a4 (sharded: the rank's own rows)
     }
     mark(2);
     // a10 needs only the tree and the nearfield list: it starts now on the side stream and

@@ -8,6 +8,7 @@
 // All (level, m) trials run as one batched launch: one CTA per trial.
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "cpqr.cuh"
 #include "vol.cuh"
@@ -358,8 +359,20 @@ int calibrate_end(h2_handle* h, CalibJob& job) {
   H2_CHECK_LAUNCH();
   h->gpu_launches += 1;
   int has[64];
-  H2_CUDA_TRY(cudaMemcpyAsync(has, hasd.p, sizeof(int) * 64, cudaMemcpyDeviceToHost, s));
-  H2_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h->nranks > 1) {  // sharded lists hold the rank's own rows: a level has a pair on SOME rank
+    Scratch all(sizeof(int) * 64 * h->nranks, s);
+    comm_allgather(h->comm, hasd.p, all.p, sizeof(int) * 64, s);
+    std::vector<int> v((size_t)64 * h->nranks);
+    H2_CUDA_TRY(cudaMemcpyAsync(v.data(), all.p, sizeof(int) * v.size(), cudaMemcpyDeviceToHost, s));
+    comm_sync(h->comm, s);
+    for (int l = 0; l < 64; l++) {
+      has[l] = 0;
+      for (int q = 0; q < h->nranks; q++) has[l] |= v[(size_t)q * 64 + l];
+    }
+  } else {
+    H2_CUDA_TRY(cudaMemcpyAsync(has, hasd.p, sizeof(int) * 64, cudaMemcpyDeviceToHost, s));
+    H2_CUDA_TRY(cudaStreamSynchronize(s));
+  }
   if (job.active) H2_CUDA_TRY(cudaStreamSynchronize(job.stream));
   std::vector<int> chosen(64, 0);  // per virtual level (l, l + 32)
   for (CalibSet* set : {&job.p0, &job.p1})  // trials of a level are in increasing m: keep the first pass

@@ -4,7 +4,8 @@
 // diagonal as diameter (reading B1), equality admissible (B2), pair-of-parents interaction lists
 // (B3) and cross-level pairs on adaptive trees (B4).  The frontier of candidate pairs
 // starts at (root, root); each step classifies every pair: admissible -> IL, both leaves -> NF,
-// otherwise expand the non-leaf side (both sides when neither is a leaf).
+// otherwise expand the non-leaf side (both sides when neither is a leaf).  A sharded build keeps
+// only its own rows (RowFilter): per-rank lists, the single-GPU lists restricted to those rows.
 #include <climits>
 
 #include "vol.cuh"
@@ -36,12 +37,24 @@ __device__ __forceinline__ bool admissible(const int* __restrict__ cell, int nno
 // exclusive scan (thread-blocked, so the output order is the frontier order), and the writes.
 constexpr int kTravThreads = 256, kTravIPT = 8, kTravTile = kTravThreads * kTravIPT;
 
+// Sharded builds: a rank keeps only the pairs whose row node it needs -- every node above the cut
+// level, and its own contiguous range at each level >= cut (shard.cu).  The children of a dropped
+// row are never needed either, so the frontier it would have grown is dropped with it.
+struct RowFilter {
+  int on, cut;
+  int lo[32], hi[32];
+};
+
 __device__ __forceinline__ void trav_classify(const int2 pr, const int* __restrict__ cell, int nnodes, int d,
                                               double tau2, const int* __restrict__ level,
                                               const int* __restrict__ is_leaf, const int* __restrict__ nchild,
-                                              long long& a, long long& b, long long& c) {
+                                              const RowFilter& rf, long long& a, long long& b, long long& c) {
   const int i = pr.x, j = pr.y;
   a = b = c = 0;
+  if (rf.on) {
+    const int li = level[i];
+    if (li >= rf.cut && (i < rf.lo[li] || i >= rf.hi[li])) return;
+  }
   if (admissible(cell, nnodes, d, i, level[i], j, level[j], tau2)) {
     a = 1;
   } else {
@@ -55,7 +68,7 @@ __global__ void __launch_bounds__(kTravThreads) trav_count_kernel(const int2* __
                                                                   const int* __restrict__ cell, int nnodes, int d,
                                                                   double tau2, const int* __restrict__ level,
                                                                   const int* __restrict__ is_leaf,
-                                                                  const int* __restrict__ nchild,
+                                                                  const int* __restrict__ nchild, RowFilter rf,
                                                                   long long* __restrict__ tile_sum,
                                                                   unsigned long long* totals) {
   __shared__ long long red[3][kTravThreads / 32];
@@ -65,7 +78,7 @@ __global__ void __launch_bounds__(kTravThreads) trav_count_kernel(const int2* __
   for (int k = 0; k < kTravIPT; k++) {
     if (base + k >= nf) break;
     long long a, b, c;
-    trav_classify(fr[base + k], cell, nnodes, d, tau2, level, is_leaf, nchild, a, b, c);
+    trav_classify(fr[base + k], cell, nnodes, d, tau2, level, is_leaf, nchild, rf, a, b, c);
     sa += a;
     sb += b;
     sc += c;
@@ -92,8 +105,8 @@ __global__ void __launch_bounds__(kTravThreads) trav_count_kernel(const int2* __
 __global__ void __launch_bounds__(kTravThreads) trav_emit_kernel(
     const int2* __restrict__ fr, int64_t nf, const int* __restrict__ cell, int nnodes, int d, double tau2,
     const int* __restrict__ level, const int* __restrict__ is_leaf, const int* __restrict__ nchild,
-    const int* __restrict__ first_child, const long long* __restrict__ tile_pre, unsigned long long* il,
-    int64_t il_base, unsigned long long* nl, int64_t nl_base, int2* next) {
+    const int* __restrict__ first_child, RowFilter rf, const long long* __restrict__ tile_pre,
+    unsigned long long* il, int64_t il_base, unsigned long long* nl, int64_t nl_base, int2* next) {
   __shared__ long long wsum[3][kTravThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int ntiles = gridDim.x;
@@ -109,7 +122,8 @@ __global__ void __launch_bounds__(kTravThreads) trav_emit_kernel(
 #pragma unroll
   for (int k = 0; k < kTravIPT; k++) {
     ca[k] = cb[k] = cc[k] = 0;
-    if (base + k < nf) trav_classify(fr[base + k], cell, nnodes, d, tau2, level, is_leaf, nchild, ca[k], cb[k], cc[k]);
+    if (base + k < nf)
+      trav_classify(fr[base + k], cell, nnodes, d, tau2, level, is_leaf, nchild, rf, ca[k], cb[k], cc[k]);
     ta += ca[k];
     tb += cb[k];
     tc += cc[k];
@@ -272,6 +286,17 @@ static void to_csr(h2_handle* h, unsigned long long* keys, int64_t m, int64_t*& 
 void build_lists(h2_handle* h) {
   cudaStream_t s = h->stream;
   const double tau2 = h->tau * h->tau;
+  RowFilter rf{};  // sharded: this rank's rows only (shard_plan ran before)
+  if (h->nranks > 1) {
+    if (h->depth >= 32) throw Error{H2_ERR_INTERNAL, "sharded lists: depth beyond the row filter"};
+    rf.on = 1;
+    rf.cut = h->cut;
+    for (int l = 0; l <= h->depth; l++) {
+      const LevelRange lr = level_range(h, l);
+      rf.lo[l] = lr.begin;
+      rf.hi[l] = lr.end;
+    }
+  }
   Grow<int2> fa(s), fb(s);
   Grow<unsigned long long> il(s), nl(s);
   fa.ensure(1, 0);
@@ -290,7 +315,7 @@ void build_lists(h2_handle* h) {
     unsigned long long* tot_d = reinterpret_cast<unsigned long long*>(ts.as<long long>() + 3 * ntiles);
     H2_CUDA_TRY(cudaMemsetAsync(tot_d, 0, 3 * sizeof(unsigned long long), s));
     trav_count_kernel<<<(unsigned)ntiles, kTravThreads, 0, s>>>(fa.p, nf, h->cell, h->nnodes, h->d, tau2, h->level,
-                                                                 h->is_leaf, h->nchild, ts.as<long long>(), tot_d);
+                                                                 h->is_leaf, h->nchild, rf, ts.as<long long>(), tot_d);
     H2_CHECK_LAUNCH();
     scan_excl_i64(reinterpret_cast<const int64_t*>(ts.as<long long>()), tp.as<int64_t>(), 3 * ntiles, s);
     H2_CUDA_TRY(cudaMemcpyAsync(tot_h, tot_d, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -300,7 +325,7 @@ void build_lists(h2_handle* h) {
     nl.ensure(nnl + tot[1], nnl);
     fb.ensure(tot[2] > 0 ? tot[2] : 1, 0);
     trav_emit_kernel<<<(unsigned)ntiles, kTravThreads, 0, s>>>(fa.p, nf, h->cell, h->nnodes, h->d, tau2, h->level,
-                                                                h->is_leaf, h->nchild, h->first_child,
+                                                                h->is_leaf, h->nchild, h->first_child, rf,
                                                                 tp.as<long long>(), il.p, nil, nl.p, nnl, fb.p);
     H2_CHECK_LAUNCH();
     h->gpu_launches += 2;

@@ -3,12 +3,13 @@
 // replicated; each level's skeleton indices and representors are exchanged with NCCL allgather;
 // top levels above the cut are computed redundantly").
 //
-// Plan (identical on every rank: the tree and lists are built redundantly and deterministically):
+// Plan (identical on every rank: the tree is built redundantly and deterministically; the plan is
+// made before the lists, which each rank then builds for its own rows only, lists.cu):
 //   * cut level c = the shallowest level with >= 64 nodes per rank (else the most populous level);
 //   * the cut-level nodes (Morton order) are split into nranks contiguous runs balanced by an
-//     integer work estimate of their subtrees (nearfield entries + 256 per interaction-list entry +
-//     64 per point); node ids of one level are in Morton order, so the nodes a rank owns at every
-//     level >= c form ONE contiguous id range;
+//     integer work estimate of their subtrees (3^d n_leaf^2 + 64 n_leaf per leaf, 65536 per node);
+//     node ids of one level are in Morton order, so the nodes a rank owns at every level >= c form
+//     ONE contiguous id range;
 //   * HiDR and the ID sweep run, at levels >= c, on the owned range only; levels < c are computed
 //     by every rank;
 //   * block rows (a9, a10, the matvec's leaf outputs) belong to the rank whose point range
@@ -23,12 +24,13 @@
 
 namespace h2 {
 
-// integer work estimate of one node (see the header comment); int64, so sums are exact and the
-// plan is bit-identical on every rank
-__global__ void shard_weight_kernel(int nnodes, int cut, const int* __restrict__ level, const int* __restrict__ parent,
-                                    const int* __restrict__ is_leaf, const int* __restrict__ nbegin,
-                                    const int* __restrict__ nend, const int64_t* __restrict__ il_off,
-                                    const int64_t* __restrict__ nf_off, const int* __restrict__ nf_idx, int cut_base,
+// integer work estimate of one node, from the tree alone (the plan precedes the lists, which are
+// then built for the rank's own rows only): a leaf's nearfield entries ~ 3^d n_leaf^2 (its
+// neighbours hold about as many points as it does) plus 64 per point, and 65536 per node (its
+// HiDR search and ID).  int64, so sums are exact and the plan is bit-identical on every rank.
+__global__ void shard_weight_kernel(int nnodes, int cut, int d, const int* __restrict__ level,
+                                    const int* __restrict__ parent, const int* __restrict__ is_leaf,
+                                    const int* __restrict__ nbegin, const int* __restrict__ nend, int cut_base,
                                     int* anc, unsigned long long* wcut) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nnodes) return;
@@ -39,13 +41,11 @@ __global__ void shard_weight_kernel(int nnodes, int cut, const int* __restrict__
   int a = i;
   while (level[a] > cut) a = parent[a];
   anc[i] = a;
+  int64_t w3 = 1;
+  for (int c = 0; c < d; c++) w3 *= 3;
   const int64_t ni = nend[i] - nbegin[i];
-  int64_t w = 256 * (il_off[i + 1] - il_off[i]) + 64 * (is_leaf[i] ? ni : 0);
-  if (is_leaf[i])
-    for (int64_t e = nf_off[i]; e < nf_off[i + 1]; e++) {
-      const int j = nf_idx[e];
-      w += ni * (nend[j] - nbegin[j]);
-    }
+  int64_t w = 65536;
+  if (is_leaf[i]) w += w3 * ni * ni + 64 * ni;
   atomicAdd(wcut + (a - cut_base), (unsigned long long)w);
 }
 
@@ -75,9 +75,8 @@ void shard_plan(h2_handle* h) {
   const int c = h->cut, base = h->lvl_start[c], ncut = (int)counts[c];
   Scratch anc(sizeof(int) * nn, s), wc(sizeof(unsigned long long) * ncut, s);
   H2_CUDA_TRY(cudaMemsetAsync(wc.p, 0, sizeof(unsigned long long) * ncut, s));
-  shard_weight_kernel<<<(nn + 255) / 256, 256, 0, s>>>(nn, c, h->level, h->parent, h->is_leaf, h->nbegin, h->nend,
-                                                       h->il_off, h->nf_off, h->nf_idx, base, anc.as<int>(),
-                                                       wc.as<unsigned long long>());
+  shard_weight_kernel<<<(nn + 255) / 256, 256, 0, s>>>(nn, c, h->d, h->level, h->parent, h->is_leaf, h->nbegin,
+                                                       h->nend, base, anc.as<int>(), wc.as<unsigned long long>());
   H2_CHECK_LAUNCH();
   std::vector<int64_t> w(ncut);
   std::vector<int> a(nn), nb(ncut);

@@ -84,6 +84,26 @@ CASES = [  # cfg, n, q override, ranks
 ]
 
 
+@pytest.mark.parametrize("R", [2, 4, 8])
+def test_sharded_lists_work_falls_as_one_over_ranks(R):
+    """a4 sharded: every rank builds the lists of its own rows only, so the largest per-rank pair
+    count falls roughly as 1/R (the top levels above the cut are the only redundant rows)."""
+    c = synth.CONFIGS[4]
+    pts = synth.points(4, 1 << 19)
+    kp = list(c["params"])
+    ref = P.H2Matrix(torch.from_numpy(pts).cuda(), c["kernel"], kp, c["id_tol"], c["q"], c["tau"],
+                     storage=P.H2_STORE_ON_THE_FLY, timing=True)
+    total = ref.info()["n_il"] + ref.info()["n_nf"]
+    hs = build_sharded(pts, R, c["kernel"], kp, c["id_tol"], c["q"], c["tau"], storage=P.H2_STORE_ON_THE_FLY)
+    per = [g.info()["n_il"] + g.info()["n_nf"] for g in hs]
+    print(f"R={R}: pairs per rank {per} of {total} (max {max(per) / total:.3f} of the total, 1/R = {1 / R:.3f}); "
+          f"lists ms {[round(g.info()['stage_ms']['lists'], 2) for g in hs]}")
+    assert sum(per) >= total
+    assert max(per) <= 1.35 * total / R
+    for g in hs:
+        g.close()
+
+
 @pytest.mark.parametrize("cfg,n,q,R", CASES)
 def test_sharded_equals_single_gpu(cfg, n, q, R):
     c = synth.CONFIGS[cfg]
@@ -113,6 +133,16 @@ def test_sharded_equals_single_gpu(cfg, n, q, R):
         assert np.array_equal(g.export("K"), k_ref)
         assert all(np.array_equal(a, b) for a, b in zip(slots(g, "SK"), sk_ref))
         ys, U = slots(g, "YS"), u_blocks(g)
+        # a4 sharded: the rank's lists are the single-GPU lists restricted to the rows it needs
+        # (every node above the cut, its own range below); the other rows are empty
+        for nm in ("IL", "NF"):
+            mine, full = slots(g, nm), slots(ref, nm)
+            need = np.zeros(info["nnodes"], bool)
+            for lvl in range(depth + 1):
+                lo, hi = rng[lvl]
+                need[lo:hi] = True
+            for i in range(info["nnodes"]):
+                assert np.array_equal(mine[i], full[i] if need[i] else full[i][:0]), (nm, r, i)
         for lvl in range(depth + 1):
             lo, hi = rng[lvl]
             for i in range(lo, hi):  # the nodes this rank computed: Y^* and U bit for bit
