@@ -72,6 +72,10 @@ def lib():
         L.orc_fps.argtypes = [vp, i32, vp, i32, i32, vp]
         L.orc_set_reduct.argtypes = [vp, i32]
         L.orc_set_nonsym.argtypes = [vp, i32]
+        L.orc_set_srrqr.argtypes = [vp, f64]
+        L.orc_srrqr_count.restype = i64
+        L.orc_srrqr_count.argtypes = [vp]
+        L.orc_id_srrqr.argtypes = [vp, i32, i32, f64, f64, vp, vp, vp]
         L.orc_set_kernel_shift.argtypes = [vp, i32]
         L.orc_calib_level_tr.argtypes = [i32, i32, f64, f64, f64, f64, i32, i32]
         L.orc_surface.argtypes = [vp, i32, vp, i32, i32, vp]
@@ -151,6 +155,18 @@ def interp_decomp(A: np.ndarray, tol: float):
     return skel[:k].copy(), U
 
 
+def interp_decomp_srrqr(A: np.ndarray, tol: float, f: float):
+    """F with SRRQR swaps: A ~= U A[skel] with max |G| <= f.  Returns (skel, U, swaps)."""
+    A = np.ascontiguousarray(A, np.float64)
+    nx, ny = A.shape
+    skel = np.empty(max(1, min(nx, ny)), np.int32)
+    Uf = np.zeros(max(1, nx * min(nx, ny)), np.float64)
+    sw = np.zeros(1, np.int32)
+    k = lib().orc_id_srrqr(_p(A), nx, ny, float(tol), float(f), _p(skel), _p(Uf), _p(sw))
+    U = Uf[: nx * k].reshape(k, nx).T.copy()
+    return skel[:k].copy(), U, int(sw[0])
+
+
 def admissible(ci, li: int, cj, lj: int, tau: float) -> bool:
     ci = np.ascontiguousarray(ci, np.int64)
     cj = np.ascontiguousarray(cj, np.int64)
@@ -212,7 +228,8 @@ def dense_rows(pts: np.ndarray, kid: int, param: float, x: np.ndarray, rows) -> 
 class OracleH2:
     """A (partition) + B (lists) on construction; then calibrate / hidr / id_sweep / matvec."""
 
-    def __init__(self, pts: np.ndarray, q: int, tau: float = 0.5, reduct: int = 0, nonsym: bool = False):
+    def __init__(self, pts: np.ndarray, q: int, tau: float = 0.5, reduct: int = 0, nonsym: bool = False,
+                 srrqr_f: float = 0.0):
         """reduct: the DataReduct of HiDR, 0 volume-based (reading C1), 1 farthest point sampling (C6),
         2 surface-based (C7).  nonsym: build row AND column bases and every ordered block (Algorithm 2
         with X^(row) != X^(col); required for kernel 7, allowed for symmetric kernels)."""
@@ -223,6 +240,7 @@ class OracleH2:
             raise ValueError("orc_new rejected the arguments")
         lib().orc_set_reduct(self._h, int(reduct))
         lib().orc_set_nonsym(self._h, int(bool(nonsym)))
+        lib().orc_set_srrqr(self._h, float(srrqr_f))
         self.nonsym = bool(nonsym)
         self.q, self.tau = q, tau
         self.kid, self.param = None, 0.0
@@ -293,6 +311,10 @@ class OracleH2:
     # --- stages ---
     def calibrate(self, kid: int, param: float, eps: float) -> int:
         return int(lib().orc_calibrate(self._h, kid, float(param), float(eps)))
+
+    def srrqr_swaps(self) -> int:
+        """SRRQR swaps made by the last id_sweep (srrqr_f > 0)."""
+        return int(lib().orc_srrqr_count(self._h))
 
     def calib_levels(self) -> np.ndarray:
         """E4: the per-level r of the last calibrate() (0 where a level has no admissible pair)."""

@@ -319,16 +319,90 @@ int orc_cpqr(double* M, int rows, int cols, double tol, int* piv) {
   return k;
 }
 
-/* Interpolative decomposition of A (nx x ny, row-major: A[b*ny + a]) by CPQR of A^T:
+/* Strong rank-revealing refinement (SRRQR, PAPER Eq.(4.1): "||G||_max is bounded by a
+ * prescribed constant"; Gu & Eisenstat's swaps at fixed rank): given the CPQR of M0 (rows x cols,
+ * column-major, untouched) with rank k and pivot order piv, while some |T_ij| > f (T = R11^{-1} R12,
+ * k x (cols - k)) swap the skeleton column at position i with the non-skeleton column at position
+ * k + j of the largest such entry (each swap multiplies |det R11| by |T_ij| > f > 1, so the loop
+ * ends), and refactor: Householder QR without pivoting of the first k columns in the new order,
+ * applied to all columns, then T by back substitution.  On return Mout holds R11 / T like orc_cpqr
+ * and piv the new order.  Returns the number of swaps.                                            */
+int orc_srrqr_swaps(const double* M0, double* Mout, int rows, int cols, int k, double f, int* piv) {
+  if (k <= 0 || k >= cols) return 0;
+  int swaps = 0;
+  double* v = (double*)malloc(sizeof(double) * (size_t)rows);
+  for (;;) {
+    double best = f;
+    int bi = -1, bj = -1;
+    for (int c = k; c < cols; c++)
+      for (int t = 0; t < k; t++) {
+        double a = fabs(Mout[t + (int64_t)rows * c]);
+        if (a > best) {
+          best = a;
+          bi = t;
+          bj = c;
+        }
+      }
+    if (bi < 0 || swaps >= 64 * k) break;
+    int tp = piv[bi];
+    piv[bi] = piv[bj];
+    piv[bj] = tp;
+    swaps++;
+    /* refactor: the columns in the new order, QR of the first k, T = R11^{-1} R12 */
+    for (int c = 0; c < cols; c++) memcpy(Mout + (int64_t)rows * c, M0 + (int64_t)rows * piv[c], sizeof(double) * (size_t)rows);
+    for (int t = 0; t < k; t++) {
+      double s2 = 0.0;
+      for (int i = t; i < rows; i++) s2 = s2 + Mout[i + (int64_t)rows * t] * Mout[i + (int64_t)rows * t];
+      double nrm = sqrt(s2);
+      double x0 = Mout[t + (int64_t)rows * t];
+      double alpha = x0 >= 0.0 ? -nrm : nrm;
+      double vtv = 0.0;
+      for (int i = t; i < rows; i++) v[i] = Mout[i + (int64_t)rows * t];
+      v[t] = x0 - alpha;
+      for (int i = t; i < rows; i++) vtv = vtv + v[i] * v[i];
+      Mout[t + (int64_t)rows * t] = alpha;
+      for (int i = t + 1; i < rows; i++) Mout[i + (int64_t)rows * t] = 0.0;
+      if (vtv > 0.0)
+        for (int j = t + 1; j < cols; j++) {
+          double* col = Mout + (int64_t)rows * j;
+          double sd = 0.0;
+          for (int i = t; i < rows; i++) sd = sd + v[i] * col[i];
+          double fct = 2.0 * sd / vtv;
+          for (int i = t; i < rows; i++) col[i] = col[i] - fct * v[i];
+        }
+    }
+    for (int c = k; c < cols; c++) {
+      double* col = Mout + (int64_t)rows * c;
+      for (int i = k - 1; i >= 0; i--) {
+        double sd = col[i];
+        for (int l = i + 1; l < k; l++) sd = sd - Mout[i + (int64_t)rows * l] * col[l];
+        col[i] = sd / Mout[i + (int64_t)rows * i];
+      }
+    }
+  }
+  free(v);
+  return swaps;
+}
+
+/* Interpolative decomposition of A (nx x ny, row-major: A[b*ny + a]) by CPQR of A^T, optionally
+ * refined by SRRQR swaps (f > 0; orc_id = f 0):
  *   A ~= U A[skel, :],  U (nx x k, column-major) has U[piv[t], t] = 1 (t < k) and
  *   U[piv[c], t] = T[t, c] for c >= k  (Eq.(4.1): K_{X Y*} = P [I; G] K_{X^ Y*}).
  * skel[0:k] = piv[0:k] (positions into the rows of A, pivot order).  Returns k.             */
-int orc_id(const double* A, int nx, int ny, double tol, int* skel, double* U) {
+int orc_id_srrqr(const double* A, int nx, int ny, double tol, double f, int* skel, double* U, int* nswaps) {
   double* M = (double*)malloc(sizeof(double) * (size_t)nx * (size_t)ny + 8);
   int* piv = (int*)malloc(sizeof(int) * (size_t)(nx > 0 ? nx : 1));
   for (int b = 0; b < nx; b++)
     for (int a = 0; a < ny; a++) M[a + (int64_t)ny * b] = A[(int64_t)b * ny + a];
+  double* M0 = NULL;
+  if (f > 0.0) {
+    M0 = (double*)malloc(sizeof(double) * (size_t)nx * (size_t)ny + 8);
+    memcpy(M0, M, sizeof(double) * (size_t)nx * (size_t)ny);
+  }
   int k = orc_cpqr(M, ny, nx, tol, piv);
+  int sw = f > 0.0 ? orc_srrqr_swaps(M0, M, ny, nx, k, f, piv) : 0;
+  if (nswaps) *nswaps = sw;
+  free(M0);
   for (int t = 0; t < k; t++) skel[t] = piv[t];
   if (U) {
     memset(U, 0, sizeof(double) * (size_t)nx * (size_t)k);
@@ -339,6 +413,10 @@ int orc_id(const double* A, int nx, int ny, double tol, int* skel, double* U) {
   free(M);
   free(piv);
   return k;
+}
+
+int orc_id(const double* A, int nx, int ny, double tol, int* skel, double* U) {
+  return orc_id_srrqr(A, nx, ny, tol, 0.0, skel, U, NULL);
 }
 
 /* ------------------------------------------------------------------------------------------ */
@@ -379,6 +457,8 @@ typedef struct orc_h2 {
   /* non-symmetric path (Algorithm 2 lines 4-12 with separate row / column sets): the
    * column bases V_i (W = stacked V of the children), skeletons X^_i^(col), ranks */
   int nonsym;
+  double srrqr_f; /* > 0: SRRQR swaps until ||G||_max <= srrqr_f; 0: plain CPQR (F1) */
+  int64_t srrqr_swaps;
   int *k_col, **sk_col, *xbar_col_n, *child_off_col;
   double** V;
   double t_stage[8];
@@ -718,6 +798,8 @@ void orc_set_reduct(orc_h2* h, int reduct) { h->reduct = reduct; }
 /* 1: build row AND column bases (Algorithm 2 line 11, both getBasis calls), blocks for all ordered
  * pairs; required for a non-symmetric kernel, allowed for a symmetric one (then V = U exactly) */
 void orc_set_nonsym(orc_h2* h, int nonsym) { h->nonsym = nonsym; }
+void orc_set_srrqr(orc_h2* h, double f) { h->srrqr_f = f; }
+int64_t orc_srrqr_count(const orc_h2* h) { return h->srrqr_swaps; }
 
 int orc_hidr(orc_h2* h, int r) {
   if (r < 1) return -1;
@@ -966,7 +1048,12 @@ static void id_sweep_one(orc_h2* h, int kid, double p, double id_tol, int tr, in
           A[(int64_t)b * ny + a] = kern_tr(kid, p, h->X + (int64_t)Xb[b] * d, h->X + (int64_t)h->ys[i][a] * d, d, tr);
       int* skel = (int*)malloc(sizeof(int) * (size_t)(nx < ny ? nx : ny));
       double* U = (double*)malloc(sizeof(double) * (size_t)nx * (size_t)(nx < ny ? nx : ny));
-      int k = orc_id(A, nx, ny, id_tol, skel, U);
+      int nsw = 0;
+      int k = orc_id_srrqr(A, nx, ny, id_tol, h->srrqr_f, skel, U, &nsw);
+      if (nsw) {
+#pragma omp atomic
+        h->srrqr_swaps += nsw;
+      }
       int* sk = (int*)malloc(sizeof(int) * (size_t)(k > 0 ? k : 1));
       for (int t = 0; t < k; t++) sk[t] = Xb[skel[t]];
       K[i] = k;
@@ -1004,6 +1091,7 @@ int orc_id_sweep(orc_h2* h, int kid, double p, double id_tol) {
   h->id_tol = id_tol;
   free_basis(nn, &h->k, &h->sk, &h->U, &h->xbar_n, &h->child_off);
   free_basis(nn, &h->k_col, &h->sk_col, &h->V, &h->xbar_col_n, &h->child_off_col);
+  h->srrqr_swaps = 0;
   h->k = (int*)calloc((size_t)nn, sizeof(int));
   h->xbar_n = (int*)calloc((size_t)nn, sizeof(int));
   h->child_off = (int*)calloc((size_t)nn, sizeof(int));

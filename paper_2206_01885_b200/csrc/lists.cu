@@ -40,9 +40,12 @@ constexpr int kTravThreads = 256, kTravIPT = 8, kTravTile = kTravThreads * kTrav
 // Sharded builds: a rank keeps only the pairs whose row node it needs -- every node above the cut
 // level, and its own contiguous range at each level >= cut (shard.cu).  The children of a dropped
 // row are never needed either, so the frontier it would have grown is dropped with it.
+// Nearfield rows are needed only by the rank that stores them (a leaf whose first point lies in its
+// point range [p_lo, p_hi), fill.cu), also above the cut.
 struct RowFilter {
-  int on, cut;
+  int on, cut, p_lo, p_hi;
   int lo[32], hi[32];
+  const int* nbegin;
 };
 
 __device__ __forceinline__ void trav_classify(const int2 pr, const int* __restrict__ cell, int nnodes, int d,
@@ -59,7 +62,7 @@ __device__ __forceinline__ void trav_classify(const int2 pr, const int* __restri
     a = 1;
   } else {
     const int li = is_leaf[i], lj = is_leaf[j];
-    if (li && lj) b = 1;
+    if (li && lj) b = !rf.on || (rf.nbegin[i] >= rf.p_lo && rf.nbegin[i] < rf.p_hi);
     else c = (long long)(li ? 1 : nchild[i]) * (lj ? 1 : nchild[j]);
   }
 }
@@ -291,6 +294,9 @@ void build_lists(h2_handle* h) {
     if (h->depth >= 32) throw Error{H2_ERR_INTERNAL, "sharded lists: depth beyond the row filter"};
     rf.on = 1;
     rf.cut = h->cut;
+    rf.p_lo = h->p_lo;
+    rf.p_hi = h->p_hi;
+    rf.nbegin = h->nbegin;
     for (int l = 0; l <= h->depth; l++) {
       const LevelRange lr = level_range(h, l);
       rf.lo[l] = lr.begin;

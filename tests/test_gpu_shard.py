@@ -134,13 +134,17 @@ def test_sharded_equals_single_gpu(cfg, n, q, R):
         assert all(np.array_equal(a, b) for a, b in zip(slots(g, "SK"), sk_ref))
         ys, U = slots(g, "YS"), u_blocks(g)
         # a4 sharded: the rank's lists are the single-GPU lists restricted to the rows it needs
-        # (every node above the cut, its own range below); the other rows are empty
+        # (interaction lists: every node above the cut and its own range below; nearfield lists: the
+        # leaves whose first point lies in its point range); the other rows are empty
+        nodes_ = ref.export("NODES").reshape(-1, 7)
         for nm in ("IL", "NF"):
             mine, full = slots(g, nm), slots(ref, nm)
             need = np.zeros(info["nnodes"], bool)
             for lvl in range(depth + 1):
                 lo, hi = rng[lvl]
                 need[lo:hi] = True
+            if nm == "NF":
+                need = (nodes_[:, 1] >= sh[3]) & (nodes_[:, 1] < sh[4])
             for i in range(info["nnodes"]):
                 assert np.array_equal(mine[i], full[i] if need[i] else full[i][:0]), (nm, r, i)
         for lvl in range(depth + 1):
