@@ -119,6 +119,9 @@ typedef struct h2_options {
   int32_t nonsymmetric;    /* 1: the non-symmetric path (row AND column bases, every ordered block)  */
                            /*    for any kernel -- for a symmetric one it reproduces V = U,          */
                            /*    X^(col) = X^(row) bit for bit; H2_KERNEL_MQSHIFT implies it         */
+  double srrqr_f;          /* > 0 (>= 1): strong rank-revealing refinement of every ID:  */
+                           /*    Gu-Eisenstat swaps at fixed rank until max |G| <= srrqr_f; 0 = the  */
+                           /*    plain column-pivoted QR (reading F1).  < 0 or in (0, 1): INVALID_ARG */
 } h2_options;
 
 /* ---- DataReduct of HiDR (h2_options.reduct) ---------------------------------------------------- */
@@ -229,6 +232,7 @@ typedef struct h2_info_t {
   int64_t hidr_up_evals;                     /* the bottom-up sweep's share of hidr_dist_evals     */
   int32_t nonsymmetric;                      /* 1: separate column bases, every ordered block      */
   int32_t kmax_col;                          /* max column skeleton size (non-symmetric path)      */
+  int64_t srrqr_swaps;                       /* SRRQR swaps made (h2_options.srrqr_f > 0)          */
 } h2_info_t;
 
 int h2_info(const h2_handle* h, h2_info_t* out);

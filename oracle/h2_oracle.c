@@ -332,18 +332,19 @@ int orc_srrqr_swaps(const double* M0, double* Mout, int rows, int cols, int k, d
   int swaps = 0;
   double* v = (double*)malloc(sizeof(double) * (size_t)rows);
   for (;;) {
-    double best = f;
+    /* the largest |T_tc| > f; ties -> the lowest original column index, then the lowest t */
+    double best = -1.0;
     int bi = -1, bj = -1;
     for (int c = k; c < cols; c++)
       for (int t = 0; t < k; t++) {
         double a = fabs(Mout[t + (int64_t)rows * c]);
-        if (a > best) {
+        if (a > f && (a > best || (a == best && (piv[c] < piv[bj] || (piv[c] == piv[bj] && t < bi))))) {
           best = a;
           bi = t;
           bj = c;
         }
       }
-    if (bi < 0 || swaps >= 64 * k) break;
+    if (bj < 0 || swaps >= 64 * k) break;
     int tp = piv[bi];
     piv[bi] = piv[bj];
     piv[bj] = tp;

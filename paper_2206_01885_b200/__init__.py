@@ -40,7 +40,7 @@ class h2_options(C.Structure):
     _fields_ = [("r_override", C.c_int32), ("storage", C.c_int32), ("mem_budget_bytes", C.c_int64),
                 ("stream", C.c_void_p), ("points_on_host", C.c_int32), ("timing", C.c_int32),
                 ("hidr_brute", C.c_int32), ("comm", C.c_void_p), ("serial_fill", C.c_int32),
-                ("reduct", C.c_int32), ("nonsymmetric", C.c_int32)]
+                ("reduct", C.c_int32), ("nonsymmetric", C.c_int32), ("srrqr_f", C.c_double)]
 
 
 class h2_info_t(C.Structure):
@@ -50,7 +50,8 @@ class h2_info_t(C.Structure):
                 ("stored_bytes", C.c_int64), ("coupling_stored", C.c_int32), ("nearfield_stored", C.c_int32),
                 ("hidr_dist_evals", C.c_int64), ("id_kernel_evals", C.c_int64), ("kmax", C.c_int32),
                 ("gpu_launches", C.c_int32), ("stage_ms", C.c_float * 9), ("hidr_dist_done", C.c_int64),
-                ("hidr_up_evals", C.c_int64), ("nonsymmetric", C.c_int32), ("kmax_col", C.c_int32)]
+                ("hidr_up_evals", C.c_int64), ("nonsymmetric", C.c_int32), ("kmax_col", C.c_int32),
+                ("srrqr_swaps", C.c_int64)]
 
 
 STAGES = ["tree", "lists", "calibrate", "hidr_up", "hidr_down", "id_sweep", "coupling_fill", "nearfield_fill",
@@ -271,9 +272,11 @@ class H2Matrix:
     def __init__(self, points, kernel_id: int, kernel_params=(), id_tol: float = 1e-6, leaf_size: int = 64,
                  admissibility: float = 0.5, r: int = 0, storage: int = H2_STORE_AUTO, stream=None,
                  timing: bool = False, mem_budget_bytes: int = 0, hidr_brute: bool = False,
-                 comm: H2Comm | None = None, reduct: int = H2_REDUCT_VOLUME, nonsymmetric: bool = False):
+                 comm: H2Comm | None = None, reduct: int = H2_REDUCT_VOLUME, nonsymmetric: bool = False,
+                 srrqr_f: float = 0.0):
         import torch
         o = h2_options_default()
+        o.srrqr_f = float(srrqr_f)
         o.reduct = int(reduct)
         o.nonsymmetric = int(bool(nonsymmetric))
         if comm is not None:

@@ -182,7 +182,8 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
   if ((!points && !base) || n < 1 || n >= (1LL << 31) - 1 || d < 1 || d > kMaxD || leaf_size < 1 || !(admissibility > 0.0) ||
       !(admissibility <= 0.7) || !(id_tol > 0.0) || !(id_tol < 1.0) || o.r_override < 0 || o.r_override > 4096 ||
       o.storage < 0 || o.storage > 2 || o.reduct < H2_REDUCT_VOLUME || o.reduct > H2_REDUCT_SURFACE ||
-      (o.reduct == H2_REDUCT_SURFACE && d != 2 && d != 3)) {
+      (o.reduct == H2_REDUCT_SURFACE && d != 2 && d != 3) || !(o.srrqr_f == 0.0 || o.srrqr_f >= 1.0) ||
+      !std::isfinite(o.srrqr_f)) {
     set_error(H2_ERR_INVALID_ARG, "invalid argument (n, d, leaf_size, admissibility, id_tol or options)");
     return nullptr;
   }
@@ -216,6 +217,7 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
   h->kp = kp;
   std::memcpy(h->kpa, kpa, sizeof(kpa));
   h->nonsym = o.nonsymmetric || kernel_id == H2_KERNEL_MQSHIFT;
+  h->srrqr_f = o.srrqr_f;
   h->id_tol = id_tol;
   h->q = leaf_size;
   h->tau = admissibility;
@@ -428,6 +430,7 @@ int h2_info(const h2_handle* h, h2_info_t* out) {
   out->hidr_up_evals = h->hidr_up_evals;
   out->nonsymmetric = h->nonsym;
   out->kmax_col = h->kmax_col;
+  out->srrqr_swaps = h->srrqr_swaps;
   out->id_kernel_evals = h->id_kernel_evals;
   out->kmax = h->kmax;
   out->gpu_launches = h->gpu_launches;

@@ -909,6 +909,7 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
       cudaEventDestroy(cl_done);
     }
     h->gpu_launches += 2;
+    srrqr_level(h, base, count, Xf, U);  // h2_options.srrqr_f > 0: SRRQR swaps (srrqr.cu)
     uused += tot[1];  // u_off[] holds global offsets into the arena
   }
   if (!exchanged) exchange_slots(h, h->k, h->sk);

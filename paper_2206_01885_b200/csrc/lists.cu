@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kTravThreads) trav_emit_kernel(
       il[il_base + oa] = ((unsigned long long)i << 32) | (unsigned)j;
     } else if (cb[k]) {
       nl[nl_base + ob] = ((unsigned long long)i << 32) | (unsigned)j;
-    } else {
+    } else if (cc[k]) {  // (a pair a sharded rank drops has no output at all)
       const int li = is_leaf[i], lj = is_leaf[j];
       const int ci = li ? 1 : nchild[i], cj = lj ? 1 : nchild[j];
       const int fi = li ? i : first_child[i], fj = lj ? j : first_child[j];
