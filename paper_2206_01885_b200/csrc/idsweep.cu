@@ -12,6 +12,7 @@
 
 #include "cpqr.cuh"
 #include "cpqr_panel.cuh"
+#include "id_warp.cuh"
 
 namespace h2 {
 
@@ -103,7 +104,8 @@ __global__ void id_sizes_kernel(int base, int count, int d, const int* __restric
                                 const int* __restrict__ nend, const int* __restrict__ first_child,
                                 const int* __restrict__ nchild, const int* __restrict__ ys_cnt,
                                 const int* __restrict__ k, int* xbar_n, int* child_off, int64_t* wsz, int64_t* usz,
-                                int* smax, int cs, int64_t cl_min, int* cl_cnt, int* cl_list, int* id_path) {
+                                int* smax, int cs, int64_t cl_min, int* cl_cnt, int* cl_list, int* id_path,
+                                int warp_level, int* wp_cnt, int* wp_list) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t > count) return;
   if (t == count) {
@@ -126,6 +128,15 @@ __global__ void id_sizes_kernel(int base, int count, int d, const int* __restric
   if (ny == 0) nx = 0;
   xbar_n[i] = nx;
   int mn = nx < ny ? nx : ny;
+  // levels with many nodes: the small ones take the warp-per-node path (id_warp.cuh)
+  if (warp_level && nx > 0 && nx <= 32 * kIdWarpMaxCols && id_warp_bytes(ny, nx) <= kIdWarpMaxBytes) {
+    wp_list[atomicAdd(wp_cnt, 1)] = t;
+    atomicMax(wp_cnt + 1, (int)id_warp_bytes(ny, nx));
+    id_path[i] = 11;
+    wsz[t] = 0;
+    usz[t] = (int64_t)nx * mn;
+    return;
+  }
   // workspace: M (ny*nx doubles) + nrm2 (nx) + v (ny) + piv/xbar (2*nx ints, as doubles)
   const int cls = id_smem_class(ny, nx, d);
   const bool big = nx > 0 && id_big(ny, nx, d, cs, cl_min);
@@ -138,7 +149,8 @@ __global__ void id_sizes_kernel(int base, int count, int d, const int* __restric
          : nx > 0 && cls < 0 ? (int64_t)ny * nx + kIdPanelNb * nx + nx + ny + nx + 2 : 0;
   usz[t] = (int64_t)nx * mn;
   // the code path (H2_EXPORT_ID_PATH): 0..6 staged shared-memory classes, 7 lean class, 8 global
-  // memory (256 threads), 9 global memory (1024 threads), 10 thread-block cluster, -1 none
+  // memory (256 threads), 9 global memory (1024 threads), 10 thread-block cluster, 11 warp per node,
+  // -1 none
   id_path[i] = nx == 0 ? -1 : big ? 10 : cls >= 0 ? cls : (8LL * nx * ny < kIdBigBlock ? 8 : 9);
   if (nx > 0 && cls >= 0) {
     atomicMax(smax + cls, (int)(cls == kIdLean ? id_lean_request(ny, nx, d) : id_smem_bytes(ny, nx, d)));
@@ -155,7 +167,7 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
     const int* __restrict__ nchild, const int* __restrict__ ys_cnt, const int* __restrict__ ys,
     const int* __restrict__ xbar_n, const int64_t* __restrict__ woff, double* work, const int64_t* __restrict__ uoff,
     double* U, int* kout, int* sk, unsigned long long* evals, int64_t min_block, int64_t max_block, int cs,
-    int64_t cl_min, int use_panel) {
+    int64_t cl_min, int use_panel, const int* __restrict__ id_path) {
   __shared__ CpqrSmem<kIdThreads> csm;
   constexpr int kNbG = kIdThreads >= 1024 ? 4 : kIdPanelNb;  // (64 registers per thread at 1024)
   __shared__ PanelSmem<kIdThreads, kNbG> psm;
@@ -171,6 +183,7 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
     if (tid == 0) kout[i] = 0;
     return;
   }
+  if (id_path[i] == 11) return;  // id_kernel_warp
   if (id_smem_class(ny, nx, d) >= 0 || id_big(ny, nx, d, cs, cl_min)) return;  // id_kernel_smem / _cluster
   const int64_t blk = 8LL * nx * ny;
   if (blk < min_block || blk >= max_block) return;  // the other thread-count variant
@@ -502,7 +515,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : (PANEL ? 6 : 8)) id_kernel
     const int* __restrict__ is_leaf, const int* __restrict__ nbegin, const int* __restrict__ first_child,
     const int* __restrict__ nchild, const int* __restrict__ ys_cnt, const int* __restrict__ ys,
     const int* __restrict__ xbar_n, const int64_t* __restrict__ uoff, double* U, int* kout, int* sk,
-    unsigned long long* evals, int cls, int use_panel) {
+    unsigned long long* evals, int cls, int use_panel, const int* __restrict__ id_path) {
   extern __shared__ double sh[];
   __shared__ PanelSmem<NT, PANEL ? kIdPanelNb : 1> psm;
   __shared__ CpqrSmem<NT> csm_cm;
@@ -512,7 +525,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : (PANEL ? 6 : 8)) id_kernel
   const int nx = xbar_n[i];
   const int ny = ys_cnt[i];
   const int tid = threadIdx.x;
-  if (nx == 0) return;
+  if (nx == 0 || id_path[i] == 11) return;  // (id_kernel_warp's nodes)
   {  // cls < 0: every node of the staged classes (merged launch)
     const int nc = id_smem_class(ny, nx, D);
     if (kLean ? nc != kIdLean : (nc < 0 || nc == kIdLean || (cls >= 0 && nc != cls))) return;
@@ -697,6 +710,10 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
     const char* e = getenv("H2_ID_PANEL");  // panel CPQR: 1 staged, 2 lean, 4 global memory
     return e ? atoi(e) : 3;
   }();
+  static const int warp_min = [] {  // H2_ID_WARP_MIN (tuning knob): levels with at least this many
+    const char* e = getenv("H2_ID_WARP_MIN");  // nodes use the warp-per-node path (0: never)
+    return e ? atoi(e) : 0;
+  }();
   static const int64_t cl_min = [] {  // H2_ID_CLMIN (tuning knob): cluster-path threshold, block entries
     const char* e = getenv("H2_ID_CLMIN");
     return e ? (int64_t)atoll(e) : (int64_t)256 * 1024;
@@ -740,10 +757,15 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
     int* cl_cnt = clw.as<int>();
     int* cl_list = cl_cnt + 1;
     H2_CUDA_TRY(cudaMemsetAsync(cl_cnt, 0, sizeof(int), s));
+    Scratch wpw(sizeof(int) * (2 + (size_t)count), s);  // warp-path node count, slot bytes, list
+    int* wp_cnt = wpw.as<int>();
+    int* wp_list = wp_cnt + 2;
+    H2_CUDA_TRY(cudaMemsetAsync(wp_cnt, 0, 2 * sizeof(int), s));
+    const int warp_level = warp_min > 0 && count >= warp_min;
     id_sizes_kernel<<<(count + 1 + 255) / 256, 256, 0, s>>>(base, count, h->d, h->is_leaf, h->nbegin, h->nend,
                                                             h->first_child, h->nchild, h->ys_cnt, h->k, h->xbar_n,
                                                             h->child_off, wsz, usz, smax, cs, cl_min, cl_cnt, cl_list,
-                                                            h->id_path);
+                                                            h->id_path, warp_level, wp_cnt, wp_list);
     scan_excl_i64(wsz, woff, count + 1, s);
     scan_excl_i64(usz, uo, count + 1, s);
     H2_CHECK_LAUNCH();
@@ -753,8 +775,9 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[1], uo + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaMemcpyAsync(smem_bytes, smax, kSmaxN * sizeof(int), cudaMemcpyDeviceToHost, s));
     const int* kinds = smem_bytes + kIdClasses + 2;
-    int ncl = 0;
+    int ncl = 0, wph[2] = {0, 0};
     H2_CUDA_TRY(cudaMemcpyAsync(&ncl, cl_cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+    H2_CUDA_TRY(cudaMemcpyAsync(wph, wp_cnt, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaStreamSynchronize(s));
     if (uused + tot[1] > ucap) {
       int64_t nc = uused + tot[1];
@@ -810,12 +833,12 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
       id_kernel<256><<<count, 256, 0, sa>>>(base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf,
                                            h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
                                            work.as<double>(), h->u_off + base, U, h->k, h->sk,
-                                           ev.as<unsigned long long>(), 0, kIdBigBlock, cs, cl_min, use_panel);
+                                           ev.as<unsigned long long>(), 0, kIdBigBlock, cs, cl_min, use_panel, h->id_path);
       id_kernel<1024><<<count, 1024, 0, sb>>>(base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf,
                                              h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
                                              work.as<double>(), h->u_off + base, U, h->k, h->sk,
                                              ev.as<unsigned long long>(), kIdBigBlock, INT64_MAX, cs, cl_min,
-                                             use_panel);
+                                             use_panel, h->id_path);
       H2_CHECK_LAUNCH();
       H2_CUDA_TRY(cudaEventRecord(gev[1], sa));
       H2_CUDA_TRY(cudaEventRecord(gev[2], sb));
@@ -876,7 +899,7 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
         base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child,          \
         h->nchild,                                                                                              \
         h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>(), cls,         \
-        use_panel);                                                                                             \
+        use_panel, h->id_path);                                                                                 \
   } while (0)
 #define H2_ID_CASE(DD)                                                                                          \
   case DD:                                                                                                      \
@@ -896,6 +919,27 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
         H2_CHECK_LAUNCH();
         h->gpu_launches += 1;
       }
+    }
+    if (wph[0] > 0) {  // the warp-per-node path, on the main stream concurrently with the class launches
+      const int slot = (wph[1] + 7) / 8;
+      const int smem = (int)(sizeof(double) * (size_t)slot * kIdWarpPerCta);
+      const unsigned g = (unsigned)((wph[0] + kIdWarpPerCta - 1) / kIdWarpPerCta);
+      switch (h->d) {
+#define H2_IDW_CASE(DD)                                                                                         \
+  case DD:                                                                                                      \
+    H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_warp<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                                     kIdWarpPerCta * kIdWarpMaxBytes + 64));                                    \
+    id_kernel_warp<DD><<<g, 32 * kIdWarpPerCta, smem, s>>>(                                                    \
+        base, wp_list, wph[0], slot, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->r, h->is_leaf, h->nbegin,      \
+        h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk,              \
+        ev.as<unsigned long long>());                                                                          \
+    break;
+        H2_IDW_CASE(1) H2_IDW_CASE(2) H2_IDW_CASE(3) H2_IDW_CASE(4)
+        H2_IDW_CASE(5) H2_IDW_CASE(6) H2_IDW_CASE(7) H2_IDW_CASE(8)
+#undef H2_IDW_CASE
+      }
+      H2_CHECK_LAUNCH();
+      h->gpu_launches += 1;
     }
     if (fan) {
       for (int a = 0; a < h2_handle::kAux && a < used; a++) {
