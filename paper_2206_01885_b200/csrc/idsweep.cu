@@ -105,7 +105,7 @@ __global__ void id_sizes_kernel(int base, int count, int d, const int* __restric
                                 const int* __restrict__ nchild, const int* __restrict__ ys_cnt,
                                 const int* __restrict__ k, int* xbar_n, int* child_off, int64_t* wsz, int64_t* usz,
                                 int* smax, int cs, int64_t cl_min, int* cl_cnt, int* cl_list, int* id_path,
-                                int warp_level, int* wp_cnt, int* wp_list) {
+                                int warp_level, int* wp_cnt, int* wp_list, int* lcnt, int* lists) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t > count) return;
   if (t == count) {
@@ -155,7 +155,15 @@ __global__ void id_sizes_kernel(int base, int count, int d, const int* __restric
   if (nx > 0 && cls >= 0) {
     atomicMax(smax + cls, (int)(cls == kIdLean ? id_lean_request(ny, nx, d) : id_smem_bytes(ny, nx, d)));
     // which instantiations the class needs: bit 0 unblocked / row-major nodes, bit 1 panel nodes
-    atomicOr(smax + kIdClasses + 2 + cls, id_panel(ny, nx, cls == kIdLean ? kIdLeanThreads : kIdSmemThreads) ? 2 : 1);
+    const int pk = id_panel(ny, nx, cls == kIdLean ? kIdLeanThreads : kIdSmemThreads) ? 1 : 0;
+    atomicOr(smax + kIdClasses + 2 + cls, pk ? 2 : 1);
+    // the launch lists: per (class, kind), and per kind over all staged classes (merged launch)
+    const int li = cls * 2 + pk;
+    lists[(int64_t)li * count + atomicAdd(lcnt + li, 1)] = t;
+    if (cls < kIdClasses) {
+      const int lm = 2 * (kIdClasses + 1) + pk;
+      lists[(int64_t)lm * count + atomicAdd(lcnt + lm, 1)] = t;
+    }
   }
 }
 
@@ -484,17 +492,15 @@ __global__ void __launch_bounds__(kIdClThreads) id_kernel_cluster(
   __syncthreads();
   // outputs: skeleton (pivot order), U (nx x k column-major): identity rows of the skeleton, T for
   // the others
+  // every CTA writes the rows of its own columns (coalesced along them): the identity for the
+  // skeleton columns, T for the others
   double* Ui = U + uoff[t];
-  if (q == 0) {
+  if (q == 0)
     for (int a = tid; a < k; a += NT) sk[(int64_t)i * r + a] = xb[col_at[a]];
-    for (int e = tid; e < k * k; e += NT) {
-      const int a = e % k, tt = e / k;
-      Ui[col_at[a] + (int64_t)nx * tt] = a == tt ? 1.0 : 0.0;
-    }
-  }
   for (int e = tid; e < wl * k; e += NT) {
     const int jl = e % wl, tt = e / wl;
-    if (pos[jl] >= k) Ui[j0 + jl + (int64_t)nx * tt] = Mq[(int64_t)ny * jl + tt];
+    const int ps = pos[jl];
+    Ui[j0 + jl + (int64_t)nx * tt] = ps < k ? (ps == tt ? 1.0 : 0.0) : Mq[(int64_t)ny * jl + tt];
   }
   if (q == 0 && tid == 0) {
     kout[i] = k;
@@ -515,13 +521,15 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : (PANEL ? 6 : 8)) id_kernel
     const int* __restrict__ is_leaf, const int* __restrict__ nbegin, const int* __restrict__ first_child,
     const int* __restrict__ nchild, const int* __restrict__ ys_cnt, const int* __restrict__ ys,
     const int* __restrict__ xbar_n, const int64_t* __restrict__ uoff, double* U, int* kout, int* sk,
-    unsigned long long* evals, int cls, int use_panel, const int* __restrict__ id_path) {
+    unsigned long long* evals, int cls, int use_panel, const int* __restrict__ id_path,
+    const int* __restrict__ list) {
   extern __shared__ double sh[];
   __shared__ PanelSmem<NT, PANEL ? kIdPanelNb : 1> psm;
   __shared__ CpqrSmem<NT> csm_cm;
   __shared__ CpqrRmSmem<NT> csm;
   constexpr bool kLean = NT == kIdLeanThreads;
-  const int i = base + blockIdx.x;
+  const int tn = list[blockIdx.x];  // the launch's node list (id_sizes_kernel: this class and kind)
+  const int i = base + tn;
   const int nx = xbar_n[i];
   const int ny = ys_cnt[i];
   const int tid = threadIdx.x;
@@ -632,7 +640,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : (PANEL ? 6 : 8)) id_kernel
       k = cta_cpqr<NT>(M, ny, nx, tol, piv, nrm2, v, csm_cm);
     }
   }
-  double* Ui = U + uoff[blockIdx.x];
+  double* Ui = U + uoff[tn];
   for (int a = tid; a < k; a += NT) sk[(int64_t)i * r + a] = xb[piv[a]];
   // T of position c: in physical column piv[c] (panel: columns never move) or c (swapped columns)
   for (int e = tid; e < nx * k; e += NT) {
@@ -757,6 +765,11 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
     int* cl_cnt = clw.as<int>();
     int* cl_list = cl_cnt + 1;
     H2_CUDA_TRY(cudaMemsetAsync(cl_cnt, 0, sizeof(int), s));
+    constexpr int kNLists = 2 * (kIdClasses + 1) + 2;  // (class, kind) lists + merged staged lists
+    Scratch lw(sizeof(int) * (kNLists + (size_t)kNLists * count), s);
+    int* lcnt = lw.as<int>();
+    int* lists = lcnt + kNLists;
+    H2_CUDA_TRY(cudaMemsetAsync(lcnt, 0, sizeof(int) * kNLists, s));
     Scratch wpw(sizeof(int) * (2 + (size_t)count), s);  // warp-path node count, slot bytes, list
     int* wp_cnt = wpw.as<int>();
     int* wp_list = wp_cnt + 2;
@@ -765,7 +778,7 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
     id_sizes_kernel<<<(count + 1 + 255) / 256, 256, 0, s>>>(base, count, h->d, h->is_leaf, h->nbegin, h->nend,
                                                             h->first_child, h->nchild, h->ys_cnt, h->k, h->xbar_n,
                                                             h->child_off, wsz, usz, smax, cs, cl_min, cl_cnt, cl_list,
-                                                            h->id_path, warp_level, wp_cnt, wp_list);
+                                                            h->id_path, warp_level, wp_cnt, wp_list, lcnt, lists);
     scan_excl_i64(wsz, woff, count + 1, s);
     scan_excl_i64(usz, uo, count + 1, s);
     H2_CHECK_LAUNCH();
@@ -775,7 +788,8 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
     H2_CUDA_TRY(cudaMemcpyAsync(&tot[1], uo + count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaMemcpyAsync(smem_bytes, smax, kSmaxN * sizeof(int), cudaMemcpyDeviceToHost, s));
     const int* kinds = smem_bytes + kIdClasses + 2;
-    int ncl = 0, wph[2] = {0, 0};
+    int ncl = 0, wph[2] = {0, 0}, lc[kNLists];
+    H2_CUDA_TRY(cudaMemcpyAsync(lc, lcnt, sizeof(int) * kNLists, cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaMemcpyAsync(&ncl, cl_cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaMemcpyAsync(wph, wp_cnt, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     H2_CUDA_TRY(cudaStreamSynchronize(s));
@@ -882,6 +896,10 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
         for (int c2 = 0; c2 < kIdClasses; c2++) kind |= kinds[c2];
       for (int pv = 0; pv < 2; pv++) {
         if (!(kind & (1 << pv))) continue;
+        const int lid = cls >= 0 ? cls * 2 + pv : 2 * (kIdClasses + 1) + pv;
+        const int nlaunch = lc[lid];
+        if (nlaunch == 0) continue;
+        const int* llist = lists + (int64_t)lid * count;
         cudaStream_t cs = s;
         if (fan) {
           const int a = used % h2_handle::kAux;
@@ -895,11 +913,11 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
   do {                                                                                                          \
     H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_smem<DD, NTT, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                      MAXS));                                                                    \
-    id_kernel_smem<DD, NTT, PV><<<count, NTT, smem, cs>>>(                                                       \
+    id_kernel_smem<DD, NTT, PV><<<nlaunch, NTT, smem, cs>>>(                                                     \
         base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf, h->nbegin, h->first_child,          \
         h->nchild,                                                                                              \
         h->ys_cnt, h->ys, h->xbar_n, h->u_off + base, U, h->k, h->sk, ev.as<unsigned long long>(), cls,         \
-        use_panel, h->id_path);                                                                                 \
+        use_panel, h->id_path, llist);                                                                          \
   } while (0)
 #define H2_ID_CASE(DD)                                                                                          \
   case DD:                                                                                                      \
