@@ -7,10 +7,12 @@
 // budget is the first m^d with e < 1e-2 eps, or m^d >= 256 (pass-through); r = max over levels.
 // All (level, m) trials run as one batched launch: one CTA per trial.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "cpqr.cuh"
+#include "cpqr_panel.cuh"
 #include "vol.cuh"
 
 namespace h2 {
@@ -25,6 +27,7 @@ struct CalWork {  // per-trial global workspace
   double nrm2[N], v[N];
   int piv[N], sel[N];
   int ns, k;  // |Z2^*| and the ID rank, passed between the trial's launches
+  int panel;  // 1: the panel CPQR ran (columns never moved: position c is physical column piv[c])
   double pnum[8], pden[8];  // the error's partial sums per column slice (calib_err_kernel)
 };
 constexpr int kErrSlices = 8;  // CTAs per trial of the error evaluation: N / 8 = 32 columns each
@@ -125,13 +128,23 @@ __global__ void __launch_bounds__(kCalThreads) calib_prep_kernel(int kid, double
 }
 
 constexpr int kCalCpqrThreads = 1024;
-__global__ void __launch_bounds__(kCalCpqrThreads) calib_cpqr_kernel(double eps, CalWork* work) {
+constexpr int kCalPanelNb = 8;
+// the trial's ID: the panel-blocked CPQR (cpqr_panel.cuh; 4 threads per column of the 256 Z1
+// candidates) or, with H2_CAL_PANEL=0, the unblocked one (cpqr.cuh)
+__global__ void __launch_bounds__(kCalCpqrThreads) calib_cpqr_kernel(double eps, int use_panel, CalWork* work) {
   __shared__ CpqrSmem<kCalCpqrThreads> csm;
+  __shared__ PanelSmem<kCalCpqrThreads, kCalPanelNb> psm;
   __shared__ double sv[N];
+  __shared__ double Fs[kCalPanelNb * N];
   CalWork& W = work[blockIdx.x];
   if (W.ns < 0) return;  // skipped trial
-  const int k = cta_cpqr<kCalCpqrThreads>(W.M, W.ns, N, 1e-3 * eps, W.piv, W.nrm2, sv, csm);
-  if (threadIdx.x == 0) W.k = k;
+  const int k = use_panel ? cta_cpqr_panel<kCalCpqrThreads, kCalPanelNb, 1>(W.M, W.ns, W.ns, N, 1e-3 * eps, 4, W.piv,
+                                                                            Fs, psm)
+                          : cta_cpqr<kCalCpqrThreads>(W.M, W.ns, N, 1e-3 * eps, W.piv, W.nrm2, sv, csm);
+  if (threadIdx.x == 0) {
+    W.k = k;
+    W.panel = use_panel;
+  }
 }
 
 // Ks[t][e] = K(Z1[piv[t]], Z2[e]) for the k skeleton rows
@@ -182,7 +195,7 @@ __global__ void __launch_bounds__(kCalThreads) calib_err_kernel(int kid, double 
     for (int t = 0; t < k; t++) {
       double tm[CPW], ks[EPL];
 #pragma unroll
-      for (int j = 0; j < CPW; j++) tm[j] = W.M[t + ns * (c0 + j)];
+      for (int j = 0; j < CPW; j++) tm[j] = W.M[t + ns * (W.panel ? W.piv[c0 + j] : c0 + j)];
 #pragma unroll
       for (int u = 0; u < EPL; u++) ks[u] = W.Ks[t * N + lane + 32 * u];
 #pragma unroll
@@ -251,6 +264,15 @@ static char* pinned_slot(int slot, size_t bytes) {
   return p[slot];
 }
 
+// H2_CAL_PANEL=0 (A/B knob, read once): the unblocked CPQR in the calibration trials
+static int cal_panel() {
+  static const int v = [] {
+    const char* e = getenv("H2_CAL_PANEL");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 // One batch of (level, m) trials on stream s; the per-trial pass flags land in job.pass_h
 // (page-locked) once the stream has reached the end of the batch.
 static void launch_trials(h2_handle* h, cudaStream_t s, int slot, const std::vector<double>& wl,
@@ -285,7 +307,7 @@ static void launch_trials(h2_handle* h, cudaStream_t s, int slot, const std::vec
   case DD:                                                                                                \
     calib_prep_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, h->tau, dw + b0, dl + b0, dm + b0,         \
                                                      skip_level, sh, job.work.as<CalWork>());              \
-    calib_cpqr_kernel<<<nb, kCalCpqrThreads, 0, s>>>(h->id_tol, job.work.as<CalWork>());                  \
+    calib_cpqr_kernel<<<nb, kCalCpqrThreads, 0, s>>>(h->id_tol, cal_panel(), job.work.as<CalWork>());     \
     calib_ks_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, job.work.as<CalWork>());                    \
     calib_err_kernel<DD><<<nb * kErrSlices, kCalThreads, 0, s>>>(h->kid, p2, job.work.as<CalWork>());        \
     break;
