@@ -167,6 +167,9 @@ __global__ void id_sizes_kernel(int base, int count, int d, const int* __restric
   }
 }
 
+// dynamic shared memory of the global-memory path: F of the panel CPQR (NB x nx, nx <= NT RMAX / 4)
+constexpr int kIdGlobalFs = 4096;
+
 template <int kIdThreads>
 __global__ void __launch_bounds__(kIdThreads) id_kernel(
     int base, int kid, double p2, double tol, const double* __restrict__ Xf, const double* __restrict__ X, int64_t n,
@@ -202,8 +205,9 @@ __global__ void __launch_bounds__(kIdThreads) id_kernel(
   const int G = Gp < 4 ? 4 : Gp;
   const bool panel = (use_panel & 4) && (int64_t)nx * G <= (int64_t)kIdThreads * kRmaxG;
   double* M = work + woff[t];
-  double* Fs = M + (int64_t)ny * nx;
-  double* nrm2 = Fs + kIdPanelNb * nx;
+  // the panel's delayed-update coefficients in shared memory (kIdGlobalFs doubles: nx <= NT RMAX / 4)
+  extern __shared__ double Fs[];
+  double* nrm2 = M + (int64_t)ny * nx + kIdPanelNb * nx;
   double* v = nrm2 + nx;
   int* piv = reinterpret_cast<int*>(v + ny);
   int* xb = piv + nx;
@@ -844,11 +848,11 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
       H2_CUDA_TRY(cudaEventRecord(gev[0], s));
       H2_CUDA_TRY(cudaStreamWaitEvent(sa, gev[0], 0));
       H2_CUDA_TRY(cudaStreamWaitEvent(sb, gev[0], 0));
-      id_kernel<256><<<count, 256, 0, sa>>>(base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf,
+      id_kernel<256><<<count, 256, sizeof(double) * kIdGlobalFs, sa>>>(base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf,
                                            h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
                                            work.as<double>(), h->u_off + base, U, h->k, h->sk,
                                            ev.as<unsigned long long>(), 0, kIdBigBlock, cs, cl_min, use_panel, h->id_path);
-      id_kernel<1024><<<count, 1024, 0, sb>>>(base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf,
+      id_kernel<1024><<<count, 1024, sizeof(double) * kIdGlobalFs, sb>>>(base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf,
                                              h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
                                              work.as<double>(), h->u_off + base, U, h->k, h->sk,
                                              ev.as<unsigned long long>(), kIdBigBlock, INT64_MAX, cs, cl_min,

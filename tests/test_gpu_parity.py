@@ -268,8 +268,6 @@ def test_parity_bench_config_full_size():
 @pytest.mark.slow
 @pytest.mark.parametrize("cfg", [2, 3, 5])
 def test_parity_full_size_other_configs(cfg):
-    if cfg == 5 and not os.environ.get("H2_RUN_VERYSLOW"):
-        pytest.skip("configs[4] at full size: ~6 min of oracle (H2_RUN_VERYSLOW=1; log in profiles/)")
     """BASELINE configs[1] (1M cube, Coulomb 1e-8), configs[2] (262k sphere, Gaussian) and configs[4]
     (262k 5-D mixture, Gaussian 1e-4) at full size: bit-exact structure and r, skeleton agreement,
     sampled-row matvec.  configs[1] and [4] need ~178 / ~198 GB of blocks, more than one GPU holds,
