@@ -289,7 +289,7 @@ def run_ours(args):
         import torch.distributed as dist
         uid = [P.H2Comm.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        comm = P.H2Comm.nccl(ws, rank, uid[0])
+        comm = P.H2Comm.nccl(ws, rank, uid[0], device=local)
     stream = torch.cuda.Stream()
     kp = list(c["params"])
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")

@@ -197,7 +197,10 @@ const char* h2_last_error_message(void);
  * All return NULL / an H2_ERR_* code on failure (h2_last_error).                                   */
 typedef struct h2_comm h2_comm;
 int h2_comm_nccl_unique_id(unsigned char id[128]);
-h2_comm* h2_comm_init_nccl(int32_t nranks, int32_t rank, const unsigned char id[128]);
+h2_comm* h2_comm_init_nccl(int32_t nranks, int32_t rank, const unsigned char id[128]);  /* current device */
+/* the same on `device`, which becomes (and stays) the calling thread's current device: every later
+ * build / matvec on this comm must run with it current (NCCL binds a communicator to one device) */
+h2_comm* h2_comm_init_nccl_dev(int32_t nranks, int32_t rank, const unsigned char id[128], int32_t device);
 h2_comm* h2_comm_init_local(int32_t nranks, int32_t rank, int64_t group_key);
 void h2_comm_free(h2_comm* comm);  /* NULL-safe; after every handle built on it is freed */
 int32_t h2_comm_size(const h2_comm* comm);

@@ -32,7 +32,7 @@ _EXPORT_DTYPE = dict(PERM=np.int32, NODES=np.int32, IL_OFF=np.int64, IL_IDX=np.i
 
 EXPORTED_SYMBOLS = ["h2_build", "h2_build_ex", "h2_rebuild_ex", "h2_options_default", "h2_matvec", "h2_matvec_ex", "h2_free", "h2_last_error",
                     "h2_last_error_message", "h2_info", "h2_export", "h2_sample_blocks", "h2_comm_nccl_unique_id",
-                    "h2_comm_init_nccl", "h2_comm_init_local", "h2_comm_free", "h2_comm_size", "h2_comm_rank",
+                    "h2_comm_init_nccl", "h2_comm_init_nccl_dev", "h2_comm_init_local", "h2_comm_free", "h2_comm_size", "h2_comm_rank",
                     "h2_shard_cut_level", "h2_shard_split"]
 
 
@@ -98,6 +98,8 @@ def lib():
         L.h2_comm_nccl_unique_id.argtypes = [vp]
         L.h2_comm_init_nccl.restype = vp
         L.h2_comm_init_nccl.argtypes = [i32, i32, vp]
+        L.h2_comm_init_nccl_dev.restype = vp
+        L.h2_comm_init_nccl_dev.argtypes = [i32, i32, vp, i32]
         L.h2_comm_init_local.restype = vp
         L.h2_comm_init_local.argtypes = [i32, i32, i64]
         L.h2_comm_free.argtypes = [vp]
@@ -228,10 +230,13 @@ class H2Comm:
         return bytes(buf)
 
     @classmethod
-    def nccl(cls, nranks: int, rank: int, uid: bytes) -> "H2Comm":
+    def nccl(cls, nranks: int, rank: int, uid: bytes, device: int | None = None) -> "H2Comm":
+        """device: the CUDA device of this rank (h2_comm_init_nccl_dev); None = the current one."""
         _nccl_hint()
         buf = (C.c_ubyte * 128).from_buffer_copy(uid)
-        return cls(lib().h2_comm_init_nccl(nranks, rank, buf))
+        if device is None:
+            return cls(lib().h2_comm_init_nccl(nranks, rank, buf))
+        return cls(lib().h2_comm_init_nccl_dev(nranks, rank, buf, int(device)))
 
     @classmethod
     def local(cls, nranks: int, rank: int, key: int) -> "H2Comm":

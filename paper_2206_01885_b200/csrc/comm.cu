@@ -277,6 +277,22 @@ h2_comm* h2_comm_init_nccl(int32_t nranks, int32_t rank, const unsigned char id[
   }
 }
 
+h2_comm* h2_comm_init_nccl_dev(int32_t nranks, int32_t rank, const unsigned char id[128], int32_t device) {
+  clear_error();
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    set_error(H2_ERR_INVALID_ARG, "h2_comm_init_nccl_dev: no such CUDA device");
+    return nullptr;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    set_error(H2_ERR_CUDA, "h2_comm_init_nccl_dev: cudaSetDevice failed");
+    return nullptr;
+  }
+  return h2_comm_init_nccl(nranks, rank, id);
+}
+
 h2_comm* h2_comm_init_local(int32_t nranks, int32_t rank, int64_t group_key) {
   clear_error();
   if (nranks < 1 || rank < 0 || rank >= nranks) {

@@ -848,6 +848,11 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
       H2_CUDA_TRY(cudaEventRecord(gev[0], s));
       H2_CUDA_TRY(cudaStreamWaitEvent(sa, gev[0], 0));
       H2_CUDA_TRY(cudaStreamWaitEvent(sb, gev[0], 0));
+      // (static + dynamic shared memory above 48 KB needs the opt-in)
+      H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(double) * kIdGlobalFs));
+      H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(double) * kIdGlobalFs));
       id_kernel<256><<<count, 256, sizeof(double) * kIdGlobalFs, sa>>>(base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf,
                                            h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
                                            work.as<double>(), h->u_off + base, U, h->k, h->sk,

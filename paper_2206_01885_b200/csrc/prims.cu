@@ -1,6 +1,7 @@
-// prims.cu -- device memory pool and the device-wide primitives used by the stages: a single-pass
-// prefix sum (decoupled look-back) and a stable LSD radix sort (8-bit digits, one count / scan /
-// scatter round per digit) -- both written here, no library kernels.
+// prims.cu -- device memory pool and the device-wide primitives used by the stages: a two-launch
+// prefix sum (per-tile reduction, then a scan of the tile sums fused with the tile scans) and a
+// stable LSD radix sort (8-bit digits, one count / scan / scatter round per digit) -- both written
+// here, no library kernels.
 #include <map>
 #include <mutex>
 #include <unordered_map>
