@@ -853,11 +853,12 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
                                        (int)sizeof(double) * kIdGlobalFs));
       H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sizeof(double) * kIdGlobalFs));
-      id_kernel<256><<<count, 256, sizeof(double) * kIdGlobalFs, sa>>>(base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf,
+      const size_t gfs = (use_panel & 4) ? sizeof(double) * kIdGlobalFs : 0;  // F only for the panel
+      id_kernel<256><<<count, 256, gfs, sa>>>(base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf,
                                            h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
                                            work.as<double>(), h->u_off + base, U, h->k, h->sk,
                                            ev.as<unsigned long long>(), 0, kIdBigBlock, cs, cl_min, use_panel, h->id_path);
-      id_kernel<1024><<<count, 1024, sizeof(double) * kIdGlobalFs, sb>>>(base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf,
+      id_kernel<1024><<<count, 1024, gfs, sb>>>(base, h->kid, p2, h->id_tol, Xf, h->X, h->n, h->d, h->r, h->is_leaf,
                                              h->nbegin, h->first_child, h->nchild, h->ys_cnt, h->ys, h->xbar_n, woff,
                                              work.as<double>(), h->u_off + base, U, h->k, h->sk,
                                              ev.as<unsigned long long>(), kIdBigBlock, INT64_MAX, cs, cl_min,
