@@ -73,6 +73,12 @@ static std::vector<T> d2h(const T* d, size_t count, cudaStream_t s) {
   return v;
 }
 
+unsigned long long* build_stats() {
+  thread_local unsigned long long* pinned = nullptr;
+  if (!pinned) H2_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&pinned), sizeof(unsigned long long) * 64));
+  return pinned;
+}
+
 // a1-a4 and a6-a7 of `base`, copied into the fresh handle h (device arrays duplicated on
 // h->stream; the base keeps its own): the geometry a rebuild for another kernel reuses
 static void clone_geometry(h2_handle* h, const h2_handle* b) {
@@ -235,6 +241,8 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   try {
     BuildStreams& bs = build_streams();
+    unsigned long long* stats = build_stats();  // the deferred statistics of this build (h2_internal.cuh)
+    for (int q = 0; q < kStatCount; q++) stats[q] = 0;
     H2_CUDA_TRY(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
     H2_CUDA_TRY(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
     // all work runs on the internal streams, ordered after what the caller queued on `user`
@@ -307,6 +315,14 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
     h->stream = user;
     for (auto& a : h->aux) a = nullptr;
     H2_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (!base) {
+      h->hidr_up_evals = (int64_t)stats[kStatHidrUp];
+      h->hidr_dist_evals = (int64_t)(stats[kStatHidrUp] + stats[kStatHidrDown]);
+      h->hidr_dist_done = (int64_t)stats[kStatHidrDone];
+    }
+    h->kmax = (int)stats[kStatKmax];
+    h->id_kernel_evals = (int64_t)(stats[kStatIdEvals] + stats[kStatIdEvalsCol]);
+    h->kmax_col = h->nonsym ? (int)stats[kStatKmaxCol] : h->kmax;
     if (h->timing) {
       nf.finish_timing(h);
       for (int i = 0; i < 6; i++) cudaEventElapsedTime(&h->stage_ms[i], ev[i], ev[i + 1]);

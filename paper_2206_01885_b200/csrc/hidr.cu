@@ -605,8 +605,7 @@ void hidr_up(h2_handle* h) {
       }
     }
   }
-  h->hidr_dist_evals = (int64_t)read1(ev.as<unsigned long long>(), h->stream);
-  h->hidr_up_evals = h->hidr_dist_evals;
+  defer_stat(h, kStatHidrUp, ev.p, sizeof(unsigned long long));
 }
 
 void hidr_down(h2_handle* h) {
@@ -626,8 +625,8 @@ void hidr_down(h2_handle* h) {
     else
       hidr_level(h, 1, l, ev.as<unsigned long long>());
   }
-  h->hidr_dist_evals += (int64_t)read1(ev.as<unsigned long long>(), h->stream);
-  h->hidr_dist_done = (int64_t)read1(evd.as<unsigned long long>(), h->stream);
+  defer_stat(h, kStatHidrDown, ev.p, sizeof(unsigned long long));
+  defer_stat(h, kStatHidrDone, evd.p, sizeof(unsigned long long));
 }
 
 }  // namespace h2

@@ -713,7 +713,7 @@ static int id_cluster_max() {
 
 // One getBasis sweep (Algorithm 2 lines 10-12) into the handle's row-basis fields, kappa's first
 // argument (Xbar) read from Xf.
-static void id_sweep_pass(h2_handle* h, const double* Xf) {
+static void id_sweep_pass(h2_handle* h, const double* Xf, int stat_kmax, int stat_evals) {
   cudaStream_t s = h->stream;
   H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   H2_CUDA_TRY(cudaFuncSetAttribute(id_kernel_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -993,8 +993,8 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
   H2_CUDA_TRY(cudaMemsetAsync(km.p, 0, sizeof(int), s));
   kmax_kernel<<<(nn + 255) / 256, 256, 0, s>>>(nn, h->k, km.as<int>());
   H2_CHECK_LAUNCH();
-  h->kmax = read1(km.as<int>(), s);
-  h->id_kernel_evals = (int64_t)read1(ev.as<unsigned long long>(), s);
+  defer_stat(h, stat_kmax, km.p, sizeof(int));
+  defer_stat(h, stat_evals, ev.p, sizeof(unsigned long long));
 }
 
 // a8: the row bases (getBasis(K_{Xbar Y*}), first argument X + a for the shifted multiquadric) and,
@@ -1003,7 +1003,7 @@ static void id_sweep_pass(h2_handle* h, const double* Xf) {
 // X - a; its results move to the *_col fields.  For a symmetric kernel the second sweep repeats the
 // first bit for bit (V = U).
 void id_sweep(h2_handle* h) {
-  id_sweep_pass(h, h->Xf);
+  id_sweep_pass(h, h->Xf, kStatKmax, kStatIdEvals);
   if (!h->nonsym) {
     h->k_col = h->k;
     h->sk_col = h->sk;
@@ -1019,7 +1019,7 @@ void id_sweep(h2_handle* h) {
   int64_t* uo = h->u_off;
   double* U = h->U;
   const int64_t ut = h->u_total, ev = h->id_kernel_evals;
-  id_sweep_pass(h, h->Xfn);
+  id_sweep_pass(h, h->Xfn, kStatKmaxCol, kStatIdEvalsCol);
   h->k_col = h->k;
   h->sk_col = h->sk;
   h->xbar_col_n = h->xbar_n;
