@@ -46,16 +46,17 @@ FP64_LANES_PER_SM = 64
 
 def workload_desc(cfg: int) -> str:
     c = synth.CONFIGS[cfg]
-    kname = {1: "Coulomb", 2: "Gaussian", 3: "Matern-3/2"}[c["kernel"]]
+    kname = {1: "Coulomb", 2: "Gaussian", 3: "Matern-3/2", 7: "shifted multiquadric (non-symmetric)"}[c["kernel"]]
     par = f" param {c['params'][0]}" if c["params"] else ""
-    return (f"BASELINE configs[{cfg - 1}]: {c['name']} n={c['n']} d={c['d']} {kname}{par} q={c['q']} "
+    src = f"BASELINE configs[{cfg - 1}]" if cfg <= 5 else "non-BASELINE extra config"
+    return (f"{src}: {c['name']} n={c['n']} d={c['d']} {kname}{par} q={c['q']} "
             f"id_tol={c['id_tol']} tau={c['tau']}; full build a1-a10, all blocks stored symmetric-once")
 
 
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r02_fp64_peak.json")
 # FP64 instructions per kernel evaluation (fill / ID block generation) and per
 # squared distance + compare (HiDR, 3d - 1 DADD/DMUL + a compare)
-KERNEL_FP64_INSTR = {1: 18, 2: 23, 3: 17, 4: 22, 5: 26, 6: 30}
+KERNEL_FP64_INSTR = {1: 18, 2: 23, 3: 17, 4: 22, 5: 26, 6: 30, 7: 7}
 
 
 def fp64_peak() -> dict:
@@ -183,15 +184,24 @@ def max_over_ranks(v: float, ws: int) -> float:
 
 
 # ------------------------------------------------------------------------------------------ oracle
+def oracle_for(cfg: int, pts):
+    """The oracle handle of a config (the non-symmetric path and the kernel shift for kernel 7)."""
+    import oracle
+    c = synth.CONFIGS[cfg]
+    ns = c["kernel"] == synth.KERNEL_MQSHIFT
+    if ns:
+        oracle.set_kernel_shift(np.array(c["params"][1:]))
+    return oracle.OracleH2(pts, c["q"], c["tau"], nonsym=ns)
+
+
 def oracle_sample_run(cfg: int, n_sample: int):
     """The fp64 oracle, as it stands, on a bounded sample of the workload (same distribution,
     n_sample points): a1-a8 plus an evaluate-only pass over every a9/a10 block."""
-    import oracle
     c = synth.CONFIGS[cfg]
     pts = synth.points(cfg, n_sample)
     kp = c["params"][0] if c["params"] else 0.0
     t0 = time.perf_counter()
-    h = oracle.OracleH2(pts, c["q"], c["tau"])
+    h = oracle_for(cfg, pts)
     h.build(c["kernel"], kp, c["id_tol"])
     entries, _ = h.fill(store=False)
     dt = time.perf_counter() - t0
@@ -209,7 +219,7 @@ def cpu_baseline(cfg: int, n_sample: int, y_gpu_rows=None) -> tuple[dict, dict |
     pts = synth.points(cfg, n_sample)
     kp = c["params"][0] if c["params"] else 0.0
     t0 = time.perf_counter()
-    h = oracle.OracleH2(pts, c["q"], c["tau"])
+    h = oracle_for(cfg, pts)
     r = h.build(c["kernel"], kp, c["id_tol"])
     entries, _ = h.fill(store=False)
     dt = time.perf_counter() - t0
@@ -433,7 +443,8 @@ def run_ours(args):
     whole = build_roofline(c, info, ex["K"], ex["XBAR_N"], np.diff(ex["YS_OFF"]), t_step, hbm, fp64)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic,
-                "kernel": "nf_fill_kernel<D=2,MATERN32> (a10, nearfield fill)", "kernel_ms": round(nf_ms, 3),
+                "kernel": f"nf_fill_kernel<D={c['d']},kernel {c['kernel']}> (a10, nearfield fill)",
+                "kernel_ms": round(nf_ms, 3),
                 "step_share": round(nf_ms / t_step, 4),
                 "note": "live: the kernel runs concurrently with a5-a9 (side stream), sharing the SMs",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650 GB/s",
@@ -486,7 +497,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--config", type=int, default=4, help="BASELINE configs[C-1] (1..5); 6 = the non-symmetric "
+                                                             "extra config (not a bench line)")
     ap.add_argument("--n", type=int, default=None, help="override n (not a bench line)")
     ap.add_argument("--storage", choices=["all", "fly", "auto"], default="all",
                     help="block storage (fly: skeleton build a1-a8, blocks evaluated in the matvec; for "

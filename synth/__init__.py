@@ -26,6 +26,7 @@ KERNEL_MATERN32 = 3
 KERNEL_LAPLACE = 4
 KERNEL_BUMP = 5
 KERNEL_COSDOT = 6  # Table 1 kappa_3 = cos(x . y)
+KERNEL_MQSHIFT = 7  # sqrt(1 + c |x - y + a|^2), non-symmetric; params (c, a_0, ..., a_{d-1})
 
 # (n, d, kernel_id, kernel_params, leaf_size, id_tol, tau, name)
 CONFIGS = {
@@ -39,6 +40,10 @@ CONFIGS = {
             name="mix2d_4M_matern0.1_1e-6"),
     5: dict(n=1 << 18, d=5, kernel=KERNEL_GAUSSIAN, params=(1.0,), q=256, id_tol=1e-4, tau=0.5,
             name="mix5d_256k_gauss1.0_1e-4"),
+    # not a BASELINE config: the non-symmetric family (the paper's shifted multiquadric of P:711-716,
+    # c = 100, here with a = [0, 0.3] so the shift lies inside the data's extent) on uniform 2-D points
+    6: dict(n=1 << 20, d=2, kernel=KERNEL_MQSHIFT, params=(100.0, 0.0, 0.3), q=128, id_tol=1e-6, tau=0.5,
+            name="mq2d_1M_shifted_multiquadric_1e-6"),
 }
 
 
@@ -54,6 +59,8 @@ def points(config: int, n: int | None = None, seed_offset: int = 0) -> np.ndarra
     rng = _rng(SEED_BASE + config + seed_offset)
     if config in (1, 2):
         x = rng.random((n, 3))
+    elif config == 6:
+        x = rng.random((n, 2))
     elif config == 3:
         g = rng.standard_normal((n, 3))
         x = g / np.linalg.norm(g, axis=1, keepdims=True)
