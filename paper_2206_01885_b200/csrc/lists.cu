@@ -184,6 +184,15 @@ __global__ void row_hist_kernel(const unsigned long long* __restrict__ keys, int
     atomicAdd(&cnt[keys[e] >> 32], 1ULL);
 }
 
+__global__ void row_scatter_kernel(const unsigned long long* __restrict__ keys, int64_t m,
+                                   const int64_t* __restrict__ off, int* fill, int* idx) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[e];
+    const int i = (int)(k >> 32);
+    idx[off[i] + atomicAdd(&fill[i], 1)] = (int)(k & 0xffffffffULL);
+  }
+}
+
 // one CTA per row: a row of <= 64 entries is sorted by warp 0 with shuffles (two per lane, no
 // barrier), a longer one by a shared-memory bitonic network of its own power-of-two size
 constexpr int kRowSortThreads = 512;
@@ -250,58 +259,22 @@ struct Grow {
   }
 };
 
-// (i << 32 | j) -> the row key i and the column j
-__global__ void split_pairs_kernel(const unsigned long long* __restrict__ keys, int64_t m, unsigned long long* row,
-                                   int* col) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long k = keys[e];
-    row[e] = k >> 32;
-    col[e] = (int)(k & 0xffffffffULL);
-  }
-}
-
-// flags[0] = the number of adjacent out-of-order pairs inside rows, flags[1] = the longest row
-__global__ void row_check_kernel(const int64_t* __restrict__ off, int nnodes, const int* __restrict__ idx,
-                                 int* flags) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nnodes) return;
-  const int64_t b = off[i], e = off[i + 1];
-  int bad = 0;
-  for (int64_t t = b + 1; t < e; t++) bad += idx[t - 1] > idx[t];
-  if (bad) atomicAdd(flags, bad);
-  atomicMax(flags + 1, (int)(e - b));
-}
-
-// CSR of the unordered pairs, rows sorted.  A STABLE radix sort by row (the pairs in emission
-// order within a row) replaces an atomic scatter + a per-row sort: the level-synchronous traversal
-// emits every row's columns in ascending order (children are expanded in frontier order, and node
-// ids are level order), so the per-row sort is needed only if the check finds a row out of order.
 static void to_csr(h2_handle* h, unsigned long long* keys, int64_t m, int64_t*& off, int*& idx) {
   cudaStream_t s = h->stream;
   const int nn = h->nnodes;
   off = halloc<int64_t>(h, nn + 1);
   idx = halloc<int>(h, m);
-  Scratch cnt(sizeof(int64_t) * (nn + 1), s), fl(2 * sizeof(int), s);
+  Scratch cnt(sizeof(int64_t) * (nn + 1), s), fill(sizeof(int) * nn, s), mx(sizeof(int), s);
   H2_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, sizeof(int64_t) * (nn + 1), s));
-  H2_CUDA_TRY(cudaMemsetAsync(fl.p, 0, 2 * sizeof(int), s));
+  H2_CUDA_TRY(cudaMemsetAsync(fill.p, 0, sizeof(int) * nn, s));
+  H2_CUDA_TRY(cudaMemsetAsync(mx.p, 0, sizeof(int), s));
   if (m > 0) row_hist_kernel<<<grid_for(m, 256), 256, 0, s>>>(keys, m, cnt.as<unsigned long long>());
   scan_excl_i64(cnt.as<int64_t>(), off, nn + 1, s);
   if (m == 0) return;
-  {
-    Scratch rk(sizeof(unsigned long long) * m, s), rko(sizeof(unsigned long long) * m, s), cv(sizeof(int) * m, s);
-    split_pairs_kernel<<<grid_for(m, 256), 256, 0, s>>>(keys, m, rk.as<unsigned long long>(), cv.as<int>());
-    int bits = 1;
-    while ((1LL << bits) < nn) bits++;
-    sort_pairs_u64_i32(rk.as<unsigned long long>(), rko.as<unsigned long long>(), cv.as<int>(), idx, m, bits, s);
-  }
-  row_check_kernel<<<(nn + 255) / 256, 256, 0, s>>>(off, nn, idx, fl.as<int>());
+  row_scatter_kernel<<<grid_for(m, 256), 256, 0, s>>>(keys, m, off, fill.as<int>(), idx);
+  max_row_kernel<<<(nn + 255) / 256, 256, 0, s>>>(off, nn, mx.as<int>());
   H2_CHECK_LAUNCH();
-  int hf[2];
-  H2_CUDA_TRY(cudaMemcpyAsync(hf, fl.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
-  H2_CUDA_TRY(cudaStreamSynchronize(s));
-  h->gpu_launches += 3;
-  if (hf[0] == 0) return;  // every row already ascending
-  const int maxlen = hf[1];
+  const int maxlen = read1(mx.as<int>(), s);
   int P = 128;
   while (P < maxlen) P <<= 1;
   const size_t smem = sizeof(int) * (size_t)P;
@@ -310,7 +283,7 @@ static void to_csr(h2_handle* h, unsigned long long* keys, int64_t m, int64_t*& 
   H2_CUDA_TRY(cudaFuncSetAttribute(row_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   row_sort_kernel<<<nn, kRowSortThreads, smem, s>>>(off, idx);
   H2_CHECK_LAUNCH();
-  h->gpu_launches += 1;
+  h->gpu_launches += 4;
 }
 
 void build_lists(h2_handle* h) {
