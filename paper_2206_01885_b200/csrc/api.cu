@@ -35,7 +35,7 @@ static void free_handle(h2_handle* h) {
 // highest priority; `side` carries the nearfield fill (a10) at the lowest, so the latency-bound
 // level kernels take SMs first whenever a fill CTA retires.
 struct BuildStreams {
-  cudaStream_t main = nullptr, side = nullptr, calib = nullptr;
+  cudaStream_t main = nullptr, side = nullptr, calib = nullptr, calib2 = nullptr;
   cudaStream_t aux[h2_handle::kAux] = {};
 };
 static BuildStreams& build_streams() {
@@ -51,6 +51,7 @@ static BuildStreams& build_streams() {
     const char* sp = getenv("H2_SIDE_PRIORITY");
     H2_CUDA_TRY(cudaStreamCreateWithPriority(&b.side, cudaStreamNonBlocking, sp && atoi(sp) ? greatest : least));
     H2_CUDA_TRY(cudaStreamCreateWithPriority(&b.calib, cudaStreamNonBlocking, greatest));
+    H2_CUDA_TRY(cudaStreamCreateWithPriority(&b.calib2, cudaStreamNonBlocking, greatest));
     for (auto& a : b.aux) H2_CUDA_TRY(cudaStreamCreateWithPriority(&a, cudaStreamNonBlocking, greatest));
   }
   return b;
@@ -282,7 +283,18 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
       if (calibrated) {  // a5 phase 0 overlaps a4 (calib.cu)
         H2_CUDA_TRY(cudaEventRecord(fork_ev, h->stream));
         H2_CUDA_TRY(cudaStreamWaitEvent(bs.calib, fork_ev, 0));
-        calibrate_begin(h, bs.calib, cal);
+        H2_CUDA_TRY(cudaStreamWaitEvent(bs.calib2, fork_ev, 0));
+        calibrate_begin(h, bs.calib, bs.calib2, cal);
+        // H2_CAL_SYNC=1 (probe knob): finish a5 before a4 starts (the trials' own duration then
+        // shows up in the lists stage)
+        static const bool cal_sync = [] {
+          const char* e = getenv("H2_CAL_SYNC");
+          return e && atoi(e) != 0;
+        }();
+        if (cal_sync) {
+          H2_CUDA_TRY(cudaStreamSynchronize(bs.calib));
+          H2_CUDA_TRY(cudaStreamSynchronize(bs.calib2));
+        }
       }
       if (h->nranks > 1) shard_plan(h);  // cut level, owned subtrees and block rows (shard.cu)
       build_lists(h);                    // a4 (sharded: the rank's own rows)

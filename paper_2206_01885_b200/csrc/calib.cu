@@ -339,11 +339,15 @@ static long long grid_size(int d, int m) {
 
 // Issued right after the tree (a1-a3) on the stream `s`, overlapping a4 -- a trial depends only on
 // the level's box width W 2^-l, not on the lists.  Phase 0: the trials with m^d <= 64 for EVERY level
-// 1..depth.  Phase 1 (speculative): the trials with m^d > 64 for every level, each exiting at once
-// when a phase-0 trial of its level passed.  calibrate_end keeps the levels that hold an admissible
-// pair; levels without one cost trials but never decide r.
-void calibrate_begin(h2_handle* h, cudaStream_t s, CalibJob& job) {
+// 1..depth.  Phase 1 (speculative): the trials with m^d > 64 for every level.  d <= 2: after phase 0
+// on `s`, each exiting at once when a phase-0 trial of its level passed.  d >= 3 (at most two
+// computed trials per level: m^d < N = 256 stops at m = 6): on `s2`, concurrently with phase 0, and
+// calibrate_end waits for it only when some level needs it (H2_CAL_MERGE=0, A/B knob: the d <= 2
+// order for every d).  calibrate_end keeps the levels that hold an admissible pair; levels without
+// one cost trials but never decide r.
+void calibrate_begin(h2_handle* h, cudaStream_t s, cudaStream_t s2, CalibJob& job) {
   job.stream = s;
+  job.stream2 = s2;
   std::vector<double> wl, wl1;
   std::vector<int> lv, mv, lv1, mv1;
   for (int o = 0; o < (h->nonsym ? 2 : 1); o++)  // o = 1: the transposed kernel (reading E7)
@@ -356,10 +360,19 @@ void calibrate_begin(h2_handle* h, cudaStream_t s, CalibJob& job) {
         (p0 ? mv : mv1).push_back(m);
         if (G >= N) break;
       }
+  static const bool split_env = [] {
+    const char* e = getenv("H2_CAL_MERGE");
+    return e ? atoi(e) != 0 : true;
+  }();
+  job.split = split_env && h->d >= 3 && !wl1.empty() && s2 != nullptr;
+  // (a previous build's unawaited phase 1 may still own the page-locked slot 1)
+  if (s2) H2_CUDA_TRY(cudaStreamSynchronize(s2));
   job.passed = Scratch(sizeof(int) * 64, s);
   H2_CUDA_TRY(cudaMemsetAsync(job.passed.p, 0, sizeof(int) * 64, s));
   launch_trials(h, s, 0, wl, lv, mv, nullptr, job.p0);
-  if (!wl1.empty()) {
+  if (job.split) {
+    launch_trials(h, s2, 1, wl1, lv1, mv1, nullptr, job.p1);
+  } else if (!wl1.empty()) {
     if (job.p0.T > 0) {
       const int* dl = reinterpret_cast<const int*>(job.p0.params.as<double>() + job.p0.T);
       const int* dpass = reinterpret_cast<const int*>(job.p0.outs.as<double>() + job.p0.T);
@@ -397,12 +410,25 @@ int calibrate_end(h2_handle* h, CalibJob& job) {
   }
   if (job.active) H2_CUDA_TRY(cudaStreamSynchronize(job.stream));
   std::vector<int> chosen(64, 0);  // per virtual level (l, l + 32)
-  for (CalibSet* set : {&job.p0, &job.p1})  // trials of a level are in increasing m: keep the first pass
-    for (int t = 0; t < set->T; t++)
-      if (set->pass_h[t] && !chosen[set->lv[t]]) chosen[set->lv[t]] = set->mv[t];
-  // release the buffers on h->stream (ordered after the synchronisation above)
+  // trials of a level are in increasing m: keep the first pass
+  auto take = [&](CalibSet& set) {
+    for (int t = 0; t < set.T; t++)
+      if (set.pass_h[t] && !chosen[set.lv[t]]) chosen[set.lv[t]] = set.mv[t];
+  };
+  take(job.p0);
+  // the split phase 1 is awaited only when a level holding a pair has no passing phase-0 trial (all
+  // phase-0 trials of every level are in job.p0, so its passes are final)
+  bool awaited = !job.split;
+  if (job.split)
+    for (int t = 0; t < job.p1.T && !awaited; t++)
+      if (has[job.p1.lv[t] & 31] && !chosen[job.p1.lv[t]]) awaited = true;
+  if (job.split && awaited) H2_CUDA_TRY(cudaStreamSynchronize(job.stream2));
+  if (awaited) take(job.p1);
+  // release the buffers on h->stream (ordered after the synchronisation above); an unawaited phase 1
+  // releases its own on stream2 (the pool reuses them only after stream2 has passed the release)
   for (CalibSet* set : {&job.p0, &job.p1}) {
-    set->work.s = set->params.s = set->outs.s = s;
+    const cudaStream_t rs = (set == &job.p1 && !awaited) ? job.stream2 : s;
+    set->work.s = set->params.s = set->outs.s = rs;
     set->work = Scratch();
     set->params = Scratch();
     set->outs = Scratch();
@@ -419,6 +445,7 @@ int calibrate_end(h2_handle* h, CalibJob& job) {
 
 CalibJob::~CalibJob() {
   if (active && stream) cudaStreamSynchronize(stream);  // error path: the trials may still run
+  if (active && stream2) cudaStreamSynchronize(stream2);
 }
 
 }  // namespace h2
