@@ -1,7 +1,8 @@
 // prims.cu -- device memory pool and the device-wide primitives used by the stages: a two-launch
 // prefix sum (per-tile reduction, then a scan of the tile sums fused with the tile scans) and a
-// stable LSD radix sort (8-bit digits, one count / scan / scatter round per digit) -- both written
-// here, no library kernels.
+// stable LSD radix sort (8-bit digits; one onesweep launch per digit: decoupled look-back over the
+// tiles' published digit counts) -- both written here, no library kernels.
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -312,13 +313,175 @@ __global__ void __launch_bounds__(kSortNT) radix_scatter_kernel(const unsigned l
   }
 }
 
+// Onesweep variant (the default): the digit histograms of ALL passes come from one read of the
+// keys (radix_hist_kernel, or fused into the producer of the keys -- tree.cu's quantisation), and
+// each pass is ONE launch: a tile takes its id from a counter (launch order, so every earlier tile
+// is resident or done), ranks its keys as above, publishes its per-digit count and finds its
+// per-digit offset by a decoupled look-back over the earlier tiles' published counts / inclusive
+// prefixes (status words: 2 flag bits + a 62-bit value), then scatters.  No count kernel, no
+// device scan per pass.
+constexpr unsigned long long kStAgg = 1ULL << 62, kStInc = 2ULL << 62, kStVal = (1ULL << 62) - 1;
+
+__global__ void __launch_bounds__(kSortNT) radix_hist_kernel(const unsigned long long* __restrict__ keys, int64_t n,
+                                                           int passes, unsigned* __restrict__ hist) {
+  __shared__ unsigned sh[8][256];
+  for (int t = threadIdx.x; t < 8 * 256; t += kSortNT) (&sh[0][0])[t] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)kSortNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kSortNT) {
+    const unsigned long long k = keys[i];
+    for (int p = 0; p < passes; p++) atomicAdd(&sh[p][(k >> (8 * p)) & 255ULL], 1u);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < passes * 256; t += kSortNT) {
+    const unsigned v = (&sh[0][0])[t];
+    if (v) atomicAdd(hist + t, v);
+  }
+}
+
+template <bool VALS>
+__global__ void __launch_bounds__(kSortNT) radix_onesweep_kernel(const unsigned long long* __restrict__ kin,
+                                                               const int* __restrict__ vin, int64_t n, int shift,
+                                                               const unsigned* __restrict__ hist,
+                                                               unsigned long long* status, unsigned* ctr,
+                                                               unsigned long long* __restrict__ kout,
+                                                               int* __restrict__ vout) {
+  __shared__ unsigned long long sk[kSortTile];
+  __shared__ int sv[VALS ? kSortTile : 1];
+  __shared__ int wcnt[kSortWarps][256];
+  __shared__ int dstart[256];
+  __shared__ long long gofs[256];
+  __shared__ BlockScanSmem<kSortNT> scan;
+  __shared__ unsigned s_tile;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(ctr, 1u);
+  for (int d = tid; d < kSortWarps * 256; d += kSortNT) (&wcnt[0][0])[d] = 0;
+  // the digit's global start: exclusive prefix of this pass's histogram
+  int dtot;
+  const int dbase = block_excl_sum<kSortNT>((int)hist[tid], &dtot, scan);  // (its barrier orders s_tile / wcnt)
+  const unsigned tile = s_tile;
+  const int64_t base = (int64_t)tile * kSortTile;
+  unsigned long long key[kSortIPT];
+  int val[kSortIPT], rank[kSortIPT];
+  auto digit_of = [&](int k, int64_t p) { return p < n ? (int)((key[k] >> shift) & 255ULL) : 256; };
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int k = 0; k < kSortIPT; k++) {
+    const int64_t p = base + w * (32 * kSortIPT) + k * 32 + lane;
+    const bool ok = p < n;
+    key[k] = ok ? kin[p] : ~0ULL;
+    if (VALS) val[k] = ok ? vin[p] : 0;
+    const int dg = digit_of(k, p);
+    const unsigned peers = __match_any_sync(0xffffffffu, dg);
+    const int before = dg < 256 ? wcnt[w][dg] : 0;
+    rank[k] = before + __popc(peers & lt);
+    __syncwarp();
+    if (dg < 256 && (peers & lt) == 0) wcnt[w][dg] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  int tcount = 0;
+  {
+    const int d = tid;
+    for (int q = 0; q < kSortWarps; q++) {
+      const int c = wcnt[q][d];
+      wcnt[q][d] = tcount;
+      tcount += c;
+    }
+  }
+  // publish this tile's count of digit tid, then look back for its exclusive prefix
+  volatile unsigned long long* st = status;
+  const int64_t me = (int64_t)tile * 256 + tid;
+  if (tile == 0) {
+    st[me] = kStInc | (unsigned long long)tcount;
+    gofs[tid] = dbase;
+  } else {
+    st[me] = kStAgg | (unsigned long long)tcount;
+    unsigned long long excl = 0;
+    for (int64_t t = (int64_t)tile - 1;; t--) {
+      unsigned long long v;
+      do {
+        v = st[t * 256 + tid];
+      } while ((v & ~kStVal) == 0);
+      excl += v & kStVal;
+      if ((v & ~kStVal) == kStInc) break;
+    }
+    st[me] = kStInc | (excl + (unsigned long long)tcount);
+    gofs[tid] = dbase + (long long)excl;
+  }
+  int total;
+  const int start = block_excl_sum<kSortNT>(tcount, &total, scan);
+  dstart[tid] = start;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kSortIPT; k++) {
+    const int64_t p = base + w * (32 * kSortIPT) + k * 32 + lane;
+    const int dg = digit_of(k, p);
+    if (dg < 256) {
+      const int pos = dstart[dg] + wcnt[w][dg] + rank[k];
+      sk[pos] = key[k];
+      if (VALS) sv[pos] = val[k];
+    }
+  }
+  __syncthreads();
+  const int valid = (int)(n - base < kSortTile ? n - base : kSortTile);
+  for (int pos = tid; pos < valid; pos += kSortNT) {
+    const unsigned long long kk = sk[pos];
+    const int d = (int)((kk >> shift) & 255ULL);
+    const int64_t o = gofs[d] + (pos - dstart[d]);
+    kout[o] = kk;
+    if (VALS) vout[o] = sv[pos];
+  }
+}
+
+// H2_SORT_ONESWEEP=0 (A/B knob): the count / scan / scatter passes
+static bool sort_onesweep() {
+  static const bool v = [] {
+    const char* e = getenv("H2_SORT_ONESWEEP");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 static void radix_sort(unsigned long long* kin, unsigned long long* kout, int* vin, int* vout, int64_t n, int end_bit,
-                       cudaStream_t s) {
+                       cudaStream_t s, const unsigned* hist_in) {
   if (n <= 0) return;
   const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
   const int passes = (end_bit + 7) / 8;
-  Scratch counts(sizeof(int64_t) * 256 * ntiles, s), offs(sizeof(int64_t) * 256 * ntiles, s);
   Scratch kt(passes > 1 ? sizeof(unsigned long long) * n : 8, s), vt(passes > 1 && vin ? sizeof(int) * n : 8, s);
+  if (sort_onesweep()) {
+    const size_t st_words = (size_t)passes * ntiles * 256;
+    Scratch ws(sizeof(unsigned long long) * st_words + sizeof(unsigned) * (8 * 256 + 8), s);
+    unsigned long long* status = ws.as<unsigned long long>();
+    unsigned* hist = reinterpret_cast<unsigned*>(status + st_words);
+    unsigned* ctr = hist + 8 * 256;
+    H2_CUDA_TRY(cudaMemsetAsync(ws.p, 0, sizeof(unsigned long long) * st_words + sizeof(unsigned) * (8 * 256 + 8), s));
+    if (!hist_in) {
+      radix_hist_kernel<<<(unsigned)grid_for(n, kSortNT, 148 * 4), kSortNT, 0, s>>>(kin, n, passes, hist);
+      H2_CHECK_LAUNCH();
+      g_prim_launches += 1;
+      hist_in = hist;
+    }
+    const unsigned long long* ksrc = kin;
+    const int* vsrc = vin;
+    for (int p = 0; p < passes; p++) {
+      const bool to_out = ((passes - 1 - p) % 2) == 0;
+      unsigned long long* kdst = to_out ? kout : kt.as<unsigned long long>();
+      int* vdst = vin ? (to_out ? vout : vt.as<int>()) : nullptr;
+      unsigned long long* stp = status + (size_t)p * ntiles * 256;
+      if (vin)
+        radix_onesweep_kernel<true><<<(unsigned)ntiles, kSortNT, 0, s>>>(ksrc, vsrc, n, 8 * p, hist_in + 256 * p, stp,
+                                                                         ctr + p, kdst, vdst);
+      else
+        radix_onesweep_kernel<false><<<(unsigned)ntiles, kSortNT, 0, s>>>(ksrc, nullptr, n, 8 * p, hist_in + 256 * p,
+                                                                          stp, ctr + p, kdst, nullptr);
+      H2_CHECK_LAUNCH();
+      g_prim_launches += 1;
+      ksrc = kdst;
+      vsrc = vdst;
+    }
+    return;
+  }
+  Scratch counts(sizeof(int64_t) * 256 * ntiles, s), offs(sizeof(int64_t) * 256 * ntiles, s);
   // ping-pong so that the last pass writes kout / vout
   const unsigned long long* ksrc = kin;
   const int* vsrc = vin;
@@ -344,12 +507,12 @@ static void radix_sort(unsigned long long* kin, unsigned long long* kout, int* v
 
 // keys_out / vals_out receive the stable sort of (keys_in, vals_in) by the key's bits [0, end_bit)
 void sort_pairs_u64_i32(unsigned long long* kin, unsigned long long* kout, int* vin, int* vout, int64_t n,
-                        int end_bit, cudaStream_t s) {
-  radix_sort(kin, kout, vin, vout, n, end_bit, s);
+                        int end_bit, cudaStream_t s, const unsigned* hist) {
+  radix_sort(kin, kout, vin, vout, n, end_bit, s, hist);
 }
 
 void sort_keys_u64(unsigned long long* kin, unsigned long long* kout, int64_t n, int end_bit, cudaStream_t s) {
-  radix_sort(kin, kout, nullptr, nullptr, n, end_bit, s);
+  radix_sort(kin, kout, nullptr, nullptr, n, end_bit, s, nullptr);
 }
 
 }  // namespace h2

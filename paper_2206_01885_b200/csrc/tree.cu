@@ -10,10 +10,6 @@
 
 namespace h2 {
 
-struct DArr {
-  double v[kMaxD];
-};
-
 // ---- a1: bounding box (min/max are order-free, so the two-pass reduction is exact) ----------
 __global__ void bbox_partial_kernel(const double* __restrict__ pts, int64_t n, int d, double* part,
                                     int* nonfinite) {
@@ -54,31 +50,88 @@ __global__ void bbox_partial_kernel(const double* __restrict__ pts, int64_t n, i
 }
 
 __global__ void bbox_final_kernel(const double* part, int nparts, int d, double* out) {
-  int c = threadIdx.x;
-  if (c >= d) return;
-  double lo = DBL_MAX, hi = -DBL_MAX;
-  for (int b = 0; b < nparts; b++) {
-    lo = fmin(lo, part[(b * 2) * kMaxD + c]);
-    hi = fmax(hi, part[(b * 2 + 1) * kMaxD + c]);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // 32 * kMaxD threads: warp w = coordinate w
+  if (w < d) {
+    double lo = DBL_MAX, hi = -DBL_MAX;
+    for (int b = lane; b < nparts; b += 32) {
+      lo = fmin(lo, part[(b * 2) * kMaxD + w]);
+      hi = fmax(hi, part[(b * 2 + 1) * kMaxD + w]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {
+      out[w] = lo;
+      out[kMaxD + w] = hi;
+    }
   }
-  out[c] = lo;
-  out[kMaxD + c] = hi;
 }
 
 // ---- a1: quantise + Morton interleave (dimension c of bit b at key bit d*b + c) --------------
-__global__ void quantize_kernel(const double* __restrict__ pts, int64_t n, int d, DArr rlo, double s, int L,
-                                long long cmax, unsigned long long* keys, int* idx) {
+// The root box (reading A1) is derived here from the device bbox with the host's operation order
+// (no contraction), so no host round trip precedes the quantisation; build_tree repeats it on the
+// host for h->W / h->rlo once the tree's first synchronisation has passed.  The digit histograms
+// of the radix sort's passes are counted on the fly (prims.cu, onesweep).
+__device__ __forceinline__ unsigned long long spread_bits(unsigned long long x, int d, int L) {
+  if (d == 1) return x;
+  if (d == 2) {  // bit b -> 2b
+    x &= 0xffffffffULL;
+    x = (x | (x << 16)) & 0x0000ffff0000ffffULL;
+    x = (x | (x << 8)) & 0x00ff00ff00ff00ffULL;
+    x = (x | (x << 4)) & 0x0f0f0f0f0f0f0f0fULL;
+    x = (x | (x << 2)) & 0x3333333333333333ULL;
+    return (x | (x << 1)) & 0x5555555555555555ULL;
+  }
+  if (d == 3) {  // bit b -> 3b (21 bits)
+    x &= 0x1fffffULL;
+    x = (x | (x << 32)) & 0x1f00000000ffffULL;
+    x = (x | (x << 16)) & 0x1f0000ff0000ffULL;
+    x = (x | (x << 8)) & 0x100f00f00f00f00fULL;
+    x = (x | (x << 4)) & 0x10c30c30c30c30c3ULL;
+    return (x | (x << 2)) & 0x1249249249249249ULL;
+  }
+  unsigned long long k = 0;
+  for (int b = 0; b < L; b++) k |= ((x >> b) & 1ULL) << (d * b);
+  return k;
+}
+
+__global__ void __launch_bounds__(256) quantize_kernel(const double* __restrict__ pts, int64_t n, int d,
+                                                       const double* __restrict__ box, int L, int passes,
+                                                       unsigned long long* keys, int* idx, unsigned* hist) {
+  __shared__ unsigned sh[8][256];
+  __shared__ double s_rlo[kMaxD], s_sc;
+  for (int t = threadIdx.x; t < 8 * 256; t += blockDim.x) (&sh[0][0])[t] = 0;
+  if (threadIdx.x == 0) {
+    double W = 0.0;
+    for (int c = 0; c < d; c++) {
+      const double wc = __dsub_rn(box[kMaxD + c], box[c]);
+      if (wc > W) W = wc;
+    }
+    for (int c = 0; c < d; c++)
+      s_rlo[c] = __dsub_rn(__dmul_rn(__dadd_rn(box[c], box[kMaxD + c]), 0.5), __dmul_rn(W, 0.5));
+    s_sc = L > 0 && W > 0.0 ? __ddiv_rn(ldexp(1.0, L), W) : -1.0;  // -1: no key bits (W == 0)
+  }
+  __syncthreads();
+  const long long cmax = L > 0 ? (1LL << L) - 1 : 0;
+  const double sc = s_sc;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     unsigned long long key = 0;
-    if (L > 0) {
+    if (sc > 0.0) {
       for (int c = 0; c < d; c++) {
-        double f = floor(__dmul_rn(__dsub_rn(pts[i * d + c], rlo.v[c]), s));
+        double f = floor(__dmul_rn(__dsub_rn(pts[i * d + c], s_rlo[c]), sc));
         long long cell = f < 0.0 ? 0 : (f > (double)cmax ? cmax : (long long)f);
-        for (int b = 0; b < L; b++) key |= (unsigned long long)((cell >> b) & 1) << (d * b + c);
+        key |= spread_bits((unsigned long long)cell, d, L) << c;
       }
     }
     keys[i] = key;
     idx[i] = (int)i;
+    for (int p = 0; p < passes; p++) atomicAdd(&sh[p][(key >> (8 * p)) & 255ULL], 1u);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < passes * 256; t += blockDim.x) {
+    const unsigned v = (&sh[0][0])[t];
+    if (v) atomicAdd(hist + t, v);
   }
 }
 
@@ -206,53 +259,57 @@ void build_tree(h2_handle* h, const double* pts) {
   const int d = h->d;
   // a1 bounding box
   const int nparts = (int)grid_for(n, 256, 148 * 2);
-  Scratch part(sizeof(double) * nparts * 2 * kMaxD + sizeof(double) * 2 * kMaxD + 64, s);
+  Scratch part(sizeof(double) * nparts * 2 * kMaxD + sizeof(double) * 2 * kMaxD + 64 + sizeof(unsigned) * 8 * 256, s);
   double* dpart = part.as<double>();
   double* dbox = dpart + nparts * 2 * kMaxD;
   int* dbad = reinterpret_cast<int*>(dbox + 2 * kMaxD);
-  H2_CUDA_TRY(cudaMemsetAsync(dbad, 0, sizeof(int), s));
+  unsigned* dhist = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(dbad) + 64);
+  H2_CUDA_TRY(cudaMemsetAsync(dbad, 0, 64 + sizeof(unsigned) * 8 * 256, s));
   bbox_partial_kernel<<<nparts, 256, 0, s>>>(pts, n, d, dpart, dbad);
-  bbox_final_kernel<<<1, 32, 0, s>>>(dpart, nparts, d, dbox);
+  bbox_final_kernel<<<1, 32 * kMaxD, 0, s>>>(dpart, nparts, d, dbox);
   H2_CHECK_LAUNCH();
   h->gpu_launches += 2;
-  double box[2 * kMaxD + 1];
+  // the box and the non-finite flag reach the host with the tree's first synchronisation below
+  thread_local double* box = nullptr;  // page-locked, per host thread
+  if (!box) H2_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&box), sizeof(double) * (2 * kMaxD + 1)));
   H2_CUDA_TRY(cudaMemcpyAsync(box, dbox, sizeof(double) * 2 * kMaxD + sizeof(int), cudaMemcpyDeviceToHost, s));
-  H2_CUDA_TRY(cudaStreamSynchronize(s));
-  int bad;
-  memcpy(&bad, box + 2 * kMaxD, sizeof(int));
-  if (bad) throw Error{H2_ERR_NONFINITE, "a coordinate is NaN or Inf"};
-  double W = 0.0;
-  for (int c = 0; c < d; c++)
-    if (box[kMaxD + c] - box[c] > W) W = box[kMaxD + c] - box[c];
-  h->W = W;
-  DArr rlo;
-  for (int c = 0; c < kMaxD; c++) rlo.v[c] = 0.0;
-  for (int c = 0; c < d; c++) rlo.v[c] = h->rlo[c] = (box[c] + box[kMaxD + c]) * 0.5 - W * 0.5;
   h->L = 63 / d < 30 ? 63 / d : 30;
-  if (W == 0.0) h->L = 0;
-  const int L = h->L;
-  const double sc = L > 0 ? ldexp(1.0, L) / W : 0.0;
-  const long long cmax = L > 0 ? (1LL << L) - 1 : 0;
+  const int Lq = h->L;  // W == 0 (every point equal) gives L = 0 below; the keys are then all 0 either way
 
   // a1 quantise, a2 stable radix sort by (key, original index)
   Scratch kin(sizeof(unsigned long long) * n, s), iin(sizeof(int) * n, s);
   h->key = halloc<unsigned long long>(h, n);
   h->perm = halloc<int>(h, n);
-  quantize_kernel<<<grid_for(n, 256), 256, 0, s>>>(pts, n, d, rlo, sc, L, cmax, kin.as<unsigned long long>(),
-                                                   iin.as<int>());
+  const int end_bit = d * Lq > 0 ? d * Lq : 1;
+  const int passes = (end_bit + 7) / 8;
+  quantize_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(pts, n, d, dbox, Lq, passes, kin.as<unsigned long long>(),
+                                                            iin.as<int>(), dhist);
   H2_CHECK_LAUNCH();
   h->gpu_launches += 1;
-  int end_bit = d * L > 0 ? d * L : 1;
-  sort_pairs_u64_i32(kin.as<unsigned long long>(), h->key, iin.as<int>(), h->perm, n, end_bit, s);
+  sort_pairs_u64_i32(kin.as<unsigned long long>(), h->key, iin.as<int>(), h->perm, n, end_bit, s, dhist);
   h->X = halloc<double>(h, (size_t)n * d);
   gather_soa_kernel<<<grid_for(n, 256), 256, 0, s>>>(pts, h->perm, n, d, h->X);
   H2_CHECK_LAUNCH();
   h->gpu_launches += 1;
+  bool box_read = false;
+  auto read_box = [&]() {  // after a stream synchronisation
+    if (box_read) return;
+    box_read = true;
+    int bad;
+    memcpy(&bad, box + 2 * kMaxD, sizeof(int));
+    if (bad) throw Error{H2_ERR_NONFINITE, "a coordinate is NaN or Inf"};
+    double W = 0.0;
+    for (int c = 0; c < d; c++)
+      if (box[kMaxD + c] - box[c] > W) W = box[kMaxD + c] - box[c];
+    h->W = W;
+    for (int c = 0; c < d; c++) h->rlo[c] = (box[c] + box[kMaxD + c]) * 0.5 - W * 0.5;
+  };
 
   // a3 level-order nodes
   int cap = 0;
   h->nnodes = 0;
   grow_nodes(h, cap, (int)(n / (h->q > 1 ? h->q : 1)) * 2 + 64);
+  int L = Lq;
   root_init_kernel<<<1, 1, 0, s>>>((int)n, h->q, L, h->level, h->nbegin, h->nend, h->parent, h->is_leaf,
                                    h->first_child, h->nchild);
   h->gpu_launches += 1;
@@ -271,6 +328,14 @@ void build_tree(h2_handle* h, const double* pts) {
     H2_CHECK_LAUNCH();
     h->gpu_launches += 1;
     const int total = (int)read1(pos.as<int64_t>() + m, s);
+    read_box();
+    if (h->W == 0.0) {  // every point equal: no key bits, the root is the only node (a leaf)
+      h->L = L = 0;
+      root_init_kernel<<<1, 1, 0, s>>>((int)n, h->q, 0, h->level, h->nbegin, h->nend, h->parent, h->is_leaf,
+                                       h->first_child, h->nchild);
+      h->gpu_launches += 1;
+      break;
+    }
     if (total == 0) break;
     grow_nodes(h, cap, h->nnodes + total);
     split_create_kernel<<<grid_for(m, 256), 256, 0, s>>>(lb, count, d, h->nnodes, l + 1, h->q, L, pos.as<int64_t>(),
@@ -291,6 +356,7 @@ void build_tree(h2_handle* h, const double* pts) {
   H2_CHECK_LAUNCH();
   h->gpu_launches += 1;
   h->nleaves = read1(nl.as<int>(), s);
+  read_box();
 }
 
 }  // namespace h2
