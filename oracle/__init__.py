@@ -66,6 +66,7 @@ def lib():
         L.orc_info.argtypes = [vp, vp, vp, vp]
         L.orc_matvec_rows.argtypes = [vp, vp, vp, i64, vp]
         L.orc_dense_rows.argtypes = [vp, i32, i32, i32, f64, vp, vp, i64, vp]
+        L.orc_kernel_block.argtypes = [i32, f64, vp, i32, vp, i32, i32, vp]
         L.orc_fill.restype = i64
         L.orc_fill.argtypes = [vp, vp, i64, vp]
         L.orc_vol.argtypes = [vp, i32, vp, i32, i32, vp]
@@ -218,6 +219,16 @@ def dense_rows(pts: np.ndarray, kid: int, param: float, x: np.ndarray, rows) -> 
     out = np.empty(len(rows), np.float64)
     lib().orc_dense_rows(_p(pts), pts.shape[0], pts.shape[1], kid, float(param), _p(x), _p(rows),
                          len(rows), _p(out))
+    return out
+
+
+def kernel_block(kid: int, param: float, A: np.ndarray, B: np.ndarray) -> np.ndarray:
+    """J. the dense block K(A_a, B_b) of two point-major sets (kappa as orc_kernel)."""
+    A = np.ascontiguousarray(A, np.float64)
+    B = np.ascontiguousarray(B, np.float64)
+    out = np.empty((A.shape[0], B.shape[0]), np.float64)
+    if out.size:
+        lib().orc_kernel_block(kid, float(param), _p(A), A.shape[0], _p(B), B.shape[0], A.shape[1], _p(out))
     return out
 
 

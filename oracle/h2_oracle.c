@@ -27,6 +27,7 @@
  *   G  coupling / nearfield blocks (Algorithm 2)              orc_fill, on the fly in H
  *   H  H^2 matvec, four passes                                   orc_matvec_rows
  *   I  dense rows of K x                                     orc_dense_rows
+ *   J  kernel blocks K(A, B) of arbitrary point sets (interpolation baseline) orc_kernel_block
  *
  * Parity pins: see tests/test_oracle_*.py.  Every function here is pinned; the calibration (E) and
  * the top-down composition of D by tests/test_oracle_calib_topdown_pins.py (Eckart-Young and
@@ -1321,6 +1322,14 @@ int orc_matvec_rows(const orc_h2* h, const double* x, const int64_t* rows, int64
 /* ------------------------------------------------------------------------------------------ */
 
 /* out[r] = sum_j kappa(p_rows[r], p_j) x_j over all n points (original order, point-major). */
+/* K(A_a, B_b) for point-major A (na x d) and B (nb x d): out[a nb + b] = kappa(A_a, B_b) (the
+ * blocks of the interpolation baseline, oracle/interp.py: Eq. (2.2)).                */
+void orc_kernel_block(int kid, double p, const double* A, int na, const double* B, int nb, int d, double* out) {
+#pragma omp parallel for schedule(static) if ((int64_t)na * nb > 65536)
+  for (int a = 0; a < na; a++)
+    for (int b = 0; b < nb; b++) out[(int64_t)a * nb + b] = orc_kernel(kid, p, A + (int64_t)a * d, B + (int64_t)b * d, d);
+}
+
 void orc_dense_rows(const double* pts, int n, int d, int kid, double p, const double* x,
                     const int64_t* rows, int64_t nrows, double* out) {
 #pragma omp parallel for schedule(dynamic, 4)

@@ -104,3 +104,16 @@ def clustered(n: int, d: int, seed: int, k: int = 4, sigma: float = 0.05) -> np.
 def equispaced_1d(n: int) -> np.ndarray:
     """n equispaced points i/(n-1) on [0,1] (the 1-D layout of the paper's Fig. 4)."""
     return (np.arange(n, dtype=np.float64) / (n - 1)).reshape(n, 1).copy()
+
+
+def three_spheres(n: int, seed: int) -> np.ndarray:
+    """The "3-sphere" dataset of PAPER §6: points on the surfaces of three intersecting unit
+    spheres whose centres form an equilateral triangle of side 1 (reading: side exactly 1, the sphere
+    of each point uniform over the three, directions normalised Gaussians).  Used by the section-6.3
+    memory comparison (n = 20000)."""
+    rng = _rng(seed)
+    centres = np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0], [0.5, np.sqrt(3.0) / 2.0, 0.0]])
+    comp = rng.integers(0, 3, n)
+    g = rng.standard_normal((n, 3))
+    x = centres[comp] + g / np.linalg.norm(g, axis=1, keepdims=True)
+    return np.ascontiguousarray(x, dtype=np.float64)
