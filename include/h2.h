@@ -122,6 +122,13 @@ typedef struct h2_options {
   double srrqr_f;          /* > 0 (>= 1): strong rank-revealing refinement of every ID:  */
                            /*    Gu-Eisenstat swaps at fixed rank until max |G| <= srrqr_f; 0 = the  */
                            /*    plain column-pivoted QR (reading F1).  < 0 or in (0, 1): INVALID_ARG */
+  int32_t interp_p;        /* > 0: the INTERPOLATION-based H^2 instead (the baseline of PAPER section  */
+                           /*    6.3; Eq. (2.2)): p Chebyshev points of the */
+                           /*    first kind per dimension on every tree cell, r = p^d, U_i = L(X_i),  */
+                           /*    transfers L^(parent)(Q_c), B_ij = K(Q_i, Q_j) (readings I1-I4);      */
+                           /*    no calibration / HiDR / ID (id_tol is validated but unused).         */
+                           /*    1 <= p <= 16, p^d <= 4096; symmetric kernels, single GPU, no rebuild; */
+                           /*    otherwise INVALID_ARG.  0 (default): the data-driven construction.   */
 } h2_options;
 
 /* ---- DataReduct of HiDR (h2_options.reduct) ---------------------------------------------------- */
@@ -267,7 +274,9 @@ enum {
                           /* memory (256 / 1024 threads), 10 thread-block cluster, -1 no basis    */
   /* the column bases of the non-symmetric path (as K, SK_*, U_*, XBAR_N for the row bases)       */
   H2_EXPORT_K_COL = 22, H2_EXPORT_SKC_OFF = 23, H2_EXPORT_SKC_IDX = 24, H2_EXPORT_V_OFF = 25,
-  H2_EXPORT_V = 26, H2_EXPORT_XBARC_N = 27
+  H2_EXPORT_V = 26, H2_EXPORT_XBARC_N = 27,
+  H2_EXPORT_INTERP_Q = 28 /* double[nnodes*r*d]: the interpolation baseline's Chebyshev nodes, node-major,
+                             point-major (slot alpha = sum_c a_c p^c); zeros where k_i = 0             */
 };
 
 /* Copies array `what` into host_buf when cap_bytes suffices; *needed_bytes receives its size.

@@ -23,12 +23,13 @@ H2_REDUCT_VOLUME, H2_REDUCT_FPS, H2_REDUCT_SURFACE = 0, 1, 2  # HiDR DataReduct 
 
 EXPORT = dict(PERM=1, NODES=2, IL_OFF=4, IL_IDX=5, NF_OFF=6, NF_IDX=7, XS_OFF=8, XS_IDX=9, YS_OFF=10,
               YS_IDX=11, K=12, SK_OFF=13, SK_IDX=14, U_OFF=15, U=16, XBAR_N=17, TREE_X=18, SHARD=19, ID_PATH=21,
-              K_COL=22, SKC_OFF=23, SKC_IDX=24, V_OFF=25, V=26, XBARC_N=27)
+              K_COL=22, SKC_OFF=23, SKC_IDX=24, V_OFF=25, V=26, XBARC_N=27, INTERP_Q=28)
 _EXPORT_DTYPE = dict(PERM=np.int32, NODES=np.int32, IL_OFF=np.int64, IL_IDX=np.int32, NF_OFF=np.int64,
                      NF_IDX=np.int32, XS_OFF=np.int64, XS_IDX=np.int32, YS_OFF=np.int64, YS_IDX=np.int32,
                      K=np.int32, SK_OFF=np.int64, SK_IDX=np.int32, U_OFF=np.int64, U=np.float64,
                      XBAR_N=np.int32, TREE_X=np.float64, SHARD=np.int64, ID_PATH=np.int32, K_COL=np.int32,
-                     SKC_OFF=np.int64, SKC_IDX=np.int32, V_OFF=np.int64, V=np.float64, XBARC_N=np.int32)
+                     SKC_OFF=np.int64, SKC_IDX=np.int32, V_OFF=np.int64, V=np.float64, XBARC_N=np.int32,
+                     INTERP_Q=np.float64)
 
 EXPORTED_SYMBOLS = ["h2_build", "h2_build_ex", "h2_rebuild_ex", "h2_options_default", "h2_matvec", "h2_matvec_ex", "h2_free", "h2_last_error",
                     "h2_last_error_message", "h2_info", "h2_export", "h2_sample_blocks", "h2_comm_nccl_unique_id",
@@ -40,7 +41,8 @@ class h2_options(C.Structure):
     _fields_ = [("r_override", C.c_int32), ("storage", C.c_int32), ("mem_budget_bytes", C.c_int64),
                 ("stream", C.c_void_p), ("points_on_host", C.c_int32), ("timing", C.c_int32),
                 ("hidr_brute", C.c_int32), ("comm", C.c_void_p), ("serial_fill", C.c_int32),
-                ("reduct", C.c_int32), ("nonsymmetric", C.c_int32), ("srrqr_f", C.c_double)]
+                ("reduct", C.c_int32), ("nonsymmetric", C.c_int32), ("srrqr_f", C.c_double),
+                ("interp_p", C.c_int32)]
 
 
 class h2_info_t(C.Structure):
@@ -278,10 +280,11 @@ class H2Matrix:
                  admissibility: float = 0.5, r: int = 0, storage: int = H2_STORE_AUTO, stream=None,
                  timing: bool = False, mem_budget_bytes: int = 0, hidr_brute: bool = False,
                  comm: H2Comm | None = None, reduct: int = H2_REDUCT_VOLUME, nonsymmetric: bool = False,
-                 srrqr_f: float = 0.0):
+                 srrqr_f: float = 0.0, interp_p: int = 0):
         import torch
         o = h2_options_default()
         o.srrqr_f = float(srrqr_f)
+        o.interp_p = int(interp_p)
         o.reduct = int(reduct)
         o.nonsymmetric = int(bool(nonsymmetric))
         if comm is not None:

@@ -190,7 +190,9 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
       !(admissibility <= 0.7) || !(id_tol > 0.0) || !(id_tol < 1.0) || o.r_override < 0 || o.r_override > 4096 ||
       o.storage < 0 || o.storage > 2 || o.reduct < H2_REDUCT_VOLUME || o.reduct > H2_REDUCT_SURFACE ||
       (o.reduct == H2_REDUCT_SURFACE && d != 2 && d != 3) || !(o.srrqr_f == 0.0 || o.srrqr_f >= 1.0) ||
-      !std::isfinite(o.srrqr_f)) {
+      !std::isfinite(o.srrqr_f) || o.interp_p < 0 || o.interp_p > kInterpMaxP ||
+      (o.interp_p > 0 && (std::pow((double)o.interp_p, d) > 4096.0 || base || o.comm || o.nonsymmetric ||
+                          kernel_id == H2_KERNEL_MQSHIFT || o.srrqr_f != 0.0))) {
     set_error(H2_ERR_INVALID_ARG, "invalid argument (n, d, leaf_size, admissibility, id_tol or options)");
     return nullptr;
   }
@@ -225,6 +227,7 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
   std::memcpy(h->kpa, kpa, sizeof(kpa));
   h->nonsym = o.nonsymmetric || kernel_id == H2_KERNEL_MQSHIFT;
   h->srrqr_f = o.srrqr_f;
+  h->interp_p = o.interp_p;
   h->id_tol = id_tol;
   h->q = leaf_size;
   h->tau = admissibility;
@@ -271,7 +274,8 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
     NfJob nf;
     CalibJob cal;
     mark(0);
-    const bool calibrated = o.r_override <= 0 && !base;
+    const bool interp = o.interp_p > 0;  // the interpolation baseline (interp.cu)
+    const bool calibrated = o.r_override <= 0 && !base && !interp;
     if (base) {
       clone_geometry(h, base);  // a1-a4, a6-a7 (and the shard plan) of the base handle
       make_first_arg_coords(h);
@@ -304,7 +308,13 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
     // overlaps a5-a9 (serial_fill: after a9 on the main stream instead)
     const bool serial = o.serial_fill || serial_fill_env();
     if (!serial) fill_nearfield_begin(h, bs.side, o.storage, o.mem_budget_bytes, nf);
-    if (!base) {
+    if (interp) {
+      int r = 1;
+      for (int c = 0; c < d; c++) r *= o.interp_p;
+      h->r = r;
+      mark(3);
+      mark(4);
+    } else if (!base) {
       h->r = calibrated ? calibrate_end(h, cal) : o.r_override;  // a5
       mark(3);
       hidr_up(h);  // a6
@@ -315,7 +325,8 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
       mark(4);
     }
     mark(5);
-    id_sweep(h);  // a8
+    if (interp) interp_sweep(h, o.interp_p);  // Eq. (2.2) bases instead of a8
+    else id_sweep(h);                         // a8
     mark(6);
     fill_coupling(h, o.storage, o.mem_budget_bytes, nf);  // a9
     if (serial) fill_nearfield_begin(h, h->stream, o.storage, o.mem_budget_bytes, nf);
@@ -332,9 +343,11 @@ static h2_handle* build_impl(const double* points, int64_t n, int32_t d, int32_t
       h->hidr_dist_evals = (int64_t)(stats[kStatHidrUp] + stats[kStatHidrDown]);
       h->hidr_dist_done = (int64_t)stats[kStatHidrDone];
     }
-    h->kmax = (int)stats[kStatKmax];
-    h->id_kernel_evals = (int64_t)(stats[kStatIdEvals] + stats[kStatIdEvalsCol]);
-    h->kmax_col = h->nonsym ? (int)stats[kStatKmaxCol] : h->kmax;
+    if (!interp) {
+      h->kmax = (int)stats[kStatKmax];
+      h->id_kernel_evals = (int64_t)(stats[kStatIdEvals] + stats[kStatIdEvalsCol]);
+      h->kmax_col = h->nonsym ? (int)stats[kStatKmaxCol] : h->kmax;
+    }
     if (h->timing) {
       nf.finish_timing(h);
       for (int i = 0; i < 6; i++) cudaEventElapsedTime(&h->stage_ms[i], ev[i], ev[i + 1]);
@@ -569,6 +582,14 @@ static std::vector<char> export_bytes(const h2_handle* h, int what) {
         v.push_back(lr.end);
       }
       return bytes(v.data(), 8 * v.size());
+    }
+    case H2_EXPORT_INTERP_Q: {
+      if (!h->Xq) break;
+      auto v = d2h(h->Xq, (size_t)h->nq * d, s);
+      std::vector<double> out((size_t)h->nq * d);
+      for (int64_t t = 0; t < h->nq; t++)
+        for (int c = 0; c < d; c++) out[(size_t)t * d + c] = v[(size_t)c * h->nq + t];
+      return bytes(out.data(), 8 * out.size());
     }
     case H2_EXPORT_TREE_X: {
       auto v = d2h(h->X, (size_t)n * d, s);

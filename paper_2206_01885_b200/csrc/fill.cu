@@ -378,12 +378,16 @@ static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_
     }
   } else {
     const int64_t blocks = ((np + 31) / 32 + 7) / 8;  // one warp per 32 pairs, 8 warps per CTA
+    // skeleton coordinates: the points, or the Chebyshev nodes of the interpolation baseline
+    const double* cXf = h->Xq ? h->Xq : h->Xf;
+    const double* cX = h->Xq ? h->Xq : h->X;
+    const int64_t cn = h->Xq ? h->nq : h->n;
     unsigned g = (unsigned)(blocks < ((int64_t)1 << 30) ? blocks : ((int64_t)1 << 30));
     switch (h->d) {
 #define H2_CP_CASE(DD)                                                                                        \
   case DD:                                                                                                    \
     cp_fill_kernel<DD, KID><<<g, kFillThreads, 0, s>>>(np, pairs, voff, h->k, h->sk, h->k_col, h->sk_col, h->r,  \
-                                                       h->Xf, h->X, h->n, cs, out);                            \
+                                                       cXf, cX, cn, cs, out);                                  \
     break;
       H2_CP_CASE(1) H2_CP_CASE(2) H2_CP_CASE(3) H2_CP_CASE(4)
       H2_CP_CASE(5) H2_CP_CASE(6) H2_CP_CASE(7) H2_CP_CASE(8)

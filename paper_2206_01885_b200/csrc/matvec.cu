@@ -574,7 +574,8 @@ static void launch_far_near(const h2_handle* h, double p2, const double* zh, dou
   } else if (which == 0 && h->n_cp > 0) {
     unsigned g = (unsigned)(h->n_cp < 148 * 64 ? h->n_cp : 148 * 64);
     coupling_kernel<D><<<g, kMvThreads, 0, s>>>(h->n_cp, h->cp_pairs, h->cp_off, h->cp_stored ? h->cp_val : nullptr,
-                                                h->kid, p2, h->Xf, h->X, h->n, h->k, h->sk, h->k_col, h->sk_col, h->r,
+                                                h->kid, p2, h->Xq ? h->Xq : h->Xf, h->Xq ? h->Xq : h->X,
+                                                h->Xq ? h->nq : (int64_t)h->n, h->k, h->sk, h->k_col, h->sk_col, h->r,
                                                 !h->nonsym, zh, yh);
   }
   if (which == 1 && h->n_np > 0 && h->np_stored && h->nf_nunits > 0) {
