@@ -125,7 +125,7 @@ typedef struct h2_options {
   int32_t interp_p;        /* > 0: the INTERPOLATION-based H^2 instead (the baseline of PAPER section  */
                            /*    6.3; Eq. (2.2)): p Chebyshev points of the */
                            /*    first kind per dimension on every tree cell, r = p^d, U_i = L(X_i),  */
-                           /*    transfers L^(parent)(Q_c), B_ij = K(Q_i, Q_j) (readings I1-I4);      */
+                           /*    transfers L^(parent)(Q_c), B_ij = K(Q_i, Q_j) (readings Q1-Q4);      */
                            /*    no calibration / HiDR / ID (id_tol is validated but unused).         */
                            /*    1 <= p <= 16, p^d <= 4096; symmetric kernels, single GPU, no rebuild; */
                            /*    otherwise INVALID_ARG.  0 (default): the data-driven construction.   */

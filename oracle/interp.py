@@ -8,16 +8,16 @@ What it computes (Eq. (2.2)): interpolating kappa(x, y) in x
 Q = {q_1..q_r},  kappa(x, y) ~= sum_a kappa(q_a, y) L_a(x),  gives K_{X_i Y_i} ~= U_i K_{Q_i Y_i} with
 U_i = [L_a(x)]_{x in X_i, a = 1..r}.  "In three dimensions, the number of interpolation nodes is k^3
 if k interpolation nodes are used in each dimension": Q_i is a tensor grid of p
-Chebyshev nodes per dimension, r = p^d.  Readings (I1-I4):
-  I1  the interpolation box of node i is its cell of the tree (root cube of the partition, width
+Chebyshev nodes per dimension, r = p^d.  Readings (Q1-Q4):
+  Q1  the interpolation box of node i is its cell of the tree (root cube of the partition, width
       W 2^-l at level l); the nodes are the Chebyshev points of the first kind
       t_a = c + (w/2) z_a, z_a = cos((2a + 1) pi / (2p)), a = 0..p-1;
-  I2  multi-index alpha = sum_c a_c p^c (dimension 0 fastest); L_alpha(x) = prod_c l_{a_c}(x_c) with
+  Q2  multi-index alpha = sum_c a_c p^c (dimension 0 fastest); L_alpha(x) = prod_c l_{a_c}(x_c) with
       the 1-D Lagrange polynomial l_a(u) = prod_{b != a} (u - z_b) / (z_a - z_b) of u = (x - c)/(w/2);
-  I3  nested bases: a non-leaf node's U holds the stacked transfers R_c = [L^(p)_alpha(q)]_{q in Q_c}
+  Q3  nested bases: a non-leaf node's U holds the stacked transfers R_c = [L^(p)_alpha(q)]_{q in Q_c}
       of its children (child order) -- the layout of the data-driven U_p (Xbar_p = the children's
       skeletons, P:474-495), with the children's Chebyshev nodes in place of their skeletons;
-  I4  a node has a basis (k_i = r) iff it or an ancestor has an admissible pair (as the data-driven
+  Q4  a node has a basis (k_i = r) iff it or an ancestor has an admissible pair (as the data-driven
       k_i > 0 iff Y_i^* is non-empty); coupling blocks B_ij = K(Q_i, Q_j) for (i, j) in IL
       (symmetric kernels: stored for i < j), nearfield blocks K(X_i, X_j) as the data-driven build.
 Memory = the stored entries of U (leaves and transfers), the coupling blocks and the nearfield
@@ -33,13 +33,13 @@ from . import OracleH2, kernel_block
 
 
 def cheb_ref(p: int) -> np.ndarray:
-    """I1: z_a = cos((2a + 1) pi / (2p)), a = 0..p-1 (Chebyshev points of the first kind on [-1, 1])."""
+    """Q1: z_a = cos((2a + 1) pi / (2p)), a = 0..p-1 (Chebyshev points of the first kind on [-1, 1])."""
     a = np.arange(p, dtype=np.float64)
     return np.cos((2.0 * a + 1.0) * math.pi / (2.0 * p))
 
 
 def lagrange_1d(z: np.ndarray, u: np.ndarray) -> np.ndarray:
-    """I2: l_a(u) = prod_{b != a} (u - z_b) / (z_a - z_b), b ascending; shape (len(u), p)."""
+    """Q2: l_a(u) = prod_{b != a} (u - z_b) / (z_a - z_b), b ascending; shape (len(u), p)."""
     u = np.asarray(u, np.float64)
     p = len(z)
     out = np.ones((u.shape[0], p), np.float64)
@@ -51,7 +51,7 @@ def lagrange_1d(z: np.ndarray, u: np.ndarray) -> np.ndarray:
 
 
 def multi_index(p: int, d: int) -> np.ndarray:
-    """I2: row alpha holds (a_0, .., a_{d-1}) with alpha = sum_c a_c p^c."""
+    """Q2: row alpha holds (a_0, .., a_{d-1}) with alpha = sum_c a_c p^c."""
     al = np.arange(p ** d)
     return np.stack([(al // p ** c) % p for c in range(d)], axis=1)
 
@@ -101,20 +101,20 @@ class InterpH2:
         rlo, W = root_box(o.pts)
         self.z = cheb_ref(self.p)
         cells = o.cells()
-        # I1: the node boxes (levels in order: ids are level-order, parents before children)
+        # Q1: the node boxes (levels in order: ids are level-order, parents before children)
         self.center = np.zeros((self.nn, d))
         self.half = np.zeros(self.nn)
         for i in range(self.nn):
             w = math.ldexp(W, -int(self.level[i]))
             self.center[i] = (rlo + cells[i] * w) + 0.5 * w
             self.half[i] = 0.5 * w
-        # I4: bases exist where the node or an ancestor has an admissible pair
+        # Q4: bases exist where the node or an ancestor has an admissible pair
         self.k = np.zeros(self.nn, np.int64)
         for i in range(self.nn):
             far = self.il_off[i + 1] > self.il_off[i] or (self.parent[i] >= 0 and self.k[self.parent[i]] > 0)
             self.k[i] = self.r if far else 0
         self.Q = {i: cheb_points(self.center[i], self.half[i], self.z) for i in range(self.nn) if self.k[i] > 0}
-        # U_i: leaves L(X_i); non-leaves the stacked transfers of their children (I3)
+        # U_i: leaves L(X_i); non-leaves the stacked transfers of their children (Q3)
         self.U = {}
         for i in range(self.nn):
             if self.k[i] == 0:

@@ -1,5 +1,5 @@
 // interp.cu -- the interpolation-based H^2 of the paper's memory comparison (section 6.3,
-// P:1069-1098): bases from Eq. (2.2) instead of HiDR + ID.  Readings I1-I4
+// P:1069-1098): bases from Eq. (2.2) instead of HiDR + ID.  Readings Q1-Q4
 // (DESIGN.md section 3): p Chebyshev points of the first kind per dimension on every tree cell,
 // r = p^d; U_leaf = [L_alpha(x)]_{x in X_i}; a non-leaf node's U stacks the transfers
 // L^(i)_alpha(Q_c) of its children in the data-driven layout (Xbar_i = the children's nodes), so
@@ -13,7 +13,7 @@ struct RloArr {
   double v[kMaxD];
 };
 
-// I4, one level: k_i = r iff node i has an admissible pair or its parent has a basis
+// Q4, one level: k_i = r iff node i has an admissible pair or its parent has a basis
 __global__ void interp_k_kernel(int base, int count, const int64_t* __restrict__ il_off,
                                 const int* __restrict__ parent, int r, int* k) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -42,7 +42,7 @@ __global__ void interp_sizes_kernel(int nn, int r, const int* __restrict__ k, co
   child_off[i] = p >= 0 ? (i - first_child[p]) * r : 0;
 }
 
-// I1: z_a = cos((2a + 1) pi / (2p))
+// Q1: z_a = cos((2a + 1) pi / (2p))
 __device__ __forceinline__ double cheb_z(int a, int p) {
   return cos(__ddiv_rn(__dmul_rn(__dadd_rn(__dmul_rn(2.0, (double)a), 1.0), 3.141592653589793), __dmul_rn(2.0, (double)p)));
 }
@@ -76,7 +76,7 @@ __global__ void interp_nodes_kernel(int nn, int d, int p, int r, const int* __re
 }
 
 // U_i, one CTA per node with a basis: rows in chunks of kIpRows; per (row, dimension) the p 1-D
-// Lagrange values l_a(u), u = (x - centre)/half (I2, b ascending), into shared memory; then the
+// Lagrange values l_a(u), u = (x - centre)/half (Q2, b ascending), into shared memory; then the
 // entries L_alpha = prod_c l_{a_c} (c ascending), row index fastest (column-major U, coalesced).
 constexpr int kIpRows = 32, kIpThreads = 256;
 __global__ void __launch_bounds__(kIpThreads) interp_u_kernel(int nn, int d, int p, int r, const int* __restrict__ k,

@@ -1,6 +1,6 @@
 """GPU parity of the interpolation baseline (h2_options.interp_p; interp.cu) against oracle/interp.py.
 
-PAPER.md Eq. (2.2), section 6.3; readings I1-I4.
+PAPER.md Eq. (2.2), section 6.3; readings Q1-Q4.
 Structure (tree, lists, k_i, |Xbar_i|) is compared exactly, the Chebyshev nodes and U element by
 element (the two sides share the operation order; only cos may differ in the last bit), the matvec
 against the oracle's interpolation matvec and against dense K x, and the stored entry counts against
