@@ -44,8 +44,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(LIBDIR, "obj")
     os.makedirs(objdir, exist_ok=True)
 
+    headers = [p for p in _deps() if not p.endswith(".cu")]
+    hdr_t = max(os.path.getmtime(p) for p in headers)
+
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        # incremental: an object newer than its source and every header is kept
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_t):
+            return obj
         cmd = [NVCC, *NVCC_FLAGS, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

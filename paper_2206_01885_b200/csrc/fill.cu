@@ -228,14 +228,17 @@ __global__ void __launch_bounds__(kNfThreads, MINB * kNfScale) nf_fill_kernel(in
   }
 }
 
-// ---- coupling: one warp per 32 consecutive pairs, entries flattened ---------------------------
+// ---- coupling: S warps per 32 consecutive pairs, entries flattened -----------------------------
 // Coupling blocks are small (k_i x k_j, ranks of a few to a few tens), so per-pair work is a
-// chain of dependent loads (pair -> ranks, offset -> skeleton indices -> coordinates).  A warp
-// takes 32 consecutive pairs at once: lane t loads pair t's metadata (one round of latency for
-// all 32), a warp scan gives the pairs' entry prefix, then the warp walks the concatenated
-// entries -- which are also consecutive in the output (blocks are stored in pair order), so every
-// store instruction writes 256 contiguous bytes -- each lane gathering its entry's two skeleton
-// points (L2-resident) and evaluating the kernel.
+// chain of dependent loads (pair -> ranks, offset -> skeleton indices -> coordinates).  A group of
+// 32 consecutive pairs is taken by S warps at once: lane t of each loads pair t's metadata (one
+// round of latency for all 32), a warp scan gives the pairs' entry prefix, then warp `sl` of the
+// S walks every S-th 32-entry row of the group's concatenated entries -- which are also
+// consecutive in the output (blocks are stored in pair order), so every store instruction writes
+// 256 contiguous bytes -- each lane gathering its entry's two skeleton points (L2-resident) and
+// evaluating the kernel.  S (host: ~256 entries per warp) sets how many independent dependent-load
+// chains are in flight: with one warp per group a group of ~8K entries was a 256-step serial chain
+// and the whole fill a few thousand such chains (latency-bound, ~1 TB/s).
 template <int D, int KID>
 __global__ void __launch_bounds__(kFillThreads) cp_fill_kernel(int64_t np, const int2* __restrict__ pairs,
                                                                const int64_t* __restrict__ voff,
@@ -244,14 +247,16 @@ __global__ void __launch_bounds__(kFillThreads) cp_fill_kernel(int64_t np, const
                                                                const int* __restrict__ skc, int r,
                                                                const double* __restrict__ Xf,
                                                                const double* __restrict__ X, int64_t n,
-                                                               double cs, double* __restrict__ out) {
+                                                               double cs, int S, double* __restrict__ out) {
   __shared__ double tab[kFillTab];
   for (int e = threadIdx.x; e < kFillTab; e += blockDim.x) tab[e] = kExp2Tab2048[e];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t nunits = (np + 31) >> 5;
+  const int64_t nunits = ((np + 31) >> 5) * S;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < nunits; u += nw) {
+  for (int64_t us = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; us < nunits; us += nw) {
+    const int64_t u = us / S;
+    const int sl = (int)(us - u * S);
     const int64_t p = (u << 5) + lane;
     int pi = 0, pj = 0, ki = 0, kj = 0;
     if (p < np) {
@@ -270,7 +275,7 @@ __global__ void __launch_bounds__(kFillThreads) cp_fill_kernel(int64_t np, const
     const int total = __shfl_sync(0xffffffffu, pre, 31);
     pre -= sz;  // exclusive
     double* o = out + voff[u << 5];
-    for (int e0 = 0; e0 < total; e0 += 32) {  // warp-uniform trip count: every shuffle is converged
+    for (int e0 = 32 * sl; e0 < total; e0 += 32 * S) {  // warp-uniform trip count: every shuffle is converged
       const int e = e0 + lane;
       // this entry's pair: the largest q with pre[q] <= e (size-0 pairs never win)
       int q = 0;
@@ -377,7 +382,11 @@ static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_
 #undef H2_NF_ARGS
     }
   } else {
-    const int64_t blocks = ((np + 31) / 32 + 7) / 8;  // one warp per 32 pairs, 8 warps per CTA
+    // S warps per 32 pairs (~256 entries per warp), 8 warps per CTA
+    const int64_t groups = (np + 31) / 32;
+    const int64_t epg = (h->cp_entries + groups - 1) / groups;
+    const int S = (int)(epg / 256 < 1 ? 1 : (epg / 256 > 64 ? 64 : epg / 256));
+    const int64_t blocks = (groups * S + 7) / 8;
     // skeleton coordinates: the points, or the Chebyshev nodes of the interpolation baseline
     const double* cXf = h->Xq ? h->Xq : h->Xf;
     const double* cX = h->Xq ? h->Xq : h->X;
@@ -387,7 +396,7 @@ static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_
 #define H2_CP_CASE(DD)                                                                                        \
   case DD:                                                                                                    \
     cp_fill_kernel<DD, KID><<<g, kFillThreads, 0, s>>>(np, pairs, voff, h->k, h->sk, h->k_col, h->sk_col, h->r,  \
-                                                       cXf, cX, cn, cs, out);                                  \
+                                                       cXf, cX, cn, cs, S, out);                               \
     break;
       H2_CP_CASE(1) H2_CP_CASE(2) H2_CP_CASE(3) H2_CP_CASE(4)
       H2_CP_CASE(5) H2_CP_CASE(6) H2_CP_CASE(7) H2_CP_CASE(8)
