@@ -11,6 +11,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "cpqr.cuh"
 #include "cpqr_panel.cuh"
 #include "vol.cuh"
@@ -29,6 +31,7 @@ struct CalWork {  // per-trial global workspace
   int ns, k;  // |Z2^*| and the ID rank, passed between the trial's launches
   int panel;  // 1: the panel CPQR ran (columns never moved: position c is physical column piv[c])
   double pnum[8], pden[8];  // the error's partial sums per column slice (calib_err_kernel)
+  int lv;     // the trial's virtual level (calib_cpqr_cluster_kernel's cancellation test)
 };
 constexpr int kErrSlices = 8;  // CTAs per trial of the error evaluation: N / 8 = 32 columns each
 
@@ -119,7 +122,10 @@ __global__ void __launch_bounds__(kCalThreads) calib_prep_kernel(int kid, double
   }
   __syncthreads();
   const int ns = s_ns;
-  if (tid == 0) W.ns = ns;
+  if (tid == 0) {
+    W.ns = ns;
+    W.lv = lv[blockIdx.x];
+  }
   // M = K(Z1, Z2*)^T : ns x N column-major (columns = Z1 candidates)
   for (int e = tid; e < ns * N; e += kCalThreads) {
     int a = e % ns, b = e / ns;
@@ -145,6 +151,220 @@ __global__ void __launch_bounds__(kCalCpqrThreads) calib_cpqr_kernel(double eps,
     W.k = k;
     W.panel = use_panel;
   }
+}
+
+// The trial's ID on a thread-block cluster (default; H2_CAL_CLUSTER=0 restores the one-CTA kernel
+// above): M (ns x 256) is too large for one SM's shared memory and on one SM every pivot step
+// re-reads it from L2 (the one-CTA kernel is L2-latency- and barrier-bound: ~10 us per step).
+// Here kCalCl CTAs each hold kCalClW = 256 / kCalCl consecutive columns (Z1 candidates) in shared
+// memory, column-major, for the whole factorisation.  The algorithm and tie rule of cta_cpqr
+// (unblocked Householder, residual norms recomputed after every update, pivot = largest norm, ties
+// to the lowest position, stop when it is < tol * |R11|), with a position map instead of column
+// swaps.  One cluster barrier per pivot step: after it every CTA reads the CTAs' candidates (DSMEM)
+// and picks the same pivot, reads the pivot column straight from its owner's shared memory, builds
+// the Householder vector (the same arithmetic in every CTA) and updates its own live columns.  The
+// owner writes the pivot's diagonal alpha only after the next barrier (the others read the column
+// until then).  At the end the slices go back to W.M and T = R11^{-1} R12 is formed column by column
+// from R11 in global memory.  Output as the panel kernel's (W.panel = 1): columns in place,
+// W.piv[position] = physical column.
+constexpr int kCalCl = 8;                    // CTAs per trial (portable cluster size)
+constexpr int kCalClNT = 256;
+constexpr int kCalClW = N / kCalCl;          // columns per CTA (= 32: one lane per column in publish)
+static_assert(kCalClW == 32, "one lane per own column");
+struct CalClCand {
+  double x;   // sqrt of the residual norm^2 (-1: no live column)
+  int pos;    // position in the pivot order
+  int j;      // physical column
+  int abort;  // (rank 0's candidate) the trial is cancelled
+};
+// dynamic shared memory: the slice (ns x kCalClW) + v (ns); ns < N
+constexpr int kCalClSmem = (int)sizeof(double) * (N * kCalClW + N);
+
+__global__ void __cluster_dims__(kCalCl, 1, 1) __launch_bounds__(kCalClNT) calib_cpqr_cluster_kernel(double eps,
+                                                                                                    CalWork* work,
+                                                                                                    const int* cancel) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  constexpr int NT = kCalClNT, NW = NT / 32, WC = kCalClW;
+  CalWork& W = work[blockIdx.x / kCalCl];
+  const int ns = W.ns;
+  if (ns < 0) return;  // a skipped trial: every CTA of the cluster leaves (no cluster barrier reached)
+  const int q = (int)cl.block_rank(), j0 = q * WC;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double tol = 1e-3 * eps;
+  extern __shared__ double sh[];
+  double* Ms = sh;               // own columns: Ms[a + ns * jl] = M[a, j0 + jl]
+  double* v = Ms + ns * WC;      // Householder vector (rows t..ns-1)
+  __shared__ double nrm2[WC];
+  __shared__ int pos[WC];        // own column -> position
+  __shared__ int col_at[N];      // position -> physical column (replicated in every CTA)
+  __shared__ CalClCand cand[2];  // this CTA's candidate by step parity (read by every CTA)
+  __shared__ CalClCand best_s;
+  __shared__ CpqrSmem<NT> csm;
+  for (int e = tid; e < ns * WC; e += NT) Ms[e] = W.M[(int64_t)ns * j0 + e];
+  for (int b = tid; b < N; b += NT) col_at[b] = b;
+  if (tid < WC) pos[tid] = j0 + tid;
+  __syncthreads();
+  for (int jl = warp; jl < WC; jl += NW) {
+    const double* col = Ms + ns * jl;
+    double s = 0.0;
+    for (int a = lane; a < ns; a += 32) s += col[a] * col[a];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) nrm2[jl] = s;
+  }
+  __syncthreads();
+  auto publish = [&](int tt) {  // lane jl = own column jl
+    if (warp == 0) {
+      const int ps = pos[lane];
+      double bx = ps >= tt ? sqrt(nrm2[lane]) : -1.0;
+      int bp = ps >= tt ? ps : INT_MAX, bj = ps >= tt ? j0 + lane : -1;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double x2 = __shfl_xor_sync(0xffffffffu, bx, o);
+        const int p2_ = __shfl_xor_sync(0xffffffffu, bp, o);
+        const int j2 = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (x2 > bx || (x2 == bx && p2_ < bp)) {
+          bx = x2;
+          bp = p2_;
+          bj = j2;
+        }
+      }
+      // cancellation (speculative phase 1, calibrate_begin): the trial's level passed in phase 0.
+      // Rank 0 alone reads the flag, so every CTA of the cluster takes the same decision.
+      int ab = 0;
+      if (cancel && q == 0 && lane == 0) ab = *reinterpret_cast<const volatile int*>(cancel + W.lv);
+      if (lane == 0) cand[tt & 1] = CalClCand{bx, bp, bj, ab};
+    }
+  };
+  publish(0);
+  const int kmax = ns < N ? ns : N;
+  double r11 = 0.0;
+  int k = 0;
+  bool aborted = false;
+  int pend_jl = -1, pend_row = 0;
+  double pend_alpha = 0.0;
+  for (int tt = 0; tt < kmax; tt++) {
+    cl.sync();  // candidates published, the previous step's updates done, its pivot column read
+    if (pend_jl >= 0 && tid == 0) Ms[ns * pend_jl + pend_row] = pend_alpha;
+    pend_jl = -1;
+    if (warp == 0) {
+      CalClCand c{-1.0, INT_MAX, -1, 0};
+      if (lane < kCalCl) c = *cl.map_shared_rank(&cand[tt & 1], lane);
+      const int ab = __shfl_sync(0xffffffffu, c.abort, 0);
+      for (int o = 16; o > 0; o >>= 1) {
+        const double x2 = __shfl_xor_sync(0xffffffffu, c.x, o);
+        const int p2_ = __shfl_xor_sync(0xffffffffu, c.pos, o);
+        const int j2 = __shfl_xor_sync(0xffffffffu, c.j, o);
+        if (x2 > c.x || (x2 == c.x && p2_ < c.pos)) c = CalClCand{x2, p2_, j2, 0};
+      }
+      c.abort = ab;
+      if (lane == 0) best_s = c;
+    }
+    __syncthreads();
+    const CalClCand b = best_s;
+    const double nrm = b.x;
+    if (b.abort) {
+      aborted = true;
+      break;
+    }
+    if (tt == 0) {
+      r11 = nrm;
+      if (r11 == 0.0) break;
+    }
+    if (b.j < 0 || nrm < tol * r11) break;
+    const int p = b.j, owner = p / WC;
+    const double* src = cl.map_shared_rank(Ms, owner) + ns * (p - owner * WC);  // DSMEM
+    const double x0 = src[tt];
+    const double alpha = x0 >= 0.0 ? -nrm : nrm;
+    double part = 0.0;
+    for (int a = tt + tid; a < ns; a += NT) {
+      const double vi = a == tt ? x0 - alpha : src[a];
+      v[a] = vi;
+      part += vi * vi;
+    }
+    const double vtv = cta_sum<NT>(part, csm);  // its barriers publish v
+    if (q == owner) {
+      pend_jl = p - j0;
+      pend_row = tt;
+      pend_alpha = alpha;
+    }
+    if (tid == 0) {  // position map: the column at position tt moves to the pivot's position
+      const int jt = col_at[tt];
+      col_at[b.pos] = jt;
+      col_at[tt] = p;
+      if (jt >= j0 && jt < j0 + WC) pos[jt - j0] = b.pos;
+      if (p >= j0 && p < j0 + WC) pos[p - j0] = tt;
+    }
+    __syncthreads();
+    for (int jl = warp; jl < WC; jl += NW) {  // own live columns: reflector, residual norm (rows > tt)
+      if (pos[jl] <= tt) continue;
+      double* col = Ms + ns * jl;
+      double nn = 0.0;
+      if (vtv > 0.0) {
+        double s0 = 0.0, s1 = 0.0;
+        int a = tt + lane;
+        for (; a + 32 < ns; a += 64) {
+          s0 += v[a] * col[a];
+          s1 += v[a + 32] * col[a + 32];
+        }
+        for (; a < ns; a += 32) s0 += v[a] * col[a];
+        double sd = s0 + s1;
+        for (int o = 16; o > 0; o >>= 1) sd += __shfl_xor_sync(0xffffffffu, sd, o);
+        const double f = 2.0 * sd / vtv;
+        for (a = tt + lane; a < ns; a += 32) {
+          const double x = col[a] - f * v[a];
+          col[a] = x;
+          if (a > tt) nn += x * x;
+        }
+      } else {
+        for (int a = tt + 1 + lane; a < ns; a += 32) nn += col[a] * col[a];
+      }
+      for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+      if (lane == 0) nrm2[jl] = nn;
+    }
+    k = tt + 1;
+    __syncthreads();
+    publish(tt + 1);
+  }
+  if (pend_jl >= 0 && tid == 0) Ms[ns * pend_jl + pend_row] = pend_alpha;
+  __syncthreads();
+  for (int e = tid; e < ns * WC; e += NT) W.M[(int64_t)ns * j0 + e] = Ms[e];
+  cl.sync();  // every R column in global memory, visible cluster-wide; no DSMEM read after this
+  // T = R11^{-1} R12 for the own columns at positions >= k: a warp per column, x in shared memory
+  // (the slice's space), column-oriented back substitution with R11's columns read contiguously
+  if (aborted) k = 0;  // a cancelled trial: rank 0, no T (its pass flag is never used)
+  double* xw = Ms + (int64_t)warp * N;
+  for (int jl = warp; jl < WC && !aborted; jl += NW) {
+    if (pos[jl] < k) continue;
+    const int pj = j0 + jl;
+    for (int a = lane; a < k; a += 32) xw[a] = W.M[a + (int64_t)ns * pj];
+    __syncwarp();
+    for (int l = k - 1; l >= 0; l--) {
+      const double* Rl = W.M + (int64_t)ns * col_at[l];  // R11[0:l+1, l]
+      const double xl = xw[l] / Rl[l];
+      for (int a = lane; a < l; a += 32) xw[a] -= Rl[a] * xl;
+      __syncwarp();
+      if (lane == 0) xw[l] = xl;
+      __syncwarp();
+    }
+    for (int a = lane; a < k; a += 32) W.M[a + (int64_t)ns * pj] = xw[a];
+    __syncwarp();
+  }
+  if (q == 0) {
+    for (int b = tid; b < N; b += NT) W.piv[b] = col_at[b];
+    if (tid == 0) {
+      W.k = k;
+      W.panel = 1;
+    }
+  }
+}
+
+// H2_CAL_CLUSTER=0 (A/B knob, read once): the one-CTA trial ID kernel instead of the cluster one
+static int cal_cluster() {
+  static const int v = [] {
+    const char* e = getenv("H2_CAL_CLUSTER");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
 }
 
 // Ks[t][e] = K(Z1[piv[t]], Z2[e]) for the k skeleton rows
@@ -277,7 +497,7 @@ static int cal_panel() {
 // (page-locked) once the stream has reached the end of the batch.
 static void launch_trials(h2_handle* h, cudaStream_t s, int slot, const std::vector<double>& wl,
                           const std::vector<int>& lv, const std::vector<int>& mv, const int* skip_level,
-                          CalibSet& job) {
+                          CalibSet& job, const int* cancel = nullptr) {
   const int T = (int)wl.size();
   job.T = T;
   if (T == 0) return;
@@ -300,6 +520,9 @@ static void launch_trials(h2_handle* h, cudaStream_t s, int slot, const std::vec
   std::memcpy(hin + sizeof(double) * T, lv.data(), sizeof(int) * T);
   std::memcpy(hin + sizeof(double) * T + sizeof(int) * T, mv.data(), sizeof(int) * T);
   H2_CUDA_TRY(cudaMemcpyAsync(dw, hin, in_bytes, cudaMemcpyHostToDevice, s));
+  if (cal_cluster())
+    H2_CUDA_TRY(cudaFuncSetAttribute(calib_cpqr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kCalClSmem));
   for (int b0 = 0; b0 < T; b0 += batch) {
     int nb = T - b0 < batch ? T - b0 : batch;
     switch (d) {
@@ -307,7 +530,10 @@ static void launch_trials(h2_handle* h, cudaStream_t s, int slot, const std::vec
   case DD:                                                                                                \
     calib_prep_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, h->tau, dw + b0, dl + b0, dm + b0,         \
                                                      skip_level, sh, job.work.as<CalWork>());              \
-    calib_cpqr_kernel<<<nb, kCalCpqrThreads, 0, s>>>(h->id_tol, cal_panel(), job.work.as<CalWork>());     \
+    if (cal_cluster()) calib_cpqr_cluster_kernel<<<nb * kCalCl, kCalClNT, kCalClSmem, s>>>(h->id_tol,        \
+                                                                                job.work.as<CalWork>(),    \
+                                                                                cancel);                   \
+    else calib_cpqr_kernel<<<nb, kCalCpqrThreads, 0, s>>>(h->id_tol, cal_panel(), job.work.as<CalWork>());  \
     calib_ks_kernel<DD><<<nb, kCalThreads, 0, s>>>(h->kid, p2, job.work.as<CalWork>());                    \
     calib_err_kernel<DD><<<nb * kErrSlices, kCalThreads, 0, s>>>(h->kid, p2, job.work.as<CalWork>());        \
     break;
@@ -369,9 +595,26 @@ void calibrate_begin(h2_handle* h, cudaStream_t s, cudaStream_t s2, CalibJob& jo
   if (s2) H2_CUDA_TRY(cudaStreamSynchronize(s2));
   job.passed = Scratch(sizeof(int) * 64, s);
   H2_CUDA_TRY(cudaMemsetAsync(job.passed.p, 0, sizeof(int) * 64, s));
+  if (job.split) {  // phase 1 reads `passed` (its cancellation flags): only after the clear above
+    cudaEvent_t clr;
+    H2_CUDA_TRY(cudaEventCreateWithFlags(&clr, cudaEventDisableTiming));
+    H2_CUDA_TRY(cudaEventRecord(clr, s));
+    H2_CUDA_TRY(cudaStreamWaitEvent(s2, clr, 0));
+    cudaEventDestroy(clr);
+  }
   launch_trials(h, s, 0, wl, lv, mv, nullptr, job.p0);
   if (job.split) {
-    launch_trials(h, s2, 1, wl1, lv1, mv1, nullptr, job.p1);
+    // the speculative phase 1 runs concurrently with phase 0; a phase-1 trial whose level passed
+    // in phase 0 stops at its next pivot step (the flags land as phase 0 ends), so an unneeded
+    // phase 1 does not keep the SMs busy into the next stages or the next build
+    if (job.p0.T > 0) {
+      const int* dl = reinterpret_cast<const int*>(job.p0.params.as<double>() + job.p0.T);
+      const int* dpass = reinterpret_cast<const int*>(job.p0.outs.as<double>() + job.p0.T);
+      level_passed_kernel<<<(job.p0.T + 127) / 128, 128, 0, s>>>(job.p0.T, dl, dpass, job.passed.as<int>());
+      H2_CHECK_LAUNCH();
+      h->gpu_launches += 1;
+    }
+    launch_trials(h, s2, 1, wl1, lv1, mv1, nullptr, job.p1, job.passed.as<int>());
   } else if (!wl1.empty()) {
     if (job.p0.T > 0) {
       const int* dl = reinterpret_cast<const int*>(job.p0.params.as<double>() + job.p0.T);
@@ -433,7 +676,7 @@ int calibrate_end(h2_handle* h, CalibJob& job) {
     set->params = Scratch();
     set->outs = Scratch();
   }
-  job.passed.s = s;
+  job.passed.s = (job.split && !awaited) ? job.stream2 : s;  // (an unawaited phase 1 still reads it)
   job.passed = Scratch();
   job.active = false;
   int r = 1;
