@@ -505,7 +505,9 @@ static bool hidr_down_level_pruned(h2_handle* h, int l, unsigned long long* ev, 
   return true;
 }
 
-static void hidr_level(h2_handle* h, int mode, int l, unsigned long long* ev) {
+// `pre`: a buffer known to hold the level's gathered candidate lists (hidr_up's bound), so the
+// level needs no host readback of their total and the up sweep is issued without a synchronisation
+static void hidr_level(h2_handle* h, int mode, int l, unsigned long long* ev, int* pre = nullptr) {
   cudaStream_t s = h->stream;
   const LevelRange lr = level_range(h, l);
   int base = lr.begin, count = lr.end - lr.begin;
@@ -516,28 +518,31 @@ static void hidr_level(h2_handle* h, int mode, int l, unsigned long long* ev) {
                                                              h->il_idx, h->xs_cnt, h->ys_cnt, sizes.as<int64_t>());
   scan_excl_i64(sizes.as<int64_t>(), off.as<int64_t>(), count + 1, s);
   H2_CHECK_LAUNCH();
-  int64_t total = read1(off.as<int64_t>() + count, s);
-  Scratch list(sizeof(int) * (total > 0 ? total : 1), s);
+  const bool bounded = pre && h->reduct == H2_REDUCT_VOLUME;
+  const int64_t total = bounded ? 0 : read1(off.as<int64_t>() + count, s);
+  Scratch list;
+  if (!bounded) list = Scratch(sizeof(int) * (total > 0 ? total : 1), s);
+  int* const lp = bounded ? pre : list.as<int>();  // (`pre` is not owned: hidr_up releases it)
   hidr_gather_kernel<<<count, kHidrThreads, 0, s>>>(mode, base, off.as<int64_t>(), h->is_leaf, h->nbegin,
                                                     h->first_child, h->nchild, h->parent, h->il_off, h->il_idx,
-                                                    h->xs_cnt, h->xs, h->ys_cnt, h->ys, h->r, list.as<int>());
+                                                    h->xs_cnt, h->xs, h->ys_cnt, h->ys, h->r, lp);
   H2_CHECK_LAUNCH();
   if (h->reduct == H2_REDUCT_SURFACE) {
     const int nq = (int)(h->surf_dirs_n);
     if (h->d == 2)
-      hidr_surface_kernel<2><<<count, kHidrThreads, 0, s>>>(h->X, h->n, base, off.as<int64_t>(), list.as<int>(),
+      hidr_surface_kernel<2><<<count, kHidrThreads, 0, s>>>(h->X, h->n, base, off.as<int64_t>(), lp,
                                                             h->r, h->surf_dirs, nq, mode == 0 ? h->xs_cnt : h->ys_cnt,
                                                             mode == 0 ? h->xs : h->ys, ev);
     else
-      hidr_surface_kernel<3><<<count, kHidrThreads, 0, s>>>(h->X, h->n, base, off.as<int64_t>(), list.as<int>(),
+      hidr_surface_kernel<3><<<count, kHidrThreads, 0, s>>>(h->X, h->n, base, off.as<int64_t>(), lp,
                                                             h->r, h->surf_dirs, nq, mode == 0 ? h->xs_cnt : h->ys_cnt,
                                                             mode == 0 ? h->xs : h->ys, ev);
   } else if (h->reduct == H2_REDUCT_FPS) {
     Scratch mind(sizeof(double) * (total > 0 ? total : 1), s);
-    launch_fps(h->d, count, s, h->X, h->n, base, off.as<int64_t>(), list.as<int>(), h->r,
+    launch_fps(h->d, count, s, h->X, h->n, base, off.as<int64_t>(), lp, h->r,
                mode == 0 ? h->xs_cnt : h->ys_cnt, mode == 0 ? h->xs : h->ys, mind.as<double>(), ev);
   } else {
-    launch_vol(h->d, count, s, h->X, h->n, base, off.as<int64_t>(), list.as<int>(), h->r,
+    launch_vol(h->d, count, s, h->X, h->n, base, off.as<int64_t>(), lp, h->r,
                mode == 0 ? h->xs_cnt : h->ys_cnt, mode == 0 ? h->xs : h->ys, ev);
   }
   H2_CHECK_LAUNCH();
@@ -594,8 +599,20 @@ void hidr_up(h2_handle* h) {
   H2_CUDA_TRY(cudaMemsetAsync(h->ys_cnt, 0, sizeof(int) * h->nnodes, h->stream));
   Scratch ev(sizeof(unsigned long long), h->stream);
   H2_CUDA_TRY(cudaMemsetAsync(ev.p, 0, sizeof(unsigned long long), h->stream));
+  // The up sweep's candidate sets S_i: a leaf's points or the children's X_c^* (<= r each), so a
+  // level's lists hold at most n + count * (2^d) * r indices.  One buffer of the largest bound
+  // serves every level (stream-ordered), when it is modest; else each level reads its total back.
+  int64_t bound = 0;
+  for (int l = 0; l <= h->depth; l++) {
+    const LevelRange lr = level_range(h, l);
+    const int64_t ch = h->d >= 8 ? 256 : (1LL << h->d);
+    const int64_t b = (int64_t)h->n + (int64_t)(lr.end - lr.begin) * ch * h->r;
+    bound = b > bound ? b : bound;
+  }
+  const bool use_bound = h->reduct == H2_REDUCT_VOLUME && bound * (int64_t)sizeof(int) <= ((int64_t)512 << 20);
+  Scratch pre(use_bound ? sizeof(int) * (size_t)bound : 0, h->stream);
   for (int l = h->depth; l >= 0; l--) {
-    hidr_level(h, 0, l, ev.as<unsigned long long>());
+    hidr_level(h, 0, l, ev.as<unsigned long long>(), use_bound ? pre.as<int>() : nullptr);
     if (h->nranks > 1 && l == h->cut) {
       // sharded: every rank's X^* of the levels >= cut, then their boxes (hidr_down.cuh)
       exchange_slots(h, h->xs_cnt, h->xs);

@@ -64,13 +64,22 @@ __host__ __device__ __forceinline__ int64_t id_smem_bytes(int ny, int nx, int d)
 constexpr int kIdLeanThreads = 512;
 constexpr int kIdLeanMax = 226 * 1024;  // dynamic shared memory of that class (+ the small static part)
 constexpr int kIdLean = kIdClasses;      // its class number
-__host__ __device__ __forceinline__ int64_t id_smem_bytes_lean(int ny, int nx) {
-  return 8LL * id_block_doubles(ny, nx, 512) + 8LL * nx + 512;
+__host__ __device__ __forceinline__ int64_t id_smem_bytes_lean(int ny, int nx, int nt = 512) {
+  return 8LL * id_block_doubles(ny, nx, nt) + 8LL * nx + 512;
 }
-// what a lean node asks for: its footprint plus staged coordinates when both fit the class
-__host__ __device__ __forceinline__ int64_t id_lean_request(int ny, int nx, int d) {
-  const int64_t b = id_smem_bytes_lean(ny, nx), bs = b + 8LL * d * (nx + ny);
-  return bs <= kIdLeanMax ? bs : b;
+// The mid class (class kIdMid = kIdClasses - 1): blocks between the staged classes and the lean one
+// (e.g. configs[1]'s 64 x ~208 leaves: 115 KB staged, 108 KB lean) run with the lean layout on 256
+// threads, two CTAs per SM, instead of one 512-thread CTA per SM (a wide block's row-major CPQR has a
+// thread per column, so 512 threads leave most idle while the SM holds a single node)
+constexpr int kIdMid = kIdClasses - 1;
+constexpr int kIdMidThreads = 256;
+constexpr int kIdMidMax = 110 * 1024;
+__host__ __device__ __forceinline__ int id_class_threads(int c);
+// what a lean (or mid) node asks for: its footprint plus staged coordinates when both fit the class
+__host__ __device__ __forceinline__ int64_t id_lean_request(int ny, int nx, int d, int nt = 512) {
+  const int64_t cap = nt >= 512 ? kIdLeanMax : kIdMidMax;
+  const int64_t b = id_smem_bytes_lean(ny, nx, nt), bs = b + 8LL * d * (nx + ny);
+  return bs <= cap ? bs : b;
 }
 // Layout of a shared-memory block: row-major with a thread per column (cta_cpqr_rm) unless the
 // block is tall enough that a warp per column (cta_cpqr, column-major) takes fewer serial steps:
@@ -81,11 +90,16 @@ __host__ __device__ __forceinline__ bool id_tall(int ny, int nx, int nt) {
   const int64_t cm = (int64_t)((nx + nt / 32 - 1) / (nt / 32)) * (ny / 32 + 24);
   return cm < rm;
 }
-// the node's class: 0..kIdClasses-1 (staged, <= kIdSmemMax), kIdLean, or -1 (global-memory path)
+// the node's class: 0..kIdMid-1 (staged, <= id_class_bound(kIdMid - 1)), kIdMid (lean layout, 256
+// threads, <= kIdMidMax), kIdLean, or -1 (global-memory path)
 __host__ __device__ __forceinline__ int id_smem_class(int ny, int nx, int d) {
   const int64_t b = id_smem_bytes(ny, nx, d);
-  if (b <= kIdSmemMax) return id_class(b);
+  if (b <= id_class_bound(kIdMid - 1)) return id_class(b);
+  if (id_smem_bytes_lean(ny, nx, kIdMidThreads) <= kIdMidMax) return kIdMid;
   return id_smem_bytes_lean(ny, nx) <= kIdLeanMax ? kIdLean : -1;
+}
+__host__ __device__ __forceinline__ int id_class_threads(int c) {
+  return c == kIdLean ? kIdLeanThreads : c == kIdMid ? kIdMidThreads : kIdSmemThreads;
 }
 
 // The largest blocks (>= kIdClusterMin entries) take the cluster path (id_kernel_cluster): on one
@@ -153,14 +167,15 @@ __global__ void id_sizes_kernel(int base, int count, int d, const int* __restric
   // -1 none
   id_path[i] = nx == 0 ? -1 : big ? 10 : cls >= 0 ? cls : (8LL * nx * ny < kIdBigBlock ? 8 : 9);
   if (nx > 0 && cls >= 0) {
-    atomicMax(smax + cls, (int)(cls == kIdLean ? id_lean_request(ny, nx, d) : id_smem_bytes(ny, nx, d)));
+    atomicMax(smax + cls, (int)(cls >= kIdMid ? id_lean_request(ny, nx, d, id_class_threads(cls))
+                                              : id_smem_bytes(ny, nx, d)));
     // which instantiations the class needs: bit 0 unblocked / row-major nodes, bit 1 panel nodes
-    const int pk = id_panel(ny, nx, cls == kIdLean ? kIdLeanThreads : kIdSmemThreads) ? 1 : 0;
+    const int pk = id_panel(ny, nx, id_class_threads(cls)) ? 1 : 0;
     atomicOr(smax + kIdClasses + 2 + cls, pk ? 2 : 1);
     // the launch lists: per (class, kind), and per kind over all staged classes (merged launch)
     const int li = cls * 2 + pk;
     lists[(int64_t)li * count + atomicAdd(lcnt + li, 1)] = t;
-    if (cls < kIdClasses) {
+    if (cls < kIdMid) {  // (the mid class has its own thread count: never merged)
       const int lm = 2 * (kIdClasses + 1) + pk;
       lists[(int64_t)lm * count + atomicAdd(lcnt + lm, 1)] = t;
     }
@@ -519,7 +534,7 @@ __global__ void __launch_bounds__(kIdClThreads) id_kernel_cluster(
 // PANEL: this instantiation runs the nodes whose blocks take the panel layout (id_panel); the other
 // one the rest (its registers stay at the unblocked CPQR's ~64, for occupancy)
 template <int D, int NT, bool PANEL>
-__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : (PANEL ? 6 : 8)) id_kernel_smem(
+__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : NT >= 256 ? 2 : (PANEL ? 6 : 8)) id_kernel_smem(
     int base, int kid, double p2, double tol, const double* __restrict__ Xf, const double* __restrict__ X, int64_t n,
     int d_unused, int r,
     const int* __restrict__ is_leaf, const int* __restrict__ nbegin, const int* __restrict__ first_child,
@@ -531,7 +546,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : (PANEL ? 6 : 8)) id_kernel
   __shared__ PanelSmem<NT, PANEL ? kIdPanelNb : 1> psm;
   __shared__ CpqrSmem<NT> csm_cm;
   __shared__ CpqrRmSmem<NT> csm;
-  constexpr bool kLean = NT == kIdLeanThreads;
+  constexpr bool kLean = NT >= kIdMidThreads;  // the lean layout (the lean and mid classes)
   const int tn = list[blockIdx.x];  // the launch's node list (id_sizes_kernel: this class and kind)
   const int i = base + tn;
   const int nx = xbar_n[i];
@@ -540,7 +555,8 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : (PANEL ? 6 : 8)) id_kernel
   if (nx == 0 || id_path[i] == 11) return;  // (id_kernel_warp's nodes)
   {  // cls < 0: every node of the staged classes (merged launch)
     const int nc = id_smem_class(ny, nx, D);
-    if (kLean ? nc != kIdLean : (nc < 0 || nc == kIdLean || (cls >= 0 && nc != cls))) return;
+    if (kLean ? nc != (NT == kIdLeanThreads ? kIdLean : kIdMid) : (nc < 0 || nc >= kIdMid || (cls >= 0 && nc != cls)))
+      return;
   }
   // the panel-blocked CPQR (cpqr_panel.cuh) when the node's columns fit the thread groups, else
   // the warp-per-column one (cpqr.cuh); both on A^T column-major, leading dimension ld <= ny + 15
@@ -566,7 +582,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : (PANEL ? 6 : 8)) id_kernel
   const bool staged = !kLean || [&] {
     unsigned dyn;
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
-    return id_smem_bytes_lean(ny, nx) + 8LL * D * (nx + ny) <= (int64_t)dyn;
+    return id_smem_bytes_lean(ny, nx, NT) + 8LL * D * (nx + ny) <= (int64_t)dyn;
   }();
   if (tid < 64) tab[tid] = kExp2Tab64[tid];
   if (is_leaf[i]) {
@@ -875,7 +891,7 @@ static void id_sweep_pass(h2_handle* h, const double* Xf, int stat_kmax, int sta
     // level run one after the other, and with few nodes each costs a node's full CPQR latency.
     // Merged when the level fits in about two waves at the largest class's occupancy.
     int smax_all = 0, ncls = 0;
-    for (int cls = 0; cls < kIdClasses; cls++) {
+    for (int cls = 0; cls < kIdMid; cls++) {
       smax_all = smem_bytes[cls] > smax_all ? smem_bytes[cls] : smax_all;
       ncls += smem_bytes[cls] > 0;
     }
@@ -886,8 +902,9 @@ static void id_sweep_pass(h2_handle* h, const double* Xf, int stat_kmax, int sta
     int launches[kIdClasses + 2], nl = 0;
     if (merge) launches[nl++] = -1;
     else
-      for (int cls = 0; cls < kIdClasses; cls++)
+      for (int cls = 0; cls < kIdMid; cls++)
         if (smem_bytes[cls] > 0) launches[nl++] = cls;
+    if (smem_bytes[kIdMid] > 0) launches[nl++] = kIdMid;
     if (smem_bytes[kIdLean] > 0) launches[nl++] = kIdLean;
     int used = 0;
     cudaEvent_t lev_ev[h2_handle::kAux + 1];
@@ -903,7 +920,7 @@ static void id_sweep_pass(h2_handle* h, const double* Xf, int stat_kmax, int sta
       int kind = 0;  // instantiations this launch needs
       if (cls >= 0) kind = kinds[cls];
       else
-        for (int c2 = 0; c2 < kIdClasses; c2++) kind |= kinds[c2];
+        for (int c2 = 0; c2 < kIdMid; c2++) kind |= kinds[c2];
       for (int pv = 0; pv < 2; pv++) {
         if (!(kind & (1 << pv))) continue;
         const int lid = cls >= 0 ? cls * 2 + pv : 2 * (kIdClasses + 1) + pv;
@@ -917,7 +934,7 @@ static void id_sweep_pass(h2_handle* h, const double* Xf, int stat_kmax, int sta
           if (used < h2_handle::kAux) H2_CUDA_TRY(cudaStreamWaitEvent(cs, lev_ev[h2_handle::kAux], 0));
           used++;
         }
-        const bool lean = cls == kIdLean;
+        const bool lean = cls == kIdLean, mid = cls == kIdMid;
         switch (h->d) {
 #define H2_ID_LAUNCH(DD, NTT, PV, MAXS)                                                                          \
   do {                                                                                                          \
@@ -934,6 +951,9 @@ static void id_sweep_pass(h2_handle* h, const double* Xf, int stat_kmax, int sta
     if (lean) {                                                                                                 \
       if (pv) H2_ID_LAUNCH(DD, kIdLeanThreads, true, kIdLeanMax);                                               \
       else H2_ID_LAUNCH(DD, kIdLeanThreads, false, kIdLeanMax);                                                 \
+    } else if (mid) {                                                                                           \
+      if (pv) H2_ID_LAUNCH(DD, kIdMidThreads, true, kIdMidMax);                                                 \
+      else H2_ID_LAUNCH(DD, kIdMidThreads, false, kIdMidMax);                                                   \
     } else {                                                                                                    \
       if (pv) H2_ID_LAUNCH(DD, kIdSmemThreads, true, kIdSmemMax);                                               \
       else H2_ID_LAUNCH(DD, kIdSmemThreads, false, kIdSmemMax);                                                 \
