@@ -27,31 +27,29 @@ constexpr int kFillThreads = 256;
 constexpr int kNfThreads = H2_NF_THREADS;
 constexpr int kNfScale = 256 / kNfThreads;
 
-// ---- symmetric-once pair lists, entry-parallel over the CSR ---------------------------------
-__device__ __forceinline__ int row_of(const int64_t* __restrict__ off, int nnodes, int64_t e) {
-  int lo = 0, hi = nnodes - 1;  // last i with off[i] <= e
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (off[mid] <= e) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
-
+// ---- symmetric-once pair lists over the CSR ----------------------------------------------------
 // a pair is stored (and applied by the matvec) by the rank owning its row: nbegin[i] in [p_lo, p_hi).
 // Symmetric: i < j (coupling), i <= j (nearfield); non-symmetric: every ordered pair (the column
 // ranks kc of the coupling blocks are the column-basis ranks).
+// a warp per CSR row (grid-stride over rows), lanes over the row's entries: the row is known
+// without a per-entry binary search over the offsets (round 2: the search's dependent loads made
+// these two kernels ~0.2-0.4 ms per list on configs[1] and configs[4])
 __global__ void pair_flag_kernel(int mode, int nonsym, int nnodes, int64_t m, const int64_t* __restrict__ off,
                                  const int* __restrict__ idx, const int* __restrict__ k, const int* __restrict__ kc,
                                  const int* __restrict__ nbegin, int p_lo, int p_hi, int64_t* flag) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= m; e += (int64_t)gridDim.x * blockDim.x) {
-    if (e == m) {
-      flag[e] = 0;
-      continue;
-    }
-    int i = row_of(off, nnodes, e), j = idx[e];
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if (w0 == 0 && lane == 0) flag[m] = 0;
+  for (int64_t i = w0; i < nnodes; i += nw) {
+    const int64_t e0 = off[i], e1 = off[i + 1];
+    if (e0 == e1) continue;
     const bool own = nbegin[i] >= p_lo && nbegin[i] < p_hi;
-    flag[e] = own && (mode == 0 ? ((nonsym || j > i) && k[i] > 0 && kc[j] > 0) : (nonsym || j >= i));
+    const bool ki = mode != 0 || k[i] > 0;
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const int j = idx[e];
+      flag[e] = own && (mode == 0 ? ((nonsym || j > i) && ki && kc[j] > 0) : (nonsym || j >= i));
+    }
   }
 }
 
@@ -60,12 +58,20 @@ __global__ void pair_emit_kernel(int mode, int nnodes, int64_t m, const int64_t*
                                  const int* __restrict__ nbegin,
                                  const int* __restrict__ nend, const int64_t* __restrict__ pos, int2* pairs,
                                  int64_t* size) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
-    if (pos[e + 1] == pos[e]) continue;
-    int i = row_of(off, nnodes, e), j = idx[e];
-    int64_t o = pos[e];
-    pairs[o] = make_int2(i, j);
-    size[o] = mode == 0 ? (int64_t)k[i] * kc[j] : (int64_t)(nend[i] - nbegin[i]) * (nend[j] - nbegin[j]);
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = w0; i < nnodes; i += nw) {
+    const int64_t e0 = off[i], e1 = off[i + 1];
+    if (e0 == e1) continue;
+    const int64_t si = mode == 0 ? (int64_t)k[i] : (int64_t)(nend[i] - nbegin[i]);
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const int64_t o = pos[e];
+      if (pos[e + 1] == o) continue;
+      const int j = idx[e];
+      pairs[o] = make_int2((int)i, j);
+      size[o] = si * (mode == 0 ? (int64_t)kc[j] : (int64_t)(nend[j] - nbegin[j]));
+    }
   }
 }
 
@@ -431,8 +437,8 @@ static void make_pairs(h2_handle* h, cudaStream_t s, int mode, int64_t& np, int2
   const int* idx = mode == 0 ? h->il_idx : h->nf_idx;
   const int64_t m = mode == 0 ? h->n_il : h->n_nf;
   Scratch flag(sizeof(int64_t) * (m + 1), s), pos(sizeof(int64_t) * (m + 1), s);
-  pair_flag_kernel<<<grid_for(m + 1, 256), 256, 0, s>>>(mode, h->nonsym, nn, m, off, idx, h->k, h->k_col, h->nbegin,
-                                                        h->p_lo, h->p_hi, flag.as<int64_t>());
+  pair_flag_kernel<<<grid_for((int64_t)nn * 32, 256), 256, 0, s>>>(mode, h->nonsym, nn, m, off, idx, h->k, h->k_col,
+                                                                   h->nbegin, h->p_lo, h->p_hi, flag.as<int64_t>());
   scan_excl_i64(flag.as<int64_t>(), pos.as<int64_t>(), m + 1, s);
   H2_CHECK_LAUNCH();
   np = read1(pos.as<int64_t>() + m, s);
@@ -441,8 +447,9 @@ static void make_pairs(h2_handle* h, cudaStream_t s, int mode, int64_t& np, int2
   Scratch size(sizeof(int64_t) * (np + 1), s);
   H2_CUDA_TRY(cudaMemsetAsync(size.as<int64_t>() + np, 0, sizeof(int64_t), s));
   if (m > 0)
-    pair_emit_kernel<<<grid_for(m, 256), 256, 0, s>>>(mode, nn, m, off, idx, h->k, h->k_col, h->nbegin, h->nend,
-                                                      pos.as<int64_t>(), pairs, size.as<int64_t>());
+    pair_emit_kernel<<<grid_for((int64_t)nn * 32, 256), 256, 0, s>>>(mode, nn, m, off, idx, h->k, h->k_col, h->nbegin,
+                                                                     h->nend, pos.as<int64_t>(), pairs,
+                                                                     size.as<int64_t>());
   scan_excl_i64(size.as<int64_t>(), voff, np + 1, s);
   H2_CHECK_LAUNCH();
   h->gpu_launches += 2;  // + the scans (prims.cu counts its own launches)
