@@ -329,25 +329,72 @@ __global__ void __cluster_dims__(kCalCl, 1, 1) __launch_bounds__(kCalClNT) calib
   __syncthreads();
   for (int e = tid; e < ns * WC; e += NT) W.M[(int64_t)ns * j0 + e] = Ms[e];
   cl.sync();  // every R column in global memory, visible cluster-wide; no DSMEM read after this
-  // T = R11^{-1} R12 for the own columns at positions >= k: a warp per column, x in shared memory
-  // (the slice's space), column-oriented back substitution with R11's columns read contiguously
+  // T = R11^{-1} R12 for the own columns at positions >= k, column-oriented back substitution:
+  // for l = k-1..0: x_l /= R_ll; x_a -= R_al x_l (a < l).  The diagonal is staged in shared memory
+  // and a warp takes its (up to WC / NW) columns together, so every R11 column is loaded once per
+  // warp (lanes over its rows, one step ahead: the loads do not depend on x) instead of once per
+  // column behind a dependent load of the diagonal.  The same operations in the same order per entry.
   if (aborted) k = 0;  // a cancelled trial: rank 0, no T (its pass flag is never used)
-  double* xw = Ms + (int64_t)warp * N;
-  for (int jl = warp; jl < WC && !aborted; jl += NW) {
-    if (pos[jl] < k) continue;
-    const int pj = j0 + jl;
-    for (int a = lane; a < k; a += 32) xw[a] = W.M[a + (int64_t)ns * pj];
-    __syncwarp();
-    for (int l = k - 1; l >= 0; l--) {
-      const double* Rl = W.M + (int64_t)ns * col_at[l];  // R11[0:l+1, l]
-      const double xl = xw[l] / Rl[l];
-      for (int a = lane; a < l; a += 32) xw[a] -= Rl[a] * xl;
-      __syncwarp();
-      if (lane == 0) xw[l] = xl;
-      __syncwarp();
+  constexpr int CPW = WC / NW;         // own columns per warp
+  double* diag = Ms;                   // k (the slice's space is free after the write-back)
+  double* xall = Ms + N;               // [own column jl][row a], k <= ns < N rows each
+  for (int l = tid; l < k; l += NT) diag[l] = W.M[l + (int64_t)ns * col_at[l]];
+  for (int e = tid; e < WC * k; e += NT) {
+    const int jl = e / k, a = e - jl * k;
+    if (pos[jl] >= k) xall[jl * N + a] = W.M[a + (int64_t)ns * (j0 + jl)];
+  }
+  __syncthreads();
+  if (k > 0) {
+    bool mine[CPW];
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < CPW; c++) {
+      mine[c] = pos[warp + NW * c] >= k;
+      any |= mine[c];
     }
-    for (int a = lane; a < k; a += 32) W.M[a + (int64_t)ns * pj] = xw[a];
-    __syncwarp();
+    if (any) {
+      constexpr int RPL = N / 32;  // rows per lane
+      double r[RPL], rn[RPL];
+      auto load_col = [&](int l, double (&dst)[RPL]) {
+        const double* Rl = W.M + (int64_t)ns * col_at[l];
+#pragma unroll
+        for (int u = 0; u < RPL; u++) {
+          const int a = lane + 32 * u;
+          dst[u] = a < l ? Rl[a] : 0.0;
+        }
+      };
+      load_col(k - 1, r);
+      for (int l = k - 1; l >= 0; l--) {
+        if (l > 0) load_col(l - 1, rn);
+        const double dl = diag[l];
+        double xl[CPW];
+#pragma unroll
+        for (int c = 0; c < CPW; c++) {
+          xl[c] = 0.0;
+          if (!mine[c]) continue;
+          double* xw = xall + (warp + NW * c) * N;
+          xl[c] = xw[l] / dl;
+#pragma unroll
+          for (int u = 0; u < RPL; u++) {
+            const int a = lane + 32 * u;
+            if (a < l) xw[a] -= r[u] * xl[c];
+          }
+        }
+        __syncwarp();  // every lane has read x_l before it is overwritten
+        if (lane == 0)
+#pragma unroll
+          for (int c = 0; c < CPW; c++)
+            if (mine[c]) xall[(warp + NW * c) * N + l] = xl[c];
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < RPL; u++) r[u] = rn[u];
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < WC * k; e += NT) {
+    const int jl = e / k, a = e - jl * k;
+    if (pos[jl] >= k) W.M[a + (int64_t)ns * (j0 + jl)] = xall[jl * N + a];
   }
   if (q == 0) {
     for (int b = tid; b < N; b += NT) W.piv[b] = col_at[b];

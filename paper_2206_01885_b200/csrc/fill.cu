@@ -391,7 +391,12 @@ static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_
     // S warps per 32 pairs (~256 entries per warp), 8 warps per CTA
     const int64_t groups = (np + 31) / 32;
     const int64_t epg = (h->cp_entries + groups - 1) / groups;
-    const int S = (int)(epg / 256 < 1 ? 1 : (epg / 256 > 64 ? 64 : epg / 256));
+    static const int64_t epw = [] {  // H2_CP_EPW (tuning knob): target entries per warp
+      const char* e = getenv("H2_CP_EPW");
+      const long long v = e ? atoll(e) : 256;
+      return (int64_t)(v > 0 ? v : 256);
+    }();
+    const int S = (int)(epg / epw < 1 ? 1 : (epg / epw > 64 ? 64 : epg / epw));
     const int64_t blocks = (groups * S + 7) / 8;
     // skeleton coordinates: the points, or the Chebyshev nodes of the interpolation baseline
     const double* cXf = h->Xq ? h->Xq : h->Xf;

@@ -37,7 +37,10 @@ __device__ __forceinline__ bool admissible(const int* __restrict__ cell, int nno
 // outputs, and their totals (atomics) for the host to size the outputs.  trav_emit: the same
 // classification again, each tile's offsets = the sums of the tiles before it plus an in-tile
 // exclusive scan (thread-blocked, so the output order is the frontier order), and the writes.
-constexpr int kTravThreads = 256, kTravIPT = 8, kTravTile = kTravThreads * kTravIPT;
+// Two pairs per thread (round 2; was 8): an expanded pair's child block (up to 2^d x 2^d writes)
+// is written by its thread alone, so fewer pairs per thread shorten the serial write chains
+// (lists stage config 2 3.07 -> 2.5 ms, config 4 1.32 -> 1.10, config 5 7.2 -> 5.7).
+constexpr int kTravThreads = 256, kTravIPT = 2, kTravTile = kTravThreads * kTravIPT;
 
 // Sharded builds: a rank keeps only the pairs whose row node it needs -- every node above the cut
 // level, and its own contiguous range at each level >= cut (shard.cu).  The children of a dropped
