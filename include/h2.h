@@ -269,9 +269,10 @@ enum {
   H2_EXPORT_SHARD = 19,   /* int64[5 + 2*(depth+1)]: nranks, rank, cut level, p_lo, p_hi, then per */
                           /* level l the node range [lo_l, hi_l) this rank computed               */
   H2_EXPORT_BLOCK_SAMPLE = 20, /* see h2_sample_blocks                                           */
-  H2_EXPORT_ID_PATH = 21, /* int32[nnodes]: the a8 code path of each node's ID: 0..6 staged       */
-                          /* shared-memory size classes, 7 lean shared-memory class, 8 / 9 global */
-                          /* memory (256 / 1024 threads), 10 thread-block cluster, -1 no basis    */
+  H2_EXPORT_ID_PATH = 21, /* int32[nnodes]: the a8 code path of each node's ID: 0..5 staged       */
+                          /* shared-memory size classes, 6 mid class (256 threads, 2 CTAs/SM),   */
+                          /* 7 lean shared-memory class, 8 / 9 global memory (256 / 1024          */
+                          /* threads), 10 thread-block cluster, 11 warp per node, -1 no basis     */
   /* the column bases of the non-symmetric path (as K, SK_*, U_*, XBAR_N for the row bases)       */
   H2_EXPORT_K_COL = 22, H2_EXPORT_SKC_OFF = 23, H2_EXPORT_SKC_IDX = 24, H2_EXPORT_V_OFF = 25,
   H2_EXPORT_V = 26, H2_EXPORT_XBARC_N = 27,

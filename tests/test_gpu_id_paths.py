@@ -2,7 +2,7 @@
 element on U / stacked R_c (Eq.(4.1): K_{X Y*} = P [I; G] K_{X^ Y*}).
 
 The sweep picks a path per node by block size (H2_EXPORT_ID_PATH): the staged shared-memory
-classes 0..6, the lean shared-memory class 7, the global-memory CTA 8 / 9, the thread-block
+classes 0..5, the mid class 6 (lean layout, 256 threads, two CTAs per SM), the lean shared-memory class 7, the global-memory CTA 8 / 9, the thread-block
 cluster 10, and (H2_ID_WARP_MIN) one warp per node 11.  Each case runs the GPU build in a subprocess (the path thresholds are read once per
 process from the environment) and compares it with the oracle on the same seeded points:
   * r, tree, lists, X^*, Y^* bit-exact;
@@ -66,7 +66,7 @@ CASES = [  # name, config, n, q, environment, {path: minimum node count}
     ("cfg1_staged", 1, 8192, 64, {"H2_ID_WARP_MIN": "0"}, {"staged": 100}),
     ("cfg4_staged", 4, 60000, 256, {"H2_ID_WARP_MIN": "0"}, {"staged": 200}),
     ("cfg3_lean_global", 3, 30000, 128, {"H2_ID_WARP_MIN": "0"}, {"lean": 20}),
-    ("cfg2_tol1e-8", 2, 60000, 200, {"H2_ID_WARP_MIN": "0"}, {"staged": 50}),
+    ("cfg2_tol1e-8", 2, 60000, 200, {"H2_ID_WARP_MIN": "0"}, {"staged": 20, "mid": 20}),
     ("cfg5_cluster", 5, 32768, 256, {"H2_ID_CLMIN": "1", "H2_ID_WARP_MIN": "0"}, {"cluster": 50, "lean": 50}),
     ("cfg5_global", 5, 32768, 256, {"H2_ID_CLUSTER": "0", "H2_ID_WARP_MIN": "0"}, {"global": 50}),
     # the warp-per-node path (off by default: measured slower; here every level)
@@ -77,10 +77,10 @@ CASES = [  # name, config, n, q, environment, {path: minimum node count}
     ("cfg5_warp", 5, 32768, 256, {"H2_ID_WARP_MIN": "1"}, {"warp": 500}),
     # the unblocked CPQR (H2_ID_PANEL=0) on the same shapes: both factorisations meet the same bar
     ("cfg3_unblocked", 3, 30000, 128, {"H2_ID_PANEL": "0", "H2_ID_WARP_MIN": "0"}, {"lean": 20}),
-    ("cfg2_unblocked", 2, 60000, 200, {"H2_ID_PANEL": "0", "H2_ID_WARP_MIN": "0"}, {"staged": 50}),
+    ("cfg2_unblocked", 2, 60000, 200, {"H2_ID_PANEL": "0", "H2_ID_WARP_MIN": "0"}, {"staged": 20, "mid": 20}),
 ]
 
-PATHS = {"staged": range(0, 7), "lean": (7,), "global": (8, 9), "cluster": (10,), "warp": (11,)}
+PATHS = {"staged": range(0, 6), "mid": (6,), "lean": (7,), "global": (8, 9), "cluster": (10,), "warp": (11,)}
 
 
 @pytest.mark.parametrize("name,cfg,n,q,env,need", CASES)
