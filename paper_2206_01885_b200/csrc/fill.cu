@@ -34,43 +34,46 @@ constexpr int kNfScale = 256 / kNfThreads;
 // a warp per CSR row (grid-stride over rows), lanes over the row's entries: the row is known
 // without a per-entry binary search over the offsets (round 2: the search's dependent loads made
 // these two kernels ~0.2-0.4 ms per list on configs[1] and configs[4])
+// flag[e] = 1 when CSR entry e is a stored pair, size[e] its block's entry count (0 otherwise)
 __global__ void pair_flag_kernel(int mode, int nonsym, int nnodes, int64_t m, const int64_t* __restrict__ off,
                                  const int* __restrict__ idx, const int* __restrict__ k, const int* __restrict__ kc,
-                                 const int* __restrict__ nbegin, int p_lo, int p_hi, int64_t* flag) {
+                                 const int* __restrict__ nbegin, const int* __restrict__ nend, int p_lo, int p_hi,
+                                 int64_t* flag, int64_t* size) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  if (w0 == 0 && lane == 0) flag[m] = 0;
+  if (w0 == 0 && lane == 0) flag[m] = size[m] = 0;
   for (int64_t i = w0; i < nnodes; i += nw) {
     const int64_t e0 = off[i], e1 = off[i + 1];
     if (e0 == e1) continue;
     const bool own = nbegin[i] >= p_lo && nbegin[i] < p_hi;
     const bool ki = mode != 0 || k[i] > 0;
+    const int64_t si = mode == 0 ? (int64_t)k[i] : (int64_t)(nend[i] - nbegin[i]);
     for (int64_t e = e0 + lane; e < e1; e += 32) {
       const int j = idx[e];
-      flag[e] = own && (mode == 0 ? ((nonsym || j > i) && ki && kc[j] > 0) : (nonsym || j >= i));
+      const bool f = own && (mode == 0 ? ((nonsym || j > i) && ki && kc[j] > 0) : (nonsym || j >= i));
+      flag[e] = f;
+      size[e] = f ? si * (mode == 0 ? (int64_t)kc[j] : (int64_t)(nend[j] - nbegin[j])) : 0;
     }
   }
 }
 
-__global__ void pair_emit_kernel(int mode, int nnodes, int64_t m, const int64_t* __restrict__ off,
-                                 const int* __restrict__ idx, const int* __restrict__ k, const int* __restrict__ kc,
-                                 const int* __restrict__ nbegin,
-                                 const int* __restrict__ nend, const int64_t* __restrict__ pos, int2* pairs,
-                                 int64_t* size) {
+// pairs[pos[e]] = (i, j) and voff[pos[e]] = the scanned size of every stored CSR entry e; voff[np] = total
+__global__ void pair_emit_kernel(int nnodes, int64_t m, const int64_t* __restrict__ off,
+                                 const int* __restrict__ idx, const int64_t* __restrict__ pos,
+                                 const int64_t* __restrict__ spos, int2* pairs, int64_t* voff) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if (w0 == 0 && lane == 0) voff[pos[m]] = spos[m];
   for (int64_t i = w0; i < nnodes; i += nw) {
     const int64_t e0 = off[i], e1 = off[i + 1];
     if (e0 == e1) continue;
-    const int64_t si = mode == 0 ? (int64_t)k[i] : (int64_t)(nend[i] - nbegin[i]);
     for (int64_t e = e0 + lane; e < e1; e += 32) {
       const int64_t o = pos[e];
       if (pos[e + 1] == o) continue;
-      const int j = idx[e];
-      pairs[o] = make_int2((int)i, j);
-      size[o] = si * (mode == 0 ? (int64_t)kc[j] : (int64_t)(nend[j] - nbegin[j]));
+      pairs[o] = make_int2((int)i, idx[e]);
+      voff[o] = spos[e];
     }
   }
 }
@@ -330,8 +333,8 @@ __global__ void scale_coords_kernel(int64_t m, const double* __restrict__ X, dou
 static int nf_units_per_warp() {
   static const int v = [] {
     const char* e = getenv("H2_NF_UPW");
-    const int u = e ? atoi(e) : 4;
-    return u > 0 ? u : 4;
+    const int u = e ? atoi(e) : 8;
+    return u > 0 ? u : 8;
   }();
   return v;
 }
@@ -441,24 +444,30 @@ static void make_pairs(h2_handle* h, cudaStream_t s, int mode, int64_t& np, int2
   const int64_t* off = mode == 0 ? h->il_off : h->nf_off;
   const int* idx = mode == 0 ? h->il_idx : h->nf_idx;
   const int64_t m = mode == 0 ? h->n_il : h->n_nf;
-  Scratch flag(sizeof(int64_t) * (m + 1), s), pos(sizeof(int64_t) * (m + 1), s);
+  // flags and block sizes per CSR entry, both scanned, the two totals read back at once: the pair
+  // count and the entry count (one host synchronisation), then the pairs and their offsets
+  Scratch fs(sizeof(int64_t) * 2 * (m + 1), s), ps(sizeof(int64_t) * 2 * (m + 1), s);
+  int64_t *flag = fs.as<int64_t>(), *size = flag + (m + 1);
+  int64_t *pos = ps.as<int64_t>(), *spos = pos + (m + 1);
   pair_flag_kernel<<<grid_for((int64_t)nn * 32, 256), 256, 0, s>>>(mode, h->nonsym, nn, m, off, idx, h->k, h->k_col,
-                                                                   h->nbegin, h->p_lo, h->p_hi, flag.as<int64_t>());
-  scan_excl_i64(flag.as<int64_t>(), pos.as<int64_t>(), m + 1, s);
+                                                                   h->nbegin, h->nend, h->p_lo, h->p_hi, flag, size);
+  scan_excl_i64(flag, pos, m + 1, s);
+  scan_excl_i64(size, spos, m + 1, s);
   H2_CHECK_LAUNCH();
-  np = read1(pos.as<int64_t>() + m, s);
+  {
+    thread_local int64_t* tot = nullptr;  // page-locked, per host thread
+    if (!tot) H2_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&tot), 2 * sizeof(int64_t)));
+    H2_CUDA_TRY(cudaMemcpyAsync(tot, pos + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    H2_CUDA_TRY(cudaMemcpyAsync(tot + 1, spos + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    H2_CUDA_TRY(cudaStreamSynchronize(s));
+    np = tot[0];
+    entries = tot[1];
+  }
   pairs = halloc<int2>(h, np);
   voff = halloc<int64_t>(h, np + 1);
-  Scratch size(sizeof(int64_t) * (np + 1), s);
-  H2_CUDA_TRY(cudaMemsetAsync(size.as<int64_t>() + np, 0, sizeof(int64_t), s));
-  if (m > 0)
-    pair_emit_kernel<<<grid_for((int64_t)nn * 32, 256), 256, 0, s>>>(mode, nn, m, off, idx, h->k, h->k_col, h->nbegin,
-                                                                     h->nend, pos.as<int64_t>(), pairs,
-                                                                     size.as<int64_t>());
-  scan_excl_i64(size.as<int64_t>(), voff, np + 1, s);
+  pair_emit_kernel<<<grid_for((int64_t)nn * 32, 256), 256, 0, s>>>(nn, m, off, idx, pos, spos, pairs, voff);
   H2_CHECK_LAUNCH();
   h->gpu_launches += 2;  // + the scans (prims.cu counts its own launches)
-  entries = read1(voff + np, s);
 }
 
 static int64_t pool_available() {
@@ -494,24 +503,30 @@ void fill_nearfield_begin(h2_handle* h, cudaStream_t side, int storage, int64_t 
   int64_t nunits = 0;
   if (store_np && h->n_np > 0) {
     const int64_t np = h->n_np;
-    Scratch units(sizeof(int64_t) * (np + 1), side);
+    // the fill's units and the matvec's items per pair, both scanned, one readback of the totals
+    Scratch units(sizeof(int64_t) * 2 * (np + 1), side);
+    int64_t* items = units.as<int64_t>() + (np + 1);
     h->nf_wc = 32 * nf_slots(h->d);
     h->nf_uoff = halloc_on<int64_t>(h, np + 1, side);
+    h->nf_ioff = halloc_on<int64_t>(h, np + 1, side);
     nf_units_kernel<<<grid_for(np + 1, 256), 256, 0, side>>>(h->nf_wc, np, h->np_pairs, h->nbegin, h->nend,
                                                              units.as<int64_t>());
+    nf_items_kernel<<<grid_for(np + 1, 256), 256, 0, side>>>(h->nf_wc, np, h->np_pairs, h->nbegin, h->nend, items);
     scan_excl_i64(units.as<int64_t>(), h->nf_uoff, np + 1, side);
+    scan_excl_i64(items, h->nf_ioff, np + 1, side);
     H2_CHECK_LAUNCH();
-    nunits = read1(h->nf_uoff + np, side);
+    {
+      thread_local int64_t* tot = nullptr;  // page-locked, per host thread
+      if (!tot) H2_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&tot), 2 * sizeof(int64_t)));
+      H2_CUDA_TRY(cudaMemcpyAsync(tot, h->nf_uoff + np, sizeof(int64_t), cudaMemcpyDeviceToHost, side));
+      H2_CUDA_TRY(cudaMemcpyAsync(tot + 1, h->nf_ioff + np, sizeof(int64_t), cudaMemcpyDeviceToHost, side));
+      H2_CUDA_TRY(cudaStreamSynchronize(side));
+      nunits = tot[0];
+      h->nf_nitems = tot[1];
+    }
     h->nf_nunits = nunits;
     h->nf_umap = halloc_on<int>(h, nunits > 0 ? nunits : 1, side);
     unit_map_kernel<<<grid_for(np, 256), 256, 0, side>>>(np, h->nf_uoff, h->nf_umap);
-    H2_CHECK_LAUNCH();
-    h->nf_ioff = halloc_on<int64_t>(h, np + 1, side);
-    nf_items_kernel<<<grid_for(np + 1, 256), 256, 0, side>>>(h->nf_wc, np, h->np_pairs, h->nbegin, h->nend,
-                                                             units.as<int64_t>());
-    scan_excl_i64(units.as<int64_t>(), h->nf_ioff, np + 1, side);
-    H2_CHECK_LAUNCH();
-    h->nf_nitems = read1(h->nf_ioff + np, side);
     h->nf_imap = halloc_on<int>(h, h->nf_nitems > 0 ? h->nf_nitems : 1, side);
     unit_map_kernel<<<grid_for(np, 256), 256, 0, side>>>(np, h->nf_ioff, h->nf_imap);
     H2_CHECK_LAUNCH();
