@@ -85,8 +85,11 @@ __global__ void pair_emit_kernel(int nnodes, int64_t m, const int64_t* __restric
 // offset of 256 s bytes from the lane's row pointer.  The inner loop is the kernel evaluation.
 __host__ __device__ constexpr int warp_slots(int D) { return D <= 2 ? 8 : (D <= 3 ? 5 : (D <= 5 ? 3 : 2)); }
 
-// H2_FILL_VARIANT (tuning knob, read once): selects the (slots, rows per iteration, min blocks)
-// instantiation of the D = 2 nearfield kernel; 0 = default (8 slots, 2 CTAs/SM: fastest measured).
+// H2_FILL_VARIANT (tuning knob, read once): selects the (slots, clamp, min blocks) instantiation of the
+// D = 2 nearfield kernel; 0 = default (8 slots, 6 CTAs of 128 threads per SM at 80 registers: round 2
+// measured config 4 builds of 18.9 ms against 19.7 for the round-1 default, variant 7, at 124 registers
+// and 4 CTAs per SM -- more resident warps hide the fill's latency, and each main-stream CTA displaces
+// a smaller share of an SM's fill throughput).
 static int nf_variant() {
   static const int v = [] {
     const char* e = getenv("H2_FILL_VARIANT");
@@ -97,7 +100,12 @@ static int nf_variant() {
 static int nf_slots(int d) {
   if (d != 2) return warp_slots(d);
   const int v = nf_variant();
-  return v == 1 || v == 2 ? 4 : (v == 3 ? 6 : (v == 5 ? 2 : 8));
+  switch (v) {  // the column slots CW of each variant's instantiation (launch_fill_kid)
+    case 1: case 2: return 4;
+    case 3: return 6;
+    case 5: return 2;
+    default: return 8;
+  }
 }
 
 
@@ -168,8 +176,10 @@ __device__ __forceinline__ void nf_unit_rows(const double* __restrict__ xr, int6
   }
 }
 
+// MINB: minimum resident CTAs per SM of 256 threads' worth (scaled by kNfScale); MINB >= 10 means
+// MINB / 10 CTAs of kNfThreads directly (the register-capped variants of H2_FILL_VARIANT 6-8)
 template <int D, int KID, int CW, int CL, int MINB>
-__global__ void __launch_bounds__(kNfThreads, MINB * kNfScale) nf_fill_kernel(int64_t nunits, const int* __restrict__ umap,
+__global__ void __launch_bounds__(kNfThreads, MINB >= 10 ? MINB / 10 : MINB * kNfScale) nf_fill_kernel(int64_t nunits, const int* __restrict__ umap,
                                                                      const int64_t* __restrict__ uoff,
                                                                      const int2* __restrict__ pairs,
                                                                      const int64_t* __restrict__ voff,
@@ -376,9 +386,11 @@ static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_
           case 3: launch_nf(nf_fill_kernel<2, KID, 6, 1, 2>, g, s, H2_NF_ARGS); break;
           case 4: launch_nf(nf_fill_kernel<2, KID, 8, 1, 1>, g, s, H2_NF_ARGS); break;
           case 5: launch_nf(nf_fill_kernel<2, KID, 2, 1, 4>, g, s, H2_NF_ARGS); break;
-          default:
-            if (clamp) launch_nf(nf_fill_kernel<2, KID, 8, 1, 2>, g, s, H2_NF_ARGS);
-            else launch_nf(nf_fill_kernel<2, KID, 8, 0, 2>, g, s, H2_NF_ARGS);
+          case 6: launch_nf(nf_fill_kernel<2, KID, 8, 0, 50>, g, s, H2_NF_ARGS); break;  // 5 CTAs/SM, 96 regs
+          case 7: launch_nf(nf_fill_kernel<2, KID, 8, 0, 2>, g, s, H2_NF_ARGS); break;   // round 1: 4 CTAs/SM, 124 regs
+          default:  // 8 slots, 6 CTAs of 128 threads per SM (80 registers, no spill): round 2's measured best
+            if (clamp) launch_nf(nf_fill_kernel<2, KID, 8, 1, 60>, g, s, H2_NF_ARGS);
+            else launch_nf(nf_fill_kernel<2, KID, 8, 0, 60>, g, s, H2_NF_ARGS);
             break;
         }
         break;
