@@ -388,6 +388,8 @@ static void launch_fill_kid(const h2_handle* h, cudaStream_t s, int mode, int64_
           case 5: launch_nf(nf_fill_kernel<2, KID, 2, 1, 4>, g, s, H2_NF_ARGS); break;
           case 6: launch_nf(nf_fill_kernel<2, KID, 8, 0, 50>, g, s, H2_NF_ARGS); break;  // 5 CTAs/SM, 96 regs
           case 7: launch_nf(nf_fill_kernel<2, KID, 8, 0, 2>, g, s, H2_NF_ARGS); break;   // round 1: 4 CTAs/SM, 124 regs
+          case 8: launch_nf(nf_fill_kernel<2, KID, 8, 0, 70>, g, s, H2_NF_ARGS); break;  // 7 CTAs/SM, 72 regs
+          case 9: launch_nf(nf_fill_kernel<2, KID, 8, 0, 80>, g, s, H2_NF_ARGS); break;  // 8 CTAs/SM, 64 regs
           default:  // 8 slots, 6 CTAs of 128 threads per SM (80 registers, no spill): round 2's measured best
             if (clamp) launch_nf(nf_fill_kernel<2, KID, 8, 1, 60>, g, s, H2_NF_ARGS);
             else launch_nf(nf_fill_kernel<2, KID, 8, 0, 60>, g, s, H2_NF_ARGS);
