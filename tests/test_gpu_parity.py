@@ -452,13 +452,18 @@ np.save(out, g.matvec(x).cpu().numpy())
 
 @pytest.mark.parametrize("knobs,cfg,n", [({"H2_MV_DYN": "0"}, 4, 200000), ({"H2_MV_PF": "0"}, 4, 200000),
                                          ({"H2_MV_ORDER": "1"}, 4, 200000), ({"H2_MV_BULK": "1"}, 4, 200000),
-                                         ({"H2_MV_BULK": "1"}, 5, 40000), ({"H2_MV_BULK": "1"}, 2, 120000)])
+                                         ({"H2_MV_BULK": "1"}, 5, 40000), ({"H2_MV_BULK": "1"}, 2, 120000),
+                                         ({"H2_FILL_VARIANT": "1"}, 4, 200000), ({"H2_FILL_VARIANT": "3"}, 4, 200000),
+                                         ({"H2_FILL_VARIANT": "5"}, 4, 200000), ({"H2_FILL_VARIANT": "7"}, 4, 200000),
+                                         ({"H2_FILL_VARIANT": "8"}, 4, 200000), ({"H2_FILL_VARIANT": "9"}, 4, 200000)])
 def test_matvec_variants_equal_default(knobs, cfg, n, tmp_path):
     """The stored-block matvec's scheduling variants (grid-stride instead of the resident wave, no L2
     prefetch, farfield chain first, the bulk-copy nearfield kernel) against the default on the same
     stored build: the same products, summed by atomics in another order (relative 1e-12).  The bulk
     variant also on configs[4] / configs[1] shapes (d = 5 / 3: units wider than one column chunk,
-    odd block widths -> row-wise copies)."""
+    odd block widths -> row-wise copies).  The 2-D nearfield-fill variants (H2_FILL_VARIANT: other
+    column-slot counts and register caps, fill.cu) write the stored blocks the default matvec then
+    reads: a misplaced or miscomputed entry moves y far beyond the 1e-12."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
